@@ -1,0 +1,163 @@
+/*
+ * msb200.h -- C ABI of libmsb200.so, the B200 (sm_100a) multispin Ising
+ * hot path: bit-packed checkerboard Metropolis sweeps over many replicas and
+ * row slabs of very large lattices.
+ *
+ * The reference (`multispin`, pure Python/numpy) has no FFI; its operator
+ * seam is the `Engine` class and `run_simulations`
+ * (pkg/src/multispin/__init__.py:26, engine.py:216-492).  Each entry point
+ * below names the reference code it replaces.  The Python drop-in
+ * (paper_2404_16990_b200.engine.Engine) binds these with ctypes; a
+ * maintainer could bind them from the reference the same way
+ * (INTEGRATION.md).
+ *
+ * Conventions
+ *   - Every function returns int status: MSB_OK (0) or a negative MSB_ERR_*;
+ *     msb_status_string() names it, msb_last_error() (thread-local) says why.
+ *     No C++ exception crosses the ABI.
+ *   - Device work is asynchronous on the caller's cudaStream_t (passed as
+ *     void*; NULL = legacy default stream).  The caller owns every device
+ *     buffer; the library keeps no mutable global state beyond lazily built
+ *     read-only tables.
+ *   - Spin layout ("colour split"): uint32 spins[n_sim][2][R][Wp], colour X
+ *     (0 = red, (c+r) even; 1 = blue), R = rows + 2*ghost buffer rows, row
+ *     pitch Wp words.  Bit b of word j of lattice row c, colour X, is the
+ *     site r = 2(32j+b) + ((c+X)&1).  Padding bits are always 0.
+ *   - Linear layout: uint64 lin[n_sim][rows*n/64], bit (i%64) of word i/64
+ *     is site i = (c-row0)*n + r of the held rows (np.packbits(...,
+ *     bitorder="little") of the reference's (m, n) lattice, engine.py:368-370).
+ *   - Reference interop layout: uint16 state[n_sim][8][m/4+2][n/32+2]
+ *     (engine.py:262, lattice.py:208-234), halos and moats included.
+ */
+#ifndef MSB200_H
+#define MSB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MSB_OK 0
+#define MSB_ERR_ARG -1         /* invalid argument (dims, sizes, null pointers) */
+#define MSB_ERR_CUDA -2        /* a CUDA runtime call failed */
+#define MSB_ERR_UNSUPPORTED -3 /* valid request outside what this build handles */
+
+#define MSB_MODE_FERRO 0   /* table has the J>0 Metropolis structure: 2 planes */
+#define MSB_MODE_ANTI 1    /* table has the J<0 structure: 2 planes, own spin inverted */
+#define MSB_MODE_GENERIC 2 /* arbitrary per-code table (tests overwrite Engine._tables) */
+
+#define MSB_MAX_PLANES 10
+
+typedef struct msb_geom {
+  int32_t n_sim;      /* replicas in the buffer */
+  int32_t m, n;       /* full lattice extents (LatticeDims, lattice.py:97-136) */
+  int32_t row0;       /* first lattice row c held (row-slab mode); 0 otherwise */
+  int32_t rows;       /* rows held (== m for a whole lattice) */
+  int32_t ghost;      /* 1 = one ghost row above/below per colour (slab mode) */
+  int64_t sim_offset; /* global replica index of replica 0 (engine.py:232-236) */
+} msb_geom;
+
+typedef struct msb_sweep_params {
+  int32_t mode;                  /* MSB_MODE_* */
+  int32_t n_planes;              /* distinct thresholds strictly inside (0, 2^23) */
+  const uint32_t *thr9;          /* device [n_planes][n_sim]: reject iff (u23 << 9) >= key */
+  int8_t code_plane[16];         /* GENERIC: plane per code 8*own+n_up; -1 never, -2 always */
+  int32_t kg;                    /* stream pieces per target row: 1,2,4,8 or 16 */
+  const uint32_t *jump;          /* device: 32 KiB nibble table of A^(4n) */
+  int32_t fault;                 /* test-only adder corruption (cli.py:467-480 analogue) */
+  int32_t block_rows;            /* 0 = automatic */
+} msb_sweep_params;
+
+/* ---- status -------------------------------------------------------------- */
+const char *msb_status_string(int status);
+const char *msb_last_error(void);
+int msb_abi_version(void);
+
+/* ---- geometry helpers ------------------------------------------------------ */
+/* Validates dims exactly as LatticeDims.__post_init__ (lattice.py:104-112). */
+int msb_check_geom(const msb_geom *g);
+int64_t msb_spin_words(const msb_geom *g);      /* uint32 words of the spin buffer */
+int32_t msb_row_pitch(const msb_geom *g);       /* Wp */
+int64_t msb_pieces_per_phase(const msb_geom *g, int32_t kg);
+int32_t msb_default_kg(const msb_geom *g);
+
+/* ---- thresholds: replaces the float64 gather+compare of engine.py:321-331 --- */
+/* tables: host float64 [n_sim][16] (Engine._tables, engine.py:257).  Decides
+ * the flip mode and writes host thr9[MSB_MAX_PLANES][n_sim] keys such that
+ * u23 * 2^-23 < table[s][code]  <=>  (u23 << 9) < key of the code's plane. */
+int msb_plan_thresholds(const double *tables, int32_t n_sim, int32_t *mode, int32_t *n_planes,
+                        int8_t code_plane[16], uint32_t *thr9_host);
+
+/* ---- RNG stream (rng.py:53-220, engine.py:259-261) ----------------------- */
+/* Host: 64 nibble tables of A^(2^b) (64 x 32 KiB) and of A^jump (32 KiB). */
+int msb_rng_power_tables(uint32_t *host_out);
+int msb_rng_jump_table(uint64_t jump, uint32_t *host_out);
+/* Device: per-piece xoshiro states.  One stream "block" is the 2n draws a
+ * stream spends on one colour phase (engine.py:336); sweep k uses blocks 2k
+ * (red) and 2k+1 (blue).  colour = -1 positions red at `block` and blue at
+ * `block`+1; colour = 0/1 positions only that colour at `block`.  Stream id
+ * (sim_offset+s)*(m/4) + cell-1 (engine.py:259-261).
+ * states: uint32[2][8][msb_pieces_per_phase(g, kg)]. */
+int msb_rng_init(const msb_geom *g, uint64_t seed, int32_t kg, uint64_t block, int32_t colour,
+                 const uint32_t *pow_tables, uint32_t *states, void *stream);
+
+/* ---- initial states (engine.py:274-300) ---------------------------------- */
+/* init="random": Xoshiro256pp(seed, 2^48 + sim_offset + s).bits(m*n).
+ * scratch: uint64[n_sim][rows*n/64] (the linear layout; left holding it). */
+int msb_init_random(const msb_geom *g, uint64_t seed, const uint32_t *pow_tables,
+                    uint64_t *scratch, uint32_t *spins, void *stream);
+/* init="all-up" (up=1) or all-down (up=0); also clears ghost rows/padding. */
+int msb_init_const(const msb_geom *g, int32_t up, uint32_t *spins, void *stream);
+/* from_lattices / unpack (engine.py:285-300, 368-370). */
+int msb_from_linear(const msb_geom *g, const uint64_t *lin, uint32_t *spins, void *stream);
+int msb_to_linear(const msb_geom *g, const uint32_t *spins, uint64_t *lin, void *stream);
+/* Engine.state interop incl. halo/moat refresh (engine.py:123-143,
+ * lattice.py:248-329).  Whole lattices only (row0 == 0, rows == m). */
+int msb_to_ref16(const msb_geom *g, const uint32_t *spins, uint16_t *state, void *stream);
+int msb_from_ref16(const msb_geom *g, const uint16_t *state, uint32_t *spins, void *stream);
+
+/* ---- the hot path: Engine.flip_red / flip_blue / sweep (engine.py:314-360) - */
+/* One colour phase (0 red, 1 blue) for every held row, advancing each
+ * piece's state by one sweep.  ext_draws (nullable): device uint32 u23 draws
+ * in the reference block order [n_sim][m/4][4][16][n/32] of this phase
+ * (whole lattices only); when given, the pieces' own streams are not used.
+ * flips: device uint64 accumulator (engine.py:331-332). */
+int msb_phase(const msb_geom *g, const msb_sweep_params *p, int32_t phase, uint32_t *spins,
+              uint32_t *states, const uint32_t *ext_draws, uint64_t *flips, void *stream);
+/* n_sweeps full sweeps (red then blue), whole lattices. */
+int msb_sweep(const msb_geom *g, const msb_sweep_params *p, uint32_t *spins, uint32_t *states,
+              int32_t n_sweeps, uint64_t *flips, void *stream);
+
+/* ---- observables (engine.py:372-386) ------------------------------------- */
+/* Adds, per replica, the number of +1 spins and the number of unsatisfied
+ * bonds owned by the held rows (bonds of red sites) into ups[n_sim] and
+ * unsat[n_sim] (device int64; caller zeroes).  |M| = |2 ups/N - 1|,
+ * E/N = -J (2N - 2 unsat)/N, evaluated on the host like the reference. */
+int msb_observe(const msb_geom *g, const uint32_t *spins, int64_t *ups, int64_t *unsat,
+                void *stream);
+
+/* ---- record/replay support (reference.py:179-208) ------------------------ */
+/* The u23 draws the next `phase` would consume, in the reference block order
+ * [n_sim][m/4][4][16][n/32], without advancing the states. */
+int msb_draws(const msb_geom *g, int32_t kg, int32_t phase, const uint32_t *states,
+              uint32_t *out, void *stream);
+
+/* ---- slab halo helpers (row-slab decomposition over GPUs) ----------------- */
+/* Pack colour `colour` of the first and last held rows into edge[2][Wp]
+ * (send buffers), and unpack received neighbour rows into the ghost rows. */
+int msb_pack_edges(const msb_geom *g, int32_t colour, const uint32_t *spins, uint32_t *edge,
+                   void *stream);
+int msb_unpack_ghosts(const msb_geom *g, int32_t colour, const uint32_t *ghost_rows,
+                      uint32_t *spins, void *stream);
+
+/* ---- measurement helpers ---------------------------------------------------- */
+/* Issue-bound INT32 microbenchmark (mixed ALU/FMA-pipe ops); ops_out = total
+ * integer ops executed, elapsed via CUDA events. */
+int msb_bench_int_peak(int32_t blocks, int32_t iters, double *ops_out, float *ms_out,
+                       void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,1122 @@
+// libmsb200: sm_100a kernels for the bit-packed checkerboard Metropolis hot
+// path of the reference `multispin` package (see include/msb200.h for the
+// ABI and DESIGN.md for the layout / roofline discussion).
+//
+// Reference algorithm being reproduced bit-exactly (pkg/src/multispin/...):
+//   stream seeding       rng.py:53-82     splitmix64 -> xoshiro256 state
+//   xoshiro256++ step    rng.py:93-105
+//   23-bit shaping       rng.py:113-115, 180-183
+//   draw consumption     engine.py:334-343 (quarter, k = 4i+ii, word)
+//   bit gated by draw    engine.py:321-331 (bit 4ii+i of the target word)
+//   quarter targets      engine.py:57-68  (FLIP_RED / FLIP_BLUE)
+//   Metropolis test      engine.py:78-94, 325-330 (float64 u < table[code])
+//   observables          engine.py:372-386
+//
+// Layout here is NOT the reference's eight folded uint16 arrays: spins are
+// split by checkerboard colour into rows of 32 same-colour sites per uint32
+// (include/msb200.h).  The fold/moat/halo structure of the WSE mapping is an
+// interop format only (msb_to_ref16 / msb_from_ref16).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/msb200.h"
+#include "gf2_jump.h"
+
+namespace {
+
+constexpr uint64_t kGolden = 0x9E3779B97F4B7C15ULL;
+constexpr int kJumpWords = 8192;  // one nibble table = 32 KiB
+constexpr uint32_t kKeyAlways = 0xFFFFFFFFu;
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& why) {
+  g_last_error = why;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                 \
+  do {                                                                                 \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess) return fail(MSB_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---------------------------------------------------------------------------
+// device: RNG
+// ---------------------------------------------------------------------------
+
+struct XState {
+  uint32_t a0, a1, b0, b1, c0, c1, d0, d1;  // s0..s3 as (lo, hi) halves
+};
+
+__device__ __forceinline__ uint32_t xor3(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+// One xoshiro256++ step (rng.py:93-105); returns the HIGH 32 bits of the
+// output, the only bits the reference shapes into a draw (rng.py:115).
+// 64-bit adds are carry chains (IADD3 + IMAD.X), rotations funnel shifts,
+// the XOR network four 3-input LOP3 pairs.
+__device__ __forceinline__ uint32_t xstep(XState& s) {
+  uint32_t x0, x1, o1;
+  asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, %5;"
+      : "=r"(x0), "=r"(x1)
+      : "r"(s.a0), "r"(s.d0), "r"(s.a1), "r"(s.d1));
+  const uint32_t r1 = __funnelshift_l(x0, x1, 23), r0 = __funnelshift_l(x1, x0, 23);
+  asm("{.reg .b32 t;\n\tadd.cc.u32 t, %1, %2;\n\taddc.u32 %0, %3, %4;}"
+      : "=r"(o1)
+      : "r"(r0), "r"(s.a0), "r"(r1), "r"(s.a1));
+  const uint32_t t0 = s.b0 << 17, t1 = __funnelshift_l(s.b0, s.b1, 17);
+  const uint32_t nc0 = xor3(s.c0, s.a0, t0), nc1 = xor3(s.c1, s.a1, t1);
+  const uint32_t nd0 = s.d0 ^ s.b0, nd1 = s.d1 ^ s.b1;
+  const uint32_t nb0 = xor3(s.b0, s.c0, s.a0), nb1 = xor3(s.b1, s.c1, s.a1);
+  const uint32_t na0 = xor3(s.a0, s.d0, s.b0), na1 = xor3(s.a1, s.d1, s.b1);
+  s.a0 = na0; s.a1 = na1; s.b0 = nb0; s.b1 = nb1; s.c0 = nc0; s.c1 = nc1;
+  s.d1 = __funnelshift_l(nd1, nd0, 13);  // rotl64(nd, 45)
+  s.d0 = __funnelshift_l(nd0, nd1, 13);
+  return o1;
+}
+
+// acc = 2*acc + [h9 >= key]  (h9 = draw << 9): one carry-out compare plus
+// one carry-in add.  [h9 >= key] is the REJECT bit of u23 < K (key = K<<9,
+// or 0xFFFFFFFF when K == 2^23).
+__device__ __forceinline__ void acc_reject(uint32_t& acc, uint32_t h9, uint32_t key) {
+  asm("{.reg .b32 t;\n\tsub.cc.u32 t, %1, %2;\n\taddc.u32 %0, %0, %0;}" : "+r"(acc) : "r"(h9), "r"(key));
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {  // rng.py:53-58
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ XState stream_state(uint64_t seed, uint64_t stream) {  // rng.py:71-82
+  uint64_t z = mix64(seed + (stream + 1) * kGolden);
+  uint64_t s[4];
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    z += kGolden;
+    s[i] = mix64(z);
+  }
+  if (!(s[0] | s[1] | s[2] | s[3])) s[0] = kGolden;
+  XState x;
+  x.a0 = (uint32_t)s[0]; x.a1 = (uint32_t)(s[0] >> 32);
+  x.b0 = (uint32_t)s[1]; x.b1 = (uint32_t)(s[1] >> 32);
+  x.c0 = (uint32_t)s[2]; x.c1 = (uint32_t)(s[2] >> 32);
+  x.d0 = (uint32_t)s[3]; x.d1 = (uint32_t)(s[3] >> 32);
+  return x;
+}
+
+// s <- M s with M given as a nibble table T[64][16][8 words] (uint4 pairs).
+__device__ __forceinline__ XState jump_apply(const XState& s, const uint4* __restrict__ T) {
+  const uint32_t w[8] = {s.a0, s.a1, s.b0, s.b1, s.c0, s.c1, s.d0, s.d1};
+  uint32_t r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+  for (int q = 0; q < 8; q++) {
+#pragma unroll
+    for (int nib = 0; nib < 8; nib++) {
+      const int p = q * 8 + nib;
+      const uint32_t v = (w[q] >> (4 * nib)) & 15u;
+      const uint4 lo = T[(p * 16 + v) * 2], hi = T[(p * 16 + v) * 2 + 1];
+      r[0] ^= lo.x; r[1] ^= lo.y; r[2] ^= lo.z; r[3] ^= lo.w;
+      r[4] ^= hi.x; r[5] ^= hi.y; r[6] ^= hi.z; r[7] ^= hi.w;
+    }
+  }
+  XState o;
+  o.a0 = r[0]; o.a1 = r[1]; o.b0 = r[2]; o.b1 = r[3];
+  o.c0 = r[4]; o.c1 = r[5]; o.d0 = r[6]; o.d1 = r[7];
+  return o;
+}
+
+__device__ __forceinline__ XState jump_by(XState s, uint64_t J, const uint4* __restrict__ pow) {
+  for (int b = 0; b < 64; b++)
+    if ((J >> b) & 1) s = jump_apply(s, pow + (size_t)b * (kJumpWords / 4));
+  return s;
+}
+
+__device__ __forceinline__ void load_state(XState& s, const uint32_t* st, long long np, long long gp) {
+  s.a0 = st[0 * np + gp]; s.a1 = st[1 * np + gp]; s.b0 = st[2 * np + gp]; s.b1 = st[3 * np + gp];
+  s.c0 = st[4 * np + gp]; s.c1 = st[5 * np + gp]; s.d0 = st[6 * np + gp]; s.d1 = st[7 * np + gp];
+}
+__device__ __forceinline__ void store_state(const XState& s, uint32_t* st, long long np, long long gp) {
+  st[0 * np + gp] = s.a0; st[1 * np + gp] = s.a1; st[2 * np + gp] = s.b0; st[3 * np + gp] = s.b1;
+  st[4 * np + gp] = s.c0; st[5 * np + gp] = s.c1; st[6 * np + gp] = s.d0; st[7 * np + gp] = s.d1;
+}
+
+// ---------------------------------------------------------------------------
+// device: geometry of the reference stream <-> colour-split rows
+// ---------------------------------------------------------------------------
+
+// For lattice row c and colour X: the reference cell (1-based gamma) whose
+// stream gates it and the quarter q (position of the target array in
+// FLIP_RED / FLIP_BLUE, engine.py:57-68).  Targets: (F,E)->0, (B,O)->1,
+// (B,E)->2, (F,O)->3 for both colours, E/O = parity of the rows r of the
+// colour's sites, (c+X)&1 (lattice.py:156-175).
+struct RowStream {
+  int gamma, q;
+};
+__device__ __host__ __forceinline__ RowStream row_stream(int m, int c, int X) {
+  const bool fwd = c < m / 2;
+  const int odd = (c + X) & 1;
+  RowStream r;
+  r.gamma = fwd ? c / 2 + 1 : (m - 1 - c) / 2 + 1;
+  r.q = fwd ? (odd ? 3 : 0) : (odd ? 1 : 2);
+  return r;
+}
+
+struct Geo {
+  int n_sim, m, n, rows, row0, ghost, R, Wp, W, words, half;
+  long long sim_offset;
+};
+
+__host__ Geo make_geo(const msb_geom* g) {
+  Geo o;
+  o.n_sim = g->n_sim; o.m = g->m; o.n = g->n; o.rows = g->rows; o.row0 = g->row0; o.ghost = g->ghost;
+  o.R = g->rows + 2 * g->ghost;
+  o.W = (g->n / 2 + 31) / 32;
+  o.Wp = (o.W + 3) & ~3;
+  o.words = g->n / 32;
+  o.half = g->n / 2;
+  o.sim_offset = g->sim_offset;
+  return o;
+}
+
+__device__ __forceinline__ int valid_bits(const Geo& G, int j) {
+  const int b = G.half - 32 * j;
+  return b >= 32 ? 32 : b;
+}
+__device__ __forceinline__ uint32_t valid_mask(const Geo& G, int j) {
+  const int b = valid_bits(G, j);
+  return b >= 32 ? 0xFFFFFFFFu : ((1u << b) - 1u);
+}
+__device__ __forceinline__ size_t row_off(const Geo& G, int s, int X, int br) {
+  return ((size_t)(s * 2 + X) * G.R + br) * G.Wp;
+}
+// buffer rows of the vertical neighbours (c-1, c+1) of buffer row br
+__device__ __forceinline__ void vert_rows(const Geo& G, int br, int& bu, int& bd) {
+  if (G.ghost) {
+    bu = br - 1; bd = br + 1;
+  } else {
+    bu = br == 0 ? G.R - 1 : br - 1;
+    bd = br + 1 == G.R ? 0 : br + 1;
+  }
+}
+
+// The second horizontal neighbour word (r+1 when p=1, r-1 when p=0) of word
+// j in the other colour's row y (same lattice row), periodic in n/2.
+__device__ __forceinline__ uint32_t h_second(const Geo& G, const uint32_t* y, int j, int p, uint32_t yj) {
+  if (p) {
+    const uint32_t nx = (j + 1 < G.W) ? y[j + 1] : y[0];
+    return (yj >> 1) | ((nx & 1u) << (valid_bits(G, j) - 1));
+  }
+  uint32_t carry;
+  if (j > 0) {
+    carry = y[j - 1] >> 31;
+  } else {
+    carry = (y[G.W - 1] >> (valid_bits(G, G.W - 1) - 1)) & 1u;
+  }
+  return ((yj << 1) | carry) & valid_mask(G, j);
+}
+
+// ---------------------------------------------------------------------------
+// device: the fused colour-phase kernel
+// ---------------------------------------------------------------------------
+
+struct PhaseArgs {
+  Geo G;
+  uint32_t* spins;
+  uint32_t* states;
+  const uint32_t* thr9;
+  const uint4* jump;
+  unsigned long long* flips;
+  const uint32_t* ext;
+  long long npieces;
+  int phase, kg, kr, np, nch, block_rows, rs;
+  uint32_t inv;
+  int fault;
+  int8_t code_plane[16];
+};
+
+// 32x32 bit-matrix transpose in registers, LSB-first: on exit bit i of a[c]
+// is what bit c of a[i] was.  Five delta-swap stages.
+template <int J>
+__device__ __forceinline__ void transpose_stage(uint32_t a[32], uint32_t m) {
+#pragma unroll
+  for (int k = 0; k < 32; k++) {
+    if ((k & J) == 0) {
+      const uint32_t t = ((a[k] >> J) ^ a[k + J]) & m;
+      a[k + J] ^= t;
+      a[k] ^= t << J;
+    }
+  }
+}
+__device__ __forceinline__ void transpose32(uint32_t a[32]) {
+  transpose_stage<16>(a, 0x0000FFFFu);
+  transpose_stage<8>(a, 0x00FF00FFu);
+  transpose_stage<4>(a, 0x0F0F0F0Fu);
+  transpose_stage<2>(a, 0x33333333u);
+  transpose_stage<1>(a, 0x55555555u);
+}
+
+// reference bit t of a uint16 word is gated by draw k = 4(t%4) + t/4 (the
+// mapping is its own inverse, engine.py:326-330)
+__device__ __forceinline__ int k_of_t(int t) { return 4 * (t & 3) + (t >> 2); }
+
+template <int NPMAX, bool GENERIC, bool EXT>
+__global__ void __launch_bounds__(256) k_phase(const PhaseArgs a) {
+  extern __shared__ uint4 smem4[];
+  uint4* jt = smem4;
+  uint32_t* buf = reinterpret_cast<uint32_t*>(smem4 + kJumpWords / 4);
+  const Geo& G = a.G;
+  const int tid = threadIdx.x;
+  const int X = a.phase;
+  const int np = GENERIC ? a.np : NPMAX;  // compile-time 2 on the fast path
+  const long long total_rows = (long long)G.n_sim * G.rows;
+
+  if (!EXT) {
+    for (int i = tid; i < kJumpWords / 4; i += blockDim.x) jt[i] = a.jump[i];
+    __syncthreads();
+  }
+
+  // ---- stage 1: each thread generates its piece of the stream -------------
+  {
+    const int rl = tid / a.kg, kgi = tid % a.kg;
+    const long long gr = (long long)blockIdx.x * a.block_rows + rl;
+    if (rl < a.block_rows && gr < total_rows) {
+      const int s = (int)(gr / G.rows), lr = (int)(gr % G.rows);
+      const int c = G.row0 + lr;
+      const long long gp = gr * a.kg + kgi;
+      uint32_t key[NPMAX > 0 ? NPMAX : 1];
+#pragma unroll
+      for (int p = 0; p < NPMAX; p++) key[p] = p < np ? a.thr9[p * G.n_sim + s] : 0u;
+      uint32_t* out = buf + rl * a.rs;
+      const int k0 = kgi * a.kr;
+      XState st;
+      uint32_t* sp = a.states + (size_t)X * 8 * a.npieces;
+      const uint32_t* ext = nullptr;
+      if (!EXT) {
+        load_state(st, sp, a.npieces, gp);
+        store_state(jump_apply(st, jt), sp, a.npieces, gp);  // next sweep's start
+      } else {
+        const RowStream rsd = row_stream(G.m, c, X);
+        ext = a.ext + ((((size_t)s * (G.m / 4) + rsd.gamma - 1) * 4 + rsd.q) * 16) * G.words;
+      }
+      for (int kk = 0; kk < a.kr; kk++) {
+        const int k = k0 + kk;
+        for (int ch = 0; ch < a.nch; ch++) {
+          const int L = min(32, G.words - 32 * ch);
+          uint32_t acc[NPMAX > 0 ? NPMAX : 1];
+#pragma unroll
+          for (int p = 0; p < NPMAX; p++) acc[p] = 0;
+          if (!EXT) {
+            int i = 0;
+            if (L == 32) {
+#pragma unroll 8
+              for (; i < 32; i++) {
+                const uint32_t h9 = xstep(st) << 9;
+#pragma unroll
+                for (int p = 0; p < NPMAX; p++)
+                  if (p < np) acc_reject(acc[p], h9, key[p]);
+              }
+            } else {
+              for (; i < L; i++) {
+                const uint32_t h9 = xstep(st) << 9;
+#pragma unroll
+                for (int p = 0; p < NPMAX; p++)
+                  if (p < np) acc_reject(acc[p], h9, key[p]);
+              }
+            }
+          } else {
+            const uint32_t* e = ext + (size_t)k * G.words + 32 * ch;
+            for (int i = 0; i < L; i++) {
+              const uint32_t h9 = e[i] << 9;
+#pragma unroll
+              for (int p = 0; p < NPMAX; p++)
+                if (p < np) acc_reject(acc[p], h9, key[p]);
+            }
+          }
+#pragma unroll
+          for (int p = 0; p < NPMAX; p++)
+            if (p < np) out[(p * 16 + k) * a.nch + ch] = (~__brev(acc[p])) >> (32 - L);
+        }
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- stage 2: transpose accept planes to row words and flip -------------
+  unsigned long long nflip = 0;
+  const int units = a.block_rows * a.nch;
+  for (int u = tid; u < units; u += blockDim.x) {
+    const int rl = u / a.nch, ch = u % a.nch;
+    const long long gr = (long long)blockIdx.x * a.block_rows + rl;
+    if (gr >= total_rows) continue;
+    const int s = (int)(gr / G.rows), lr = (int)(gr % G.rows);
+    const int c = G.row0 + lr, br = lr + G.ghost;
+    const int p = (c + X) & 1;
+    uint32_t* bp = buf + rl * a.rs;
+    // transpose each pair of planes in place: slot (p, k, ch) -> word j'
+#pragma unroll
+    for (int pp = 0; pp < NPMAX; pp += 2) {
+      if (pp >= np) break;
+      uint32_t m32[32];
+#pragma unroll
+      for (int t = 0; t < 16; t++) {
+        m32[t] = bp[(pp * 16 + k_of_t(t)) * a.nch + ch];
+        m32[16 + t] = pp + 1 < np ? bp[((pp + 1) * 16 + k_of_t(t)) * a.nch + ch] : 0u;
+      }
+      transpose32(m32);  // m32[w'] : bits 0-15 plane pp (bit t), 16-31 plane pp+1
+#pragma unroll
+      for (int jj = 0; jj < 16; jj++) {
+        bp[(pp * 16 + jj) * a.nch + ch] = __byte_perm(m32[2 * jj], m32[2 * jj + 1], 0x5410);
+        if (pp + 1 < np) bp[((pp + 1) * 16 + jj) * a.nch + ch] = __byte_perm(m32[2 * jj], m32[2 * jj + 1], 0x7632);
+      }
+    }
+    uint32_t* own = a.spins + row_off(G, s, X, br);
+    int bu, bd;
+    vert_rows(G, br, bu, bd);
+    const uint32_t* yc = a.spins + row_off(G, s, 1 - X, br);
+    const uint32_t* yu = a.spins + row_off(G, s, 1 - X, bu);
+    const uint32_t* yd = a.spins + row_off(G, s, 1 - X, bd);
+    const int jmax = min(16, G.W - 16 * ch);
+    for (int jj = 0; jj < jmax; jj++) {
+      const int j = 16 * ch + jj;
+      const uint32_t o = own[j];
+      const uint32_t y0 = yc[j];
+      const uint32_t n1 = yu[j], n2 = yd[j], n3 = y0, n4 = h_second(G, yc, j, p, y0);
+      uint32_t flip;
+      if (!GENERIC) {
+        const uint32_t A4 = bp[(0 * 16 + jj) * a.nch + ch];
+        const uint32_t A8 = bp[(1 * 16 + jj) * a.nch + ch];
+        const uint32_t ow = o ^ a.inv;
+        const uint32_t x1 = n1 ^ ow, x2 = n2 ^ ow, x3 = n3 ^ ow;
+        const uint32_t x4 = a.fault ? 0u : (n4 ^ ow);
+        const uint32_t o12 = x1 | x2, a12 = x1 & x2, o34 = x3 | x4, a34 = x3 & x4;
+        const uint32_t ge2 = a12 | a34 | (o12 & o34);  // >= 2 disagreeing neighbours
+        const uint32_t any = o12 | o34;
+        flip = ge2 | (any & ~ge2 & A4) | (~any & A8);
+      } else {
+        // neighbour up-count bit planes (bitkernels.py:63-79 restated)
+        const uint32_t s1 = n1 ^ n2, c1 = n1 & n2, s2 = n3 ^ n4, c2 = n3 & n4;
+        uint32_t ones = s1 ^ s2;
+        const uint32_t twos = c1 ^ c2 ^ (s1 & s2), fours = c1 & c2;
+        if (a.fault) ones = s1;
+        flip = 0;
+        for (int code = 0; code < 16; code++) {
+          const int pl = a.code_plane[code];
+          if (pl == -1) continue;
+          const int u = code & 7;
+          if (u > 4) continue;
+          const uint32_t msk = ((code & 8) ? o : ~o) & ((u & 1) ? ones : ~ones) & ((u & 2) ? twos : ~twos) &
+                               ((u & 4) ? fours : ~fours);
+          flip |= pl == -2 ? msk : (msk & bp[(pl * 16 + jj) * a.nch + ch]);
+        }
+      }
+      flip &= valid_mask(G, j);
+      own[j] = o ^ flip;
+      nflip += __popc(flip);
+    }
+  }
+  // one atomic per warp
+  const unsigned lane = tid & 31;
+#pragma unroll
+  for (int off = 16; off; off >>= 1) nflip += __shfl_down_sync(0xFFFFFFFFu, nflip, off);
+  if (lane == 0 && nflip) atomicAdd(a.flips, nflip);
+}
+
+// ---------------------------------------------------------------------------
+// device: state initialisation and layout conversions
+// ---------------------------------------------------------------------------
+
+// Piece start states.  Colour X's pieces are positioned at stream block
+// `blockX` (one block = the 2n draws a stream spends on one colour phase,
+// engine.py:336): piece (row c, kgi) starts at draw
+// blockX*2n + q*(n/2) + kgi*(16/kg)*(n/32) of stream (sim_offset+s)*(m/4) + gamma-1.
+__global__ void k_rng_init(Geo G, uint64_t seed, int kg, int kr, long long npieces, uint64_t block0,
+                           int colour, const uint4* __restrict__ pow, uint32_t* states) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int ncol = colour < 0 ? 2 : 1;
+  if (i >= ncol * npieces) return;
+  const int X = colour < 0 ? (int)(i / npieces) : colour;
+  const uint64_t block = colour < 0 ? block0 + (uint64_t)X : block0;
+  const long long gp = i % npieces;
+  const long long gr = gp / kg;
+  const int kgi = (int)(gp % kg);
+  const int s = (int)(gr / G.rows), lr = (int)(gr % G.rows);
+  const int c = G.row0 + lr;
+  const RowStream rs = row_stream(G.m, c, X);
+  const uint64_t cells = (uint64_t)(G.m / 4);
+  const uint64_t stream = ((uint64_t)G.sim_offset + (uint64_t)s) * cells + (uint64_t)(rs.gamma - 1);
+  const uint64_t n = (uint64_t)G.n;
+  const uint64_t offset = block * 2 * n + (uint64_t)rs.q * (n / 2) + (uint64_t)kgi * kr * (uint64_t)G.words;
+  XState st = jump_by(stream_state(seed, stream), offset, pow);
+  store_state(st, states + (size_t)X * 8 * npieces, npieces, gp);
+}
+
+// Reference-stream order outputs of init="random" (engine.py:279-281):
+// linear word o of replica s = brev64(output (row0*n/64 + o) of stream
+// 2^48 + sim_offset + s), i.e. bit i%64 <-> site i (little-endian order).
+constexpr int kInitPiece = 2048;
+__global__ void k_init_linear(Geo G, uint64_t seed, long long words_per_sim, const uint4* __restrict__ pow,
+                              unsigned long long* lin) {
+  const long long per_sim = (words_per_sim + kInitPiece - 1) / kInitPiece;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= per_sim * G.n_sim) return;
+  const int s = (int)(i / per_sim);
+  const long long o0 = (i % per_sim) * kInitPiece;
+  const long long o1 = min(o0 + kInitPiece, words_per_sim);
+  const uint64_t first = (uint64_t)G.row0 * (uint64_t)G.n / 64;
+  XState st = stream_state(seed, (1ULL << 48) + (uint64_t)G.sim_offset + (uint64_t)s);
+  st = jump_by(st, first + (uint64_t)o0, pow);
+  unsigned long long* out = lin + (size_t)s * words_per_sim;
+  for (long long o = o0; o < o1; o++) {
+    // full 64-bit output needed here (rng.py:139-147 uses all 64 bits)
+    const uint64_t a = ((uint64_t)st.a1 << 32) | st.a0, d = ((uint64_t)st.d1 << 32) | st.d0;
+    const uint64_t x = a + d;
+    const uint64_t r = ((x << 23) | (x >> 41)) + a;
+    xstep(st);
+    out[o] = __brevll(r);
+  }
+}
+
+__device__ __forceinline__ uint32_t even_bits(uint64_t x) {
+  x &= 0x5555555555555555ULL;
+  x = (x | (x >> 1)) & 0x3333333333333333ULL;
+  x = (x | (x >> 2)) & 0x0F0F0F0F0F0F0F0FULL;
+  x = (x | (x >> 4)) & 0x00FF00FF00FF00FFULL;
+  x = (x | (x >> 8)) & 0x0000FFFF0000FFFFULL;
+  x = (x | (x >> 16)) & 0x00000000FFFFFFFFULL;
+  return (uint32_t)x;
+}
+__device__ __forceinline__ uint64_t spread_bits(uint32_t v) {  // bit b -> bit 2b
+  uint64_t x = v;
+  x = (x | (x << 16)) & 0x0000FFFF0000FFFFULL;
+  x = (x | (x << 8)) & 0x00FF00FF00FF00FFULL;
+  x = (x | (x << 4)) & 0x0F0F0F0F0F0F0F0FULL;
+  x = (x | (x << 2)) & 0x3333333333333333ULL;
+  x = (x | (x << 1)) & 0x5555555555555555ULL;
+  return x;
+}
+
+// Thread per (s, held row lr, word j < Wp): both colours' word j from the
+// 64 sites r in [64j, 64j+64) of the row (clipped at n).
+__global__ void k_from_linear(Geo G, const unsigned long long* __restrict__ lin, uint32_t* spins) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long total = (long long)G.n_sim * G.rows * G.Wp;
+  if (i >= total) return;
+  const int j = (int)(i % G.Wp);
+  const long long gr = i / G.Wp;
+  const int s = (int)(gr / G.rows), lr = (int)(gr % G.rows);
+  const int c = G.row0 + lr, br = lr + G.ghost;
+  uint32_t e = 0, od = 0;
+  if (j < G.W) {
+    const long long words_per_sim = (long long)G.rows * G.n / 64;
+    const unsigned long long* L = lin + (size_t)s * words_per_sim;
+    const long long bit0 = (long long)lr * G.n + 64LL * j;
+    const int nsite = min(64, G.n - 64 * j);
+    uint64_t v;
+    if ((bit0 & 63) == 0) {
+      v = L[bit0 >> 6];
+    } else {  // starts at bit 32 of a linear word
+      const uint64_t lo = L[bit0 >> 6] >> 32;
+      const uint64_t hi = nsite > 32 ? L[(bit0 >> 6) + 1] << 32 : 0ULL;
+      v = lo | hi;
+    }
+    if (nsite < 64) v &= (1ULL << nsite) - 1;
+    e = even_bits(v);
+    od = even_bits(v >> 1);
+  }
+  // even r -> colour c&1, odd r -> colour (c+1)&1
+  spins[row_off(G, s, c & 1, br) + j] = e;
+  spins[row_off(G, s, (c + 1) & 1, br) + j] = od;
+}
+
+// Thread per linear word o of a replica.
+__global__ void k_to_linear(Geo G, const uint32_t* __restrict__ spins, unsigned long long* lin) {
+  const long long words_per_sim = (long long)G.rows * G.n / 64;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= words_per_sim * G.n_sim) return;
+  const int s = (int)(i / words_per_sim);
+  const long long o = i % words_per_sim;
+  uint64_t v = 0;
+#pragma unroll
+  for (int hh = 0; hh < 2; hh++) {
+    const long long site = o * 64 + 32 * hh;
+    const int lr = (int)(site / G.n), r0 = (int)(site % G.n);
+    const int c = G.row0 + lr, br = lr + G.ghost;
+    const int j = r0 / 64, sh = (r0 % 64) / 2;  // 0 or 16
+    const uint32_t e = (spins[row_off(G, s, c & 1, br) + j] >> sh) & 0xFFFFu;
+    const uint32_t od = (spins[row_off(G, s, (c + 1) & 1, br) + j] >> sh) & 0xFFFFu;
+    const uint64_t w = spread_bits(e) | (spread_bits(od) << 1);  // 32 sites
+    v |= (w & 0xFFFFFFFFULL) << (32 * hh);
+  }
+  lin[i] = v;
+}
+
+__global__ void k_init_const(Geo G, uint32_t up, uint32_t* spins) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long total = (long long)G.n_sim * 2 * G.R * G.Wp;
+  if (i >= total) return;
+  const int j = (int)(i % G.Wp);
+  const int br = (int)((i / G.Wp) % G.R);
+  const bool ghost_row = G.ghost && (br == 0 || br == G.R - 1);
+  spins[i] = (up && j < G.W && !ghost_row) ? valid_mask(G, j) : 0u;
+}
+
+// Canonical source of a state element (lattice.py:283-329), evaluated per
+// element; codes in ALL_CODES order RFE RBO RBE RFO BFE BBO BBE BFO.
+__global__ void k_to_ref16(Geo G, const uint32_t* __restrict__ spins, uint16_t* state) {
+  const int cells = G.m / 4, words = G.words;
+  const int cols = cells + 2, vec = words + 2;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long total = (long long)G.n_sim * 8 * cols * vec;
+  if (i >= total) return;
+  int e = (int)(i % vec);
+  int g = (int)((i / vec) % cols);
+  int a = (int)((i / ((long long)vec * cols)) % 8);
+  const int s = (int)(i / (8LL * vec * cols));
+  const bool in_moat = g == 0 || g == cols - 1, in_halo = e == 0 || e == vec - 1;
+  uint16_t val = 0;
+  bool live = true;
+  if (in_moat && in_halo) {
+    live = false;
+  } else if (in_moat) {
+    const bool red = a < 4, fill_right = red ? (a % 4) < 2 : (a % 4) >= 2;
+    if (fill_right && g == cols - 1) { a ^= 2; g = cells; }
+    else if (!fill_right && g == 0) { a ^= 2; g = 1; }
+    else live = false;
+  } else if (in_halo) {
+    const bool copy_top = (a % 2) == 0;
+    if (copy_top && e == vec - 1) e = 1;
+    else if (!copy_top && e == 0) e = words;
+    else live = false;
+  }
+  if (live) {
+    const bool red = a < 4, fwd = (a % 4) == 0 || (a % 4) == 3, even = (a % 2) == 0;
+    const int p0 = even ? 0 : 1, cpar = red ? p0 : 1 - p0;
+    const int c = fwd ? 2 * (g - 1) + cpar : G.m - 2 * g + cpar;  // lattice.py:190-196
+    const int X = red ? 0 : 1;
+    const int w0 = e - 1;
+    const uint32_t word = spins[row_off(G, s, X, c) + w0 / 2];
+    val = (uint16_t)((word >> (16 * (w0 & 1))) & 0xFFFFu);
+  }
+  state[i] = val;
+}
+
+__global__ void k_from_ref16(Geo G, const uint16_t* __restrict__ state, uint32_t* spins) {
+  const int cells = G.m / 4, words = G.words;
+  const int cols = cells + 2, vec = words + 2;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long total = (long long)G.n_sim * 2 * G.m * G.Wp;
+  if (i >= total) return;
+  const int j = (int)(i % G.Wp);
+  const int c = (int)((i / G.Wp) % G.m);
+  const int X = (int)((i / ((long long)G.Wp * G.m)) % 2);
+  const int s = (int)(i / (2LL * G.Wp * G.m));
+  uint32_t v = 0;
+  if (j < G.W) {
+    const RowStream rs = row_stream(G.m, c, X);
+    const int a = 4 * X + rs.q;
+    const uint16_t* col = state + (((size_t)s * 8 + a) * cols + rs.gamma) * vec;
+    v = col[2 * j + 1];
+    if (2 * j + 2 <= words) v |= (uint32_t)col[2 * j + 2] << 16;
+  }
+  spins[row_off(G, s, X, c) + j] = v;
+}
+
+// ---------------------------------------------------------------------------
+// device: observables (engine.py:372-386)
+// ---------------------------------------------------------------------------
+
+__global__ void k_observe(Geo G, const uint32_t* __restrict__ spins, long long* ups, long long* unsat) {
+  const long long gr = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long total = (long long)G.n_sim * G.rows;
+  int s = -1;
+  uint32_t u = 0, b = 0;
+  if (gr < total) {
+    s = (int)(gr / G.rows);
+    const int lr = (int)(gr % G.rows);
+    const int c = G.row0 + lr, br = lr + G.ghost;
+    const int p = c & 1;  // red sites of row c sit at rows r with parity c&1
+    int bu, bd;
+    vert_rows(G, br, bu, bd);
+    const uint32_t* red = spins + row_off(G, s, 0, br);
+    const uint32_t* blu = spins + row_off(G, s, 1, br);
+    const uint32_t* yu = spins + row_off(G, s, 1, bu);
+    const uint32_t* yd = spins + row_off(G, s, 1, bd);
+    for (int j = 0; j < G.W; j++) {
+      const uint32_t o = red[j], y0 = blu[j];
+      const uint32_t vm = valid_mask(G, j);
+      u += __popc(o) + __popc(y0);
+      b += __popc((o ^ yu[j]) & vm) + __popc((o ^ yd[j]) & vm) + __popc((o ^ y0) & vm) +
+           __popc((o ^ h_second(G, blu, j, p, y0)) & vm);
+    }
+  }
+  // segmented warp reduction by replica
+  const unsigned lanes = __match_any_sync(0xFFFFFFFFu, s);
+  const uint32_t su = __reduce_add_sync(lanes, u), sb = __reduce_add_sync(lanes, b);
+  const int leader = __ffs(lanes) - 1;
+  if (s >= 0 && (int)(threadIdx.x & 31) == leader) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(ups + s), (unsigned long long)su);
+    atomicAdd(reinterpret_cast<unsigned long long*>(unsat + s), (unsigned long long)sb);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// device: record/replay, slab halos, INT microbenchmark
+// ---------------------------------------------------------------------------
+
+__global__ void k_draws(Geo G, int X, int kg, int kr, long long npieces, const uint32_t* __restrict__ states,
+                        uint32_t* out) {
+  const long long gp = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gp >= npieces) return;
+  const long long gr = gp / kg;
+  const int kgi = (int)(gp % kg);
+  const int s = (int)(gr / G.rows), c = (int)(gr % G.rows);
+  XState st;
+  load_state(st, states + (size_t)X * 8 * npieces, npieces, gp);
+  const RowStream rs = row_stream(G.m, c, X);
+  uint32_t* o = out + (((size_t)s * (G.m / 4) + rs.gamma - 1) * 4 + rs.q) * 16 * G.words;
+  for (int k = kgi * kr; k < (kgi + 1) * kr; k++)
+    for (int w = 0; w < G.words; w++) o[(size_t)k * G.words + w] = xstep(st) & 0x7FFFFFu;
+}
+
+__global__ void k_pack_edges(Geo G, int X, const uint32_t* __restrict__ spins, uint32_t* edge) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= G.n_sim * 2 * G.Wp) return;
+  const int j = i % G.Wp, which = (i / G.Wp) % 2, s = i / (2 * G.Wp);
+  const int br = which == 0 ? G.ghost : G.ghost + G.rows - 1;
+  edge[i] = spins[row_off(G, s, X, br) + j];
+}
+
+__global__ void k_unpack_ghosts(Geo G, int X, const uint32_t* __restrict__ ghost_rows, uint32_t* spins) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= G.n_sim * 2 * G.Wp) return;
+  const int j = i % G.Wp, which = (i / G.Wp) % 2, s = i / (2 * G.Wp);
+  const int br = which == 0 ? 0 : G.R - 1;
+  spins[row_off(G, s, X, br) + j] = ghost_rows[i];
+}
+
+constexpr int kPeakChains = 8;
+__global__ void k_int_peak(uint32_t* out, uint32_t seed, int iters) {
+  uint32_t a[kPeakChains], b[kPeakChains];
+#pragma unroll
+  for (int i = 0; i < kPeakChains; i++) {
+    a[i] = seed * (threadIdx.x + i + 1);
+    b[i] = a[i] ^ 0x9e3779b9u;
+  }
+  const uint32_t k1 = seed | 1u, k2 = seed >> 3;
+  for (int it = 0; it < iters; it++) {
+#pragma unroll
+    for (int i = 0; i < kPeakChains; i++) {
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(a[i]) : "r"(b[i]), "r"(k1));
+      asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(b[i]) : "r"(k1), "r"(k2));
+    }
+  }
+  uint32_t acc = 0;
+#pragma unroll
+  for (int i = 0; i < kPeakChains; i++) acc ^= a[i] ^ b[i];
+  if (acc == 0x12345678u) out[threadIdx.x] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// host helpers
+// ---------------------------------------------------------------------------
+
+int check_geom(const msb_geom* g) {
+  if (!g) return fail(MSB_ERR_ARG, "null geometry");
+  if (g->m < 4 || g->m % 4)
+    return fail(MSB_ERR_ARG, "m=" + std::to_string(g->m) + ": the cell-axis extent must be a multiple of 4 (and >= 4)");
+  if (g->n < 32 || g->n % 32)
+    return fail(MSB_ERR_ARG, "n=" + std::to_string(g->n) + ": the memory-axis extent must be a multiple of 32 (and >= 32)");
+  if (g->n_sim < 1) return fail(MSB_ERR_ARG, "need at least one replica");
+  if (g->ghost != 0 && g->ghost != 1) return fail(MSB_ERR_ARG, "ghost must be 0 or 1");
+  if (g->rows < 2 || g->row0 < 0 || g->row0 + g->rows > g->m || (g->rows % 2) || (g->row0 % 2))
+    return fail(MSB_ERR_ARG, "held rows must be an even-aligned, even-sized range inside [0, m)");
+  if (!g->ghost && (g->row0 != 0 || g->rows != g->m))
+    return fail(MSB_ERR_ARG, "a buffer without ghost rows must hold the whole lattice");
+  if (g->sim_offset < 0) return fail(MSB_ERR_ARG, "sim_offset must be non-negative");
+  return MSB_OK;
+}
+
+inline unsigned blocks_for(long long n, int bt) { return (unsigned)((n + bt - 1) / bt); }
+
+template <int NPMAX, bool GENERIC, bool EXT>
+int launch_phase(const PhaseArgs& a, size_t smem, unsigned grid, int threads, cudaStream_t st) {
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(k_phase<NPMAX, GENERIC, EXT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    227 * 1024);
+  });
+  if (attr_err != cudaSuccess) return fail(MSB_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
+  k_phase<NPMAX, GENERIC, EXT><<<grid, threads, smem, st>>>(a);
+  CUDA_TRY(cudaGetLastError());
+  return MSB_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+
+extern "C" {
+
+const char* msb_status_string(int status) {
+  switch (status) {
+    case MSB_OK: return "ok";
+    case MSB_ERR_ARG: return "invalid argument";
+    case MSB_ERR_CUDA: return "CUDA error";
+    case MSB_ERR_UNSUPPORTED: return "unsupported";
+    default: return "unknown status";
+  }
+}
+
+const char* msb_last_error(void) { return g_last_error.c_str(); }
+
+int msb_abi_version(void) { return 1; }
+
+int msb_check_geom(const msb_geom* g) { return check_geom(g); }
+
+int64_t msb_spin_words(const msb_geom* g) {
+  if (check_geom(g)) return -1;
+  const Geo G = make_geo(g);
+  return (int64_t)G.n_sim * 2 * G.R * G.Wp;
+}
+
+int32_t msb_row_pitch(const msb_geom* g) {
+  if (check_geom(g)) return -1;
+  return make_geo(g).Wp;
+}
+
+int64_t msb_pieces_per_phase(const msb_geom* g, int32_t kg) {
+  if (check_geom(g)) return -1;
+  return (int64_t)g->n_sim * g->rows * kg;
+}
+
+int32_t msb_default_kg(const msb_geom* g) {
+  if (check_geom(g)) return -1;
+  // Enough pieces to fill 148 SMs x ~24 warps, but pieces long enough that
+  // the per-sweep jump (~500 ops) stays a few percent of the draws.
+  const long long rows = (long long)g->n_sim * g->rows;
+  const int words = g->n / 32;
+  int kg = 1;
+  while (kg < 16 && rows * kg < 148LL * 24 * 32 && (16 / (kg * 2)) * words >= 256) kg *= 2;
+  return kg;
+}
+
+int msb_plan_thresholds(const double* tables, int32_t n_sim, int32_t* mode, int32_t* n_planes,
+                        int8_t code_plane[16], uint32_t* thr9) {
+  if (!tables || n_sim < 1 || !mode || !n_planes || !code_plane || !thr9)
+    return fail(MSB_ERR_ARG, "msb_plan_thresholds: null argument");
+  constexpr uint32_t kFull = 1u << 23;
+  auto K = [&](int s, int code) -> uint32_t {
+    const double v = tables[(size_t)s * 16 + code];
+    if (!(v > 0.0)) return 0u;  // also NaN: u < NaN is false
+    const double x = v * 8388608.0;
+    if (!(x < 8388608.0)) return kFull;
+    return (uint32_t)std::ceil(x);  // #{k : k 2^-23 < v}
+  };
+  auto key = [&](uint32_t k) -> uint32_t { return k >= kFull ? kKeyAlways : (k << 9); };
+  // J>0 / J<0 structure: codes with >= 2 disagreeing neighbours always flip,
+  // exactly-one and none share one threshold each across own = 0/1.
+  for (int anti = 0; anti < 2; anti++) {
+    bool ok = true;
+    for (int s = 0; s < n_sim && ok; s++) {
+      for (int own = 0; own < 2 && ok; own++)
+        for (int u = 0; u < 5 && ok; u++) {
+          const int d = (own ^ anti) ? 4 - u : u;
+          if (d >= 2 && K(s, 8 * own + u) != kFull) ok = false;
+        }
+      const int e4a = anti ? 3 : 1, e4b = anti ? 9 : 11, e8a = anti ? 4 : 0, e8b = anti ? 8 : 12;
+      if (K(s, e4a) != K(s, e4b) || K(s, e8a) != K(s, e8b)) ok = false;
+    }
+    if (!ok) continue;
+    *mode = anti ? MSB_MODE_ANTI : MSB_MODE_FERRO;
+    *n_planes = 2;
+    for (int code = 0; code < 16; code++) {
+      const int own = code >> 3, u = code & 7;
+      if (u > 4) { code_plane[code] = -1; continue; }
+      const int d = (own ^ anti) ? 4 - u : u;
+      code_plane[code] = (int8_t)(d >= 2 ? -2 : d == 1 ? 0 : 1);
+    }
+    for (int s = 0; s < n_sim; s++) {
+      thr9[0 * n_sim + s] = key(K(s, anti ? 3 : 1));
+      thr9[1 * n_sim + s] = key(K(s, anti ? 4 : 0));
+    }
+    return MSB_OK;
+  }
+  // generic: one plane per distinct per-replica threshold vector
+  int np = 0;
+  int rep[MSB_MAX_PLANES];
+  for (int code = 0; code < 16; code++) {
+    const int u = code & 7;
+    if (u > 4) { code_plane[code] = -1; continue; }
+    bool all_full = true, all_zero = true;
+    for (int s = 0; s < n_sim; s++) {
+      const uint32_t k = K(s, code);
+      all_full &= k == kFull;
+      all_zero &= k == 0;
+    }
+    if (all_full) { code_plane[code] = -2; continue; }
+    if (all_zero) { code_plane[code] = -1; continue; }
+    int found = -1;
+    for (int p = 0; p < np && found < 0; p++) {
+      bool same = true;
+      for (int s = 0; s < n_sim && same; s++) same = K(s, rep[p]) == K(s, code);
+      if (same) found = p;
+    }
+    if (found < 0) {
+      found = np;
+      rep[np++] = code;
+    }
+    code_plane[code] = (int8_t)found;
+  }
+  for (int p = 0; p < np; p++)
+    for (int s = 0; s < n_sim; s++) thr9[p * n_sim + s] = key(K(s, rep[p]));
+  *mode = MSB_MODE_GENERIC;
+  *n_planes = np;
+  return MSB_OK;
+}
+
+int msb_rng_power_tables(uint32_t* host_out) {
+  if (!host_out) return fail(MSB_ERR_ARG, "null output");
+  msb::power_tables(host_out);
+  return MSB_OK;
+}
+
+int msb_rng_jump_table(uint64_t jump, uint32_t* host_out) {
+  if (!host_out) return fail(MSB_ERR_ARG, "null output");
+  msb::jump_table(jump, host_out);
+  return MSB_OK;
+}
+
+int msb_rng_init(const msb_geom* g, uint64_t seed, int32_t kg, uint64_t block, int32_t colour,
+                 const uint32_t* pow_tables, uint32_t* states, void* stream) {
+  if (int r = check_geom(g)) return r;
+  if (kg != 1 && kg != 2 && kg != 4 && kg != 8 && kg != 16) return fail(MSB_ERR_ARG, "kg must be 1, 2, 4, 8 or 16");
+  if (colour < -1 || colour > 1) return fail(MSB_ERR_ARG, "colour must be -1 (both), 0 or 1");
+  if (!pow_tables || !states) return fail(MSB_ERR_ARG, "null buffer");
+  const Geo G = make_geo(g);
+  const long long np = (long long)g->n_sim * g->rows * kg;
+  const long long n = (colour < 0 ? 2 : 1) * np;
+  k_rng_init<<<blocks_for(n, 128), 128, 0, as_stream(stream)>>>(
+      G, seed, kg, 16 / kg, np, block, colour, reinterpret_cast<const uint4*>(pow_tables), states);
+  CUDA_TRY(cudaGetLastError());
+  return MSB_OK;
+}
+
+int msb_init_random(const msb_geom* g, uint64_t seed, const uint32_t* pow_tables, uint64_t* scratch,
+                    uint32_t* spins, void* stream) {
+  if (int r = check_geom(g)) return r;
+  if (!pow_tables || !scratch || !spins) return fail(MSB_ERR_ARG, "null buffer");
+  const Geo G = make_geo(g);
+  const long long wps = (long long)g->rows * g->n / 64;
+  const long long pieces = (wps + kInitPiece - 1) / kInitPiece * g->n_sim;
+  k_init_linear<<<blocks_for(pieces, 64), 64, 0, as_stream(stream)>>>(
+      G, seed, wps, reinterpret_cast<const uint4*>(pow_tables), reinterpret_cast<unsigned long long*>(scratch));
+  CUDA_TRY(cudaGetLastError());
+  if (int r = msb_init_const(g, 0, spins, stream)) return r;
+  return msb_from_linear(g, scratch, spins, stream);
+}
+
+int msb_init_const(const msb_geom* g, int32_t up, uint32_t* spins, void* stream) {
+  if (int r = check_geom(g)) return r;
+  if (!spins) return fail(MSB_ERR_ARG, "null buffer");
+  const Geo G = make_geo(g);
+  const long long total = (long long)G.n_sim * 2 * G.R * G.Wp;
+  k_init_const<<<blocks_for(total, 256), 256, 0, as_stream(stream)>>>(G, up ? 1u : 0u, spins);
+  CUDA_TRY(cudaGetLastError());
+  return MSB_OK;
+}
+
+int msb_from_linear(const msb_geom* g, const uint64_t* lin, uint32_t* spins, void* stream) {
+  if (int r = check_geom(g)) return r;
+  if (!lin || !spins) return fail(MSB_ERR_ARG, "null buffer");
+  const Geo G = make_geo(g);
+  const long long total = (long long)G.n_sim * G.rows * G.Wp;
+  k_from_linear<<<blocks_for(total, 256), 256, 0, as_stream(stream)>>>(
+      G, reinterpret_cast<const unsigned long long*>(lin), spins);
+  CUDA_TRY(cudaGetLastError());
+  return MSB_OK;
+}
+
+int msb_to_linear(const msb_geom* g, const uint32_t* spins, uint64_t* lin, void* stream) {
+  if (int r = check_geom(g)) return r;
+  if (!lin || !spins) return fail(MSB_ERR_ARG, "null buffer");
+  const Geo G = make_geo(g);
+  const long long total = (long long)G.n_sim * G.rows * G.n / 64;
+  k_to_linear<<<blocks_for(total, 256), 256, 0, as_stream(stream)>>>(G, spins,
+                                                                       reinterpret_cast<unsigned long long*>(lin));
+  CUDA_TRY(cudaGetLastError());
+  return MSB_OK;
+}
+
+int msb_to_ref16(const msb_geom* g, const uint32_t* spins, uint16_t* state, void* stream) {
+  if (int r = check_geom(g)) return r;
+  if (g->ghost) return fail(MSB_ERR_UNSUPPORTED, "ref16 interop needs a whole lattice");
+  if (!spins || !state) return fail(MSB_ERR_ARG, "null buffer");
+  const Geo G = make_geo(g);
+  const long long total = (long long)G.n_sim * 8 * (G.m / 4 + 2) * (G.words + 2);
+  k_to_ref16<<<blocks_for(total, 256), 256, 0, as_stream(stream)>>>(G, spins, state);
+  CUDA_TRY(cudaGetLastError());
+  return MSB_OK;
+}
+
+int msb_from_ref16(const msb_geom* g, const uint16_t* state, uint32_t* spins, void* stream) {
+  if (int r = check_geom(g)) return r;
+  if (g->ghost) return fail(MSB_ERR_UNSUPPORTED, "ref16 interop needs a whole lattice");
+  if (!spins || !state) return fail(MSB_ERR_ARG, "null buffer");
+  const Geo G = make_geo(g);
+  const long long total = (long long)G.n_sim * 2 * G.m * G.Wp;
+  k_from_ref16<<<blocks_for(total, 256), 256, 0, as_stream(stream)>>>(G, state, spins);
+  CUDA_TRY(cudaGetLastError());
+  return MSB_OK;
+}
+
+int msb_phase(const msb_geom* g, const msb_sweep_params* p, int32_t phase, uint32_t* spins, uint32_t* states,
+              const uint32_t* ext_draws, uint64_t* flips, void* stream) {
+  if (int r = check_geom(g)) return r;
+  if (!p || !spins || !flips) return fail(MSB_ERR_ARG, "null argument");
+  if (phase != 0 && phase != 1) return fail(MSB_ERR_ARG, "phase must be 0 (red) or 1 (blue)");
+  const int kg = p->kg;
+  if (kg != 1 && kg != 2 && kg != 4 && kg != 8 && kg != 16) return fail(MSB_ERR_ARG, "kg must be 1, 2, 4, 8 or 16");
+  if (p->n_planes < 0 || p->n_planes > MSB_MAX_PLANES) return fail(MSB_ERR_ARG, "bad plane count");
+  const bool generic = p->mode == MSB_MODE_GENERIC;
+  if (!generic && p->n_planes != 2) return fail(MSB_ERR_ARG, "ferro/anti modes use exactly 2 planes");
+  if (p->n_planes > 0 && !p->thr9) return fail(MSB_ERR_ARG, "null thresholds");
+  if (ext_draws && g->ghost) return fail(MSB_ERR_UNSUPPORTED, "external draws need a whole lattice");
+  if (!ext_draws && (!states || !p->jump)) return fail(MSB_ERR_ARG, "null RNG state or jump table");
+  const Geo G = make_geo(g);
+  PhaseArgs a;
+  a.G = G;
+  a.spins = spins;
+  a.states = states;
+  a.thr9 = p->thr9;
+  a.jump = reinterpret_cast<const uint4*>(p->jump);
+  a.flips = reinterpret_cast<unsigned long long*>(flips);
+  a.ext = ext_draws;
+  a.npieces = (long long)g->n_sim * g->rows * kg;
+  a.phase = phase;
+  a.kg = kg;
+  a.kr = 16 / kg;
+  a.np = p->n_planes;
+  a.nch = (G.words + 31) / 32;
+  a.inv = p->mode == MSB_MODE_ANTI ? 0xFFFFFFFFu : 0u;
+  a.fault = p->fault;
+  std::memcpy(a.code_plane, p->code_plane, 16);
+  const int npl = std::max(a.np, 1);
+  a.rs = npl * 16 * a.nch + 1;  // odd row stride: conflict-free per-row access
+  const long long total_rows = (long long)g->n_sim * g->rows;
+  int block_rows = p->block_rows > 0 ? p->block_rows : 256 / kg;
+  if (block_rows * kg > 256) block_rows = 256 / kg;
+  const size_t base = ext_draws ? 0 : (size_t)kJumpWords * 4;
+  while (block_rows > 1 && base + (size_t)block_rows * a.rs * 4 > 227 * 1024) block_rows /= 2;
+  // small problems: spread rows over more blocks
+  while (block_rows > 1 && (total_rows + block_rows - 1) / block_rows < 2 * 148 && block_rows * kg > 64)
+    block_rows /= 2;
+  a.block_rows = block_rows;
+  const size_t smem = base + (size_t)block_rows * a.rs * 4;
+  if (smem > 227 * 1024) return fail(MSB_ERR_UNSUPPORTED, "lattice rows too long for the shared-memory plan");
+  const unsigned grid = (unsigned)((total_rows + block_rows - 1) / block_rows);
+  const int threads = ((block_rows * kg + 31) / 32) * 32;
+  cudaStream_t st = as_stream(stream);
+  if (!generic) {
+    return ext_draws ? launch_phase<2, false, true>(a, smem, grid, threads, st)
+                     : launch_phase<2, false, false>(a, smem, grid, threads, st);
+  }
+  return ext_draws ? launch_phase<MSB_MAX_PLANES, true, true>(a, smem, grid, threads, st)
+                   : launch_phase<MSB_MAX_PLANES, true, false>(a, smem, grid, threads, st);
+}
+
+int msb_sweep(const msb_geom* g, const msb_sweep_params* p, uint32_t* spins, uint32_t* states, int32_t n_sweeps,
+              uint64_t* flips, void* stream) {
+  if (int r = check_geom(g)) return r;
+  if (g->ghost) return fail(MSB_ERR_UNSUPPORTED, "msb_sweep runs whole lattices; slabs use msb_phase + halo exchange");
+  if (n_sweeps < 0) return fail(MSB_ERR_ARG, "sweep count must be non-negative");
+  for (int k = 0; k < n_sweeps; k++) {
+    if (int r = msb_phase(g, p, 0, spins, states, nullptr, flips, stream)) return r;
+    if (int r = msb_phase(g, p, 1, spins, states, nullptr, flips, stream)) return r;
+  }
+  return MSB_OK;
+}
+
+int msb_observe(const msb_geom* g, const uint32_t* spins, int64_t* ups, int64_t* unsat, void* stream) {
+  if (int r = check_geom(g)) return r;
+  if (!spins || !ups || !unsat) return fail(MSB_ERR_ARG, "null buffer");
+  const Geo G = make_geo(g);
+  const long long total = (long long)g->n_sim * g->rows;
+  k_observe<<<blocks_for(total, 256), 256, 0, as_stream(stream)>>>(G, spins, reinterpret_cast<long long*>(ups),
+                                                                    reinterpret_cast<long long*>(unsat));
+  CUDA_TRY(cudaGetLastError());
+  return MSB_OK;
+}
+
+int msb_draws(const msb_geom* g, int32_t kg, int32_t phase, const uint32_t* states, uint32_t* out, void* stream) {
+  if (int r = check_geom(g)) return r;
+  if (g->ghost) return fail(MSB_ERR_UNSUPPORTED, "draw export needs a whole lattice");
+  if (kg != 1 && kg != 2 && kg != 4 && kg != 8 && kg != 16) return fail(MSB_ERR_ARG, "kg must be 1, 2, 4, 8 or 16");
+  if (phase != 0 && phase != 1) return fail(MSB_ERR_ARG, "phase must be 0 or 1");
+  if (!states || !out) return fail(MSB_ERR_ARG, "null buffer");
+  const Geo G = make_geo(g);
+  const long long np = (long long)g->n_sim * g->rows * kg;
+  k_draws<<<blocks_for(np, 128), 128, 0, as_stream(stream)>>>(G, phase, kg, 16 / kg, np, states, out);
+  CUDA_TRY(cudaGetLastError());
+  return MSB_OK;
+}
+
+int msb_pack_edges(const msb_geom* g, int32_t colour, const uint32_t* spins, uint32_t* edge, void* stream) {
+  if (int r = check_geom(g)) return r;
+  if (!g->ghost) return fail(MSB_ERR_ARG, "edge exchange needs a slab buffer (ghost = 1)");
+  if (!spins || !edge) return fail(MSB_ERR_ARG, "null buffer");
+  const Geo G = make_geo(g);
+  k_pack_edges<<<blocks_for((long long)G.n_sim * 2 * G.Wp, 256), 256, 0, as_stream(stream)>>>(G, colour & 1, spins, edge);
+  CUDA_TRY(cudaGetLastError());
+  return MSB_OK;
+}
+
+int msb_unpack_ghosts(const msb_geom* g, int32_t colour, const uint32_t* ghost_rows, uint32_t* spins, void* stream) {
+  if (int r = check_geom(g)) return r;
+  if (!g->ghost) return fail(MSB_ERR_ARG, "ghost rows need a slab buffer (ghost = 1)");
+  if (!spins || !ghost_rows) return fail(MSB_ERR_ARG, "null buffer");
+  const Geo G = make_geo(g);
+  k_unpack_ghosts<<<blocks_for((long long)G.n_sim * 2 * G.Wp, 256), 256, 0, as_stream(stream)>>>(G, colour & 1,
+                                                                                                  ghost_rows, spins);
+  CUDA_TRY(cudaGetLastError());
+  return MSB_OK;
+}
+
+int msb_bench_int_peak(int32_t blocks, int32_t iters, double* ops_out, float* ms_out, void* stream) {
+  if (blocks < 1 || iters < 1 || !ops_out || !ms_out) return fail(MSB_ERR_ARG, "bad arguments");
+  cudaStream_t st = as_stream(stream);
+  uint32_t* d = nullptr;
+  CUDA_TRY(cudaMalloc(&d, 4096));
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  k_int_peak<<<blocks, 256, 0, st>>>(d, 7u, iters);  // warm-up
+  CUDA_TRY(cudaEventRecord(e0, st));
+  k_int_peak<<<blocks, 256, 0, st>>>(d, 7u, iters);
+  CUDA_TRY(cudaEventRecord(e1, st));
+  CUDA_TRY(cudaEventSynchronize(e1));
+  CUDA_TRY(cudaEventElapsedTime(ms_out, e0, e1));
+  *ops_out = (double)blocks * 256 * iters * kPeakChains * 2;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  return MSB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,593 @@
+"""Drop-in B200 ``Engine`` / ``run_simulations`` for the reference `multispin`.
+
+Same constructor, methods, attributes, counters and error behaviour as the
+reference engine (pkg/src/multispin/engine.py:216-492), but the spins live
+on the GPU in a colour-split bit layout and every sweep runs as two fused
+sm_100a kernels (libmsb200, include/msb200.h): per colour phase, each piece
+of a reference xoshiro256++ stream generates its draws, compares them with
+integer Boltzmann thresholds and flips its row's spins with bit-sliced
+neighbour logic.  Results are bit-identical to the reference on identical
+seeds, dimensions, temperatures and couplings.
+
+Reference surfaces kept (file:line in pkg/src/multispin/engine.py):
+  ``Engine(dims, temperatures, seed, init, coupling, sim_offset)`` 238-272
+  ``from_lattices``                                               284-300
+  ``update_red_bc`` / ``update_blue_bc`` (called from ``sweep``)    304-310
+  ``flip_red`` / ``flip_blue`` / ``sweep``                          345-360
+  ``packed`` / ``lattice`` / ``abs_magnetization`` /
+  ``energy_per_spin`` / ``halo_mismatches``                         364-397
+  ``run`` -> ``Trajectory``                                        401-440
+  ``run_simulations``                                              443-492
+  attributes ``dims temperatures n_sim seed coupling sim_offset init state
+  _tables streams sweeps_done attempts flips recorder``.
+``state`` is a host mirror of the device spins in the reference's uint16
+layout: reading it materialises the eight arrays with halos; in-place edits
+are detected and written back before the next device operation.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import threading
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+from . import _lib
+from ._lib import call, geom, SweepParams, MSB_MAX_PLANES
+from .layout import (
+    ALL_CODES, ArrayCode, LatticeDims, PackedArrays, check_spins, halo_audit_index, unpack,
+)
+from .observables import Trajectory
+from .rng import DeviceStreams
+
+__all__ = ["FLIP_RED", "FLIP_BLUE", "build_exp_table", "Engine", "run_simulations"]
+
+_C = ArrayCode
+# (target, lateral source, vertical source, up, right) -- engine.py:57-68.
+# The order is the RNG consumption order of a colour phase.
+FLIP_RED = (
+    (_C.RFE, _C.BFE, _C.BFO, False, False),
+    (_C.RBO, _C.BBO, _C.BBE, True, False),
+    (_C.RBE, _C.BBE, _C.BBO, False, True),
+    (_C.RFO, _C.BFO, _C.BFE, True, True),
+)
+FLIP_BLUE = (
+    (_C.BFE, _C.RFE, _C.RFO, False, True),
+    (_C.BBO, _C.RBO, _C.RBE, True, True),
+    (_C.BBE, _C.RBE, _C.RBO, False, False),
+    (_C.BFO, _C.RFO, _C.RFE, True, False),
+)
+
+_M64 = (1 << 64) - 1
+_UNIT = 2.0 ** -23
+
+
+def build_exp_table(T: float, J: float = 1.0) -> np.ndarray:
+    """Acceptance table indexed by 8*own + n_up (engine.py:78-94): flipping a
+    spin of sign s with u of 4 neighbours up costs 2 J s (2u - 4); the entry
+    is min(1, exp(-cost/T)) with CPython's math.exp (bit-identical doubles);
+    impossible up-counts 5..7 stay 0."""
+    if T <= 0:
+        raise ValueError("temperature must be positive")
+    table = np.zeros(16, dtype=np.float64)
+    for own in (0, 1):
+        s = 2 * own - 1
+        for u in range(5):
+            cost = 2.0 * J * s * (2 * u - 4)
+            table[8 * own + u] = 1.0 if cost <= 0 else math.exp(-cost / T)
+    return table
+
+
+# ---------------------------------------------------------------------------
+# per-device read-only tables (built once per process and device)
+# ---------------------------------------------------------------------------
+
+_TABLE_LOCK = threading.Lock()
+_POW_HOST: np.ndarray | None = None
+_DEV_TABLES: dict = {}
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _resolve_device(device):
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2404_16990_b200.Engine needs a CUDA device (B200); "
+                           "there is no CPU fallback")
+    _lib.lib()  # fail loudly now if the native library is missing
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    dev = torch.device(device)
+    if dev.type != "cuda":
+        raise ValueError(f"device must be a CUDA device, got {dev}")
+    return torch.device("cuda", dev.index if dev.index is not None else torch.cuda.current_device())
+
+
+def _pow_tables(device):
+    """Device copy of the 64 nibble tables of A^(2^b) (2 MiB)."""
+    global _POW_HOST
+    torch = _torch()
+    with _TABLE_LOCK:
+        key = ("pow", device.index)
+        if key not in _DEV_TABLES:
+            if _POW_HOST is None:
+                host = np.empty(64 * 8192, np.uint32)
+                call("msb_rng_power_tables", host.ctypes.data_as(ctypes.c_void_p))
+                _POW_HOST = host
+            _DEV_TABLES[key] = torch.from_numpy(_POW_HOST.view(np.int32)).to(device)
+        return _DEV_TABLES[key]
+
+
+def _sweep_jump_table(device, n: int):
+    """Device nibble table of A^(4n): advances a stream piece by one sweep."""
+    torch = _torch()
+    with _TABLE_LOCK:
+        key = ("jump", device.index, n)
+        if key not in _DEV_TABLES:
+            host = np.empty(8192, np.uint32)
+            call("msb_rng_jump_table", ctypes.c_uint64(4 * n), host.ctypes.data_as(ctypes.c_void_p))
+            _DEV_TABLES[key] = torch.from_numpy(host.view(np.int32)).to(device)
+        return _DEV_TABLES[key]
+
+
+def _p(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class Engine:
+    """Packed checkerboard Metropolis over ``n_sim`` replicas on one GPU.
+
+    Extra keyword-only arguments beyond the reference signature:
+    ``device`` (CUDA device; default current) and ``kg`` (stream pieces per
+    target row, 1/2/4/8/16; default chosen by the library).
+    """
+
+    def __init__(self, dims: LatticeDims, temperatures, seed: int, init: str = "random",
+                 coupling: float = 1.0, sim_offset: int = 0, *, device=None, kg: int | None = None):
+        self.dims = dims
+        self.temperatures = tuple(float(t) for t in temperatures)
+        if not self.temperatures:
+            raise ValueError("need at least one simulation temperature")
+        self.n_sim = len(self.temperatures)
+        self.seed = int(seed)
+        self.coupling = float(coupling)
+        self.sim_offset = int(sim_offset)
+        self.init = init
+        self._tables = np.stack([build_exp_table(t, coupling) for t in self.temperatures])
+        if init not in ("random", "all-up"):
+            raise ValueError(f"unknown init mode {init!r} (expected 'random' or 'all-up')")
+
+        torch = _torch()
+        self.device = _resolve_device(device)
+        self._stream = torch.cuda.Stream(device=self.device)
+        self._cs = ctypes.c_void_p(self._stream.cuda_stream)
+        self._g = geom(self.n_sim, dims.m, dims.n, sim_offset=self.sim_offset)
+        call("msb_check_geom", ctypes.byref(self._g))
+        self.kg = int(kg) if kg is not None else int(_lib.lib().msb_default_kg(ctypes.byref(self._g)))
+        self._words_per_sim = int(_lib.lib().msb_spin_words(ctypes.byref(self._g))) // self.n_sim
+        n_pieces = int(_lib.lib().msb_pieces_per_phase(ctypes.byref(self._g), self.kg))
+        with torch.cuda.device(self.device), torch.cuda.stream(self._stream):
+            self._spins = torch.empty(self._words_per_sim * self.n_sim, dtype=torch.int32, device=self.device)
+            self._states = torch.empty(2 * 8 * n_pieces, dtype=torch.int32, device=self.device)
+            self._thr = torch.zeros(MSB_MAX_PLANES * self.n_sim, dtype=torch.int32, device=self.device)
+            self._flips_dev = torch.zeros(1, dtype=torch.int64, device=self.device)
+            self._obs = torch.zeros(2 * self.n_sim, dtype=torch.int64, device=self.device)
+        self._pow = _pow_tables(self.device)
+        self._jump = _sweep_jump_table(self.device, dims.n)
+        self._params = SweepParams()
+        self._params.kg = self.kg
+        self._params.jump = self._jump.data_ptr()
+        self._params.thr9 = self._thr.data_ptr()
+        self._tab_key = None
+        self.fault = 0  # test-only adder corruption (selftest seam, cli.py:467-480)
+
+        if init == "random":
+            with torch.cuda.stream(self._stream):
+                scratch = torch.empty(self.n_sim * dims.sites // 64, dtype=torch.int64, device=self.device)
+            call("msb_init_random", ctypes.byref(self._g), ctypes.c_uint64(self.seed & _M64), _p(self._pow),
+                 _p(scratch), _p(self._spins), self._cs)
+            scratch.record_stream(self._stream)
+            del scratch
+        else:
+            call("msb_init_const", ctypes.byref(self._g), 1, _p(self._spins), self._cs)
+        call("msb_rng_init", ctypes.byref(self._g), ctypes.c_uint64(self.seed & _M64), self.kg,
+             ctypes.c_uint64(0), -1, _p(self._pow), _p(self._states), self._cs)
+        self.streams = DeviceStreams(self.seed, self.n_sim * dims.cells, self.sim_offset * dims.cells)
+        self._blocks = 0        # stream blocks consumed (one per colour phase)
+        self._pos = [0, 1]      # block each colour's pieces are positioned at
+        self._ver = 0           # device-state version
+        self._mirror = None     # host uint16 state mirror
+        self._mirror_snap = None
+        self._mirror_ver = -1
+        self._obs_ver = -1
+        self._obs_host = None
+
+        self.sweeps_done = 0
+        self.attempts = 0
+        self._flips_base = 0
+        self.recorder = None
+        self.update_red_bc()
+        self.update_blue_bc()
+
+    # -- construction from explicit lattices (engine.py:284-300) -------------
+
+    @classmethod
+    def from_lattices(cls, lattices, temperatures, seed: int, coupling: float = 1.0,
+                      sim_offset: int = 0, **kw) -> "Engine":
+        lattices = [np.asarray(l) for l in lattices]
+        dims = check_spins(lattices[0])
+        eng = cls(dims, temperatures, seed, init="all-up", coupling=coupling, sim_offset=sim_offset, **kw)
+        if len(lattices) != eng.n_sim:
+            raise ValueError("one lattice per temperature required")
+        for spins in lattices:
+            if check_spins(spins) != dims:
+                raise ValueError("all lattices must share the same dims")
+        eng._upload_lattices(lattices)
+        eng.update_red_bc()
+        eng.update_blue_bc()
+        return eng
+
+    def _upload_lattices(self, lattices) -> None:
+        torch = _torch()
+        lin = np.stack([np.packbits(np.asarray(l).reshape(-1) > 0, bitorder="little") for l in lattices])
+        with torch.cuda.stream(self._stream):
+            dev = torch.from_numpy(lin.view(np.int64).copy()).to(self.device, non_blocking=False)
+        call("msb_from_linear", ctypes.byref(self._g), _p(dev), _p(self._spins), self._cs)
+        self._stream.synchronize()
+        self._touch()
+
+    # -- boundary updates (engine.py:304-310) ----------------------------------
+
+    def update_red_bc(self) -> None:
+        """Halo/moat refresh of the red arrays.  On the GPU periodicity is
+        index arithmetic inside the kernels, so there is nothing to copy; the
+        call is kept so wrappers around it (test_acceptance.py:59-69) see the
+        same two updates per sweep as the reference."""
+
+    def update_blue_bc(self) -> None:
+        """See ``update_red_bc``."""
+
+    # -- thresholds (engine.py:257, 321-331) ---------------------------------
+
+    def _sync_tables(self) -> None:
+        tab = np.ascontiguousarray(self._tables, dtype=np.float64)
+        if tab.shape != (self.n_sim, 16):
+            raise ValueError(f"_tables must have shape {(self.n_sim, 16)}")
+        key = tab.tobytes()
+        if key == self._tab_key:
+            return
+        mode, npl = ctypes.c_int32(), ctypes.c_int32()
+        codes = (ctypes.c_int8 * 16)()
+        thr = np.zeros(MSB_MAX_PLANES * self.n_sim, np.uint32)
+        call("msb_plan_thresholds", tab.ctypes.data_as(ctypes.c_void_p), self.n_sim, ctypes.byref(mode),
+             ctypes.byref(npl), codes, thr.ctypes.data_as(ctypes.c_void_p))
+        torch = _torch()
+        with torch.cuda.stream(self._stream):
+            self._thr.copy_(torch.from_numpy(thr.view(np.int32)))
+        self._stream.synchronize()
+        self._params.mode = mode.value
+        self._params.n_planes = npl.value
+        self._params.code_plane[:] = list(codes)
+        self._tab_key = key
+
+    @property
+    def flip_mode(self) -> int:
+        self._sync_tables()
+        return int(self._params.mode)
+
+    # -- host mirror of the reference state layout ---------------------------
+
+    def _touch(self) -> None:
+        self._ver += 1
+
+    def _push_host_edits(self) -> None:
+        m = self._mirror
+        if m is not None and self._mirror_ver == self._ver and not np.array_equal(m, self._mirror_snap):
+            self._upload_state(m)
+
+    def _upload_state(self, arr: np.ndarray) -> None:
+        torch = _torch()
+        with torch.cuda.stream(self._stream):
+            dev = torch.from_numpy(np.ascontiguousarray(arr).view(np.int16)).to(self.device)
+        call("msb_from_ref16", ctypes.byref(self._g), _p(dev), _p(self._spins), self._cs)
+        self._stream.synchronize()
+        self._touch()
+
+    @property
+    def state(self) -> np.ndarray:
+        """uint16 (n_sim, 8, cells+2, words+2) view in the reference layout."""
+        if self._mirror is not None and self._mirror_ver == self._ver:
+            return self._mirror
+        torch = _torch()
+        d = self.dims
+        shape = (self.n_sim, len(ALL_CODES), d.cols, d.vec_len)
+        with torch.cuda.stream(self._stream):
+            dev = torch.empty(int(np.prod(shape)), dtype=torch.int16, device=self.device)
+        call("msb_to_ref16", ctypes.byref(self._g), _p(self._spins), _p(dev), self._cs)
+        self._stream.synchronize()
+        host = dev.cpu().numpy().view(np.uint16).reshape(shape)
+        if self._mirror is not None and self._mirror.shape == shape:
+            self._mirror[...] = host
+        else:
+            self._mirror = host.copy()
+        self._mirror_snap = host
+        self._mirror_ver = self._ver
+        return self._mirror
+
+    @state.setter
+    def state(self, value) -> None:
+        d = self.dims
+        arr = np.asarray(value)
+        shape = (self.n_sim, len(ALL_CODES), d.cols, d.vec_len)
+        if arr.shape != shape or arr.dtype != np.uint16:
+            raise ValueError(f"expected uint16 state of shape {shape}, got {arr.dtype} {arr.shape}")
+        self._upload_state(arr)
+
+    # -- flips (engine.py:314-360) -------------------------------------------
+
+    def _host_draws(self, phase: int):
+        """Draws from a user-supplied ``streams`` object (duck-typed seam,
+        engine.py:336): u23 integers in the reference block order."""
+        torch = _torch()
+        d = self.dims
+        block = np.asarray(self.streams.unit_block(4 * 16 * d.words), dtype=np.float64)
+        expect = (4 * 16 * d.words, self.n_sim * d.cells)
+        if block.shape != expect:
+            raise ValueError(f"streams.unit_block returned {block.shape}, expected {expect}")
+        u = block * (1 << 23)
+        k = np.floor(u)
+        if not ((k == u) & (block >= 0.0) & (block < 1.0)).all():
+            raise ValueError("host draws must be multiples of 2**-23 in [0, 1) (rng.py:113-115 shaping)")
+        draws = np.ascontiguousarray(k.T.astype(np.uint32))  # (n_sim*cells, 64*words) = block order
+        with torch.cuda.stream(self._stream):
+            return torch.from_numpy(draws.view(np.int32).reshape(-1)).to(self.device)
+
+    def _record(self, phase: int) -> None:
+        """Feed the recorder hook exactly as engine.py:327-328 does."""
+        torch = _torch()
+        d = self.dims
+        with torch.cuda.stream(self._stream):
+            out = torch.empty(self.n_sim * d.cells * 64 * d.words, dtype=torch.int32, device=self.device)
+        call("msb_draws", ctypes.byref(self._g), self.kg, phase, _p(self._states), _p(out), self._cs)
+        self._stream.synchronize()
+        draws = out.cpu().numpy().view(np.uint32).reshape(self.n_sim, d.cells, 4, 16, d.words)
+        quarters = FLIP_RED if phase == 0 else FLIP_BLUE
+        for q, (target, *_rest) in enumerate(quarters):
+            for i in range(4):
+                for ii in range(4):
+                    r = draws[:, :, q, 4 * i + ii, :].astype(np.float64) * _UNIT
+                    self.recorder.record(self.sweeps_done, target, 4 * ii + i, r)
+
+    def _phase(self, phase: int) -> None:
+        self._push_host_edits()
+        self._sync_tables()
+        self._params.fault = int(bool(self.fault))
+        h = self._blocks
+        ext = None
+        if not isinstance(self.streams, DeviceStreams):
+            ext = self._host_draws(phase)
+            self._pos[phase] = None
+        else:
+            if self._pos[phase] != h:
+                call("msb_rng_init", ctypes.byref(self._g), ctypes.c_uint64(self.seed & _M64), self.kg,
+                     ctypes.c_uint64(h), phase, _p(self._pow), _p(self._states), self._cs)
+            if self.recorder is not None:
+                self._record(phase)
+        call("msb_phase", ctypes.byref(self._g), ctypes.byref(self._params), phase, _p(self._spins),
+             _p(self._states), _p(ext) if ext is not None else None, _p(self._flips_dev), self._cs)
+        if ext is not None:
+            ext.record_stream(self._stream)
+        else:
+            self._pos[phase] = h + 2
+        self._blocks += 1
+        self._touch()
+
+    def flip_red(self) -> None:
+        """Attempt every red spin once."""
+        self._phase(0)
+
+    def flip_blue(self) -> None:
+        """Attempt every blue spin once."""
+        self._phase(1)
+
+    def sweep(self) -> None:
+        """One full sweep: red flips, red copies, blue flips, blue copies."""
+        self.flip_red()
+        self.update_red_bc()
+        self.flip_blue()
+        self.update_blue_bc()
+        self.sweeps_done += 1
+        self.attempts += self.dims.sites * self.n_sim
+
+    def _fast_path_ok(self) -> bool:
+        cls = type(self)
+        for name in ("sweep", "flip_red", "flip_blue", "update_red_bc", "update_blue_bc"):
+            if name in self.__dict__ or getattr(cls, name) is not getattr(Engine, name):
+                return False
+        return (self.recorder is None and isinstance(self.streams, DeviceStreams)
+                and self._pos == [self._blocks, self._blocks + 1])
+
+    def _sweeps(self, k: int) -> None:
+        """k sweeps in one library call (2k kernel launches, no host sync)."""
+        if k <= 0:
+            return
+        if not self._fast_path_ok():
+            for _ in range(k):
+                self.sweep()
+            return
+        self._push_host_edits()
+        self._sync_tables()
+        self._params.fault = int(bool(self.fault))
+        call("msb_sweep", ctypes.byref(self._g), ctypes.byref(self._params), _p(self._spins),
+             _p(self._states), k, _p(self._flips_dev), self._cs)
+        self._blocks += 2 * k
+        self._pos = [self._blocks, self._blocks + 1]
+        self.sweeps_done += k
+        self.attempts += self.dims.sites * self.n_sim * k
+        self._touch()
+
+    def synchronize(self) -> None:
+        self._stream.synchronize()
+
+    @property
+    def flips(self) -> int:
+        """Accepted flips so far (engine.py:331-332); synchronises the stream."""
+        self._stream.synchronize()
+        return self._flips_base + int(self._flips_dev.item())
+
+    @flips.setter
+    def flips(self, value: int) -> None:
+        self._stream.synchronize()
+        self._flips_base = int(value) - int(self._flips_dev.item())
+
+    # -- observables (engine.py:364-397) ---------------------------------------
+
+    def packed(self, sim: int) -> PackedArrays:
+        return PackedArrays(self.dims, self.state[sim])
+
+    def lattices(self) -> np.ndarray:
+        """All replicas' +/-1 lattices, int8 (n_sim, m, n)."""
+        return self._lattice_range(0, self.n_sim)
+
+    def lattice(self, sim: int) -> np.ndarray:
+        """Unpacked +/-1 lattice of one replica (engine.py:368-370)."""
+        if not -self.n_sim <= sim < self.n_sim:
+            raise IndexError(f"simulation {sim} out of range")
+        sim %= self.n_sim
+        return self._lattice_range(sim, sim + 1)[0]
+
+    def _lattice_range(self, lo: int, hi: int) -> np.ndarray:
+        self._push_host_edits()
+        torch = _torch()
+        d = self.dims
+        g = geom(hi - lo, d.m, d.n, sim_offset=self.sim_offset + lo)
+        with torch.cuda.stream(self._stream):
+            lin = torch.empty((hi - lo) * d.sites // 64, dtype=torch.int64, device=self.device)
+        base = ctypes.c_void_p(self._spins.data_ptr() + 4 * lo * self._words_per_sim)
+        call("msb_to_linear", ctypes.byref(g), base, _p(lin), self._cs)
+        self._stream.synchronize()
+        bits = np.unpackbits(lin.cpu().numpy().view(np.uint8), bitorder="little")
+        return np.where(bits == 1, 1, -1).astype(np.int8).reshape(hi - lo, d.m, d.n)
+
+    def _observe(self):
+        self._push_host_edits()
+        if self._obs_ver != self._ver:
+            with _torch().cuda.stream(self._stream):
+                self._obs.zero_()
+            ups = self._obs[: self.n_sim]
+            uns = self._obs[self.n_sim:]
+            call("msb_observe", ctypes.byref(self._g), _p(self._spins), _p(ups), _p(uns), self._cs)
+            self._stream.synchronize()
+            host = self._obs.cpu().numpy()
+            self._obs_host = (host[: self.n_sim].copy(), host[self.n_sim:].copy())
+            self._obs_ver = self._ver
+        return self._obs_host
+
+    def abs_magnetization(self) -> np.ndarray:
+        """Per-replica |M| = |2 ups/N - 1| (engine.py:372-375)."""
+        ups, _ = self._observe()
+        return np.abs(2.0 * ups / self.dims.sites - 1.0)
+
+    def energy_per_spin(self) -> np.ndarray:
+        """Per-replica bond energy per spin (engine.py:377-386): bonds =
+        sum s_i s_j = 2N - 2 * (unsatisfied bonds), evaluated as
+        -J * bonds / N in float64 exactly as the reference."""
+        _, unsat = self._observe()
+        bonds = 2 * self.dims.sites - 2 * unsat
+        return -self.coupling * bonds / self.dims.sites
+
+    def halo_mismatches(self) -> int:
+        """Halo/moat words of ``state`` differing from their canonical source."""
+        st = self.state
+        (la, lg, lw), (sa, sg, sw), (da, dg, dw) = halo_audit_index(self.dims)
+        bad = int((st[:, la, lg, lw] != st[:, sa, sg, sw]).sum())
+        bad += int((st[:, da, dg, dw] != 0).sum())
+        return bad
+
+    # -- driving (engine.py:401-440) -------------------------------------------
+
+    def run(self, n_sweeps: int, measure_interval: int = 100) -> Trajectory:
+        if n_sweeps < 0:
+            raise ValueError("sweep count must be non-negative")
+        if measure_interval < 1:
+            raise ValueError("measurement interval must be positive")
+        sweeps_at, abs_m, energy = [], [], []
+        start_attempts = self.attempts
+        t0 = time.perf_counter()
+        k = 0
+        while k < n_sweeps:
+            nxt = min((k // measure_interval + 1) * measure_interval, n_sweeps)
+            self._sweeps(nxt - k)
+            k = nxt
+            sweeps_at.append(self.sweeps_done)
+            abs_m.append(self.abs_magnetization())
+            energy.append(self.energy_per_spin())
+        self._stream.synchronize()
+        elapsed = time.perf_counter() - t0
+        return Trajectory(
+            sweeps=np.array(sweeps_at, dtype=np.int64),
+            abs_m=np.array(abs_m, dtype=np.float64).reshape(len(sweeps_at), self.n_sim),
+            energy=np.array(energy, dtype=np.float64).reshape(len(sweeps_at), self.n_sim),
+            temperatures=self.temperatures,
+            meta={
+                "m": self.dims.m, "n": self.dims.n, "seed": self.seed, "coupling": self.coupling,
+                "init": self.init, "sim_offset": self.sim_offset, "measure_interval": measure_interval,
+                "sweeps_run": n_sweeps, "attempts": self.attempts - start_attempts, "elapsed_s": elapsed,
+                "device": str(self.device),
+            },
+        )
+
+
+def run_simulations(dims: LatticeDims, temperatures, seed: int, n_sweeps: int, measure_interval: int = 100,
+                    init: str = "random", coupling: float = 1.0, threads: int = 1, devices=None) -> Trajectory:
+    """Replica fan-out with global stream indexing (engine.py:443-492).
+
+    Replicas split into contiguous slices exactly as the reference does
+    (np.linspace bounds, sim_offset = slice start), so any split is
+    bit-identical to one engine.  Slices are assigned round-robin to
+    ``devices`` (default: every visible GPU) and driven from host threads.
+    """
+    torch = _torch()
+    temperatures = tuple(float(t) for t in temperatures)
+    threads = max(1, int(threads))
+    if devices is None:
+        devices = list(range(torch.cuda.device_count())) if torch.cuda.is_available() else [None]
+    devices = list(devices) or [None]
+    t0 = time.perf_counter()
+    if threads == 1 or len(temperatures) == 1:
+        traj = Engine(dims, temperatures, seed, init=init, coupling=coupling, device=devices[0]).run(
+            n_sweeps, measure_interval)
+        traj.meta["elapsed_s"] = time.perf_counter() - t0
+        traj.meta["threads"] = 1
+        return traj
+    threads = min(threads, len(temperatures))
+    bounds = np.linspace(0, len(temperatures), threads + 1).astype(int)
+    slices = [(int(a), int(b)) for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
+
+    def run_slice(i_ab):
+        i, (lo, hi) = i_ab
+        dev = devices[i % len(devices)]
+        eng = Engine(dims, temperatures[lo:hi], seed, init=init, coupling=coupling, sim_offset=lo, device=dev)
+        return eng.run(n_sweeps, measure_interval)
+
+    with ThreadPoolExecutor(max_workers=len(slices)) as pool:
+        parts = list(pool.map(run_slice, enumerate(slices)))
+    merged = Trajectory(
+        sweeps=parts[0].sweeps,
+        abs_m=np.concatenate([p.abs_m for p in parts], axis=1),
+        energy=np.concatenate([p.energy for p in parts], axis=1),
+        temperatures=temperatures,
+        meta=dict(parts[0].meta),
+    )
+    merged.meta["sim_offset"] = 0
+    merged.meta["attempts"] = sum(p.meta["attempts"] for p in parts)
+    merged.meta["elapsed_s"] = time.perf_counter() - t0
+    merged.meta["threads"] = len(slices)
+    merged.meta["devices"] = sorted({p.meta["device"] for p in parts})
+    return merged
