@@ -118,16 +118,34 @@ int msb_to_ref16(const msb_geom *g, const uint32_t *spins, uint16_t *state, void
 int msb_from_ref16(const msb_geom *g, const uint16_t *state, uint32_t *spins, void *stream);
 
 /* ---- the hot path: Engine.flip_red / flip_blue / sweep (engine.py:314-360) - */
-/* One colour phase (0 red, 1 blue) for every held row, advancing each
- * piece's state by one sweep.  ext_draws (nullable): device uint32 u23 draws
- * in the reference block order [n_sim][m/4][4][16][n/32] of this phase
- * (whole lattices only); when given, the pieces' own streams are not used.
- * flips: device uint64 accumulator (engine.py:331-332). */
+/* A sweep is split in two because the reference's draws never depend on the
+ * spins (engine.py:336-341 draws a whole block before flipping):
+ *   msb_rng_planes: every stream piece generates its draws and reduces each
+ *     to n_planes accept bits (u23 < K_p), written as bit planes in the
+ *     colour-split layout: planes[2][n_planes][n_sim][rows][Pp] uint32,
+ *     msb_plane_words() words per buffer.  Advances the pieces by a sweep.
+ *   msb_flip: one colour phase -- bit-sliced neighbour classes select the
+ *     plane bit, flips by XOR, counts accepted flips into
+ *     flips[MSB_FLIP_SLOTS] (device uint64; the total is their sum,
+ *     engine.py:331-332).
+ * ext_draws (nullable, one colour of a whole lattice): device uint32 u23
+ * draws in the reference block order [n_sim][m/4][4][16][n/32] of the phase;
+ * when given, the pieces' own streams are neither used nor advanced. */
+#define MSB_FLIP_SLOTS 256
+int64_t msb_plane_words(const msb_geom *g, int32_t n_planes);
+int msb_rng_planes(const msb_geom *g, const msb_sweep_params *p, int32_t colour, uint32_t *states,
+                   const uint32_t *ext_draws, uint32_t *planes, void *stream);
+int msb_flip(const msb_geom *g, const msb_sweep_params *p, int32_t colour, uint32_t *spins,
+             const uint32_t *planes, uint64_t *flips, void *stream);
+/* One colour phase = msb_rng_planes(colour) + msb_flip(colour). */
 int msb_phase(const msb_geom *g, const msb_sweep_params *p, int32_t phase, uint32_t *spins,
-              uint32_t *states, const uint32_t *ext_draws, uint64_t *flips, void *stream);
-/* n_sweeps full sweeps (red then blue), whole lattices. */
+              uint32_t *states, const uint32_t *ext_draws, uint32_t *planes, uint64_t *flips,
+              void *stream);
+/* n_sweeps full sweeps (red then blue) of a whole lattice.  planes must hold
+ * 2 * msb_plane_words().  overlap != 0 runs the accept-plane generation of
+ * sweep k+1 on a helper stream concurrently with the flips of sweep k. */
 int msb_sweep(const msb_geom *g, const msb_sweep_params *p, uint32_t *spins, uint32_t *states,
-              int32_t n_sweeps, uint64_t *flips, void *stream);
+              uint32_t *planes, int32_t n_sweeps, int32_t overlap, uint64_t *flips, void *stream);
 
 /* ---- observables (engine.py:372-386) ------------------------------------- */
 /* Adds, per replica, the number of +1 spins and the number of unsatisfied

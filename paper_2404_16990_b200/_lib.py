@@ -21,6 +21,7 @@ MSB_MODE_FERRO = 0
 MSB_MODE_ANTI = 1
 MSB_MODE_GENERIC = 2
 MSB_MAX_PLANES = 10
+MSB_FLIP_SLOTS = 256
 
 
 class MsbError(RuntimeError):
@@ -57,7 +58,7 @@ EXPORTS = (
     "msb_row_pitch", "msb_pieces_per_phase", "msb_default_kg", "msb_plan_thresholds",
     "msb_rng_power_tables", "msb_rng_jump_table", "msb_rng_init", "msb_init_random",
     "msb_init_const", "msb_from_linear", "msb_to_linear", "msb_to_ref16", "msb_from_ref16",
-    "msb_phase", "msb_sweep", "msb_observe", "msb_draws", "msb_pack_edges", "msb_unpack_ghosts",
+    "msb_plane_words", "msb_rng_planes", "msb_flip", "msb_phase", "msb_sweep", "msb_observe", "msb_draws", "msb_pack_edges", "msb_unpack_ghosts",
     "msb_bench_int_peak",
 )
 
@@ -103,8 +104,11 @@ def lib() -> ctypes.CDLL:
         "msb_to_linear": ([G, vp, vp, vp], ctypes.c_int),
         "msb_to_ref16": ([G, vp, vp, vp], ctypes.c_int),
         "msb_from_ref16": ([G, vp, vp, vp], ctypes.c_int),
-        "msb_phase": ([G, P, i32, vp, vp, vp, vp, vp], ctypes.c_int),
-        "msb_sweep": ([G, P, vp, vp, i32, vp, vp], ctypes.c_int),
+        "msb_plane_words": ([G, i32], i64),
+        "msb_rng_planes": ([G, P, i32, vp, vp, vp, vp], ctypes.c_int),
+        "msb_flip": ([G, P, i32, vp, vp, vp, vp], ctypes.c_int),
+        "msb_phase": ([G, P, i32, vp, vp, vp, vp, vp, vp], ctypes.c_int),
+        "msb_sweep": ([G, P, vp, vp, vp, i32, i32, vp, vp], ctypes.c_int),
         "msb_observe": ([G, vp, vp, vp, vp], ctypes.c_int),
         "msb_draws": ([G, i32, i32, vp, vp, vp], ctypes.c_int),
         "msb_pack_edges": ([G, i32, vp, vp, vp], ctypes.c_int),

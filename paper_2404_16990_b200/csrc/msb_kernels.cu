@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -230,22 +231,27 @@ __device__ __forceinline__ uint32_t h_second(const Geo& G, const uint32_t* y, in
 }
 
 // ---------------------------------------------------------------------------
-// device: the fused colour-phase kernel
+// device: accept-plane generation (the RNG half of a sweep)
 // ---------------------------------------------------------------------------
+//
+// The reference's draws never depend on the spins (engine.py:336-341 draws a
+// whole block before any flip), so a sweep splits into
+//   (1) k_rng_planes: every stream piece generates its draws and reduces each
+//       to NP accept bits (u23 < K_p), written as bit planes in the spins'
+//       colour-split layout: planes[X][p][s][lr][Pp];
+//   (2) k_flip (per colour): bit-sliced neighbour classes select the plane.
+// (1) is INT-pipe bound and state independent, so it can run a sweep ahead
+// of (2), which is a light memory-bound pass over L2/HBM.
 
-struct PhaseArgs {
+struct RngArgs {
   Geo G;
-  uint32_t* spins;
   uint32_t* states;
   const uint32_t* thr9;
   const uint4* jump;
-  unsigned long long* flips;
   const uint32_t* ext;
+  uint32_t* planes;
   long long npieces;
-  int phase, kg, kr, np, nch, block_rows, rs;
-  uint32_t inv;
-  int fault;
-  int8_t code_plane[16];
+  int colour0, kg, kr, np, nch, block_rows, rs, Pp;
 };
 
 // 32x32 bit-matrix transpose in registers, LSB-first: on exit bit i of a[c]
@@ -273,21 +279,25 @@ __device__ __forceinline__ void transpose32(uint32_t a[32]) {
 // mapping is its own inverse, engine.py:326-330)
 __device__ __forceinline__ int k_of_t(int t) { return 4 * (t & 3) + (t >> 2); }
 
-template <int NPMAX, bool GENERIC, bool EXT>
-__global__ void __launch_bounds__(256) k_phase(const PhaseArgs a) {
-  extern __shared__ uint4 smem4[];
-  uint4* jt = smem4;
-  uint32_t* buf = reinterpret_cast<uint32_t*>(smem4 + kJumpWords / 4);
-  const Geo& G = a.G;
-  const int tid = threadIdx.x;
-  const int X = a.phase;
-  const int np = GENERIC ? a.np : NPMAX;  // compile-time 2 on the fast path
-  const long long total_rows = (long long)G.n_sim * G.rows;
+__device__ __forceinline__ size_t plane_off(const Geo& G, int Pp, int np, int X, int p, int s, int lr) {
+  return ((((size_t)X * np + p) * G.n_sim + s) * G.rows + lr) * Pp;
+}
 
-  if (!EXT) {
-    for (int i = tid; i < kJumpWords / 4; i += blockDim.x) jt[i] = a.jump[i];
+// grid: (row blocks, colours).  Block = block_rows target rows x kg pieces.
+template <int NPMAX, bool EXT, bool JSMEM>
+__global__ void __launch_bounds__(256) k_rng_planes(const RngArgs a) {
+  extern __shared__ uint4 smem4[];
+  uint32_t* buf = reinterpret_cast<uint32_t*>(JSMEM ? smem4 + kJumpWords / 4 : smem4);
+  const uint4* jt = JSMEM ? smem4 : a.jump;
+  if (JSMEM && !EXT) {
+    for (int i = threadIdx.x; i < kJumpWords / 4; i += blockDim.x) smem4[i] = a.jump[i];
     __syncthreads();
   }
+  const Geo& G = a.G;
+  const int tid = threadIdx.x;
+  const int X = a.colour0 + blockIdx.y;
+  const int np = NPMAX == 2 ? 2 : a.np;
+  const long long total_rows = (long long)G.n_sim * G.rows;
 
   // ---- stage 1: each thread generates its piece of the stream -------------
   {
@@ -297,7 +307,7 @@ __global__ void __launch_bounds__(256) k_phase(const PhaseArgs a) {
       const int s = (int)(gr / G.rows), lr = (int)(gr % G.rows);
       const int c = G.row0 + lr;
       const long long gp = gr * a.kg + kgi;
-      uint32_t key[NPMAX > 0 ? NPMAX : 1];
+      uint32_t key[NPMAX];
 #pragma unroll
       for (int p = 0; p < NPMAX; p++) key[p] = p < np ? a.thr9[p * G.n_sim + s] : 0u;
       uint32_t* out = buf + rl * a.rs;
@@ -316,21 +326,20 @@ __global__ void __launch_bounds__(256) k_phase(const PhaseArgs a) {
         const int k = k0 + kk;
         for (int ch = 0; ch < a.nch; ch++) {
           const int L = min(32, G.words - 32 * ch);
-          uint32_t acc[NPMAX > 0 ? NPMAX : 1];
+          uint32_t acc[NPMAX];
 #pragma unroll
           for (int p = 0; p < NPMAX; p++) acc[p] = 0;
           if (!EXT) {
-            int i = 0;
             if (L == 32) {
 #pragma unroll 8
-              for (; i < 32; i++) {
+              for (int i = 0; i < 32; i++) {
                 const uint32_t h9 = xstep(st) << 9;
 #pragma unroll
                 for (int p = 0; p < NPMAX; p++)
                   if (p < np) acc_reject(acc[p], h9, key[p]);
               }
             } else {
-              for (; i < L; i++) {
+              for (int i = 0; i < L; i++) {
                 const uint32_t h9 = xstep(st) << 9;
 #pragma unroll
                 for (int p = 0; p < NPMAX; p++)
@@ -355,18 +364,14 @@ __global__ void __launch_bounds__(256) k_phase(const PhaseArgs a) {
   }
   __syncthreads();
 
-  // ---- stage 2: transpose accept planes to row words and flip -------------
-  unsigned long long nflip = 0;
+  // ---- stage 2: transpose (k, w) bit matrices into row words --------------
   const int units = a.block_rows * a.nch;
   for (int u = tid; u < units; u += blockDim.x) {
     const int rl = u / a.nch, ch = u % a.nch;
     const long long gr = (long long)blockIdx.x * a.block_rows + rl;
     if (gr >= total_rows) continue;
     const int s = (int)(gr / G.rows), lr = (int)(gr % G.rows);
-    const int c = G.row0 + lr, br = lr + G.ghost;
-    const int p = (c + X) & 1;
-    uint32_t* bp = buf + rl * a.rs;
-    // transpose each pair of planes in place: slot (p, k, ch) -> word j'
+    const uint32_t* bp = buf + rl * a.rs;
 #pragma unroll
     for (int pp = 0; pp < NPMAX; pp += 2) {
       if (pp >= np) break;
@@ -377,62 +382,107 @@ __global__ void __launch_bounds__(256) k_phase(const PhaseArgs a) {
         m32[16 + t] = pp + 1 < np ? bp[((pp + 1) * 16 + k_of_t(t)) * a.nch + ch] : 0u;
       }
       transpose32(m32);  // m32[w'] : bits 0-15 plane pp (bit t), 16-31 plane pp+1
+      uint4* o0 = reinterpret_cast<uint4*>(a.planes + plane_off(G, a.Pp, np, X, pp, s, lr) + 16 * ch);
 #pragma unroll
-      for (int jj = 0; jj < 16; jj++) {
-        bp[(pp * 16 + jj) * a.nch + ch] = __byte_perm(m32[2 * jj], m32[2 * jj + 1], 0x5410);
-        if (pp + 1 < np) bp[((pp + 1) * 16 + jj) * a.nch + ch] = __byte_perm(m32[2 * jj], m32[2 * jj + 1], 0x7632);
+      for (int q = 0; q < 4; q++)
+        o0[q] = make_uint4(__byte_perm(m32[8 * q + 0], m32[8 * q + 1], 0x5410),
+                           __byte_perm(m32[8 * q + 2], m32[8 * q + 3], 0x5410),
+                           __byte_perm(m32[8 * q + 4], m32[8 * q + 5], 0x5410),
+                           __byte_perm(m32[8 * q + 6], m32[8 * q + 7], 0x5410));
+      if (pp + 1 < np) {
+        uint4* o1 = reinterpret_cast<uint4*>(a.planes + plane_off(G, a.Pp, np, X, pp + 1, s, lr) + 16 * ch);
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+          o1[q] = make_uint4(__byte_perm(m32[8 * q + 0], m32[8 * q + 1], 0x7632),
+                             __byte_perm(m32[8 * q + 2], m32[8 * q + 3], 0x7632),
+                             __byte_perm(m32[8 * q + 4], m32[8 * q + 5], 0x7632),
+                             __byte_perm(m32[8 * q + 6], m32[8 * q + 7], 0x7632));
       }
-    }
-    uint32_t* own = a.spins + row_off(G, s, X, br);
-    int bu, bd;
-    vert_rows(G, br, bu, bd);
-    const uint32_t* yc = a.spins + row_off(G, s, 1 - X, br);
-    const uint32_t* yu = a.spins + row_off(G, s, 1 - X, bu);
-    const uint32_t* yd = a.spins + row_off(G, s, 1 - X, bd);
-    const int jmax = min(16, G.W - 16 * ch);
-    for (int jj = 0; jj < jmax; jj++) {
-      const int j = 16 * ch + jj;
-      const uint32_t o = own[j];
-      const uint32_t y0 = yc[j];
-      const uint32_t n1 = yu[j], n2 = yd[j], n3 = y0, n4 = h_second(G, yc, j, p, y0);
-      uint32_t flip;
-      if (!GENERIC) {
-        const uint32_t A4 = bp[(0 * 16 + jj) * a.nch + ch];
-        const uint32_t A8 = bp[(1 * 16 + jj) * a.nch + ch];
-        const uint32_t ow = o ^ a.inv;
-        const uint32_t x1 = n1 ^ ow, x2 = n2 ^ ow, x3 = n3 ^ ow;
-        const uint32_t x4 = a.fault ? 0u : (n4 ^ ow);
-        const uint32_t o12 = x1 | x2, a12 = x1 & x2, o34 = x3 | x4, a34 = x3 & x4;
-        const uint32_t ge2 = a12 | a34 | (o12 & o34);  // >= 2 disagreeing neighbours
-        const uint32_t any = o12 | o34;
-        flip = ge2 | (any & ~ge2 & A4) | (~any & A8);
-      } else {
-        // neighbour up-count bit planes (bitkernels.py:63-79 restated)
-        const uint32_t s1 = n1 ^ n2, c1 = n1 & n2, s2 = n3 ^ n4, c2 = n3 & n4;
-        uint32_t ones = s1 ^ s2;
-        const uint32_t twos = c1 ^ c2 ^ (s1 & s2), fours = c1 & c2;
-        if (a.fault) ones = s1;
-        flip = 0;
-        for (int code = 0; code < 16; code++) {
-          const int pl = a.code_plane[code];
-          if (pl == -1) continue;
-          const int u = code & 7;
-          if (u > 4) continue;
-          const uint32_t msk = ((code & 8) ? o : ~o) & ((u & 1) ? ones : ~ones) & ((u & 2) ? twos : ~twos) &
-                               ((u & 4) ? fours : ~fours);
-          flip |= pl == -2 ? msk : (msk & bp[(pl * 16 + jj) * a.nch + ch]);
-        }
-      }
-      flip &= valid_mask(G, j);
-      own[j] = o ^ flip;
-      nflip += __popc(flip);
     }
   }
-  // one atomic per warp
-  const unsigned lane = tid & 31;
-#pragma unroll
-  for (int off = 16; off; off >>= 1) nflip += __shfl_down_sync(0xFFFFFFFFu, nflip, off);
-  if (lane == 0 && nflip) atomicAdd(a.flips, nflip);
+}
+
+// ---------------------------------------------------------------------------
+// device: the flip pass (one colour)
+// ---------------------------------------------------------------------------
+
+struct FlipArgs {
+  Geo G;
+  uint32_t* spins;
+  const uint32_t* planes;
+  unsigned long long* flips;
+  int X, np, Pp;
+  uint32_t inv;
+  int fault;
+  int8_t code_plane[16];
+};
+
+constexpr int kFlipSlots = 256;
+
+// Thread per (replica, held row, word): neighbours are the other colour's
+// rows c-1, c+1 (same word) and row c at words j, j+-1 (include/msb200.h).
+template <bool GENERIC>
+__global__ void __launch_bounds__(256) k_flip(const FlipArgs a) {
+  const Geo& G = a.G;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long total = (long long)G.n_sim * G.rows * G.W;
+  unsigned cnt = 0;
+  if (i < total) {
+    const int j = (int)(i % G.W);
+    const long long gr = i / G.W;
+    const int s = (int)(gr / G.rows), lr = (int)(gr % G.rows);
+    const int X = a.X, c = G.row0 + lr, br = lr + G.ghost;
+    int bu, bd;
+    vert_rows(G, br, bu, bd);
+    uint32_t* own = a.spins + row_off(G, s, X, br);
+    const uint32_t* yc = a.spins + row_off(G, s, 1 - X, br);
+    const uint32_t o = own[j];
+    const uint32_t y0 = __ldg(yc + j);
+    const uint32_t n1 = __ldg(a.spins + row_off(G, s, 1 - X, bu) + j);
+    const uint32_t n2 = __ldg(a.spins + row_off(G, s, 1 - X, bd) + j);
+    const uint32_t n4 = h_second(G, yc, j, (c + X) & 1, y0);
+    const uint32_t* pl = a.planes + plane_off(G, a.Pp, a.np, X, 0, s, lr) + j;
+    const size_t pstride = (size_t)G.n_sim * G.rows * a.Pp;
+    uint32_t flip;
+    if (!GENERIC) {
+      const uint32_t A4 = __ldg(pl), A8 = __ldg(pl + pstride);
+      const uint32_t ow = o ^ a.inv;
+      const uint32_t x1 = n1 ^ ow, x2 = n2 ^ ow, x3 = y0 ^ ow;
+      const uint32_t x4 = a.fault ? 0u : (n4 ^ ow);
+      const uint32_t o12 = x1 | x2, a12 = x1 & x2, o34 = x3 | x4, a34 = x3 & x4;
+      const uint32_t ge2 = a12 | a34 | (o12 & o34);  // >= 2 disagreeing neighbours
+      const uint32_t any = o12 | o34;
+      flip = ge2 | (any & ~ge2 & A4) | (~any & A8);
+    } else {
+      // neighbour up-count bit planes (bitkernels.py:63-79 restated)
+      const uint32_t s1 = n1 ^ n2, c1 = n1 & n2, s2 = y0 ^ n4, c2 = y0 & n4;
+      uint32_t ones = s1 ^ s2;
+      const uint32_t twos = c1 ^ c2 ^ (s1 & s2), fours = c1 & c2;
+      if (a.fault) ones = s1;
+      flip = 0;
+      for (int code = 0; code < 16; code++) {
+        const int pidx = a.code_plane[code];
+        const int u = code & 7;
+        if (pidx == -1 || u > 4) continue;
+        const uint32_t msk = ((code & 8) ? o : ~o) & ((u & 1) ? ones : ~ones) & ((u & 2) ? twos : ~twos) &
+                             ((u & 4) ? fours : ~fours);
+        flip |= pidx == -2 ? msk : (msk & __ldg(pl + pidx * pstride));
+      }
+    }
+    flip &= valid_mask(G, j);
+    own[j] = o ^ flip;
+    cnt = __popc(flip);
+  }
+  // block reduction, one atomic per block into one of kFlipSlots counters
+  __shared__ unsigned red[8];
+  cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += red[w];
+    if (t) atomicAdd(a.flips + (blockIdx.x % kFlipSlots), t);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -752,16 +802,102 @@ int check_geom(const msb_geom* g) {
 
 inline unsigned blocks_for(long long n, int bt) { return (unsigned)((n + bt - 1) / bt); }
 
-template <int NPMAX, bool GENERIC, bool EXT>
-int launch_phase(const PhaseArgs& a, size_t smem, unsigned grid, int threads, cudaStream_t st) {
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(k_phase<NPMAX, GENERIC, EXT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    227 * 1024);
+template <typename K>
+int set_smem_attr(K kernel, std::once_flag& once, cudaError_t& err) {
+  std::call_once(once, [&] {
+    err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   });
-  if (attr_err != cudaSuccess) return fail(MSB_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
-  k_phase<NPMAX, GENERIC, EXT><<<grid, threads, smem, st>>>(a);
+  if (err != cudaSuccess) return fail(MSB_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(err));
+  return MSB_OK;
+}
+
+int plane_pitch(const Geo& G) { return (G.W + 15) & ~15; }
+
+int check_params(const msb_sweep_params* p) {
+  if (!p) return fail(MSB_ERR_ARG, "null sweep parameters");
+  const int kg = p->kg;
+  if (kg != 1 && kg != 2 && kg != 4 && kg != 8 && kg != 16) return fail(MSB_ERR_ARG, "kg must be 1, 2, 4, 8 or 16");
+  if (p->n_planes < 0 || p->n_planes > MSB_MAX_PLANES) return fail(MSB_ERR_ARG, "bad plane count");
+  if (p->mode != MSB_MODE_GENERIC && p->n_planes != 2) return fail(MSB_ERR_ARG, "ferro/anti modes use exactly 2 planes");
+  if (p->mode < 0 || p->mode > 2) return fail(MSB_ERR_ARG, "bad mode");
+  if (p->n_planes > 0 && !p->thr9) return fail(MSB_ERR_ARG, "null thresholds");
+  return MSB_OK;
+}
+
+int rng_planes(const msb_geom* g, const msb_sweep_params* p, int colour, uint32_t* states, const uint32_t* ext,
+               uint32_t* planes, cudaStream_t st) {
+  const Geo G = make_geo(g);
+  RngArgs a;
+  a.G = G;
+  a.states = states;
+  a.thr9 = p->thr9;
+  a.jump = reinterpret_cast<const uint4*>(p->jump);
+  a.ext = ext;
+  a.planes = planes;
+  a.kg = p->kg;
+  a.kr = 16 / p->kg;
+  a.npieces = (long long)g->n_sim * g->rows * p->kg;
+  a.np = p->n_planes;
+  a.nch = (G.words + 31) / 32;
+  a.Pp = plane_pitch(G);
+  a.colour0 = colour < 0 ? 0 : colour;
+  const int ncol = colour < 0 ? 2 : 1;
+  a.rs = std::max(a.np, 1) * 16 * a.nch + 1;  // odd row stride: conflict-free per-row access
+  const long long total_rows = (long long)g->n_sim * g->rows;
+  static const int env_threads = [] { const char* e = getenv("MSB_RNG_THREADS"); return e ? atoi(e) : 0; }();
+  static const int env_jsmem = [] { const char* e = getenv("MSB_JUMP_SMEM"); return e ? atoi(e) : 1; }();
+  const bool jsmem = env_jsmem != 0 && !ext;
+  int threads_target = env_threads > 0 ? env_threads : 128;
+  int block_rows = p->block_rows > 0 ? p->block_rows : std::max(1, threads_target / p->kg);
+  block_rows = std::min(block_rows, 256 / p->kg);
+  const size_t jbytes = jsmem ? (size_t)kJumpWords * 4 : 0;
+  while (block_rows > 1 && jbytes + (size_t)block_rows * a.rs * 4 > 227 * 1024) block_rows /= 2;
+  while (block_rows > 1 && ((total_rows + block_rows - 1) / block_rows) * ncol < 2 * 148 && block_rows * p->kg > 64)
+    block_rows /= 2;
+  a.block_rows = block_rows;
+  const size_t smem = jbytes + (size_t)block_rows * a.rs * 4;
+  if (smem > 227 * 1024) return fail(MSB_ERR_UNSUPPORTED, "lattice rows too long for the shared-memory plan");
+  const dim3 grid((unsigned)((total_rows + block_rows - 1) / block_rows), ncol);
+  const int threads = ((block_rows * p->kg + 31) / 32) * 32;
+#define MSB_LAUNCH_RNG(NP, EXT, JS)                                           \
+  do {                                                                        \
+    static std::once_flag o;                                                  \
+    static cudaError_t e;                                                     \
+    if (int r = set_smem_attr(k_rng_planes<NP, EXT, JS>, o, e)) return r;     \
+    k_rng_planes<NP, EXT, JS><<<grid, threads, smem, st>>>(a);                \
+  } while (0)
+  if (p->mode != MSB_MODE_GENERIC) {
+    if (ext) MSB_LAUNCH_RNG(2, true, false);
+    else if (jsmem) MSB_LAUNCH_RNG(2, false, true);
+    else MSB_LAUNCH_RNG(2, false, false);
+  } else {
+    if (ext) MSB_LAUNCH_RNG(MSB_MAX_PLANES, true, false);
+    else MSB_LAUNCH_RNG(MSB_MAX_PLANES, false, false);
+  }
+#undef MSB_LAUNCH_RNG
+  CUDA_TRY(cudaGetLastError());
+  return MSB_OK;
+}
+
+int flip(const msb_geom* g, const msb_sweep_params* p, int colour, uint32_t* spins, const uint32_t* planes,
+         uint64_t* flips, cudaStream_t st) {
+  const Geo G = make_geo(g);
+  FlipArgs a;
+  a.G = G;
+  a.spins = spins;
+  a.planes = planes;
+  a.flips = reinterpret_cast<unsigned long long*>(flips);
+  a.X = colour;
+  a.np = p->n_planes;
+  a.Pp = plane_pitch(G);
+  a.inv = p->mode == MSB_MODE_ANTI ? 0xFFFFFFFFu : 0u;
+  a.fault = p->fault;
+  std::memcpy(a.code_plane, p->code_plane, 16);
+  const long long total = (long long)g->n_sim * g->rows * G.W;
+  if (p->mode == MSB_MODE_GENERIC)
+    k_flip<true><<<blocks_for(total, 256), 256, 0, st>>>(a);
+  else
+    k_flip<false><<<blocks_for(total, 256), 256, 0, st>>>(a);
   CUDA_TRY(cudaGetLastError());
   return MSB_OK;
 }
@@ -986,71 +1122,90 @@ int msb_from_ref16(const msb_geom* g, const uint16_t* state, uint32_t* spins, vo
   return MSB_OK;
 }
 
-int msb_phase(const msb_geom* g, const msb_sweep_params* p, int32_t phase, uint32_t* spins, uint32_t* states,
-              const uint32_t* ext_draws, uint64_t* flips, void* stream) {
-  if (int r = check_geom(g)) return r;
-  if (!p || !spins || !flips) return fail(MSB_ERR_ARG, "null argument");
-  if (phase != 0 && phase != 1) return fail(MSB_ERR_ARG, "phase must be 0 (red) or 1 (blue)");
-  const int kg = p->kg;
-  if (kg != 1 && kg != 2 && kg != 4 && kg != 8 && kg != 16) return fail(MSB_ERR_ARG, "kg must be 1, 2, 4, 8 or 16");
-  if (p->n_planes < 0 || p->n_planes > MSB_MAX_PLANES) return fail(MSB_ERR_ARG, "bad plane count");
-  const bool generic = p->mode == MSB_MODE_GENERIC;
-  if (!generic && p->n_planes != 2) return fail(MSB_ERR_ARG, "ferro/anti modes use exactly 2 planes");
-  if (p->n_planes > 0 && !p->thr9) return fail(MSB_ERR_ARG, "null thresholds");
-  if (ext_draws && g->ghost) return fail(MSB_ERR_UNSUPPORTED, "external draws need a whole lattice");
-  if (!ext_draws && (!states || !p->jump)) return fail(MSB_ERR_ARG, "null RNG state or jump table");
+int64_t msb_plane_words(const msb_geom* g, int32_t n_planes) {
+  if (check_geom(g)) return -1;
+  if (n_planes < 0 || n_planes > MSB_MAX_PLANES) return -1;
   const Geo G = make_geo(g);
-  PhaseArgs a;
-  a.G = G;
-  a.spins = spins;
-  a.states = states;
-  a.thr9 = p->thr9;
-  a.jump = reinterpret_cast<const uint4*>(p->jump);
-  a.flips = reinterpret_cast<unsigned long long*>(flips);
-  a.ext = ext_draws;
-  a.npieces = (long long)g->n_sim * g->rows * kg;
-  a.phase = phase;
-  a.kg = kg;
-  a.kr = 16 / kg;
-  a.np = p->n_planes;
-  a.nch = (G.words + 31) / 32;
-  a.inv = p->mode == MSB_MODE_ANTI ? 0xFFFFFFFFu : 0u;
-  a.fault = p->fault;
-  std::memcpy(a.code_plane, p->code_plane, 16);
-  const int npl = std::max(a.np, 1);
-  a.rs = npl * 16 * a.nch + 1;  // odd row stride: conflict-free per-row access
-  const long long total_rows = (long long)g->n_sim * g->rows;
-  int block_rows = p->block_rows > 0 ? p->block_rows : 256 / kg;
-  if (block_rows * kg > 256) block_rows = 256 / kg;
-  const size_t base = ext_draws ? 0 : (size_t)kJumpWords * 4;
-  while (block_rows > 1 && base + (size_t)block_rows * a.rs * 4 > 227 * 1024) block_rows /= 2;
-  // small problems: spread rows over more blocks
-  while (block_rows > 1 && (total_rows + block_rows - 1) / block_rows < 2 * 148 && block_rows * kg > 64)
-    block_rows /= 2;
-  a.block_rows = block_rows;
-  const size_t smem = base + (size_t)block_rows * a.rs * 4;
-  if (smem > 227 * 1024) return fail(MSB_ERR_UNSUPPORTED, "lattice rows too long for the shared-memory plan");
-  const unsigned grid = (unsigned)((total_rows + block_rows - 1) / block_rows);
-  const int threads = ((block_rows * kg + 31) / 32) * 32;
-  cudaStream_t st = as_stream(stream);
-  if (!generic) {
-    return ext_draws ? launch_phase<2, false, true>(a, smem, grid, threads, st)
-                     : launch_phase<2, false, false>(a, smem, grid, threads, st);
-  }
-  return ext_draws ? launch_phase<MSB_MAX_PLANES, true, true>(a, smem, grid, threads, st)
-                   : launch_phase<MSB_MAX_PLANES, true, false>(a, smem, grid, threads, st);
+  return 2LL * std::max(n_planes, 1) * g->n_sim * g->rows * plane_pitch(G);
 }
 
-int msb_sweep(const msb_geom* g, const msb_sweep_params* p, uint32_t* spins, uint32_t* states, int32_t n_sweeps,
-              uint64_t* flips, void* stream) {
+int msb_rng_planes(const msb_geom* g, const msb_sweep_params* p, int32_t colour, uint32_t* states,
+                   const uint32_t* ext_draws, uint32_t* planes, void* stream) {
   if (int r = check_geom(g)) return r;
-  if (g->ghost) return fail(MSB_ERR_UNSUPPORTED, "msb_sweep runs whole lattices; slabs use msb_phase + halo exchange");
+  if (int r = check_params(p)) return r;
+  if (colour < -1 || colour > 1) return fail(MSB_ERR_ARG, "colour must be -1 (both), 0 or 1");
+  if (!planes) return fail(MSB_ERR_ARG, "null planes buffer");
+  if (ext_draws && (g->ghost || colour < 0)) return fail(MSB_ERR_UNSUPPORTED, "external draws: one colour of a whole lattice");
+  if (!ext_draws && (!states || !p->jump)) return fail(MSB_ERR_ARG, "null RNG state or jump table");
+  return rng_planes(g, p, colour, states, ext_draws, planes, as_stream(stream));
+}
+
+int msb_flip(const msb_geom* g, const msb_sweep_params* p, int32_t colour, uint32_t* spins, const uint32_t* planes,
+             uint64_t* flips, void* stream) {
+  if (int r = check_geom(g)) return r;
+  if (int r = check_params(p)) return r;
+  if (colour != 0 && colour != 1) return fail(MSB_ERR_ARG, "colour must be 0 (red) or 1 (blue)");
+  if (!spins || !planes || !flips) return fail(MSB_ERR_ARG, "null buffer");
+  return flip(g, p, colour, spins, planes, flips, as_stream(stream));
+}
+
+int msb_phase(const msb_geom* g, const msb_sweep_params* p, int32_t phase, uint32_t* spins, uint32_t* states,
+              const uint32_t* ext_draws, uint32_t* planes, uint64_t* flips, void* stream) {
+  if (phase != 0 && phase != 1) return fail(MSB_ERR_ARG, "phase must be 0 (red) or 1 (blue)");
+  if (int r = msb_rng_planes(g, p, phase, states, ext_draws, planes, stream)) return r;
+  return msb_flip(g, p, phase, spins, planes, flips, stream);
+}
+
+int msb_sweep(const msb_geom* g, const msb_sweep_params* p, uint32_t* spins, uint32_t* states, uint32_t* planes,
+              int32_t n_sweeps, int32_t overlap, uint64_t* flips, void* stream) {
+  if (int r = check_geom(g)) return r;
+  if (int r = check_params(p)) return r;
   if (n_sweeps < 0) return fail(MSB_ERR_ARG, "sweep count must be non-negative");
-  for (int k = 0; k < n_sweeps; k++) {
-    if (int r = msb_phase(g, p, 0, spins, states, nullptr, flips, stream)) return r;
-    if (int r = msb_phase(g, p, 1, spins, states, nullptr, flips, stream)) return r;
+  if (!spins || !states || !planes || !flips || !p->jump) return fail(MSB_ERR_ARG, "null buffer");
+  if (g->ghost) return fail(MSB_ERR_UNSUPPORTED, "msb_sweep runs whole lattices; slabs use the per-phase calls");
+  cudaStream_t st = as_stream(stream);
+  if (n_sweeps == 0) return MSB_OK;
+  if (!overlap) {
+    for (int k = 0; k < n_sweeps; k++) {
+      if (int r = rng_planes(g, p, -1, states, nullptr, planes, st)) return r;
+      if (int r = flip(g, p, 0, spins, planes, flips, st)) return r;
+      if (int r = flip(g, p, 1, spins, planes, flips, st)) return r;
+    }
+    return MSB_OK;
   }
-  return MSB_OK;
+  // Two plane buffers; the RNG of sweep k+1 (helper stream) overlaps the
+  // flips of sweep k (caller stream).
+  const int64_t pw = msb_plane_words(g, p->n_planes);
+  cudaStream_t aux;
+  CUDA_TRY(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+  cudaEvent_t ev_start, ev_r[2], ev_f[2];
+  CUDA_TRY(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
+  for (int b = 0; b < 2; b++) {
+    CUDA_TRY(cudaEventCreateWithFlags(&ev_r[b], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&ev_f[b], cudaEventDisableTiming));
+  }
+  int status = MSB_OK;
+  CUDA_TRY(cudaEventRecord(ev_start, st));
+  CUDA_TRY(cudaStreamWaitEvent(aux, ev_start, 0));
+  for (int k = 0; k < n_sweeps && status == MSB_OK; k++) {
+    const int b = k & 1;
+    uint32_t* buf = planes + (size_t)b * pw;
+    if (k >= 2) CUDA_TRY(cudaStreamWaitEvent(aux, ev_f[b], 0));
+    status = rng_planes(g, p, -1, states, nullptr, buf, aux);
+    if (status) break;
+    CUDA_TRY(cudaEventRecord(ev_r[b], aux));
+    CUDA_TRY(cudaStreamWaitEvent(st, ev_r[b], 0));
+    status = flip(g, p, 0, spins, buf, flips, st);
+    if (!status) status = flip(g, p, 1, spins, buf, flips, st);
+    CUDA_TRY(cudaEventRecord(ev_f[b], st));
+  }
+  cudaEventDestroy(ev_start);
+  for (int b = 0; b < 2; b++) {
+    cudaEventDestroy(ev_r[b]);
+    cudaEventDestroy(ev_f[b]);
+  }
+  cudaStreamDestroy(aux);
+  return status;
 }
 
 int msb_observe(const msb_geom* g, const uint32_t* spins, int64_t* ups, int64_t* unsat, void* stream) {

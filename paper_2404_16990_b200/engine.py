@@ -36,7 +36,7 @@ from concurrent.futures import ThreadPoolExecutor
 import numpy as np
 
 from . import _lib
-from ._lib import call, geom, SweepParams, MSB_MAX_PLANES
+from ._lib import call, geom, SweepParams, MSB_FLIP_SLOTS, MSB_MAX_PLANES
 from .layout import (
     ALL_CODES, ArrayCode, LatticeDims, PackedArrays, check_spins, halo_audit_index, unpack,
 )
@@ -176,7 +176,10 @@ class Engine:
             self._spins = torch.empty(self._words_per_sim * self.n_sim, dtype=torch.int32, device=self.device)
             self._states = torch.empty(2 * 8 * n_pieces, dtype=torch.int32, device=self.device)
             self._thr = torch.zeros(MSB_MAX_PLANES * self.n_sim, dtype=torch.int32, device=self.device)
-            self._flips_dev = torch.zeros(1, dtype=torch.int64, device=self.device)
+            self._flips_dev = torch.zeros(MSB_FLIP_SLOTS, dtype=torch.int64, device=self.device)
+            pw = int(_lib.lib().msb_plane_words(ctypes.byref(self._g), MSB_MAX_PLANES))
+            self._plane_words = pw
+            self._planes = torch.empty(2 * pw, dtype=torch.int32, device=self.device)
             self._obs = torch.zeros(2 * self.n_sim, dtype=torch.int64, device=self.device)
         self._pow = _pow_tables(self.device)
         self._jump = _sweep_jump_table(self.device, dims.n)
@@ -186,6 +189,7 @@ class Engine:
         self._params.thr9 = self._thr.data_ptr()
         self._tab_key = None
         self.fault = 0  # test-only adder corruption (selftest seam, cli.py:467-480)
+        self.overlap = True  # run the next sweep's RNG concurrently with this sweep's flips
 
         if init == "random":
             with torch.cuda.stream(self._stream):
@@ -380,7 +384,8 @@ class Engine:
             if self.recorder is not None:
                 self._record(phase)
         call("msb_phase", ctypes.byref(self._g), ctypes.byref(self._params), phase, _p(self._spins),
-             _p(self._states), _p(ext) if ext is not None else None, _p(self._flips_dev), self._cs)
+             _p(self._states), _p(ext) if ext is not None else None, _p(self._planes), _p(self._flips_dev),
+             self._cs)
         if ext is not None:
             ext.record_stream(self._stream)
         else:
@@ -425,11 +430,32 @@ class Engine:
         self._sync_tables()
         self._params.fault = int(bool(self.fault))
         call("msb_sweep", ctypes.byref(self._g), ctypes.byref(self._params), _p(self._spins),
-             _p(self._states), k, _p(self._flips_dev), self._cs)
+             _p(self._states), _p(self._planes), k, int(self.overlap and k > 1), _p(self._flips_dev), self._cs)
         self._blocks += 2 * k
         self._pos = [self._blocks, self._blocks + 1]
         self.sweeps_done += k
         self.attempts += self.dims.sites * self.n_sim * k
+        self._touch()
+
+    def _timed_sweep(self, ev0, ev1, ev2) -> None:
+        """One sweep as its three kernels with CUDA events between them
+        (accept planes | red flips + blue flips); used by bench.py."""
+        if not self._fast_path_ok():
+            raise RuntimeError("timed sweeps need the engine's own sweep path")
+        self._push_host_edits()
+        self._sync_tables()
+        self._params.fault = int(bool(self.fault))
+        g, prm = ctypes.byref(self._g), ctypes.byref(self._params)
+        ev0.record(self._stream)
+        call("msb_rng_planes", g, prm, -1, _p(self._states), None, _p(self._planes), self._cs)
+        ev1.record(self._stream)
+        call("msb_flip", g, prm, 0, _p(self._spins), _p(self._planes), _p(self._flips_dev), self._cs)
+        call("msb_flip", g, prm, 1, _p(self._spins), _p(self._planes), _p(self._flips_dev), self._cs)
+        ev2.record(self._stream)
+        self._blocks += 2
+        self._pos = [self._blocks, self._blocks + 1]
+        self.sweeps_done += 1
+        self.attempts += self.dims.sites * self.n_sim
         self._touch()
 
     def synchronize(self) -> None:
@@ -439,12 +465,12 @@ class Engine:
     def flips(self) -> int:
         """Accepted flips so far (engine.py:331-332); synchronises the stream."""
         self._stream.synchronize()
-        return self._flips_base + int(self._flips_dev.item())
+        return self._flips_base + int(self._flips_dev.sum().item())
 
     @flips.setter
     def flips(self, value: int) -> None:
         self._stream.synchronize()
-        self._flips_base = int(value) - int(self._flips_dev.item())
+        self._flips_base = int(value) - int(self._flips_dev.sum().item())
 
     # -- observables (engine.py:364-397) ---------------------------------------
 
@@ -474,6 +500,61 @@ class Engine:
         self._stream.synchronize()
         bits = np.unpackbits(lin.cpu().numpy().view(np.uint8), bitorder="little")
         return np.where(bits == 1, 1, -1).astype(np.int8).reshape(hi - lo, d.m, d.n)
+
+    # -- host-buffer interop (bit-packed lattices) -----------------------------
+
+    def packed_nbytes(self) -> int:
+        """Bytes of all replicas' lattices as bit-packed linear sites."""
+        return self.n_sim * self.dims.sites // 8
+
+    def load_packed(self, src) -> None:
+        """Replace every replica's lattice from bit-packed host (or device)
+        memory: bit i%8 of byte i//8 of replica s is site i = c*n + r
+        (np.packbits(lattice > 0, bitorder="little")).  Pinned torch host
+        tensors are copied asynchronously on the engine's stream."""
+        torch = _torch()
+        self._push_host_edits()
+        if isinstance(src, np.ndarray):
+            src = torch.from_numpy(np.ascontiguousarray(src).view(np.uint8).reshape(-1))
+        if src.numel() * src.element_size() != self.packed_nbytes():
+            raise ValueError(f"expected {self.packed_nbytes()} bytes of packed lattices")
+        with torch.cuda.stream(self._stream):
+            if src.device.type != "cuda":
+                if not hasattr(self, "_lin_buf") or self._lin_buf.numel() != self.packed_nbytes() // 8:
+                    self._lin_buf = torch.empty(self.packed_nbytes() // 8, dtype=torch.int64, device=self.device)
+                self._lin_buf.view(torch.uint8).copy_(src.view(torch.uint8).reshape(-1), non_blocking=True)
+                dev = self._lin_buf
+            else:
+                dev = src
+        call("msb_from_linear", ctypes.byref(self._g), _p(dev), _p(self._spins), self._cs)
+        self._touch()
+
+    def store_packed(self, dst) -> None:
+        """Write every replica's lattice, bit-packed as in ``load_packed``,
+        into ``dst`` (pinned host tensor: asynchronous; call ``synchronize``)."""
+        torch = _torch()
+        self._push_host_edits()
+        if dst.numel() * dst.element_size() != self.packed_nbytes():
+            raise ValueError(f"expected {self.packed_nbytes()} bytes of packed lattices")
+        with torch.cuda.stream(self._stream):
+            if not hasattr(self, "_lin_buf") or self._lin_buf.numel() != self.packed_nbytes() // 8:
+                self._lin_buf = torch.empty(self.packed_nbytes() // 8, dtype=torch.int64, device=self.device)
+        call("msb_to_linear", ctypes.byref(self._g), _p(self._spins), _p(self._lin_buf), self._cs)
+        with torch.cuda.stream(self._stream):
+            dst.view(torch.uint8).reshape(-1).copy_(self._lin_buf.view(torch.uint8), non_blocking=True)
+
+    def observe_async(self, ups_out, unsat_out) -> None:
+        """Enqueue the integer observables (ups, unsatisfied bonds per replica)
+        into pinned host int64 tensors without synchronising."""
+        torch = _torch()
+        self._push_host_edits()
+        with torch.cuda.stream(self._stream):
+            self._obs.zero_()
+        call("msb_observe", ctypes.byref(self._g), _p(self._spins), _p(self._obs[: self.n_sim]),
+             _p(self._obs[self.n_sim:]), self._cs)
+        with torch.cuda.stream(self._stream):
+            ups_out.copy_(self._obs[: self.n_sim], non_blocking=True)
+            unsat_out.copy_(self._obs[self.n_sim:], non_blocking=True)
 
     def _observe(self):
         self._push_host_edits()
