@@ -66,7 +66,9 @@ typedef struct msb_sweep_params {
   int32_t kg;                    /* stream pieces per target row: 1,2,4,8 or 16 */
   const uint32_t *jump;          /* device: 32 KiB nibble table of A^(4n) */
   int32_t fault;                 /* test-only adder corruption (cli.py:467-480 analogue) */
-  int32_t block_rows;            /* 0 = automatic */
+  int32_t block_rows;            /* reserved, 0 */
+  uint32_t *work;                /* device: 2 uint32 scratch counters, zeroed once by the caller;
+                                    the accept-plane kernel leaves them zeroed */
 } msb_sweep_params;
 
 /* ---- status -------------------------------------------------------------- */

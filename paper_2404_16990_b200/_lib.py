@@ -50,6 +50,7 @@ class SweepParams(ctypes.Structure):
         ("jump", ctypes.c_void_p),
         ("fault", ctypes.c_int32),
         ("block_rows", ctypes.c_int32),
+        ("work", ctypes.c_void_p),
     ]
 
 

@@ -78,7 +78,10 @@ __device__ __forceinline__ uint32_t xstep(XState& s) {
   asm("{.reg .b32 t;\n\tadd.cc.u32 t, %1, %2;\n\taddc.u32 %0, %3, %4;}"
       : "=r"(o1)
       : "r"(r0), "r"(s.a0), "r"(r1), "r"(s.a1));
-  const uint32_t t0 = s.b0 << 17, t1 = __funnelshift_l(s.b0, s.b1, 17);
+  // t = s1 << 17 through IMAD.WIDE (FMA pipe): lo = b0 << 17, hi = b0 >> 15
+  uint64_t w17;
+  asm("mul.wide.u32 %0, %1, 131072;" : "=l"(w17) : "r"(s.b0));
+  const uint32_t t0 = (uint32_t)w17, t1 = s.b1 * 131072u + (uint32_t)(w17 >> 32);
   const uint32_t nc0 = xor3(s.c0, s.a0, t0), nc1 = xor3(s.c1, s.a1, t1);
   const uint32_t nd0 = s.d0 ^ s.b0, nd1 = s.d1 ^ s.b1;
   const uint32_t nb0 = xor3(s.b0, s.c0, s.a0), nb1 = xor3(s.b1, s.c1, s.a1);
@@ -176,8 +179,21 @@ __device__ __host__ __forceinline__ RowStream row_stream(int m, int c, int X) {
   return r;
 }
 
+// ---------------------------------------------------------------------------
+// device: the interleaved colour-split layout
+// ---------------------------------------------------------------------------
+//
+// Row (c, X) holds the n/2 sites of colour X (X = 0 red: (c+r) even), site
+// index i = r >> 1, split as i = 16 w + t (w < n/32, t < 16) -- exactly the
+// reference's packing of a column vector into uint16 words, word w bit t
+// (lattice.py:199-202).  Our uint32 word (ch, t) of the row holds bit t of
+// the reference words w = 32 ch + b, b = 0..31: a 32-way transpose of the
+// reference words, so the draws a stream consumes for one k (= one t, every
+// w in order, engine.py:321-330) accumulate straight into one word per
+// chunk.  Row pitch Wp = 16 * nch words, nch = ceil((n/32) / 32).
+
 struct Geo {
-  int n_sim, m, n, rows, row0, ghost, R, Wp, W, words, half;
+  int n_sim, m, n, rows, row0, ghost, R, Wp, words, nch;
   long long sim_offset;
 };
 
@@ -185,20 +201,20 @@ __host__ Geo make_geo(const msb_geom* g) {
   Geo o;
   o.n_sim = g->n_sim; o.m = g->m; o.n = g->n; o.rows = g->rows; o.row0 = g->row0; o.ghost = g->ghost;
   o.R = g->rows + 2 * g->ghost;
-  o.W = (g->n / 2 + 31) / 32;
-  o.Wp = (o.W + 3) & ~3;
   o.words = g->n / 32;
-  o.half = g->n / 2;
+  o.nch = (o.words + 31) / 32;
+  o.Wp = 16 * o.nch;
   o.sim_offset = g->sim_offset;
   return o;
 }
 
-__device__ __forceinline__ int valid_bits(const Geo& G, int j) {
-  const int b = G.half - 32 * j;
+// valid bits of chunk ch (w = 32 ch + b < n/32)
+__device__ __forceinline__ int chunk_bits(const Geo& G, int ch) {
+  const int b = G.words - 32 * ch;
   return b >= 32 ? 32 : b;
 }
-__device__ __forceinline__ uint32_t valid_mask(const Geo& G, int j) {
-  const int b = valid_bits(G, j);
+__device__ __forceinline__ uint32_t chunk_mask(const Geo& G, int ch) {
+  const int b = chunk_bits(G, ch);
   return b >= 32 ? 0xFFFFFFFFu : ((1u << b) - 1u);
 }
 __device__ __forceinline__ size_t row_off(const Geo& G, int s, int X, int br) {
@@ -214,20 +230,19 @@ __device__ __forceinline__ void vert_rows(const Geo& G, int br, int& bu, int& bd
   }
 }
 
-// The second horizontal neighbour word (r+1 when p=1, r-1 when p=0) of word
-// j in the other colour's row y (same lattice row), periodic in n/2.
-__device__ __forceinline__ uint32_t h_second(const Geo& G, const uint32_t* y, int j, int p, uint32_t yj) {
+// The second horizontal neighbour (site i+1 when p=1, i-1 when p=0, periodic
+// in n/2) of word (ch, t), read from the other colour's row y.  Interior t
+// just uses word t+-1; t = 15 / t = 0 wrap into the next / previous w.
+__device__ __forceinline__ uint32_t h_second(const Geo& G, const uint32_t* y, int ch, int t, int p) {
   if (p) {
-    const uint32_t nx = (j + 1 < G.W) ? y[j + 1] : y[0];
-    return (yj >> 1) | ((nx & 1u) << (valid_bits(G, j) - 1));
+    if (t < 15) return y[ch * 16 + t + 1];
+    const int chn = ch + 1 < G.nch ? ch + 1 : 0;
+    return (y[ch * 16] >> 1) | ((y[chn * 16] & 1u) << (chunk_bits(G, ch) - 1));
   }
-  uint32_t carry;
-  if (j > 0) {
-    carry = y[j - 1] >> 31;
-  } else {
-    carry = (y[G.W - 1] >> (valid_bits(G, G.W - 1) - 1)) & 1u;
-  }
-  return ((yj << 1) | carry) & valid_mask(G, j);
+  if (t > 0) return y[ch * 16 + t - 1];
+  const uint32_t carry = ch > 0 ? (y[(ch - 1) * 16 + 15] >> 31)
+                                : ((y[(G.nch - 1) * 16 + 15] >> (chunk_bits(G, G.nch - 1) - 1)) & 1u);
+  return ((y[ch * 16 + 15] << 1) | carry) & chunk_mask(G, ch);
 }
 
 // ---------------------------------------------------------------------------
@@ -237,11 +252,10 @@ __device__ __forceinline__ uint32_t h_second(const Geo& G, const uint32_t* y, in
 // The reference's draws never depend on the spins (engine.py:336-341 draws a
 // whole block before any flip), so a sweep splits into
 //   (1) k_rng_planes: every stream piece generates its draws and reduces each
-//       to NP accept bits (u23 < K_p), written as bit planes in the spins'
-//       colour-split layout: planes[X][p][s][lr][Pp];
+//       to NP accept bits (u23 < K_p), accumulated per (k, chunk) straight
+//       into planes[X][p][s][lr][ch*16 + t(k)] (same layout as the spins);
 //   (2) k_flip (per colour): bit-sliced neighbour classes select the plane.
-// (1) is INT-pipe bound and state independent, so it can run a sweep ahead
-// of (2), which is a light memory-bound pass over L2/HBM.
+// (1) is INT-pipe bound and state independent; (2) is a light pass over L2.
 
 struct RngArgs {
   Geo G;
@@ -250,154 +264,146 @@ struct RngArgs {
   const uint4* jump;
   const uint32_t* ext;
   uint32_t* planes;
+  unsigned* work;
   long long npieces;
-  int colour0, kg, kr, np, nch, block_rows, rs, Pp;
+  int colour0, ncol, kg, kr, np;
 };
-
-// 32x32 bit-matrix transpose in registers, LSB-first: on exit bit i of a[c]
-// is what bit c of a[i] was.  Five delta-swap stages.
-template <int J>
-__device__ __forceinline__ void transpose_stage(uint32_t a[32], uint32_t m) {
-#pragma unroll
-  for (int k = 0; k < 32; k++) {
-    if ((k & J) == 0) {
-      const uint32_t t = ((a[k] >> J) ^ a[k + J]) & m;
-      a[k + J] ^= t;
-      a[k] ^= t << J;
-    }
-  }
-}
-__device__ __forceinline__ void transpose32(uint32_t a[32]) {
-  transpose_stage<16>(a, 0x0000FFFFu);
-  transpose_stage<8>(a, 0x00FF00FFu);
-  transpose_stage<4>(a, 0x0F0F0F0Fu);
-  transpose_stage<2>(a, 0x33333333u);
-  transpose_stage<1>(a, 0x55555555u);
-}
 
 // reference bit t of a uint16 word is gated by draw k = 4(t%4) + t/4 (the
 // mapping is its own inverse, engine.py:326-330)
-__device__ __forceinline__ int k_of_t(int t) { return 4 * (t & 3) + (t >> 2); }
+__device__ __forceinline__ int t_of_k(int k) { return 4 * (k & 3) + (k >> 2); }
 
-__device__ __forceinline__ size_t plane_off(const Geo& G, int Pp, int np, int X, int p, int s, int lr) {
-  return ((((size_t)X * np + p) * G.n_sim + s) * G.rows + lr) * Pp;
+__device__ __forceinline__ size_t plane_off(const Geo& G, int np, int X, int p, int s, int lr) {
+  return ((((size_t)X * np + p) * G.n_sim + s) * G.rows + lr) * G.Wp;
 }
 
-// grid: (row blocks, colours).  Block = block_rows target rows x kg pieces.
-template <int NPMAX, bool EXT, bool JSMEM>
-__global__ void __launch_bounds__(256) k_rng_planes(const RngArgs a) {
-  extern __shared__ uint4 smem4[];
-  uint32_t* buf = reinterpret_cast<uint32_t*>(JSMEM ? smem4 + kJumpWords / 4 : smem4);
-  const uint4* jt = JSMEM ? smem4 : a.jump;
-  if (JSMEM && !EXT) {
-    for (int i = threadIdx.x; i < kJumpWords / 4; i += blockDim.x) smem4[i] = a.jump[i];
+// Persistent kernel: one 1024-thread CTA per SM shares one copy of the
+// sweep-jump table in shared memory; warps claim 32 consecutive pieces at a
+// time from a self-resetting counter (work[0] = next unit, work[1] = warps
+// done), so SMs stay balanced whatever the piece count.  Each lane runs one
+// piece: it generates the piece's draws (k-range x all w) and, spread through
+// the generation loop, performs the 64 nibble lookups of its jump to the
+// next sweep, so table reads overlap other warps' ALU work.
+constexpr int kRngThreads = 1024;
+
+template <int NPMAX, bool EXT>
+__global__ void __launch_bounds__(kRngThreads, 1) k_rng_planes(const RngArgs a) {
+  extern __shared__ uint4 jt[];  // nibble table of A^(4n), 32 KiB
+  const Geo& G = a.G;
+  const int np = NPMAX == 2 ? 2 : a.np;
+  const int lane = threadIdx.x & 31;
+  if (!EXT) {
+    for (int i = threadIdx.x; i < kJumpWords / 4; i += blockDim.x) jt[i] = a.jump[i];
     __syncthreads();
   }
-  const Geo& G = a.G;
-  const int tid = threadIdx.x;
-  const int X = a.colour0 + blockIdx.y;
-  const int np = NPMAX == 2 ? 2 : a.np;
-  const long long total_rows = (long long)G.n_sim * G.rows;
-
-  // ---- stage 1: each thread generates its piece of the stream -------------
-  {
-    const int rl = tid / a.kg, kgi = tid % a.kg;
-    const long long gr = (long long)blockIdx.x * a.block_rows + rl;
-    if (rl < a.block_rows && gr < total_rows) {
-      const int s = (int)(gr / G.rows), lr = (int)(gr % G.rows);
-      const int c = G.row0 + lr;
-      const long long gp = gr * a.kg + kgi;
-      uint32_t key[NPMAX];
+  const long long total = a.npieces * a.ncol;
+  const long long units = (total + 31) / 32;
+  const size_t pstride = (size_t)G.n_sim * G.rows * G.Wp;
+  const int lk = 64 / a.kr;  // jump lookups per k-segment (multiple of 4)
+  // first unit: static, interleaved across SMs (unit w*gridDim + cta) so every
+  // SM gets an equal share of the first round; later units: dynamic
+  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+  long long u = (long long)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+  for (;; ) {
+    if (u >= units) break;
+    const long long gi = u * 32 + lane;
+    if (gi < total) {
+    const int X = a.colour0 + (int)(gi / a.npieces);
+    const long long gp = gi - (gi / a.npieces) * a.npieces;
+    const long long gr = gp / a.kg;
+    const int kgi = (int)(gp - gr * a.kg);
+    const int s = (int)(gr / G.rows), lr = (int)(gr - (long long)s * G.rows);
+    uint32_t key[NPMAX];
 #pragma unroll
-      for (int p = 0; p < NPMAX; p++) key[p] = p < np ? a.thr9[p * G.n_sim + s] : 0u;
-      uint32_t* out = buf + rl * a.rs;
-      const int k0 = kgi * a.kr;
-      XState st;
-      uint32_t* sp = a.states + (size_t)X * 8 * a.npieces;
-      const uint32_t* ext = nullptr;
-      if (!EXT) {
-        load_state(st, sp, a.npieces, gp);
-        store_state(jump_apply(st, jt), sp, a.npieces, gp);  // next sweep's start
-      } else {
-        const RowStream rsd = row_stream(G.m, c, X);
-        ext = a.ext + ((((size_t)s * (G.m / 4) + rsd.gamma - 1) * 4 + rsd.q) * 16) * G.words;
-      }
-      for (int kk = 0; kk < a.kr; kk++) {
-        const int k = k0 + kk;
-        for (int ch = 0; ch < a.nch; ch++) {
-          const int L = min(32, G.words - 32 * ch);
-          uint32_t acc[NPMAX];
+    for (int p = 0; p < NPMAX; p++) key[p] = p < np ? a.thr9[p * G.n_sim + s] : 0u;
+    uint32_t* out = a.planes + plane_off(G, np, X, 0, s, lr);
+    XState st;
+    const uint32_t* ext = nullptr;
+    uint32_t* sp = a.states + (size_t)X * 8 * a.npieces;
+    // jump bookkeeping: the piece's start state, consumed 4 bits at a time
+    uint32_t jw0 = 0, jw1 = 0, jw2 = 0, jw3 = 0, jw4 = 0, jw5 = 0, jw6 = 0, jw7 = 0;
+    uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0, r4 = 0, r5 = 0, r6 = 0, r7 = 0;
+    int nib = 0;
+    if (!EXT) {
+      load_state(st, sp, a.npieces, gp);
+      jw0 = st.a0; jw1 = st.a1; jw2 = st.b0; jw3 = st.b1; jw4 = st.c0; jw5 = st.c1; jw6 = st.d0; jw7 = st.d1;
+    } else {
+      const RowStream rsd = row_stream(G.m, G.row0 + lr, X);
+      ext = a.ext + ((((size_t)s * (G.m / 4) + rsd.gamma - 1) * 4 + rsd.q) * 16) * G.words;
+    }
+    for (int kk = 0; kk < a.kr; kk++) {
+      const int k = kgi * a.kr + kk;
+      const int t = t_of_k(k);
+      for (int ch = 0; ch < G.nch; ch++) {
+        const int L = chunk_bits(G, ch);
+        uint32_t acc[NPMAX];
 #pragma unroll
-          for (int p = 0; p < NPMAX; p++) acc[p] = 0;
-          if (!EXT) {
-            if (L == 32) {
+        for (int p = 0; p < NPMAX; p++) acc[p] = 0;
+        if (!EXT) {
+          if (L == 32) {
 #pragma unroll 8
-              for (int i = 0; i < 32; i++) {
-                const uint32_t h9 = xstep(st) << 9;
+            for (int i = 0; i < 32; i++) {
+              const uint32_t h9 = xstep(st) << 9;
 #pragma unroll
-                for (int p = 0; p < NPMAX; p++)
-                  if (p < np) acc_reject(acc[p], h9, key[p]);
-              }
-            } else {
-              for (int i = 0; i < L; i++) {
-                const uint32_t h9 = xstep(st) << 9;
-#pragma unroll
-                for (int p = 0; p < NPMAX; p++)
-                  if (p < np) acc_reject(acc[p], h9, key[p]);
-              }
+              for (int p = 0; p < NPMAX; p++)
+                if (p < np) acc_reject(acc[p], h9, key[p]);
             }
           } else {
-            const uint32_t* e = ext + (size_t)k * G.words + 32 * ch;
             for (int i = 0; i < L; i++) {
-              const uint32_t h9 = e[i] << 9;
+              const uint32_t h9 = xstep(st) << 9;
 #pragma unroll
               for (int p = 0; p < NPMAX; p++)
                 if (p < np) acc_reject(acc[p], h9, key[p]);
             }
           }
+        } else {
+          const uint32_t* e = ext + (size_t)k * G.words + 32 * ch;
+          for (int i = 0; i < L; i++) {
+            const uint32_t h9 = e[i] << 9;
 #pragma unroll
-          for (int p = 0; p < NPMAX; p++)
-            if (p < np) out[(p * 16 + k) * a.nch + ch] = (~__brev(acc[p])) >> (32 - L);
+            for (int p = 0; p < NPMAX; p++)
+              if (p < np) acc_reject(acc[p], h9, key[p]);
+          }
+        }
+        // acc holds REJECT bits, newest draw in bit 0: reverse and invert
+#pragma unroll
+        for (int p = 0; p < NPMAX; p++)
+          if (p < np) out[p * pstride + ch * 16 + t] = (~__brev(acc[p])) >> (32 - L);
+      }
+      // jump lookups: 64/KR per k-segment, one 32-bit state word (8 nibbles)
+      // at a time, XORs paired into 3-input LOP3s
+      if (!EXT && ((kk + 1) * lk) % 8 == 0) {
+        for (int wcount = (kk + 1) * lk / 8 - nib / 8; wcount > 0; wcount--) {
+          const uint4* e = jt + nib * 32;
+#pragma unroll
+          for (int j = 0; j < 8; j += 2) {
+            const uint4* ea = e + j * 32 + ((jw0 >> (4 * j)) & 15u) * 2;
+            const uint4* eb = e + (j + 1) * 32 + ((jw0 >> (4 * j + 4)) & 15u) * 2;
+            const uint4 la = ea[0], ha = ea[1], lb = eb[0], hb = eb[1];
+            r0 = xor3(r0, la.x, lb.x); r1 = xor3(r1, la.y, lb.y); r2 = xor3(r2, la.z, lb.z); r3 = xor3(r3, la.w, lb.w);
+            r4 = xor3(r4, ha.x, hb.x); r5 = xor3(r5, ha.y, hb.y); r6 = xor3(r6, ha.z, hb.z); r7 = xor3(r7, ha.w, hb.w);
+          }
+          nib += 8;
+          jw0 = jw1; jw1 = jw2; jw2 = jw3; jw3 = jw4; jw4 = jw5; jw5 = jw6; jw6 = jw7;
         }
       }
     }
+    if (!EXT) {
+      XState nx;
+      nx.a0 = r0; nx.a1 = r1; nx.b0 = r2; nx.b1 = r3; nx.c0 = r4; nx.c1 = r5; nx.d0 = r6; nx.d1 = r7;
+      store_state(nx, sp, a.npieces, gp);  // next sweep's start
+    }
+    }
+    long long nu = 0;
+    if (lane == 0) nu = nwarps + (long long)atomicAdd(a.work, 1u);
+    u = __shfl_sync(0xFFFFFFFFu, nu, 0);
   }
-  __syncthreads();
-
-  // ---- stage 2: transpose (k, w) bit matrices into row words --------------
-  const int units = a.block_rows * a.nch;
-  for (int u = tid; u < units; u += blockDim.x) {
-    const int rl = u / a.nch, ch = u % a.nch;
-    const long long gr = (long long)blockIdx.x * a.block_rows + rl;
-    if (gr >= total_rows) continue;
-    const int s = (int)(gr / G.rows), lr = (int)(gr % G.rows);
-    const uint32_t* bp = buf + rl * a.rs;
-#pragma unroll
-    for (int pp = 0; pp < NPMAX; pp += 2) {
-      if (pp >= np) break;
-      uint32_t m32[32];
-#pragma unroll
-      for (int t = 0; t < 16; t++) {
-        m32[t] = bp[(pp * 16 + k_of_t(t)) * a.nch + ch];
-        m32[16 + t] = pp + 1 < np ? bp[((pp + 1) * 16 + k_of_t(t)) * a.nch + ch] : 0u;
-      }
-      transpose32(m32);  // m32[w'] : bits 0-15 plane pp (bit t), 16-31 plane pp+1
-      uint4* o0 = reinterpret_cast<uint4*>(a.planes + plane_off(G, a.Pp, np, X, pp, s, lr) + 16 * ch);
-#pragma unroll
-      for (int q = 0; q < 4; q++)
-        o0[q] = make_uint4(__byte_perm(m32[8 * q + 0], m32[8 * q + 1], 0x5410),
-                           __byte_perm(m32[8 * q + 2], m32[8 * q + 3], 0x5410),
-                           __byte_perm(m32[8 * q + 4], m32[8 * q + 5], 0x5410),
-                           __byte_perm(m32[8 * q + 6], m32[8 * q + 7], 0x5410));
-      if (pp + 1 < np) {
-        uint4* o1 = reinterpret_cast<uint4*>(a.planes + plane_off(G, a.Pp, np, X, pp + 1, s, lr) + 16 * ch);
-#pragma unroll
-        for (int q = 0; q < 4; q++)
-          o1[q] = make_uint4(__byte_perm(m32[8 * q + 0], m32[8 * q + 1], 0x7632),
-                             __byte_perm(m32[8 * q + 2], m32[8 * q + 3], 0x7632),
-                             __byte_perm(m32[8 * q + 4], m32[8 * q + 5], 0x7632),
-                             __byte_perm(m32[8 * q + 6], m32[8 * q + 7], 0x7632));
-      }
+  // self-reset of the work counter by the last warp to finish claiming
+  if (lane == 0) {
+    const unsigned warps = gridDim.x * (blockDim.x >> 5);
+    if (atomicAdd(a.work + 1, 1u) == warps - 1) {
+      atomicExch(a.work, 0u);
+      atomicExch(a.work + 1, 0u);
     }
   }
 }
@@ -411,7 +417,7 @@ struct FlipArgs {
   uint32_t* spins;
   const uint32_t* planes;
   unsigned long long* flips;
-  int X, np, Pp;
+  int X, np;
   uint32_t inv;
   int fault;
   int8_t code_plane[16];
@@ -419,59 +425,92 @@ struct FlipArgs {
 
 constexpr int kFlipSlots = 256;
 
-// Thread per (replica, held row, word): neighbours are the other colour's
-// rows c-1, c+1 (same word) and row c at words j, j+-1 (include/msb200.h).
+__device__ __forceinline__ uint32_t flip_word(const FlipArgs& a, bool generic, uint32_t o, uint32_t n1, uint32_t n2,
+                                              uint32_t y0, uint32_t n4, const uint32_t* pl, size_t pstride,
+                                              uint32_t A4, uint32_t A8) {
+  if (!generic) {
+    const uint32_t ow = o ^ a.inv;
+    const uint32_t x1 = n1 ^ ow, x2 = n2 ^ ow, x3 = y0 ^ ow;
+    const uint32_t x4 = a.fault ? 0u : (n4 ^ ow);
+    const uint32_t o12 = x1 | x2, a12 = x1 & x2, o34 = x3 | x4, a34 = x3 & x4;
+    const uint32_t ge2 = a12 | a34 | (o12 & o34);  // >= 2 disagreeing neighbours
+    const uint32_t any = o12 | o34;
+    return ge2 | (any & ~ge2 & A4) | (~any & A8);
+  }
+  // neighbour up-count bit planes (bitkernels.py:63-79 restated)
+  const uint32_t s1 = n1 ^ n2, c1 = n1 & n2, s2 = y0 ^ n4, c2 = y0 & n4;
+  uint32_t ones = s1 ^ s2;
+  const uint32_t twos = c1 ^ c2 ^ (s1 & s2), fours = c1 & c2;
+  if (a.fault) ones = s1;
+  uint32_t flip = 0;
+  for (int code = 0; code < 16; code++) {
+    const int pidx = a.code_plane[code];
+    const int u = code & 7;
+    if (pidx == -1 || u > 4) continue;
+    const uint32_t msk = ((code & 8) ? o : ~o) & ((u & 1) ? ones : ~ones) & ((u & 2) ? twos : ~twos) &
+                         ((u & 4) ? fours : ~fours);
+    flip |= pidx == -2 ? msk : (msk & __ldg(pl + pidx * pstride));
+  }
+  return flip;
+}
+
+// Thread per (replica, held row, chunk, quad of 4 t-words).  Vertical
+// neighbours are the other colour's rows c-1, c+1 (same word); horizontal
+// ones are the other colour's row c at sites i and i+-1 (h_second).
 template <bool GENERIC>
 __global__ void __launch_bounds__(256) k_flip(const FlipArgs a) {
   const Geo& G = a.G;
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long total = (long long)G.n_sim * G.rows * G.W;
+  const unsigned quads = (unsigned)G.Wp >> 2;
+  const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned total = (unsigned)G.n_sim * (unsigned)G.rows * quads;
   unsigned cnt = 0;
   if (i < total) {
-    const int j = (int)(i % G.W);
-    const long long gr = i / G.W;
-    const int s = (int)(gr / G.rows), lr = (int)(gr % G.rows);
+    const unsigned gr = i / quads, qq = i - gr * quads;
+    const int s = (int)(gr / (unsigned)G.rows), lr = (int)(gr - (unsigned)s * G.rows);
     const int X = a.X, c = G.row0 + lr, br = lr + G.ghost;
+    const int ch = (int)(qq >> 2), t0 = 4 * (int)(qq & 3);
+    const int w0 = ch * 16 + t0;
     int bu, bd;
     vert_rows(G, br, bu, bd);
     uint32_t* own = a.spins + row_off(G, s, X, br);
     const uint32_t* yc = a.spins + row_off(G, s, 1 - X, br);
-    const uint32_t o = own[j];
-    const uint32_t y0 = __ldg(yc + j);
-    const uint32_t n1 = __ldg(a.spins + row_off(G, s, 1 - X, bu) + j);
-    const uint32_t n2 = __ldg(a.spins + row_off(G, s, 1 - X, bd) + j);
-    const uint32_t n4 = h_second(G, yc, j, (c + X) & 1, y0);
-    const uint32_t* pl = a.planes + plane_off(G, a.Pp, a.np, X, 0, s, lr) + j;
-    const size_t pstride = (size_t)G.n_sim * G.rows * a.Pp;
-    uint32_t flip;
+    const uint4 O = *reinterpret_cast<const uint4*>(own + w0);
+    const uint4 Y = __ldg(reinterpret_cast<const uint4*>(yc + w0));
+    const uint4 U = __ldg(reinterpret_cast<const uint4*>(a.spins + row_off(G, s, 1 - X, bu) + w0));
+    const uint4 D = __ldg(reinterpret_cast<const uint4*>(a.spins + row_off(G, s, 1 - X, bd) + w0));
+    const size_t pstride = (size_t)G.n_sim * G.rows * G.Wp;
+    const uint32_t* pl = a.planes + plane_off(G, a.np, X, 0, s, lr) + w0;
+    uint4 P4 = make_uint4(0, 0, 0, 0), P8 = make_uint4(0, 0, 0, 0);
     if (!GENERIC) {
-      const uint32_t A4 = __ldg(pl), A8 = __ldg(pl + pstride);
-      const uint32_t ow = o ^ a.inv;
-      const uint32_t x1 = n1 ^ ow, x2 = n2 ^ ow, x3 = y0 ^ ow;
-      const uint32_t x4 = a.fault ? 0u : (n4 ^ ow);
-      const uint32_t o12 = x1 | x2, a12 = x1 & x2, o34 = x3 | x4, a34 = x3 & x4;
-      const uint32_t ge2 = a12 | a34 | (o12 & o34);  // >= 2 disagreeing neighbours
-      const uint32_t any = o12 | o34;
-      flip = ge2 | (any & ~ge2 & A4) | (~any & A8);
-    } else {
-      // neighbour up-count bit planes (bitkernels.py:63-79 restated)
-      const uint32_t s1 = n1 ^ n2, c1 = n1 & n2, s2 = y0 ^ n4, c2 = y0 & n4;
-      uint32_t ones = s1 ^ s2;
-      const uint32_t twos = c1 ^ c2 ^ (s1 & s2), fours = c1 & c2;
-      if (a.fault) ones = s1;
-      flip = 0;
-      for (int code = 0; code < 16; code++) {
-        const int pidx = a.code_plane[code];
-        const int u = code & 7;
-        if (pidx == -1 || u > 4) continue;
-        const uint32_t msk = ((code & 8) ? o : ~o) & ((u & 1) ? ones : ~ones) & ((u & 2) ? twos : ~twos) &
-                             ((u & 4) ? fours : ~fours);
-        flip |= pidx == -2 ? msk : (msk & __ldg(pl + pidx * pstride));
-      }
+      P4 = __ldg(reinterpret_cast<const uint4*>(pl));
+      P8 = __ldg(reinterpret_cast<const uint4*>(pl + pstride));
     }
-    flip &= valid_mask(G, j);
-    own[j] = o ^ flip;
-    cnt = __popc(flip);
+    const int p = (c + X) & 1;
+    const uint32_t y[4] = {Y.x, Y.y, Y.z, Y.w};
+    const uint32_t o[4] = {O.x, O.y, O.z, O.w};
+    const uint32_t u4[4] = {U.x, U.y, U.z, U.w};
+    const uint32_t d4[4] = {D.x, D.y, D.z, D.w};
+    const uint32_t a4[4] = {P4.x, P4.y, P4.z, P4.w};
+    const uint32_t a8[4] = {P8.x, P8.y, P8.z, P8.w};
+    // the one neighbour word outside the quad (t0+4 if p, t0-1 otherwise);
+    // the t = 15 / t = 0 wrap cases go through h_second
+    uint32_t edge = 0;
+    if (p && t0 + 4 < 16) edge = __ldg(yc + w0 + 4);
+    if (!p && t0 > 0) edge = __ldg(yc + w0 - 1);
+    const uint32_t vm = chunk_mask(G, ch);
+    uint32_t res[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const int t = t0 + k;
+      uint32_t n4;
+      if (p) n4 = k < 3 ? y[k + 1] : (t < 15 ? edge : h_second(G, yc, ch, 15, 1));
+      else n4 = k > 0 ? y[k - 1] : (t > 0 ? edge : h_second(G, yc, ch, 0, 0));
+      uint32_t f = flip_word(a, GENERIC, o[k], u4[k], d4[k], y[k], n4, pl + k, pstride, a4[k], a8[k]);
+      f &= vm;
+      res[k] = o[k] ^ f;
+      cnt += __popc(f);
+    }
+    *reinterpret_cast<uint4*>(own + w0) = make_uint4(res[0], res[1], res[2], res[3]);
   }
   // block reduction, one atomic per block into one of kFlipSlots counters
   __shared__ unsigned red[8];
@@ -479,9 +518,9 @@ __global__ void __launch_bounds__(256) k_flip(const FlipArgs a) {
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;
   __syncthreads();
   if (threadIdx.x == 0) {
-    unsigned long long t = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += red[w];
-    if (t) atomicAdd(a.flips + (blockIdx.x % kFlipSlots), t);
+    unsigned long long tot = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) tot += red[w];
+    if (tot) atomicAdd(a.flips + (blockIdx.x % kFlipSlots), tot);
   }
 }
 
@@ -540,77 +579,46 @@ __global__ void k_init_linear(Geo G, uint64_t seed, long long words_per_sim, con
   }
 }
 
-__device__ __forceinline__ uint32_t even_bits(uint64_t x) {
-  x &= 0x5555555555555555ULL;
-  x = (x | (x >> 1)) & 0x3333333333333333ULL;
-  x = (x | (x >> 2)) & 0x0F0F0F0F0F0F0F0FULL;
-  x = (x | (x >> 4)) & 0x00FF00FF00FF00FFULL;
-  x = (x | (x >> 8)) & 0x0000FFFF0000FFFFULL;
-  x = (x | (x >> 16)) & 0x00000000FFFFFFFFULL;
-  return (uint32_t)x;
-}
-__device__ __forceinline__ uint64_t spread_bits(uint32_t v) {  // bit b -> bit 2b
-  uint64_t x = v;
-  x = (x | (x << 16)) & 0x0000FFFF0000FFFFULL;
-  x = (x | (x << 8)) & 0x00FF00FF00FF00FFULL;
-  x = (x | (x << 4)) & 0x0F0F0F0F0F0F0F0FULL;
-  x = (x | (x << 2)) & 0x3333333333333333ULL;
-  x = (x | (x << 1)) & 0x5555555555555555ULL;
-  return x;
-}
-
-// Thread per (s, held row lr, word j < Wp): both colours' word j from the
-// 64 sites r in [64j, 64j+64) of the row (clipped at n).
-__global__ void k_from_linear(Geo G, const unsigned long long* __restrict__ lin, uint32_t* spins) {
+// Thread per (s, held row lr, word (ch, t)): both colours' word from the
+// linear row, read as uint32 words (linear bit i -> bit i%32 of word i/32).
+// Sites of word (ch, t): r = 32 w + 2 t + {0, 1}, w = 32 ch + b; the even r
+// belongs to colour c&1, the odd one to (c+1)&1.
+__global__ void k_from_linear(Geo G, const uint32_t* __restrict__ lin, uint32_t* spins) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long total = (long long)G.n_sim * G.rows * G.Wp;
   if (i >= total) return;
-  const int j = (int)(i % G.Wp);
+  const int wd = (int)(i % G.Wp);
   const long long gr = i / G.Wp;
   const int s = (int)(gr / G.rows), lr = (int)(gr % G.rows);
   const int c = G.row0 + lr, br = lr + G.ghost;
+  const int ch = wd >> 4, t = wd & 15;
+  const uint32_t* L = lin + ((size_t)s * G.rows + lr) * (G.n / 32) + 32 * ch;
+  const int nb = chunk_bits(G, ch);
   uint32_t e = 0, od = 0;
-  if (j < G.W) {
-    const long long words_per_sim = (long long)G.rows * G.n / 64;
-    const unsigned long long* L = lin + (size_t)s * words_per_sim;
-    const long long bit0 = (long long)lr * G.n + 64LL * j;
-    const int nsite = min(64, G.n - 64 * j);
-    uint64_t v;
-    if ((bit0 & 63) == 0) {
-      v = L[bit0 >> 6];
-    } else {  // starts at bit 32 of a linear word
-      const uint64_t lo = L[bit0 >> 6] >> 32;
-      const uint64_t hi = nsite > 32 ? L[(bit0 >> 6) + 1] << 32 : 0ULL;
-      v = lo | hi;
-    }
-    if (nsite < 64) v &= (1ULL << nsite) - 1;
-    e = even_bits(v);
-    od = even_bits(v >> 1);
+  for (int b = 0; b < nb; b++) {
+    const uint32_t v = L[b] >> (2 * t);
+    e |= (v & 1u) << b;
+    od |= ((v >> 1) & 1u) << b;
   }
-  // even r -> colour c&1, odd r -> colour (c+1)&1
-  spins[row_off(G, s, c & 1, br) + j] = e;
-  spins[row_off(G, s, (c + 1) & 1, br) + j] = od;
+  spins[row_off(G, s, c & 1, br) + wd] = e;
+  spins[row_off(G, s, (c + 1) & 1, br) + wd] = od;
 }
 
-// Thread per linear word o of a replica.
-__global__ void k_to_linear(Geo G, const uint32_t* __restrict__ spins, unsigned long long* lin) {
-  const long long words_per_sim = (long long)G.rows * G.n / 64;
+// Thread per linear uint32 word (s, lr, w): sites r = 32 w .. 32 w + 31.
+__global__ void k_to_linear(Geo G, const uint32_t* __restrict__ spins, uint32_t* lin) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= words_per_sim * G.n_sim) return;
-  const int s = (int)(i / words_per_sim);
-  const long long o = i % words_per_sim;
-  uint64_t v = 0;
+  const long long total = (long long)G.n_sim * G.rows * G.words;
+  if (i >= total) return;
+  const int w = (int)(i % G.words);
+  const long long gr = i / G.words;
+  const int s = (int)(gr / G.rows), lr = (int)(gr % G.rows);
+  const int c = G.row0 + lr, br = lr + G.ghost;
+  const int ch = w >> 5, b = w & 31;
+  const uint32_t* E = spins + row_off(G, s, c & 1, br) + ch * 16;
+  const uint32_t* Od = spins + row_off(G, s, (c + 1) & 1, br) + ch * 16;
+  uint32_t v = 0;
 #pragma unroll
-  for (int hh = 0; hh < 2; hh++) {
-    const long long site = o * 64 + 32 * hh;
-    const int lr = (int)(site / G.n), r0 = (int)(site % G.n);
-    const int c = G.row0 + lr, br = lr + G.ghost;
-    const int j = r0 / 64, sh = (r0 % 64) / 2;  // 0 or 16
-    const uint32_t e = (spins[row_off(G, s, c & 1, br) + j] >> sh) & 0xFFFFu;
-    const uint32_t od = (spins[row_off(G, s, (c + 1) & 1, br) + j] >> sh) & 0xFFFFu;
-    const uint64_t w = spread_bits(e) | (spread_bits(od) << 1);  // 32 sites
-    v |= (w & 0xFFFFFFFFULL) << (32 * hh);
-  }
+  for (int t = 0; t < 16; t++) v |= (((E[t] >> b) & 1u) << (2 * t)) | (((Od[t] >> b) & 1u) << (2 * t + 1));
   lin[i] = v;
 }
 
@@ -618,10 +626,10 @@ __global__ void k_init_const(Geo G, uint32_t up, uint32_t* spins) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long total = (long long)G.n_sim * 2 * G.R * G.Wp;
   if (i >= total) return;
-  const int j = (int)(i % G.Wp);
+  const int wd = (int)(i % G.Wp);
   const int br = (int)((i / G.Wp) % G.R);
   const bool ghost_row = G.ghost && (br == 0 || br == G.R - 1);
-  spins[i] = (up && j < G.W && !ghost_row) ? valid_mask(G, j) : 0u;
+  spins[i] = (up && !ghost_row) ? chunk_mask(G, wd >> 4) : 0u;
 }
 
 // Canonical source of a state element (lattice.py:283-329), evaluated per
@@ -657,9 +665,12 @@ __global__ void k_to_ref16(Geo G, const uint32_t* __restrict__ spins, uint16_t* 
     const int p0 = even ? 0 : 1, cpar = red ? p0 : 1 - p0;
     const int c = fwd ? 2 * (g - 1) + cpar : G.m - 2 * g + cpar;  // lattice.py:190-196
     const int X = red ? 0 : 1;
-    const int w0 = e - 1;
-    const uint32_t word = spins[row_off(G, s, X, c) + w0 / 2];
-    val = (uint16_t)((word >> (16 * (w0 & 1))) & 0xFFFFu);
+    const int w = e - 1;
+    const uint32_t* row = spins + row_off(G, s, X, c) + (w >> 5) * 16;
+    uint32_t v = 0;
+#pragma unroll
+    for (int t = 0; t < 16; t++) v |= ((row[t] >> (w & 31)) & 1u) << t;
+    val = (uint16_t)v;
   }
   state[i] = val;
 }
@@ -670,19 +681,18 @@ __global__ void k_from_ref16(Geo G, const uint16_t* __restrict__ state, uint32_t
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long total = (long long)G.n_sim * 2 * G.m * G.Wp;
   if (i >= total) return;
-  const int j = (int)(i % G.Wp);
+  const int wd = (int)(i % G.Wp);
   const int c = (int)((i / G.Wp) % G.m);
   const int X = (int)((i / ((long long)G.Wp * G.m)) % 2);
   const int s = (int)(i / (2LL * G.Wp * G.m));
+  const int ch = wd >> 4, t = wd & 15;
+  const RowStream rs = row_stream(G.m, c, X);
+  const int a = 4 * X + rs.q;
+  const uint16_t* col = state + (((size_t)s * 8 + a) * cols + rs.gamma) * vec + 1 + 32 * ch;
+  const int nb = chunk_bits(G, ch);
   uint32_t v = 0;
-  if (j < G.W) {
-    const RowStream rs = row_stream(G.m, c, X);
-    const int a = 4 * X + rs.q;
-    const uint16_t* col = state + (((size_t)s * 8 + a) * cols + rs.gamma) * vec;
-    v = col[2 * j + 1];
-    if (2 * j + 2 <= words) v |= (uint32_t)col[2 * j + 2] << 16;
-  }
-  spins[row_off(G, s, X, c) + j] = v;
+  for (int b = 0; b < nb; b++) v |= ((uint32_t)(col[b] >> t) & 1u) << b;
+  spins[row_off(G, s, X, c) + wd] = v;
 }
 
 // ---------------------------------------------------------------------------
@@ -705,12 +715,15 @@ __global__ void k_observe(Geo G, const uint32_t* __restrict__ spins, long long* 
     const uint32_t* blu = spins + row_off(G, s, 1, br);
     const uint32_t* yu = spins + row_off(G, s, 1, bu);
     const uint32_t* yd = spins + row_off(G, s, 1, bd);
-    for (int j = 0; j < G.W; j++) {
-      const uint32_t o = red[j], y0 = blu[j];
-      const uint32_t vm = valid_mask(G, j);
-      u += __popc(o) + __popc(y0);
-      b += __popc((o ^ yu[j]) & vm) + __popc((o ^ yd[j]) & vm) + __popc((o ^ y0) & vm) +
-           __popc((o ^ h_second(G, blu, j, p, y0)) & vm);
+    for (int ch = 0; ch < G.nch; ch++) {
+      const uint32_t vm = chunk_mask(G, ch);
+      for (int t = 0; t < 16; t++) {
+        const int wd = ch * 16 + t;
+        const uint32_t o = red[wd], y0 = blu[wd];
+        u += __popc(o) + __popc(y0);
+        b += __popc((o ^ yu[wd]) & vm) + __popc((o ^ yd[wd]) & vm) + __popc((o ^ y0) & vm) +
+             __popc((o ^ h_second(G, blu, ch, t, p)) & vm);
+      }
     }
   }
   // segmented warp reduction by replica
@@ -758,6 +771,8 @@ __global__ void k_unpack_ghosts(Geo G, int X, const uint32_t* __restrict__ ghost
   spins[row_off(G, s, X, br) + j] = ghost_rows[i];
 }
 
+// Issue-bound INT32 peak: independent LOP3 (ALU pipe) and IMAD (FMA pipe)
+// chains, 1:1, no cross-chain dependences.
 constexpr int kPeakChains = 8;
 __global__ void k_int_peak(uint32_t* out, uint32_t seed, int iters) {
   uint32_t a[kPeakChains], b[kPeakChains];
@@ -766,11 +781,11 @@ __global__ void k_int_peak(uint32_t* out, uint32_t seed, int iters) {
     a[i] = seed * (threadIdx.x + i + 1);
     b[i] = a[i] ^ 0x9e3779b9u;
   }
-  const uint32_t k1 = seed | 1u, k2 = seed >> 3;
+  const uint32_t k1 = seed | 1u, k2 = seed >> 3, k3 = seed * 7u;
   for (int it = 0; it < iters; it++) {
 #pragma unroll
     for (int i = 0; i < kPeakChains; i++) {
-      asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(a[i]) : "r"(b[i]), "r"(k1));
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(a[i]) : "r"(k3), "r"(k1));
       asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(b[i]) : "r"(k1), "r"(k2));
     }
   }
@@ -811,7 +826,6 @@ int set_smem_attr(K kernel, std::once_flag& once, cudaError_t& err) {
   return MSB_OK;
 }
 
-int plane_pitch(const Geo& G) { return (G.W + 15) & ~15; }
 
 int check_params(const msb_sweep_params* p) {
   if (!p) return fail(MSB_ERR_ARG, "null sweep parameters");
@@ -821,6 +835,7 @@ int check_params(const msb_sweep_params* p) {
   if (p->mode != MSB_MODE_GENERIC && p->n_planes != 2) return fail(MSB_ERR_ARG, "ferro/anti modes use exactly 2 planes");
   if (p->mode < 0 || p->mode > 2) return fail(MSB_ERR_ARG, "bad mode");
   if (p->n_planes > 0 && !p->thr9) return fail(MSB_ERR_ARG, "null thresholds");
+  if (!p->work) return fail(MSB_ERR_ARG, "null work counter (2 zeroed uint32 per engine)");
   return MSB_OK;
 }
 
@@ -838,41 +853,30 @@ int rng_planes(const msb_geom* g, const msb_sweep_params* p, int colour, uint32_
   a.kr = 16 / p->kg;
   a.npieces = (long long)g->n_sim * g->rows * p->kg;
   a.np = p->n_planes;
-  a.nch = (G.words + 31) / 32;
-  a.Pp = plane_pitch(G);
   a.colour0 = colour < 0 ? 0 : colour;
-  const int ncol = colour < 0 ? 2 : 1;
-  a.rs = std::max(a.np, 1) * 16 * a.nch + 1;  // odd row stride: conflict-free per-row access
-  const long long total_rows = (long long)g->n_sim * g->rows;
-  static const int env_threads = [] { const char* e = getenv("MSB_RNG_THREADS"); return e ? atoi(e) : 0; }();
-  static const int env_jsmem = [] { const char* e = getenv("MSB_JUMP_SMEM"); return e ? atoi(e) : 1; }();
-  const bool jsmem = env_jsmem != 0 && !ext;
-  int threads_target = env_threads > 0 ? env_threads : 128;
-  int block_rows = p->block_rows > 0 ? p->block_rows : std::max(1, threads_target / p->kg);
-  block_rows = std::min(block_rows, 256 / p->kg);
-  const size_t jbytes = jsmem ? (size_t)kJumpWords * 4 : 0;
-  while (block_rows > 1 && jbytes + (size_t)block_rows * a.rs * 4 > 227 * 1024) block_rows /= 2;
-  while (block_rows > 1 && ((total_rows + block_rows - 1) / block_rows) * ncol < 2 * 148 && block_rows * p->kg > 64)
-    block_rows /= 2;
-  a.block_rows = block_rows;
-  const size_t smem = jbytes + (size_t)block_rows * a.rs * 4;
-  if (smem > 227 * 1024) return fail(MSB_ERR_UNSUPPORTED, "lattice rows too long for the shared-memory plan");
-  const dim3 grid((unsigned)((total_rows + block_rows - 1) / block_rows), ncol);
-  const int threads = ((block_rows * p->kg + 31) / 32) * 32;
-#define MSB_LAUNCH_RNG(NP, EXT, JS)                                           \
+  a.ncol = colour < 0 ? 2 : 1;
+  a.work = p->work;
+  int dev = 0, sms = 148;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const long long units = (a.npieces * a.ncol + 31) / 32;
+  const long long per_cta = kRngThreads / 32;
+  (void)per_cta;
+  const unsigned grid = (unsigned)std::max(1LL, std::min<long long>(sms, units));
+  const size_t smem = ext ? 0 : (size_t)kJumpWords * 4;
+#define MSB_LAUNCH_RNG(NP, EXT)                                               \
   do {                                                                        \
     static std::once_flag o;                                                  \
     static cudaError_t e;                                                     \
-    if (int r = set_smem_attr(k_rng_planes<NP, EXT, JS>, o, e)) return r;     \
-    k_rng_planes<NP, EXT, JS><<<grid, threads, smem, st>>>(a);                \
+    if (int r = set_smem_attr(k_rng_planes<NP, EXT>, o, e)) return r;         \
+    k_rng_planes<NP, EXT><<<grid, kRngThreads, smem, st>>>(a);                \
   } while (0)
   if (p->mode != MSB_MODE_GENERIC) {
-    if (ext) MSB_LAUNCH_RNG(2, true, false);
-    else if (jsmem) MSB_LAUNCH_RNG(2, false, true);
-    else MSB_LAUNCH_RNG(2, false, false);
+    if (ext) MSB_LAUNCH_RNG(2, true);
+    else MSB_LAUNCH_RNG(2, false);
   } else {
-    if (ext) MSB_LAUNCH_RNG(MSB_MAX_PLANES, true, false);
-    else MSB_LAUNCH_RNG(MSB_MAX_PLANES, false, false);
+    if (ext) MSB_LAUNCH_RNG(MSB_MAX_PLANES, true);
+    else MSB_LAUNCH_RNG(MSB_MAX_PLANES, false);
   }
 #undef MSB_LAUNCH_RNG
   CUDA_TRY(cudaGetLastError());
@@ -889,11 +893,11 @@ int flip(const msb_geom* g, const msb_sweep_params* p, int colour, uint32_t* spi
   a.flips = reinterpret_cast<unsigned long long*>(flips);
   a.X = colour;
   a.np = p->n_planes;
-  a.Pp = plane_pitch(G);
   a.inv = p->mode == MSB_MODE_ANTI ? 0xFFFFFFFFu : 0u;
   a.fault = p->fault;
   std::memcpy(a.code_plane, p->code_plane, 16);
-  const long long total = (long long)g->n_sim * g->rows * G.W;
+  const long long total = (long long)g->n_sim * g->rows * (G.Wp / 4);
+  if (total >= (1LL << 31)) return fail(MSB_ERR_UNSUPPORTED, "too many words for one flip launch");
   if (p->mode == MSB_MODE_GENERIC)
     k_flip<true><<<blocks_for(total, 256), 256, 0, st>>>(a);
   else
@@ -1084,7 +1088,7 @@ int msb_from_linear(const msb_geom* g, const uint64_t* lin, uint32_t* spins, voi
   const Geo G = make_geo(g);
   const long long total = (long long)G.n_sim * G.rows * G.Wp;
   k_from_linear<<<blocks_for(total, 256), 256, 0, as_stream(stream)>>>(
-      G, reinterpret_cast<const unsigned long long*>(lin), spins);
+      G, reinterpret_cast<const uint32_t*>(lin), spins);
   CUDA_TRY(cudaGetLastError());
   return MSB_OK;
 }
@@ -1093,9 +1097,8 @@ int msb_to_linear(const msb_geom* g, const uint32_t* spins, uint64_t* lin, void*
   if (int r = check_geom(g)) return r;
   if (!lin || !spins) return fail(MSB_ERR_ARG, "null buffer");
   const Geo G = make_geo(g);
-  const long long total = (long long)G.n_sim * G.rows * G.n / 64;
-  k_to_linear<<<blocks_for(total, 256), 256, 0, as_stream(stream)>>>(G, spins,
-                                                                       reinterpret_cast<unsigned long long*>(lin));
+  const long long total = (long long)G.n_sim * G.rows * G.words;
+  k_to_linear<<<blocks_for(total, 256), 256, 0, as_stream(stream)>>>(G, spins, reinterpret_cast<uint32_t*>(lin));
   CUDA_TRY(cudaGetLastError());
   return MSB_OK;
 }
@@ -1126,7 +1129,7 @@ int64_t msb_plane_words(const msb_geom* g, int32_t n_planes) {
   if (check_geom(g)) return -1;
   if (n_planes < 0 || n_planes > MSB_MAX_PLANES) return -1;
   const Geo G = make_geo(g);
-  return 2LL * std::max(n_planes, 1) * g->n_sim * g->rows * plane_pitch(G);
+  return 2LL * std::max(n_planes, 1) * g->n_sim * g->rows * G.Wp;
 }
 
 int msb_rng_planes(const msb_geom* g, const msb_sweep_params* p, int32_t colour, uint32_t* states,

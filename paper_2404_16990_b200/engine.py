@@ -180,6 +180,7 @@ class Engine:
             pw = int(_lib.lib().msb_plane_words(ctypes.byref(self._g), MSB_MAX_PLANES))
             self._plane_words = pw
             self._planes = torch.empty(2 * pw, dtype=torch.int32, device=self.device)
+            self._work = torch.zeros(2, dtype=torch.int32, device=self.device)
             self._obs = torch.zeros(2 * self.n_sim, dtype=torch.int64, device=self.device)
         self._pow = _pow_tables(self.device)
         self._jump = _sweep_jump_table(self.device, dims.n)
@@ -187,6 +188,7 @@ class Engine:
         self._params.kg = self.kg
         self._params.jump = self._jump.data_ptr()
         self._params.thr9 = self._thr.data_ptr()
+        self._params.work = self._work.data_ptr()
         self._tab_key = None
         self.fault = 0  # test-only adder corruption (selftest seam, cli.py:467-480)
         self.overlap = True  # run the next sweep's RNG concurrently with this sweep's flips

@@ -124,6 +124,58 @@ __global__ void kxoshiro(uint32_t* out, uint32_t seed, int nsteps, uint32_t one)
   if ((acc0 ^ acc1) == 0x12345678u) out[0] = acc0;
 }
 
+__device__ __forceinline__ uint32_t lop3x(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d; asm("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(d) : "r"(a), "r"(b), "r"(c)); return d;
+}
+// 64-bit product of a 32-bit value and an immediate power of two through
+// the FMA pipe (mul.wide.u32); lo/hi halves.
+template <int K>
+__device__ __forceinline__ void wide_pow2(uint32_t x, uint32_t& lo, uint32_t& hi) {
+  uint64_t r;
+  asm("mul.wide.u32 %0, %1, %2;" : "=l"(r) : "r"(x), "n"(1u << K));
+  lo = (uint32_t)r; hi = (uint32_t)(r >> 32);
+}
+
+// VAR 5: t via WIDE; VAR 6: + rotl13 via WIDE+IMAD; VAR 7: + r0 via WIDE+IMAD
+template <int VAR>
+__global__ void kxo2(uint32_t* out, uint32_t seed, int nsteps) {
+  uint64_t s0 = 0x9E3779B97F4B7C15ull * (blockIdx.x * blockDim.x + threadIdx.x + 1) ^ seed;
+  uint64_t s1 = s0 * 3 + 1, s2 = s0 ^ 0xdeadbeef12345ull, s3 = s1 * 7 + 11;
+  uint32_t acc0 = 0, acc1 = 0, K0 = 0x300000u << 9, K1 = 0x80000u << 9;
+  uint32_t a0 = (uint32_t)s0, a1 = s0 >> 32, b0 = (uint32_t)s1, b1 = s1 >> 32;
+  uint32_t c0 = (uint32_t)s2, c1 = s2 >> 32, d0 = (uint32_t)s3, d1 = s3 >> 32;
+#pragma unroll 8
+  for (int i = 0; i < nsteps; i++) {
+    uint32_t x0, x1, o1;
+    asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, %5;" : "=r"(x0), "=r"(x1) : "r"(a0), "r"(d0), "r"(a1), "r"(d1));
+    uint32_t r1 = fsl(x0, x1, 23), r0;
+    if (VAR >= 7) { uint32_t wl, wh; wide_pow2<23>(x1, wl, wh); r0 = x0 * (1u << 23) + wh; }
+    else r0 = fsl(x1, x0, 23);
+    asm("{.reg .b32 t; add.cc.u32 t, %1, %2;\n\taddc.u32 %0, %3, %4;}" : "=r"(o1) : "r"(r0), "r"(a0), "r"(r1), "r"(a1));
+    uint32_t hi9 = o1 << 9;
+    asm("{.reg .b32 t; sub.cc.u32 t, %1, %2;\n\taddc.u32 %0, %0, %0;}" : "+r"(acc0) : "r"(hi9), "r"(K0));
+    asm("{.reg .b32 t; sub.cc.u32 t, %1, %2;\n\taddc.u32 %0, %0, %0;}" : "+r"(acc1) : "r"(hi9), "r"(K1));
+    uint32_t t0, t1;
+    { uint32_t wh; wide_pow2<17>(b0, t0, wh); t1 = b1 * (1u << 17) + wh; }
+    const uint32_t nc0 = lop3x(c0, a0, t0), nc1 = lop3x(c1, a1, t1);
+    const uint32_t nd0 = d0 ^ b0, nd1 = d1 ^ b1;
+    const uint32_t nb0 = lop3x(b0, c0, a0), nb1 = lop3x(b1, c1, a1);
+    const uint32_t na0 = lop3x(a0, d0, b0), na1 = lop3x(a1, d1, b1);
+    a0 = na0; a1 = na1; b0 = nb0; b1 = nb1; c0 = nc0; c1 = nc1;
+    if (VAR >= 6) {
+      uint32_t l0, h0, l1, h1;
+      wide_pow2<13>(nd0, l0, h0);
+      wide_pow2<13>(nd1, l1, h1);
+      d1 = nd0 * (1u << 13) + h1;   // (nd0 << 13) | (nd1 >> 19)
+      d0 = nd1 * (1u << 13) + h0;   // (nd1 << 13) | (nd0 >> 19)
+    } else {
+      d1 = fsl(nd1, nd0, 13);
+      d0 = fsl(nd0, nd1, 13);
+    }
+  }
+  if ((acc0 ^ acc1) == 0x12345678u) out[0] = acc0 ^ a0 ^ b1 ^ c0 ^ d1;
+}
+
 int main() {
   uint32_t* d; cudaMalloc(&d, 4096);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
@@ -162,6 +214,21 @@ int main() {
         case 2: kxoshiro<2><<<bl, 256>>>(d, 3, ns, 1); break;
         case 3: kxoshiro<3><<<bl, 256>>>(d, 3, ns, 1); break;
         case 4: kxoshiro<4><<<bl, 256>>>(d, 3, ns, 1); break;
+      }
+    };
+    launch();
+    cudaEventRecord(e0); launch(); cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    printf("xoshiro VAR %d blocks=%d: %.3f ms  %.3f T draws/s\n", var, bl, ms, (double)bl * 256 * ns / ms / 1e9);
+  }
+  for (int var = 5; var < 8; var++)
+  for (int bl : {148 * 4, 148 * 8}) {
+    int ns = 1 << 13;
+    auto launch = [&]() {
+      switch (var) {
+        case 5: kxo2<5><<<bl, 256>>>(d, 3, ns); break;
+        case 6: kxo2<6><<<bl, 256>>>(d, 3, ns); break;
+        case 7: kxo2<7><<<bl, 256>>>(d, 3, ns); break;
       }
     };
     launch();
