@@ -67,8 +67,8 @@ typedef struct msb_sweep_params {
   const uint32_t *jump;          /* device: 32 KiB nibble table of A^(4n) */
   int32_t fault;                 /* test-only adder corruption (cli.py:467-480 analogue) */
   int32_t block_rows;            /* reserved, 0 */
-  uint32_t *work;                /* device: 2 uint32 scratch counters, zeroed once by the caller;
-                                    the accept-plane kernel leaves them zeroed */
+  uint32_t *work;                /* device: 4 uint32 scratch counters, zeroed once by the caller;
+                                    every kernel leaves them zeroed */
 } msb_sweep_params;
 
 /* ---- status -------------------------------------------------------------- */
@@ -143,11 +143,21 @@ int msb_flip(const msb_geom *g, const msb_sweep_params *p, int32_t colour, uint3
 int msb_phase(const msb_geom *g, const msb_sweep_params *p, int32_t phase, uint32_t *spins,
               uint32_t *states, const uint32_t *ext_draws, uint32_t *planes, uint64_t *flips,
               void *stream);
-/* n_sweeps full sweeps (red then blue) of a whole lattice.  planes must hold
- * 2 * msb_plane_words().  overlap != 0 runs the accept-plane generation of
- * sweep k+1 on a helper stream concurrently with the flips of sweep k. */
+/* n_sweeps full sweeps (red then blue) of a whole lattice.  planes holds
+ * two msb_plane_words() buffers.  FERRO/ANTI modes run one cooperative,
+ * warp-specialised kernel per sweep: the flips of sweep k (from one buffer)
+ * overlap the accept planes of sweep k+1 (into the other).  Lookahead flags:
+ *   MSB_SWEEP_AHEAD_IN  buffer *cur_io already holds the first sweep's planes
+ *                       (the piece states are then one sweep ahead);
+ *   MSB_SWEEP_AHEAD_OUT leave the next sweep's planes generated, in buffer
+ *                       *cur_io on return (states one sweep ahead);
+ *   MSB_SWEEP_SERIAL    separate launches, no overlap. */
+#define MSB_SWEEP_AHEAD_IN 1
+#define MSB_SWEEP_AHEAD_OUT 2
+#define MSB_SWEEP_SERIAL 4
 int msb_sweep(const msb_geom *g, const msb_sweep_params *p, uint32_t *spins, uint32_t *states,
-              uint32_t *planes, int32_t n_sweeps, int32_t overlap, uint64_t *flips, void *stream);
+              uint32_t *planes, int32_t n_sweeps, int32_t flags, int32_t *cur_io, uint64_t *flips,
+              void *stream);
 
 /* ---- observables (engine.py:372-386) ------------------------------------- */
 /* Adds, per replica, the number of +1 spins and the number of unsatisfied

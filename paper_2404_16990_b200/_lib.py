@@ -22,6 +22,9 @@ MSB_MODE_ANTI = 1
 MSB_MODE_GENERIC = 2
 MSB_MAX_PLANES = 10
 MSB_FLIP_SLOTS = 256
+MSB_SWEEP_AHEAD_IN = 1
+MSB_SWEEP_AHEAD_OUT = 2
+MSB_SWEEP_SERIAL = 4
 
 
 class MsbError(RuntimeError):
@@ -109,7 +112,7 @@ def lib() -> ctypes.CDLL:
         "msb_rng_planes": ([G, P, i32, vp, vp, vp, vp], ctypes.c_int),
         "msb_flip": ([G, P, i32, vp, vp, vp, vp], ctypes.c_int),
         "msb_phase": ([G, P, i32, vp, vp, vp, vp, vp, vp], ctypes.c_int),
-        "msb_sweep": ([G, P, vp, vp, vp, i32, i32, vp, vp], ctypes.c_int),
+        "msb_sweep": ([G, P, vp, vp, vp, i32, i32, vp, vp, vp], ctypes.c_int),
         "msb_observe": ([G, vp, vp, vp, vp], ctypes.c_int),
         "msb_draws": ([G, i32, i32, vp, vp, vp], ctypes.c_int),
         "msb_pack_edges": ([G, i32, vp, vp, vp], ctypes.c_int),

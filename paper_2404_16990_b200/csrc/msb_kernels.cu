@@ -286,25 +286,38 @@ __device__ __forceinline__ size_t plane_off(const Geo& G, int np, int X, int p, 
 // next sweep, so table reads overlap other warps' ALU work.
 constexpr int kRngThreads = 1024;
 
+// Work counters (caller-owned, zeroed once, left zeroed by every kernel):
+//   work[0] next dynamic producer unit    work[1] consumer barrier arrivals
+//   work[2] warps finished (last one resets all four)
+constexpr int kWork = 4;
+
+__device__ __forceinline__ void finish_warp(unsigned* work, unsigned total_warps) {
+  if ((threadIdx.x & 31) == 0) {
+    __threadfence();
+    if (atomicAdd(work + 2, 1u) == total_warps - 1) {
+      atomicExch(work, 0u);
+      atomicExch(work + 1, 0u);
+      atomicExch(work + 2, 0u);
+    }
+  }
+}
+
+// One producer warp's share of a sweep's accept planes.  `role_warp` /
+// `role_warps` number the producer warps of the grid; their first unit is
+// static (interleaved across CTAs), later ones come from work[0].
 template <int NPMAX, bool EXT>
-__global__ void __launch_bounds__(kRngThreads, 1) k_rng_planes(const RngArgs a) {
-  extern __shared__ uint4 jt[];  // nibble table of A^(4n), 32 KiB
+__device__ __forceinline__ void rng_produce(const RngArgs& a, const uint4* __restrict__ jt, int role_warp,
+                                            int role_warps) {
   const Geo& G = a.G;
   const int np = NPMAX == 2 ? 2 : a.np;
   const int lane = threadIdx.x & 31;
-  if (!EXT) {
-    for (int i = threadIdx.x; i < kJumpWords / 4; i += blockDim.x) jt[i] = a.jump[i];
-    __syncthreads();
-  }
   const long long total = a.npieces * a.ncol;
   const long long units = (total + 31) / 32;
   const size_t pstride = (size_t)G.n_sim * G.rows * G.Wp;
   const int lk = 64 / a.kr;  // jump lookups per k-segment (multiple of 4)
-  // first unit: static, interleaved across SMs (unit w*gridDim + cta) so every
-  // SM gets an equal share of the first round; later units: dynamic
-  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
-  long long u = (long long)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
-  for (;; ) {
+  const long long nwarps = (long long)role_warps * gridDim.x;
+  long long u = (long long)role_warp * gridDim.x + blockIdx.x;
+  for (;;) {
     if (u >= units) break;
     const long long gi = u * 32 + lane;
     if (gi < total) {
@@ -398,14 +411,17 @@ __global__ void __launch_bounds__(kRngThreads, 1) k_rng_planes(const RngArgs a) 
     if (lane == 0) nu = nwarps + (long long)atomicAdd(a.work, 1u);
     u = __shfl_sync(0xFFFFFFFFu, nu, 0);
   }
-  // self-reset of the work counter by the last warp to finish claiming
-  if (lane == 0) {
-    const unsigned warps = gridDim.x * (blockDim.x >> 5);
-    if (atomicAdd(a.work + 1, 1u) == warps - 1) {
-      atomicExch(a.work, 0u);
-      atomicExch(a.work + 1, 0u);
-    }
+}
+
+template <int NPMAX, bool EXT>
+__global__ void __launch_bounds__(kRngThreads, 1) k_rng_planes(const RngArgs a) {
+  extern __shared__ uint4 jt[];  // nibble table of A^(4n), 32 KiB
+  if (!EXT) {
+    for (int i = threadIdx.x; i < kJumpWords / 4; i += blockDim.x) jt[i] = a.jump[i];
+    __syncthreads();
   }
+  rng_produce<NPMAX, EXT>(a, jt, threadIdx.x >> 5, blockDim.x >> 5);
+  finish_warp(a.work, gridDim.x * (blockDim.x >> 5));
 }
 
 // ---------------------------------------------------------------------------
@@ -417,7 +433,7 @@ struct FlipArgs {
   uint32_t* spins;
   const uint32_t* planes;
   unsigned long long* flips;
-  int X, np;
+  int X, np, cwarps;
   uint32_t inv;
   int fault;
   int8_t code_plane[16];
@@ -454,74 +470,151 @@ __device__ __forceinline__ uint32_t flip_word(const FlipArgs& a, bool generic, u
   return flip;
 }
 
-// Thread per (replica, held row, chunk, quad of 4 t-words).  Vertical
-// neighbours are the other colour's rows c-1, c+1 (same word); horizontal
-// ones are the other colour's row c at sites i and i+-1 (h_second).
-template <bool GENERIC>
-__global__ void __launch_bounds__(256) k_flip(const FlipArgs a) {
+// One quad of 4 t-words (t0..t0+3 of chunk ch) of row (s, lr) in colour
+// a.X.  Vertical neighbours are the other colour's rows c-1, c+1 (same
+// word); horizontal ones the other colour's row c at sites i and i+-1
+// (h_second).  COHERENT: other-colour words were written earlier in the same
+// kernel by other SMs, so read them through L2 (ld.global.cg).
+template <bool GENERIC, bool COHERENT>
+__device__ __forceinline__ unsigned flip_quad(const FlipArgs& a, unsigned i, int X) {
   const Geo& G = a.G;
   const unsigned quads = (unsigned)G.Wp >> 2;
-  const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
-  const unsigned total = (unsigned)G.n_sim * (unsigned)G.rows * quads;
+  const unsigned gr = i / quads, qq = i - gr * quads;
+  const int s = (int)(gr / (unsigned)G.rows), lr = (int)(gr - (unsigned)s * G.rows);
+  const int c = G.row0 + lr, br = lr + G.ghost;
+  const int ch = (int)(qq >> 2), t0 = 4 * (int)(qq & 3);
+  const int w0 = ch * 16 + t0;
+  int bu, bd;
+  vert_rows(G, br, bu, bd);
+  uint32_t* own = a.spins + row_off(G, s, X, br);
+  const uint32_t* yc = a.spins + row_off(G, s, 1 - X, br);
+  auto ld4 = [](const uint32_t* q) {
+    return COHERENT ? __ldcg(reinterpret_cast<const uint4*>(q)) : __ldg(reinterpret_cast<const uint4*>(q));
+  };
+  auto ld1 = [](const uint32_t* q) { return COHERENT ? __ldcg(q) : __ldg(q); };
+  const uint4 O = *reinterpret_cast<const uint4*>(own + w0);
+  const uint4 Y = ld4(yc + w0);
+  const uint4 U = ld4(a.spins + row_off(G, s, 1 - X, bu) + w0);
+  const uint4 D = ld4(a.spins + row_off(G, s, 1 - X, bd) + w0);
+  const size_t pstride = (size_t)G.n_sim * G.rows * G.Wp;
+  const uint32_t* pl = a.planes + plane_off(G, a.np, X, 0, s, lr) + w0;
+  uint4 P4 = make_uint4(0, 0, 0, 0), P8 = make_uint4(0, 0, 0, 0);
+  if (!GENERIC) {
+    P4 = __ldg(reinterpret_cast<const uint4*>(pl));
+    P8 = __ldg(reinterpret_cast<const uint4*>(pl + pstride));
+  }
+  const int p = (c + X) & 1;
+  const uint32_t y[4] = {Y.x, Y.y, Y.z, Y.w};
+  const uint32_t o[4] = {O.x, O.y, O.z, O.w};
+  const uint32_t u4[4] = {U.x, U.y, U.z, U.w};
+  const uint32_t d4[4] = {D.x, D.y, D.z, D.w};
+  const uint32_t a4[4] = {P4.x, P4.y, P4.z, P4.w};
+  const uint32_t a8[4] = {P8.x, P8.y, P8.z, P8.w};
+  // the neighbour word just outside the quad (t0+4 if p, t0-1 otherwise) or,
+  // at t = 15 / t = 0, the shifted word of the next / previous w
+  uint32_t edge;
+  const int vb = chunk_bits(G, ch);
+  if (p) {
+    if (t0 + 4 < 16) {
+      edge = ld1(yc + w0 + 4);
+    } else {
+      const int chn = ch + 1 < G.nch ? ch + 1 : 0;
+      edge = (ld1(yc + ch * 16) >> 1) | ((ld1(yc + chn * 16) & 1u) << (vb - 1));
+    }
+  } else {
+    if (t0 > 0) {
+      edge = ld1(yc + w0 - 1);
+    } else {
+      const uint32_t carry = ch > 0 ? (ld1(yc + (ch - 1) * 16 + 15) >> 31)
+                                    : ((ld1(yc + (G.nch - 1) * 16 + 15) >> (chunk_bits(G, G.nch - 1) - 1)) & 1u);
+      edge = ((ld1(yc + ch * 16 + 15) << 1) | carry) & chunk_mask(G, ch);
+    }
+  }
+  const uint32_t vm = chunk_mask(G, ch);
+  uint32_t res[4];
   unsigned cnt = 0;
-  if (i < total) {
-    const unsigned gr = i / quads, qq = i - gr * quads;
-    const int s = (int)(gr / (unsigned)G.rows), lr = (int)(gr - (unsigned)s * G.rows);
-    const int X = a.X, c = G.row0 + lr, br = lr + G.ghost;
-    const int ch = (int)(qq >> 2), t0 = 4 * (int)(qq & 3);
-    const int w0 = ch * 16 + t0;
-    int bu, bd;
-    vert_rows(G, br, bu, bd);
-    uint32_t* own = a.spins + row_off(G, s, X, br);
-    const uint32_t* yc = a.spins + row_off(G, s, 1 - X, br);
-    const uint4 O = *reinterpret_cast<const uint4*>(own + w0);
-    const uint4 Y = __ldg(reinterpret_cast<const uint4*>(yc + w0));
-    const uint4 U = __ldg(reinterpret_cast<const uint4*>(a.spins + row_off(G, s, 1 - X, bu) + w0));
-    const uint4 D = __ldg(reinterpret_cast<const uint4*>(a.spins + row_off(G, s, 1 - X, bd) + w0));
-    const size_t pstride = (size_t)G.n_sim * G.rows * G.Wp;
-    const uint32_t* pl = a.planes + plane_off(G, a.np, X, 0, s, lr) + w0;
-    uint4 P4 = make_uint4(0, 0, 0, 0), P8 = make_uint4(0, 0, 0, 0);
-    if (!GENERIC) {
-      P4 = __ldg(reinterpret_cast<const uint4*>(pl));
-      P8 = __ldg(reinterpret_cast<const uint4*>(pl + pstride));
-    }
-    const int p = (c + X) & 1;
-    const uint32_t y[4] = {Y.x, Y.y, Y.z, Y.w};
-    const uint32_t o[4] = {O.x, O.y, O.z, O.w};
-    const uint32_t u4[4] = {U.x, U.y, U.z, U.w};
-    const uint32_t d4[4] = {D.x, D.y, D.z, D.w};
-    const uint32_t a4[4] = {P4.x, P4.y, P4.z, P4.w};
-    const uint32_t a8[4] = {P8.x, P8.y, P8.z, P8.w};
-    // the one neighbour word outside the quad (t0+4 if p, t0-1 otherwise);
-    // the t = 15 / t = 0 wrap cases go through h_second
-    uint32_t edge = 0;
-    if (p && t0 + 4 < 16) edge = __ldg(yc + w0 + 4);
-    if (!p && t0 > 0) edge = __ldg(yc + w0 - 1);
-    const uint32_t vm = chunk_mask(G, ch);
-    uint32_t res[4];
 #pragma unroll
-    for (int k = 0; k < 4; k++) {
-      const int t = t0 + k;
-      uint32_t n4;
-      if (p) n4 = k < 3 ? y[k + 1] : (t < 15 ? edge : h_second(G, yc, ch, 15, 1));
-      else n4 = k > 0 ? y[k - 1] : (t > 0 ? edge : h_second(G, yc, ch, 0, 0));
-      uint32_t f = flip_word(a, GENERIC, o[k], u4[k], d4[k], y[k], n4, pl + k, pstride, a4[k], a8[k]);
-      f &= vm;
-      res[k] = o[k] ^ f;
-      cnt += __popc(f);
-    }
-    *reinterpret_cast<uint4*>(own + w0) = make_uint4(res[0], res[1], res[2], res[3]);
+  for (int k = 0; k < 4; k++) {
+    const uint32_t n4 = p ? (k < 3 ? y[k + 1] : edge) : (k > 0 ? y[k - 1] : edge);
+    uint32_t f = flip_word(a, GENERIC, o[k], u4[k], d4[k], y[k], n4, pl + k, pstride, a4[k], a8[k]);
+    f &= vm;
+    res[k] = o[k] ^ f;
+    cnt += __popc(f);
   }
-  // block reduction, one atomic per block into one of kFlipSlots counters
-  __shared__ unsigned red[8];
+  *reinterpret_cast<uint4*>(own + w0) = make_uint4(res[0], res[1], res[2], res[3]);
+  return cnt;
+}
+
+__device__ __forceinline__ void add_flips(unsigned long long* flips, unsigned cnt) {
   cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;
+  if ((threadIdx.x & 31) == 0 && cnt)
+    atomicAdd(flips + ((blockIdx.x * 32 + (threadIdx.x >> 5)) % kFlipSlots), (unsigned long long)cnt);
+}
+
+template <bool GENERIC>
+__global__ void __launch_bounds__(256) k_flip(const FlipArgs a) {
+  const unsigned quads = (unsigned)a.G.Wp >> 2;
+  const unsigned total = (unsigned)a.G.n_sim * (unsigned)a.G.rows * quads;
+  const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned cnt = i < total ? flip_quad<GENERIC, false>(a, i, a.X) : 0u;
+  add_flips(a.flips, cnt);
+}
+
+// ---------------------------------------------------------------------------
+// device: fused sweep -- flips of sweep k overlapped with the planes of k+1
+// ---------------------------------------------------------------------------
+//
+// Cooperative persistent kernel, one 1024-thread CTA per SM.  Warps
+// [0, kProducerWarps) generate sweep k+1's accept planes (rng_produce) into
+// one buffer; the other warps flip sweep k from the other buffer: red quads,
+// a grid barrier among flip warps, then blue quads.  The flip pass is
+// latency-bound and the RNG ALU-bound, so sharing the SMs hides the flips.
+// flip warps per CTA: FlipArgs::cwarps (the rest produce planes)
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int NPMAX>
+__global__ void __launch_bounds__(kRngThreads, 1) k_sweep_fused(const RngArgs ra, const FlipArgs fa) {
+  const int kFlipWarps = fa.cwarps;
+  const int kProducerWarps = (kRngThreads >> 5) - kFlipWarps;
+  extern __shared__ uint4 jt[];
+  for (int i = threadIdx.x; i < kJumpWords / 4; i += blockDim.x) jt[i] = ra.jump[i];
   __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long tot = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); w++) tot += red[w];
-    if (tot) atomicAdd(a.flips + (blockIdx.x % kFlipSlots), tot);
+  const int warp = threadIdx.x >> 5;
+  const unsigned total_warps = gridDim.x * (blockDim.x >> 5);
+  if (warp < kProducerWarps) {
+    rng_produce<NPMAX, false>(ra, jt, warp, kProducerWarps);
+  } else {
+    const unsigned quads = (unsigned)fa.G.Wp >> 2;
+    const unsigned total = (unsigned)fa.G.n_sim * (unsigned)fa.G.rows * quads;
+    const unsigned stride = gridDim.x * kFlipWarps * 32;
+    const unsigned first = ((warp - kProducerWarps) * gridDim.x + blockIdx.x) * 32 + (threadIdx.x & 31);
+    unsigned cnt = 0;
+    for (int X = 0; X < 2; X++) {
+      if (X == 0) {
+        for (unsigned i = first; i < total; i += stride) cnt += flip_quad<false, false>(fa, i, 0);
+      } else {
+        for (unsigned i = first; i < total; i += stride) cnt += flip_quad<false, true>(fa, i, 1);
+      }
+      if (X == 0) {  // grid barrier among the flip warps
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) {
+          __threadfence();
+          atomicAdd(ra.work + 1, 1u);
+          const unsigned need = gridDim.x * kFlipWarps;
+          while (ld_acquire(ra.work + 1) < need) __nanosleep(64);
+        }
+        __syncwarp();
+        __threadfence();
+      }
+    }
+    add_flips(fa.flips, cnt);
   }
+  finish_warp(ra.work, total_warps);
 }
 
 // ---------------------------------------------------------------------------
@@ -839,11 +932,9 @@ int check_params(const msb_sweep_params* p) {
   return MSB_OK;
 }
 
-int rng_planes(const msb_geom* g, const msb_sweep_params* p, int colour, uint32_t* states, const uint32_t* ext,
-               uint32_t* planes, cudaStream_t st) {
-  const Geo G = make_geo(g);
-  RngArgs a;
-  a.G = G;
+void fill_rng_args(RngArgs& a, const msb_geom* g, const msb_sweep_params* p, int colour, uint32_t* states,
+                   const uint32_t* ext, uint32_t* planes) {
+  a.G = make_geo(g);
   a.states = states;
   a.thr9 = p->thr9;
   a.jump = reinterpret_cast<const uint4*>(p->jump);
@@ -856,6 +947,25 @@ int rng_planes(const msb_geom* g, const msb_sweep_params* p, int colour, uint32_
   a.colour0 = colour < 0 ? 0 : colour;
   a.ncol = colour < 0 ? 2 : 1;
   a.work = p->work;
+}
+
+void fill_flip_args(FlipArgs& a, const msb_geom* g, const msb_sweep_params* p, int colour, uint32_t* spins,
+                    const uint32_t* planes, uint64_t* flips) {
+  a.G = make_geo(g);
+  a.spins = spins;
+  a.planes = planes;
+  a.flips = reinterpret_cast<unsigned long long*>(flips);
+  a.X = colour;
+  a.np = p->n_planes;
+  a.inv = p->mode == MSB_MODE_ANTI ? 0xFFFFFFFFu : 0u;
+  a.fault = p->fault;
+  std::memcpy(a.code_plane, p->code_plane, 16);
+}
+
+int rng_planes(const msb_geom* g, const msb_sweep_params* p, int colour, uint32_t* states, const uint32_t* ext,
+               uint32_t* planes, cudaStream_t st) {
+  RngArgs a;
+  fill_rng_args(a, g, p, colour, states, ext, planes);
   int dev = 0, sms = 148;
   CUDA_TRY(cudaGetDevice(&dev));
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -887,15 +997,7 @@ int flip(const msb_geom* g, const msb_sweep_params* p, int colour, uint32_t* spi
          uint64_t* flips, cudaStream_t st) {
   const Geo G = make_geo(g);
   FlipArgs a;
-  a.G = G;
-  a.spins = spins;
-  a.planes = planes;
-  a.flips = reinterpret_cast<unsigned long long*>(flips);
-  a.X = colour;
-  a.np = p->n_planes;
-  a.inv = p->mode == MSB_MODE_ANTI ? 0xFFFFFFFFu : 0u;
-  a.fault = p->fault;
-  std::memcpy(a.code_plane, p->code_plane, 16);
+  fill_flip_args(a, g, p, colour, spins, planes, flips);
   const long long total = (long long)g->n_sim * g->rows * (G.Wp / 4);
   if (total >= (1LL << 31)) return fail(MSB_ERR_UNSUPPORTED, "too many words for one flip launch");
   if (p->mode == MSB_MODE_GENERIC)
@@ -906,6 +1008,52 @@ int flip(const msb_geom* g, const msb_sweep_params* p, int colour, uint32_t* spi
   return MSB_OK;
 }
 
+
+// flips of the sweep whose planes are in `cur` + planes of the next sweep
+// into `next`, one cooperative launch (FERRO/ANTI whole lattices).
+int fused_sweep(const msb_geom* g, const msb_sweep_params* p, uint32_t* spins, uint32_t* states, const uint32_t* cur,
+                uint32_t* next, uint64_t* flips, cudaStream_t st) {
+  RngArgs ra;
+  fill_rng_args(ra, g, p, -1, states, nullptr, next);
+  FlipArgs fa;
+  fill_flip_args(fa, g, p, 0, spins, cur, flips);
+  {
+    // split the CTA's 32 warps between plane producers and flip consumers in
+    // proportion to the work: a flip quad costs ~1/16 of a piece's draws per
+    // word, but is latency-bound, so weight it up
+    static const int env_cw = [] { const char* e = getenv("MSB_FLIP_WARPS"); return e ? atoi(e) : 0; }();
+    const Geo G = make_geo(g);
+    const double draws = 2.0 * g->n_sim * g->rows * (double)(g->n / 2);
+    const double quads = 2.0 * g->n_sim * g->rows * (G.Wp / 4);
+    int cw = (int)std::lround(32.0 * (quads * 48.0) / (draws + quads * 48.0));
+    cw = std::max(4, std::min(12, cw));
+    // never add a producer round: keep ceil(units / (SMs * producers)) minimal
+    const long long units = (2LL * g->n_sim * g->rows * p->kg + 31) / 32;
+    const int sms_est = 148;
+    auto rounds = [&](int c) { return (units + (long long)sms_est * (32 - c) - 1) / ((long long)sms_est * (32 - c)); };
+    if (rounds(2) == 1)  // single-round problems: every producer warp counts
+      while (cw > 2 && rounds(cw) > 1) cw--;
+    fa.cwarps = env_cw > 0 ? std::min(28, env_cw) : cw;
+  }
+  int dev = 0, sms = 148;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  static std::once_flag o;
+  static cudaError_t e;
+  if (int r = set_smem_attr(k_sweep_fused<2>, o, e)) return r;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)sms);
+  cfg.blockDim = dim3(kRngThreads);
+  cfg.dynamicSmemBytes = (size_t)kJumpWords * 4;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, k_sweep_fused<2>, ra, fa));
+  return MSB_OK;
+}
 }  // namespace
 
 // ===========================================================================
@@ -948,12 +1096,12 @@ int64_t msb_pieces_per_phase(const msb_geom* g, int32_t kg) {
 
 int32_t msb_default_kg(const msb_geom* g) {
   if (check_geom(g)) return -1;
-  // Enough pieces to fill 148 SMs x ~24 warps, but pieces long enough that
-  // the per-sweep jump (~500 ops) stays a few percent of the draws.
-  const long long rows = (long long)g->n_sim * g->rows;
-  const int words = g->n / 32;
+  // Smallest split giving ~one warp-unit (32 pieces) per producer warp of
+  // every SM (148 SMs x 28 warps); longer pieces amortise the per-sweep
+  // jump (64 table lookups) better.
+  const long long rows2 = 2LL * g->n_sim * g->rows;
   int kg = 1;
-  while (kg < 16 && rows * kg < 148LL * 24 * 32 && (16 / (kg * 2)) * words >= 256) kg *= 2;
+  while (kg < 16 && rows2 * kg < 118000) kg *= 2;
   return kg;
 }
 
@@ -1160,55 +1308,47 @@ int msb_phase(const msb_geom* g, const msb_sweep_params* p, int32_t phase, uint3
 }
 
 int msb_sweep(const msb_geom* g, const msb_sweep_params* p, uint32_t* spins, uint32_t* states, uint32_t* planes,
-              int32_t n_sweeps, int32_t overlap, uint64_t* flips, void* stream) {
+              int32_t n_sweeps, int32_t flags, int32_t* cur_io, uint64_t* flips, void* stream) {
   if (int r = check_geom(g)) return r;
   if (int r = check_params(p)) return r;
   if (n_sweeps < 0) return fail(MSB_ERR_ARG, "sweep count must be non-negative");
   if (!spins || !states || !planes || !flips || !p->jump) return fail(MSB_ERR_ARG, "null buffer");
   if (g->ghost) return fail(MSB_ERR_UNSUPPORTED, "msb_sweep runs whole lattices; slabs use the per-phase calls");
+  if ((flags & (MSB_SWEEP_AHEAD_IN | MSB_SWEEP_AHEAD_OUT)) && !cur_io)
+    return fail(MSB_ERR_ARG, "lookahead flags need cur_io");
   cudaStream_t st = as_stream(stream);
-  if (n_sweeps == 0) return MSB_OK;
-  if (!overlap) {
-    for (int k = 0; k < n_sweeps; k++) {
-      if (int r = rng_planes(g, p, -1, states, nullptr, planes, st)) return r;
-      if (int r = flip(g, p, 0, spins, planes, flips, st)) return r;
-      if (int r = flip(g, p, 1, spins, planes, flips, st)) return r;
+  const int64_t pw = msb_plane_words(g, p->n_planes);
+  int cur = (flags & MSB_SWEEP_AHEAD_IN) ? (*cur_io & 1) : 0;
+  const bool fused_ok = p->mode != MSB_MODE_GENERIC && !(flags & MSB_SWEEP_SERIAL);
+  if (n_sweeps == 0) {
+    if ((flags & MSB_SWEEP_AHEAD_OUT) && !(flags & MSB_SWEEP_AHEAD_IN)) {
+      if (int r = rng_planes(g, p, -1, states, nullptr, planes + (size_t)cur * pw, st)) return r;
     }
+    if (cur_io) *cur_io = cur;
     return MSB_OK;
   }
-  // Two plane buffers; the RNG of sweep k+1 (helper stream) overlaps the
-  // flips of sweep k (caller stream).
-  const int64_t pw = msb_plane_words(g, p->n_planes);
-  cudaStream_t aux;
-  CUDA_TRY(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
-  cudaEvent_t ev_start, ev_r[2], ev_f[2];
-  CUDA_TRY(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
-  for (int b = 0; b < 2; b++) {
-    CUDA_TRY(cudaEventCreateWithFlags(&ev_r[b], cudaEventDisableTiming));
-    CUDA_TRY(cudaEventCreateWithFlags(&ev_f[b], cudaEventDisableTiming));
+  if (!(flags & MSB_SWEEP_AHEAD_IN)) {
+    if (int r = rng_planes(g, p, -1, states, nullptr, planes + (size_t)cur * pw, st)) return r;
   }
-  int status = MSB_OK;
-  CUDA_TRY(cudaEventRecord(ev_start, st));
-  CUDA_TRY(cudaStreamWaitEvent(aux, ev_start, 0));
-  for (int k = 0; k < n_sweeps && status == MSB_OK; k++) {
-    const int b = k & 1;
-    uint32_t* buf = planes + (size_t)b * pw;
-    if (k >= 2) CUDA_TRY(cudaStreamWaitEvent(aux, ev_f[b], 0));
-    status = rng_planes(g, p, -1, states, nullptr, buf, aux);
-    if (status) break;
-    CUDA_TRY(cudaEventRecord(ev_r[b], aux));
-    CUDA_TRY(cudaStreamWaitEvent(st, ev_r[b], 0));
-    status = flip(g, p, 0, spins, buf, flips, st);
-    if (!status) status = flip(g, p, 1, spins, buf, flips, st);
-    CUDA_TRY(cudaEventRecord(ev_f[b], st));
+  for (int k = 0; k < n_sweeps; k++) {
+    uint32_t* bc = planes + (size_t)cur * pw;
+    uint32_t* bn = planes + (size_t)(1 - cur) * pw;
+    const bool last = k + 1 == n_sweeps;
+    if (last && !(flags & MSB_SWEEP_AHEAD_OUT)) {
+      if (int r = flip(g, p, 0, spins, bc, flips, st)) return r;
+      if (int r = flip(g, p, 1, spins, bc, flips, st)) return r;
+    } else if (fused_ok) {
+      if (int r = fused_sweep(g, p, spins, states, bc, bn, flips, st)) return r;
+      cur = 1 - cur;
+    } else {
+      if (int r = flip(g, p, 0, spins, bc, flips, st)) return r;
+      if (int r = flip(g, p, 1, spins, bc, flips, st)) return r;
+      if (int r = rng_planes(g, p, -1, states, nullptr, bn, st)) return r;
+      cur = 1 - cur;
+    }
   }
-  cudaEventDestroy(ev_start);
-  for (int b = 0; b < 2; b++) {
-    cudaEventDestroy(ev_r[b]);
-    cudaEventDestroy(ev_f[b]);
-  }
-  cudaStreamDestroy(aux);
-  return status;
+  if (cur_io) *cur_io = cur;
+  return MSB_OK;
 }
 
 int msb_observe(const msb_geom* g, const uint32_t* spins, int64_t* ups, int64_t* unsat, void* stream) {

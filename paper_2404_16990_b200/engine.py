@@ -36,7 +36,8 @@ from concurrent.futures import ThreadPoolExecutor
 import numpy as np
 
 from . import _lib
-from ._lib import call, geom, SweepParams, MSB_FLIP_SLOTS, MSB_MAX_PLANES
+from ._lib import (call, geom, SweepParams, MSB_FLIP_SLOTS, MSB_MAX_PLANES, MSB_SWEEP_AHEAD_IN,
+                   MSB_SWEEP_AHEAD_OUT, MSB_SWEEP_SERIAL)
 from .layout import (
     ALL_CODES, ArrayCode, LatticeDims, PackedArrays, check_spins, halo_audit_index, unpack,
 )
@@ -180,7 +181,7 @@ class Engine:
             pw = int(_lib.lib().msb_plane_words(ctypes.byref(self._g), MSB_MAX_PLANES))
             self._plane_words = pw
             self._planes = torch.empty(2 * pw, dtype=torch.int32, device=self.device)
-            self._work = torch.zeros(2, dtype=torch.int32, device=self.device)
+            self._work = torch.zeros(4, dtype=torch.int32, device=self.device)
             self._obs = torch.zeros(2 * self.n_sim, dtype=torch.int64, device=self.device)
         self._pow = _pow_tables(self.device)
         self._jump = _sweep_jump_table(self.device, dims.n)
@@ -207,6 +208,9 @@ class Engine:
         self.streams = DeviceStreams(self.seed, self.n_sim * dims.cells, self.sim_offset * dims.cells)
         self._blocks = 0        # stream blocks consumed (one per colour phase)
         self._pos = [0, 1]      # block each colour's pieces are positioned at
+        self._ahead = False     # next sweep's accept planes already generated (states one sweep on)
+        self._ahead_key = None
+        self._cur = 0           # plane buffer holding the lookahead
         self._ver = 0           # device-state version
         self._mirror = None     # host uint16 state mirror
         self._mirror_snap = None
@@ -370,7 +374,17 @@ class Engine:
                     r = draws[:, :, q, 4 * i + ii, :].astype(np.float64) * _UNIT
                     self.recorder.record(self.sweeps_done, target, 4 * ii + i, r)
 
+    def _drop_ahead(self) -> None:
+        """Discard pre-generated planes: put the stream pieces back at the
+        logical position (the next unconsumed block)."""
+        if self._ahead:
+            call("msb_rng_init", ctypes.byref(self._g), ctypes.c_uint64(self.seed & _M64), self.kg,
+                 ctypes.c_uint64(self._blocks), -1, _p(self._pow), _p(self._states), self._cs)
+            self._pos = [self._blocks, self._blocks + 1]
+            self._ahead = False
+
     def _phase(self, phase: int) -> None:
+        self._drop_ahead()
         self._push_host_edits()
         self._sync_tables()
         self._params.fault = int(bool(self.fault))
@@ -431,31 +445,38 @@ class Engine:
         self._push_host_edits()
         self._sync_tables()
         self._params.fault = int(bool(self.fault))
-        call("msb_sweep", ctypes.byref(self._g), ctypes.byref(self._params), _p(self._spins),
-             _p(self._states), _p(self._planes), k, int(self.overlap and k > 1), _p(self._flips_dev), self._cs)
-        self._blocks += 2 * k
-        self._pos = [self._blocks, self._blocks + 1]
+        self._sweep_call(k)
         self.sweeps_done += k
         self.attempts += self.dims.sites * self.n_sim * k
         self._touch()
 
-    def _timed_sweep(self, ev0, ev1, ev2) -> None:
-        """One sweep as its three kernels with CUDA events between them
-        (accept planes | red flips + blue flips); used by bench.py."""
+    def _sweep_call(self, k: int) -> None:
+        if self._ahead and self._ahead_key != self._tab_key:
+            self._drop_ahead()
+        flags = MSB_SWEEP_AHEAD_OUT | (MSB_SWEEP_AHEAD_IN if self._ahead else 0)
+        if not self.overlap:
+            flags |= MSB_SWEEP_SERIAL
+        cur = ctypes.c_int32(self._cur)
+        call("msb_sweep", ctypes.byref(self._g), ctypes.byref(self._params), _p(self._spins),
+             _p(self._states), _p(self._planes), k, flags, ctypes.byref(cur), _p(self._flips_dev), self._cs)
+        self._cur = cur.value
+        self._ahead = True
+        self._ahead_key = self._tab_key
+        self._blocks += 2 * k
+        self._pos = [self._blocks, self._blocks + 1]
+
+    def _timed_sweep(self, ev0, ev1) -> None:
+        """One sweep of the fast path bracketed by CUDA events (bench.py):
+        in steady state one fused launch (flips of this sweep + planes of
+        the next)."""
         if not self._fast_path_ok():
             raise RuntimeError("timed sweeps need the engine's own sweep path")
         self._push_host_edits()
         self._sync_tables()
         self._params.fault = int(bool(self.fault))
-        g, prm = ctypes.byref(self._g), ctypes.byref(self._params)
         ev0.record(self._stream)
-        call("msb_rng_planes", g, prm, -1, _p(self._states), None, _p(self._planes), self._cs)
+        self._sweep_call(1)
         ev1.record(self._stream)
-        call("msb_flip", g, prm, 0, _p(self._spins), _p(self._planes), _p(self._flips_dev), self._cs)
-        call("msb_flip", g, prm, 1, _p(self._spins), _p(self._planes), _p(self._flips_dev), self._cs)
-        ev2.record(self._stream)
-        self._blocks += 2
-        self._pos = [self._blocks, self._blocks + 1]
         self.sweeps_done += 1
         self.attempts += self.dims.sites * self.n_sim
         self._touch()
