@@ -1,0 +1,164 @@
+"""The C-ABI library on the host (no GPU): it loads, exports every symbol
+include/msb200.h declares, validates geometry like LatticeDims, and its host
+pieces -- the threshold planner and the GF(2) jump-ahead tables -- are exact
+against the float64 compare and the oracle's stream."""
+import ctypes
+import math
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from paper_2404_16990_b200 import _lib
+from paper_2404_16990_b200._lib import call, geom
+from paper_2404_16990_b200.engine import build_exp_table
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def test_exports_every_declared_symbol():
+    header = (ROOT / "include" / "msb200.h").read_text()
+    declared = set(re.findall(r"^\s*(?:const\s+)?[\w\s\*]+?\b(msb_\w+)\s*\(", header, re.M))
+    assert len(declared) >= 25
+    L = _lib.lib()
+    missing = [name for name in sorted(declared) if not hasattr(L, name)]
+    assert not missing, missing
+    assert set(_lib.EXPORTS) <= declared
+    assert L.msb_abi_version() == 1
+
+
+def test_geometry_validation_messages():
+    L = _lib.lib()
+    assert L.msb_check_geom(ctypes.byref(geom(1, 12, 96))) == 0
+    for g, text in [(geom(1, 6, 96), "multiple of 4"), (geom(1, 12, 48), "multiple of 32"),
+                    (geom(0, 12, 96), "replica"), (geom(1, 12, 96, row0=2, rows=4), "whole lattice")]:
+        assert L.msb_check_geom(ctypes.byref(g)) == -1
+        assert text in L.msb_last_error().decode()
+    with pytest.raises(_lib.MsbError, match="multiple of 4"):
+        call("msb_check_geom", ctypes.byref(geom(1, 10, 96)))
+
+
+def test_sizes():
+    L = _lib.lib()
+    g = geom(64, 1024, 1024)
+    assert L.msb_row_pitch(ctypes.byref(g)) == 16             # 32 words of 16 bits -> 16 uint32
+    assert L.msb_spin_words(ctypes.byref(g)) == 64 * 2 * 1024 * 16
+    assert L.msb_pieces_per_phase(ctypes.byref(g), 2) == 64 * 1024 * 2
+    assert L.msb_default_kg(ctypes.byref(g)) == 1
+    assert L.msb_default_kg(ctypes.byref(geom(1, 14336, 14336))) == 8
+
+
+def plan(tables):
+    tables = np.ascontiguousarray(tables, np.float64)
+    n_sim = tables.shape[0]
+    mode, npl = ctypes.c_int32(), ctypes.c_int32()
+    codes = (ctypes.c_int8 * 16)()
+    thr = np.zeros(10 * n_sim, np.uint32)
+    call("msb_plan_thresholds", tables.ctypes.data_as(ctypes.c_void_p), n_sim, ctypes.byref(mode),
+         ctypes.byref(npl), codes, thr.ctypes.data_as(ctypes.c_void_p))
+    return mode.value, npl.value, list(codes), thr.reshape(10, n_sim)
+
+
+def accepts(key, u):
+    """Device rule: reject iff (u << 9) >= key (uint32)."""
+    return ((u.astype(np.uint64) << 9) & 0xFFFFFFFF) < key if key != 0xFFFFFFFF else np.ones_like(u, bool)
+
+
+@pytest.mark.parametrize("T,J", [(2.269, 1.0), (0.5, 1.0), (1.0, 1.0), (5.0, 1.0), (1e-6, 1.0), (3.0, 2.0),
+                                 (1.5, -1.0), (2.0, 0.0), (1e300, 1.0)])
+def test_integer_keys_equal_float64_compare(T, J):
+    """For every 23-bit draw, (u<<9) < key  <=>  u * 2**-23 < table[code]
+    (engine.py:325-330), exhaustively."""
+    table = build_exp_table(T, J)
+    mode, npl, codes, thr = plan(table[None, :])
+    assert mode == (1 if J < 0 else 0)
+    u = np.arange(1 << 23, dtype=np.uint32)
+    r = u.astype(np.float64) * 2.0 ** -23
+    for code in range(16):
+        if code & 7 > 4:
+            continue
+        pl = codes[code]
+        want = r < table[code]
+        if pl == -2:
+            got = np.ones_like(want)
+        elif pl == -1:
+            got = np.zeros_like(want)
+        else:
+            got = accepts(int(thr[pl, 0]), u)
+        assert (got == want).all(), (T, J, code)
+
+
+def test_generic_planes_for_forced_tables():
+    n = 3
+    for value, planes in [(0.5, 1), (0.0, 0), (1.0, 0)]:
+        mode, npl, codes, thr = plan(np.full((n, 16), value))
+        if value == 1.0:
+            assert mode == 0  # all-accept fits the ferro structure
+        else:
+            assert mode == 2 and npl == planes
+    rng = np.random.default_rng(1)
+    t = rng.random((4, 16))
+    mode, npl, codes, thr = plan(t)
+    assert mode == 2 and npl == 10  # every valid code distinct
+    u = np.arange(0, 1 << 23, 977, dtype=np.uint32)
+    r = u.astype(np.float64) * 2.0 ** -23
+    for s in range(4):
+        for code in range(16):
+            if code & 7 <= 4:
+                assert (accepts(int(thr[codes[code], s]), u) == (r < t[s, code])).all()
+
+
+# ---- GF(2) jump-ahead vs the oracle's sequential stream -------------------
+
+M64 = (1 << 64) - 1
+
+
+def apply_table(table, s):
+    """Host application of a nibble table to a state [s0..s3] (uint64)."""
+    words = []
+    for v in s:
+        words += [v & 0xFFFFFFFF, v >> 32]
+    r = np.zeros(8, np.uint64)
+    t = table.reshape(64, 16, 8).astype(np.uint64)
+    for p in range(64):
+        nib = (words[p // 8] >> (4 * (p % 8))) & 15
+        r ^= t[p, nib]
+    return [int(r[2 * k]) | (int(r[2 * k + 1]) << 32) for k in range(4)]
+
+
+def xnext(s):
+    x = (s[0] + s[3]) & M64
+    out = ((((x << 23) | (x >> 41)) & M64) + s[0]) & M64
+    t = (s[1] << 17) & M64
+    s[2] ^= s[0]; s[3] ^= s[1]; s[1] ^= s[2]; s[0] ^= s[3]; s[2] ^= t
+    s[3] = ((s[3] << 45) | (s[3] >> 19)) & M64
+    return out
+
+
+@pytest.mark.parametrize("J", [1, 7, 64, 4 * 1024, 4 * 14336, 123456789, (1 << 40) + 5])
+def test_jump_table_equals_sequential_stream(J):
+    table = np.empty(8192, np.uint32)
+    call("msb_rng_jump_table", ctypes.c_uint64(J), table.ctypes.data_as(ctypes.c_void_p))
+    s = apply_table(table, orc.stream_state(2024, 5))
+    got = [xnext(s) for _ in range(4)]
+    if J < 10 ** 6:
+        want = [int(v) for v in orc.raw64(2024, 5, 4, skip=J)]
+        assert got == want
+    else:  # compose two smaller jumps instead of stepping 2^40 times
+        half = np.empty(8192, np.uint32)
+        call("msb_rng_jump_table", ctypes.c_uint64(J // 2), half.ctypes.data_as(ctypes.c_void_p))
+        s2 = apply_table(half, apply_table(half, orc.stream_state(2024, 5)))
+        if J % 2:
+            xnext(s2)
+        assert got == [xnext(s2) for _ in range(4)]
+
+
+def test_power_tables_are_powers_of_two_jumps():
+    pw = np.empty(64 * 8192, np.uint32)
+    call("msb_rng_power_tables", pw.ctypes.data_as(ctypes.c_void_p))
+    for b in (0, 1, 5, 17, 33, 63):
+        one = np.empty(8192, np.uint32)
+        call("msb_rng_jump_table", ctypes.c_uint64(1 << b), one.ctypes.data_as(ctypes.c_void_p))
+        assert (pw[b * 8192:(b + 1) * 8192] == one).all()
