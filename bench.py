@@ -220,7 +220,7 @@ def run_ours(args, cfg):
     n_sim = cfg["n_sim"]
     temps = list(cfg["temps"](n_sim))
     eng = Engine(LatticeDims(cfg["m"], cfg["n"]), temps, cfg["seed"], init=cfg["init"],
-                 sim_offset=rank * n_sim, device=dev, kg=args.kg)
+                 sim_offset=rank * n_sim, device=dev, kg=args.kg, stream=args.stream)
     st = eng._stream
     attempts_step = n_sim * cfg["m"] * cfg["n"]
     peak = int_peak_tops(st)
@@ -329,6 +329,8 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2")
     ap.add_argument("--kg", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--stream", choices=["xoshiro", "philox"], default="xoshiro",
+                    help="xoshiro: the reference's own streams (default); philox: counter-based (SURVEY F1)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

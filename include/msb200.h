@@ -49,6 +49,16 @@ extern "C" {
 
 #define MSB_MAX_PLANES 10
 
+/* Flip-draw streams.  XOSHIRO: the reference's own per-(replica, cell)
+ * xoshiro256++ streams (rng.py:150-220), persistent per-piece states + GF(2)
+ * jump-ahead.  PHILOX: counter-based Philox4x32-10, draw d of stream S =
+ * low 23 bits of word d&3 of Philox(counter = (d>>2, S), key = seed); the
+ * same stream on the host is paper_2404_16990_b200.rng.PhiloxStreams, which
+ * the reference Engine accepts through its duck-typed `streams` seam
+ * (engine.py:259-261, 336). */
+#define MSB_RNG_XOSHIRO 0
+#define MSB_RNG_PHILOX 1
+
 typedef struct msb_geom {
   int32_t n_sim;      /* replicas in the buffer */
   int32_t m, n;       /* full lattice extents (LatticeDims, lattice.py:97-136) */
@@ -69,6 +79,10 @@ typedef struct msb_sweep_params {
   int32_t block_rows;            /* reserved, 0 */
   uint32_t *work;                /* device: 4 uint32 scratch counters, zeroed once by the caller;
                                     every kernel leaves them zeroed */
+  int32_t rng;                   /* MSB_RNG_XOSHIRO (reference streams) or MSB_RNG_PHILOX */
+  uint64_t seed;                 /* Philox key (the engine's master seed) */
+  uint64_t block;                /* Philox: stream block (2 per sweep; red = even) of the first
+                                    phase whose draws the call generates */
 } msb_sweep_params;
 
 /* ---- status -------------------------------------------------------------- */
@@ -170,7 +184,7 @@ int msb_observe(const msb_geom *g, const uint32_t *spins, int64_t *ups, int64_t 
 /* ---- record/replay support (reference.py:179-208) ------------------------ */
 /* The u23 draws the next `phase` would consume, in the reference block order
  * [n_sim][m/4][4][16][n/32], without advancing the states. */
-int msb_draws(const msb_geom *g, int32_t kg, int32_t phase, const uint32_t *states,
+int msb_draws(const msb_geom *g, const msb_sweep_params *p, int32_t phase, const uint32_t *states,
               uint32_t *out, void *stream);
 
 /* ---- slab halo helpers (row-slab decomposition over GPUs) ----------------- */

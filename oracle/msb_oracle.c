@@ -284,3 +284,68 @@ void orc_draw_map_sweep(int m, int n, uint64_t *states, double *map) {
     }
   }
 }
+
+/* ---- counter-based stream (paper_2404_16990_b200.rng.PhiloxStreams)
+ * Philox4x32-10 (Salmon et al., SC'11).  Draw d of stream S under seed K:
+ * low 23 bits of word d&3 of Philox(counter = (d>>2 lo, hi, S lo, hi),
+ * key = (K lo, K hi)).  Consumed by the reference Engine exactly like its
+ * xoshiro streams (engine.py:336): a phase takes the stream's next 2n draws. */
+static void philox10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+  for (int r = 0; r < 10; r++) {
+    const uint64_t p0 = (uint64_t)c[0] * 0xD2511F53u, p1 = (uint64_t)c[2] * 0xCD9E8D57u;
+    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c[1] ^ k0, n2 = (uint32_t)(p0 >> 32) ^ c[3] ^ k1;
+    c[1] = (uint32_t)p1;
+    c[3] = (uint32_t)p0;
+    c[0] = n0;
+    c[2] = n2;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
+uint32_t orc_philox_draw(uint64_t seed, uint64_t stream, uint64_t d) {
+  uint32_t c[4] = {(uint32_t)(d >> 2), (uint32_t)(d >> 34), (uint32_t)stream, (uint32_t)(stream >> 32)};
+  philox10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+  return c[d & 3] & 0x7FFFFF;
+}
+
+typedef struct { int m, n, phase; uint64_t seed, sim_offset, block; const double *table; int8_t *spins; } pphase_ctx;
+static void pphase_body(long lo, long hi, void *vctx, uint64_t *acc) {
+  pphase_ctx *x = (pphase_ctx *)vctx;
+  const int m = x->m, n = x->n, cells = m / 4, words = n / 32, red = x->phase == 0;
+  const uint64_t sites = (uint64_t)m * n;
+  for (long sg = lo; sg < hi; sg++) {
+    const int s = (int)(sg / cells), g = (int)(sg % cells) + 1;
+    const uint64_t stream = (x->sim_offset + (uint64_t)s) * (uint64_t)cells + (uint64_t)(g - 1);
+    int8_t *lat = x->spins + (uint64_t)s * sites;
+    const double *tab = x->table + 16 * s;
+    uint64_t d = x->block * 2 * (uint64_t)n, local = 0;
+    for (int q = 0; q < 4; q++) {
+      const int even = Q_EVEN[q];
+      const int c = target_column(m, red, Q_FWD[q], even, g);
+      const int p0 = even ? 0 : 1;
+      const int8_t *up = lat + (uint64_t)((c + 1) % m) * n, *dn = lat + (uint64_t)((c + m - 1) % m) * n;
+      int8_t *row = lat + (uint64_t)c * n;
+      for (int k = 0; k < 16; k++) {
+        const int t = 4 * (k % 4) + k / 4;
+        for (int w = 0; w < words; w++, d++) {
+          const double u = (double)orc_philox_draw(x->seed, stream, d) * (1.0 / 8388608.0);
+          const int r = 32 * w + 2 * t + p0;
+          const int ru = r + 1 == n ? 0 : r + 1, rd = r == 0 ? n - 1 : r - 1;
+          const int own = row[r] > 0;
+          const int n_up = (up[r] > 0) + (dn[r] > 0) + (row[ru] > 0) + (row[rd] > 0);
+          if (u < tab[8 * own + n_up]) {
+            row[r] = (int8_t)-row[r];
+            local++;
+          }
+        }
+      }
+    }
+    *acc += local;
+  }
+}
+void orc_flip_phase_philox(int n_sim, int m, int n, int phase, uint64_t seed, uint64_t sim_offset, uint64_t block,
+                           const double *table, int8_t *spins, uint64_t *flips) {
+  pphase_ctx x = {m, n, phase, seed, sim_offset, block, table, spins};
+  *flips += par_for((long)n_sim * (m / 4), pphase_body, &x);
+}

@@ -50,6 +50,9 @@ def lib():
         L.orc_observe.argtypes = [i32, i32, i32, vp, vp, vp]
         L.orc_draw_map_sweep.argtypes = [i32, i32, vp, vp]
         L.orc_set_threads.argtypes = [i32]
+        L.orc_flip_phase_philox.argtypes = [i32, i32, i32, i32, u64, u64, u64, vp, vp, vp]
+        L.orc_philox_draw.argtypes = [u64, u64, u64]
+        L.orc_philox_draw.restype = ctypes.c_uint32
         L.orc_num_threads.restype = i32
         _lib = L
     return _lib
@@ -109,7 +112,7 @@ class OracleEngine:
     """Plain-lattice restatement of the reference ``Engine``."""
 
     def __init__(self, m, n, temperatures, seed, init="random", coupling=1.0, sim_offset=0,
-                 lattices=None):
+                 lattices=None, stream="xoshiro"):
         if m < 4 or m % 4 or n < 32 or n % 32:
             raise ValueError("bad dims")
         self.m, self.n = int(m), int(n)
@@ -129,6 +132,7 @@ class OracleEngine:
             lib().orc_init_random(self.n_sim, m, n, _u64(self.seed), self.sim_offset, _p(self.spins))
         elif init != "all-up":
             raise ValueError(f"unknown init mode {init!r}")
+        self.stream = stream
         self.sweeps_done = 0
         self.attempts = 0
         self._flips = np.zeros(1, np.uint64)
@@ -143,8 +147,15 @@ class OracleEngine:
 
     def sweep(self, n_sweeps: int = 1) -> None:
         tab = np.ascontiguousarray(self.tables, dtype=np.float64)
-        lib().orc_sweeps(self.n_sim, self.m, self.n, int(n_sweeps), _p(self.states), _p(tab),
-                         _p(self.spins), _p(self._flips))
+        if self.stream == "philox":
+            for k in range(n_sweeps):
+                for ph in (0, 1):
+                    lib().orc_flip_phase_philox(self.n_sim, self.m, self.n, ph, _u64(self.seed), self.sim_offset,
+                                                2 * (self.sweeps_done + k) + ph, _p(tab), _p(self.spins),
+                                                _p(self._flips))
+        else:
+            lib().orc_sweeps(self.n_sim, self.m, self.n, int(n_sweeps), _p(self.states), _p(tab),
+                             _p(self.spins), _p(self._flips))
         self.sweeps_done += n_sweeps
         self.attempts += self.sites * self.n_sim * n_sweeps
 

@@ -15,7 +15,8 @@ import subprocess
 from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libmsb200.so"
+# MSB200_LIB overrides the in-tree library (tuning builds); default is the in-tree .so
+LIB_PATH = Path(os.environ.get("MSB200_LIB", str(_HERE / "libmsb200.so")))
 
 MSB_MODE_FERRO = 0
 MSB_MODE_ANTI = 1
@@ -25,6 +26,8 @@ MSB_FLIP_SLOTS = 256
 MSB_SWEEP_AHEAD_IN = 1
 MSB_SWEEP_AHEAD_OUT = 2
 MSB_SWEEP_SERIAL = 4
+MSB_RNG_XOSHIRO = 0
+MSB_RNG_PHILOX = 1
 
 
 class MsbError(RuntimeError):
@@ -54,6 +57,9 @@ class SweepParams(ctypes.Structure):
         ("fault", ctypes.c_int32),
         ("block_rows", ctypes.c_int32),
         ("work", ctypes.c_void_p),
+        ("rng", ctypes.c_int32),
+        ("seed", ctypes.c_uint64),
+        ("block", ctypes.c_uint64),
     ]
 
 
@@ -114,7 +120,7 @@ def lib() -> ctypes.CDLL:
         "msb_phase": ([G, P, i32, vp, vp, vp, vp, vp, vp], ctypes.c_int),
         "msb_sweep": ([G, P, vp, vp, vp, i32, i32, vp, vp, vp], ctypes.c_int),
         "msb_observe": ([G, vp, vp, vp, vp], ctypes.c_int),
-        "msb_draws": ([G, i32, i32, vp, vp, vp], ctypes.c_int),
+        "msb_draws": ([G, P, i32, vp, vp, vp], ctypes.c_int),
         "msb_pack_edges": ([G, i32, vp, vp, vp], ctypes.c_int),
         "msb_unpack_ghosts": ([G, i32, vp, vp, vp], ctypes.c_int),
         "msb_bench_int_peak": ([i32, i32, vp, vp, vp], ctypes.c_int),

@@ -99,6 +99,25 @@ __device__ __forceinline__ void acc_reject(uint32_t& acc, uint32_t h9, uint32_t 
   asm("{.reg .b32 t;\n\tsub.cc.u32 t, %1, %2;\n\taddc.u32 %0, %0, %0;}" : "+r"(acc) : "r"(h9), "r"(key));
 }
 
+// Philox4x32-10 (Salmon et al., SC'11), the counter-based stream of
+// paper_2404_16990_b200.rng.PhiloxStreams: counter (c0..c3), key (k0, k1).
+// Each round is two IMAD.WIDE (FMA pipe) and two 3-input XORs (ALU); the
+// round keys are warp-uniform.
+__device__ __forceinline__ void philox10(uint32_t& c0, uint32_t& c1, uint32_t& c2, uint32_t& c3, uint32_t k0,
+                                         uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; r++) {
+    const uint64_t p0 = (uint64_t)c0 * 0xD2511F53u, p1 = (uint64_t)c2 * 0xCD9E8D57u;
+    const uint32_t n0 = xor3((uint32_t)(p1 >> 32), c1, k0), n2 = xor3((uint32_t)(p0 >> 32), c3, k1);
+    c1 = (uint32_t)p1;
+    c3 = (uint32_t)p0;
+    c0 = n0;
+    c2 = n2;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {  // rng.py:53-58
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
@@ -192,9 +211,28 @@ __device__ __host__ __forceinline__ RowStream row_stream(int m, int c, int X) {
 // w in order, engine.py:321-330) accumulate straight into one word per
 // chunk.  Row pitch Wp = 16 * nch words, nch = ceil((n/32) / 32).
 
+// Division by a run-time invariant 32-bit divisor with a multiply-high
+// (round-up method): q = (t + ((x - t) >> s1)) >> s2, t = umulhi(x, m).
+struct FastDiv {
+  uint32_t d, m, s1, s2;
+  __host__ void init(uint32_t div) {
+    d = div;
+    uint32_t l = 0;
+    while (l < 32 && (1ull << l) < div) l++;
+    m = (uint32_t)(((1ull << 32) * ((1ull << l) - div)) / div + 1);
+    s1 = l < 1 ? l : 1;
+    s2 = l > 0 ? l - 1 : 0;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t x) const {
+    const uint32_t t = __umulhi(x, m);
+    return (t + ((x - t) >> s1)) >> s2;
+  }
+};
+
 struct Geo {
   int n_sim, m, n, rows, row0, ghost, R, Wp, words, nch;
   long long sim_offset;
+  FastDiv rows_div, quads_div;
 };
 
 __host__ Geo make_geo(const msb_geom* g) {
@@ -205,6 +243,8 @@ __host__ Geo make_geo(const msb_geom* g) {
   o.nch = (o.words + 31) / 32;
   o.Wp = 16 * o.nch;
   o.sim_offset = g->sim_offset;
+  o.rows_div.init((uint32_t)o.rows);
+  o.quads_div.init((uint32_t)(o.Wp / 4));
   return o;
 }
 
@@ -266,8 +306,16 @@ struct RngArgs {
   uint32_t* planes;
   unsigned* work;
   long long npieces;
-  int colour0, ncol, kg, kr, np;
+  int colour0, ncol, kg, kr, np, kg_shift;
+  FastDiv pieces_div;
+  uint32_t seed_lo, seed_hi;  // Philox key
+  unsigned long long block0;  // Philox: stream block of colour0's phase
 };
+
+// draw sources of the producer
+constexpr int kSrcXoshiro = 0;  // persistent per-piece reference streams
+constexpr int kSrcExt = 1;      // host-supplied u23 draws
+constexpr int kSrcPhilox = 2;   // counter-based Philox4x32-10
 
 // reference bit t of a uint16 word is gated by draw k = 4(t%4) + t/4 (the
 // mapping is its own inverse, engine.py:326-330)
@@ -285,12 +333,14 @@ __device__ __forceinline__ size_t plane_off(const Geo& G, int np, int X, int p, 
 // the generation loop, performs the 64 nibble lookups of its jump to the
 // next sweep, so table reads overlap other warps' ALU work.
 constexpr int kRngThreads = 1024;
+#ifndef MSB_CHUNK_UNROLL
+#define MSB_CHUNK_UNROLL 16
+#endif
+constexpr int kChunkUnroll = MSB_CHUNK_UNROLL;
 
 // Work counters (caller-owned, zeroed once, left zeroed by every kernel):
 //   work[0] next dynamic producer unit    work[1] consumer barrier arrivals
 //   work[2] warps finished (last one resets all four)
-constexpr int kWork = 4;
-
 __device__ __forceinline__ void finish_warp(unsigned* work, unsigned total_warps) {
   if ((threadIdx.x & 31) == 0) {
     __threadfence();
@@ -305,9 +355,11 @@ __device__ __forceinline__ void finish_warp(unsigned* work, unsigned total_warps
 // One producer warp's share of a sweep's accept planes.  `role_warp` /
 // `role_warps` number the producer warps of the grid; their first unit is
 // static (interleaved across CTAs), later ones come from work[0].
-template <int NPMAX, bool EXT>
+template <int NPMAX, int SRC>
 __device__ __forceinline__ void rng_produce(const RngArgs& a, const uint4* __restrict__ jt, int role_warp,
                                             int role_warps) {
+  constexpr bool EXT = SRC == kSrcExt;
+  constexpr bool XO = SRC == kSrcXoshiro;
   const Geo& G = a.G;
   const int np = NPMAX == 2 ? 2 : a.np;
   const int lane = threadIdx.x & 31;
@@ -321,11 +373,12 @@ __device__ __forceinline__ void rng_produce(const RngArgs& a, const uint4* __res
     if (u >= units) break;
     const long long gi = u * 32 + lane;
     if (gi < total) {
-    const int X = a.colour0 + (int)(gi / a.npieces);
-    const long long gp = gi - (gi / a.npieces) * a.npieces;
-    const long long gr = gp / a.kg;
-    const int kgi = (int)(gp - gr * a.kg);
-    const int s = (int)(gr / G.rows), lr = (int)(gr - (long long)s * G.rows);
+    const unsigned xi = a.pieces_div.div((unsigned)gi);
+    const int X = a.colour0 + (int)xi;
+    const long long gp = gi - (long long)xi * a.npieces;
+    const unsigned gr = (unsigned)gp >> a.kg_shift;
+    const int kgi = (int)(gp - ((long long)gr << a.kg_shift));
+    const int s = (int)G.rows_div.div(gr), lr = (int)(gr - (unsigned)s * G.rows);
     uint32_t key[NPMAX];
 #pragma unroll
     for (int p = 0; p < NPMAX; p++) key[p] = p < np ? a.thr9[p * G.n_sim + s] : 0u;
@@ -337,12 +390,24 @@ __device__ __forceinline__ void rng_produce(const RngArgs& a, const uint4* __res
     uint32_t jw0 = 0, jw1 = 0, jw2 = 0, jw3 = 0, jw4 = 0, jw5 = 0, jw6 = 0, jw7 = 0;
     uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0, r4 = 0, r5 = 0, r6 = 0, r7 = 0;
     int nib = 0;
-    if (!EXT) {
+    uint32_t ps0 = 0, ps1 = 0;              // Philox: stream id
+    unsigned long long pd0 = 0;             // Philox: draw index of this piece's first draw
+    if (XO) {
       load_state(st, sp, a.npieces, gp);
       jw0 = st.a0; jw1 = st.a1; jw2 = st.b0; jw3 = st.b1; jw4 = st.c0; jw5 = st.c1; jw6 = st.d0; jw7 = st.d1;
     } else {
       const RowStream rsd = row_stream(G.m, G.row0 + lr, X);
-      ext = a.ext + ((((size_t)s * (G.m / 4) + rsd.gamma - 1) * 4 + rsd.q) * 16) * G.words;
+      if (EXT) {
+        ext = a.ext + ((((size_t)s * (G.m / 4) + rsd.gamma - 1) * 4 + rsd.q) * 16) * G.words;
+      } else {
+        const unsigned long long sid =
+            ((unsigned long long)G.sim_offset + (unsigned long long)s) * (unsigned long long)(G.m / 4) +
+            (unsigned long long)(rsd.gamma - 1);
+        ps0 = (uint32_t)sid;
+        ps1 = (uint32_t)(sid >> 32);
+        const unsigned long long n = (unsigned long long)G.n;
+        pd0 = (a.block0 + (unsigned long long)(X - a.colour0)) * 2 * n + (unsigned long long)rsd.q * (n / 2);
+      }
     }
     for (int kk = 0; kk < a.kr; kk++) {
       const int k = kgi * a.kr + kk;
@@ -352,9 +417,37 @@ __device__ __forceinline__ void rng_produce(const RngArgs& a, const uint4* __res
         uint32_t acc[NPMAX];
 #pragma unroll
         for (int p = 0; p < NPMAX; p++) acc[p] = 0;
-        if (!EXT) {
+        if (SRC == kSrcPhilox) {
+          const unsigned long long d0 = pd0 + (unsigned long long)k * G.words + 32 * ch;
+          if ((d0 & 3) == 0 && (L & 3) == 0) {
+            for (int i = 0; i < L; i += 4) {
+              const unsigned long long c = (d0 + i) >> 2;
+              uint32_t x0 = (uint32_t)c, x1 = (uint32_t)(c >> 32), x2 = ps0, x3 = ps1;
+              philox10(x0, x1, x2, x3, a.seed_lo, a.seed_hi);
+              const uint32_t xs[4] = {x0, x1, x2, x3};
+#pragma unroll
+              for (int j = 0; j < 4; j++) {
+                const uint32_t h9 = xs[j] << 9;
+#pragma unroll
+                for (int p = 0; p < NPMAX; p++)
+                  if (p < np) acc_reject(acc[p], h9, key[p]);
+              }
+            }
+          } else {  // draw groups straddle the piece: one block per draw
+            for (int i = 0; i < L; i++) {
+              const unsigned long long d = d0 + i, c = d >> 2;
+              uint32_t x0 = (uint32_t)c, x1 = (uint32_t)(c >> 32), x2 = ps0, x3 = ps1;
+              philox10(x0, x1, x2, x3, a.seed_lo, a.seed_hi);
+              const int e = (int)(d & 3);
+              const uint32_t h9 = (e == 0 ? x0 : e == 1 ? x1 : e == 2 ? x2 : x3) << 9;
+#pragma unroll
+              for (int p = 0; p < NPMAX; p++)
+                if (p < np) acc_reject(acc[p], h9, key[p]);
+            }
+          }
+        } else if (!EXT) {
           if (L == 32) {
-#pragma unroll 8
+#pragma unroll kChunkUnroll
             for (int i = 0; i < 32; i++) {
               const uint32_t h9 = xstep(st) << 9;
 #pragma unroll
@@ -385,7 +478,7 @@ __device__ __forceinline__ void rng_produce(const RngArgs& a, const uint4* __res
       }
       // jump lookups: 64/KR per k-segment, one 32-bit state word (8 nibbles)
       // at a time, XORs paired into 3-input LOP3s
-      if (!EXT && ((kk + 1) * lk) % 8 == 0) {
+      if (XO && ((kk + 1) * lk) % 8 == 0) {
         for (int wcount = (kk + 1) * lk / 8 - nib / 8; wcount > 0; wcount--) {
           const uint4* e = jt + nib * 32;
 #pragma unroll
@@ -401,7 +494,7 @@ __device__ __forceinline__ void rng_produce(const RngArgs& a, const uint4* __res
         }
       }
     }
-    if (!EXT) {
+    if (XO) {
       XState nx;
       nx.a0 = r0; nx.a1 = r1; nx.b0 = r2; nx.b1 = r3; nx.c0 = r4; nx.c1 = r5; nx.d0 = r6; nx.d1 = r7;
       store_state(nx, sp, a.npieces, gp);  // next sweep's start
@@ -413,14 +506,14 @@ __device__ __forceinline__ void rng_produce(const RngArgs& a, const uint4* __res
   }
 }
 
-template <int NPMAX, bool EXT>
+template <int NPMAX, int SRC>
 __global__ void __launch_bounds__(kRngThreads, 1) k_rng_planes(const RngArgs a) {
   extern __shared__ uint4 jt[];  // nibble table of A^(4n), 32 KiB
-  if (!EXT) {
+  if (SRC == kSrcXoshiro) {
     for (int i = threadIdx.x; i < kJumpWords / 4; i += blockDim.x) jt[i] = a.jump[i];
     __syncthreads();
   }
-  rng_produce<NPMAX, EXT>(a, jt, threadIdx.x >> 5, blockDim.x >> 5);
+  rng_produce<NPMAX, SRC>(a, jt, threadIdx.x >> 5, blockDim.x >> 5);
   finish_warp(a.work, gridDim.x * (blockDim.x >> 5));
 }
 
@@ -479,8 +572,8 @@ template <bool GENERIC, bool COHERENT>
 __device__ __forceinline__ unsigned flip_quad(const FlipArgs& a, unsigned i, int X) {
   const Geo& G = a.G;
   const unsigned quads = (unsigned)G.Wp >> 2;
-  const unsigned gr = i / quads, qq = i - gr * quads;
-  const int s = (int)(gr / (unsigned)G.rows), lr = (int)(gr - (unsigned)s * G.rows);
+  const unsigned gr = G.quads_div.div(i), qq = i - gr * quads;
+  const int s = (int)G.rows_div.div(gr), lr = (int)(gr - (unsigned)s * G.rows);
   const int c = G.row0 + lr, br = lr + G.ghost;
   const int ch = (int)(qq >> 2), t0 = 4 * (int)(qq & 3);
   const int w0 = ch * 16 + t0;
@@ -577,17 +670,19 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   return v;
 }
 
-template <int NPMAX>
+template <int NPMAX, int SRC>
 __global__ void __launch_bounds__(kRngThreads, 1) k_sweep_fused(const RngArgs ra, const FlipArgs fa) {
   const int kFlipWarps = fa.cwarps;
   const int kProducerWarps = (kRngThreads >> 5) - kFlipWarps;
   extern __shared__ uint4 jt[];
-  for (int i = threadIdx.x; i < kJumpWords / 4; i += blockDim.x) jt[i] = ra.jump[i];
-  __syncthreads();
+  if (SRC == kSrcXoshiro) {
+    for (int i = threadIdx.x; i < kJumpWords / 4; i += blockDim.x) jt[i] = ra.jump[i];
+    __syncthreads();
+  }
   const int warp = threadIdx.x >> 5;
   const unsigned total_warps = gridDim.x * (blockDim.x >> 5);
   if (warp < kProducerWarps) {
-    rng_produce<NPMAX, false>(ra, jt, warp, kProducerWarps);
+    rng_produce<NPMAX, SRC>(ra, jt, warp, kProducerWarps);
   } else {
     const unsigned quads = (unsigned)fa.G.Wp >> 2;
     const unsigned total = (unsigned)fa.G.n_sim * (unsigned)fa.G.rows * quads;
@@ -834,18 +929,32 @@ __global__ void k_observe(Geo G, const uint32_t* __restrict__ spins, long long* 
 // ---------------------------------------------------------------------------
 
 __global__ void k_draws(Geo G, int X, int kg, int kr, long long npieces, const uint32_t* __restrict__ states,
-                        uint32_t* out) {
+                        int philox, uint32_t seed_lo, uint32_t seed_hi, unsigned long long block, uint32_t* out) {
   const long long gp = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (gp >= npieces) return;
   const long long gr = gp / kg;
   const int kgi = (int)(gp % kg);
   const int s = (int)(gr / G.rows), c = (int)(gr % G.rows);
-  XState st;
-  load_state(st, states + (size_t)X * 8 * npieces, npieces, gp);
   const RowStream rs = row_stream(G.m, c, X);
   uint32_t* o = out + (((size_t)s * (G.m / 4) + rs.gamma - 1) * 4 + rs.q) * 16 * G.words;
+  if (!philox) {
+    XState st;
+    load_state(st, states + (size_t)X * 8 * npieces, npieces, gp);
+    for (int k = kgi * kr; k < (kgi + 1) * kr; k++)
+      for (int w = 0; w < G.words; w++) o[(size_t)k * G.words + w] = xstep(st) & 0x7FFFFFu;
+    return;
+  }
+  const unsigned long long sid = ((unsigned long long)G.sim_offset + s) * (unsigned long long)(G.m / 4) + rs.gamma - 1;
+  const unsigned long long n = (unsigned long long)G.n;
+  const unsigned long long d0 = block * 2 * n + (unsigned long long)rs.q * (n / 2);
   for (int k = kgi * kr; k < (kgi + 1) * kr; k++)
-    for (int w = 0; w < G.words; w++) o[(size_t)k * G.words + w] = xstep(st) & 0x7FFFFFu;
+    for (int w = 0; w < G.words; w++) {
+      const unsigned long long d = d0 + (unsigned long long)k * G.words + w, cc = d >> 2;
+      uint32_t x0 = (uint32_t)cc, x1 = (uint32_t)(cc >> 32), x2 = (uint32_t)sid, x3 = (uint32_t)(sid >> 32);
+      philox10(x0, x1, x2, x3, seed_lo, seed_hi);
+      const int e = (int)(d & 3);
+      o[(size_t)k * G.words + w] = (e == 0 ? x0 : e == 1 ? x1 : e == 2 ? x2 : x3) & 0x7FFFFFu;
+    }
 }
 
 __global__ void k_pack_edges(Geo G, int X, const uint32_t* __restrict__ spins, uint32_t* edge) {
@@ -921,6 +1030,7 @@ int set_smem_attr(K kernel, std::once_flag& once, cudaError_t& err) {
 
 
 int check_params(const msb_sweep_params* p) {
+  // (piece and quad counts are checked against 2^31 where launched)
   if (!p) return fail(MSB_ERR_ARG, "null sweep parameters");
   const int kg = p->kg;
   if (kg != 1 && kg != 2 && kg != 4 && kg != 8 && kg != 16) return fail(MSB_ERR_ARG, "kg must be 1, 2, 4, 8 or 16");
@@ -928,7 +1038,8 @@ int check_params(const msb_sweep_params* p) {
   if (p->mode != MSB_MODE_GENERIC && p->n_planes != 2) return fail(MSB_ERR_ARG, "ferro/anti modes use exactly 2 planes");
   if (p->mode < 0 || p->mode > 2) return fail(MSB_ERR_ARG, "bad mode");
   if (p->n_planes > 0 && !p->thr9) return fail(MSB_ERR_ARG, "null thresholds");
-  if (!p->work) return fail(MSB_ERR_ARG, "null work counter (2 zeroed uint32 per engine)");
+  if (!p->work) return fail(MSB_ERR_ARG, "null work counter (4 zeroed uint32 per engine)");
+  if (p->rng != MSB_RNG_XOSHIRO && p->rng != MSB_RNG_PHILOX) return fail(MSB_ERR_ARG, "unknown rng");
   return MSB_OK;
 }
 
@@ -947,6 +1058,11 @@ void fill_rng_args(RngArgs& a, const msb_geom* g, const msb_sweep_params* p, int
   a.colour0 = colour < 0 ? 0 : colour;
   a.ncol = colour < 0 ? 2 : 1;
   a.work = p->work;
+  a.kg_shift = p->kg == 1 ? 0 : p->kg == 2 ? 1 : p->kg == 4 ? 2 : p->kg == 8 ? 3 : 4;
+  a.pieces_div.init((uint32_t)a.npieces);
+  a.seed_lo = (uint32_t)p->seed;
+  a.seed_hi = (uint32_t)(p->seed >> 32);
+  a.block0 = p->block;
 }
 
 void fill_flip_args(FlipArgs& a, const msb_geom* g, const msb_sweep_params* p, int colour, uint32_t* spins,
@@ -964,6 +1080,7 @@ void fill_flip_args(FlipArgs& a, const msb_geom* g, const msb_sweep_params* p, i
 
 int rng_planes(const msb_geom* g, const msb_sweep_params* p, int colour, uint32_t* states, const uint32_t* ext,
                uint32_t* planes, cudaStream_t st) {
+  if (2LL * g->n_sim * g->rows * p->kg >= (1LL << 31)) return fail(MSB_ERR_UNSUPPORTED, "too many stream pieces");
   RngArgs a;
   fill_rng_args(a, g, p, colour, states, ext, planes);
   int dev = 0, sms = 148;
@@ -973,20 +1090,23 @@ int rng_planes(const msb_geom* g, const msb_sweep_params* p, int colour, uint32_
   const long long per_cta = kRngThreads / 32;
   (void)per_cta;
   const unsigned grid = (unsigned)std::max(1LL, std::min<long long>(sms, units));
-  const size_t smem = ext ? 0 : (size_t)kJumpWords * 4;
-#define MSB_LAUNCH_RNG(NP, EXT)                                               \
+  const size_t smem = (ext || p->rng == MSB_RNG_PHILOX) ? 0 : (size_t)kJumpWords * 4;
+#define MSB_LAUNCH_RNG(NP, SRC)                                               \
   do {                                                                        \
     static std::once_flag o;                                                  \
     static cudaError_t e;                                                     \
-    if (int r = set_smem_attr(k_rng_planes<NP, EXT>, o, e)) return r;         \
-    k_rng_planes<NP, EXT><<<grid, kRngThreads, smem, st>>>(a);                \
+    if (int r = set_smem_attr(k_rng_planes<NP, SRC>, o, e)) return r;         \
+    k_rng_planes<NP, SRC><<<grid, kRngThreads, smem, st>>>(a);                \
   } while (0)
+  const int src = ext ? kSrcExt : (p->rng == MSB_RNG_PHILOX ? kSrcPhilox : kSrcXoshiro);
   if (p->mode != MSB_MODE_GENERIC) {
-    if (ext) MSB_LAUNCH_RNG(2, true);
-    else MSB_LAUNCH_RNG(2, false);
+    if (src == kSrcExt) MSB_LAUNCH_RNG(2, kSrcExt);
+    else if (src == kSrcPhilox) MSB_LAUNCH_RNG(2, kSrcPhilox);
+    else MSB_LAUNCH_RNG(2, kSrcXoshiro);
   } else {
-    if (ext) MSB_LAUNCH_RNG(MSB_MAX_PLANES, true);
-    else MSB_LAUNCH_RNG(MSB_MAX_PLANES, false);
+    if (src == kSrcExt) MSB_LAUNCH_RNG(MSB_MAX_PLANES, kSrcExt);
+    else if (src == kSrcPhilox) MSB_LAUNCH_RNG(MSB_MAX_PLANES, kSrcPhilox);
+    else MSB_LAUNCH_RNG(MSB_MAX_PLANES, kSrcXoshiro);
   }
 #undef MSB_LAUNCH_RNG
   CUDA_TRY(cudaGetLastError());
@@ -1038,20 +1158,23 @@ int fused_sweep(const msb_geom* g, const msb_sweep_params* p, uint32_t* spins, u
   int dev = 0, sms = 148;
   CUDA_TRY(cudaGetDevice(&dev));
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  static std::once_flag o;
-  static cudaError_t e;
-  if (int r = set_smem_attr(k_sweep_fused<2>, o, e)) return r;
+  const bool philox = p->rng == MSB_RNG_PHILOX;
+  static std::once_flag o, o2;
+  static cudaError_t e, e2;
+  if (int r = set_smem_attr(k_sweep_fused<2, kSrcXoshiro>, o, e)) return r;
+  if (int r = set_smem_attr(k_sweep_fused<2, kSrcPhilox>, o2, e2)) return r;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)sms);
   cfg.blockDim = dim3(kRngThreads);
-  cfg.dynamicSmemBytes = (size_t)kJumpWords * 4;
+  cfg.dynamicSmemBytes = philox ? 0 : (size_t)kJumpWords * 4;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, k_sweep_fused<2>, ra, fa));
+  if (philox) CUDA_TRY(cudaLaunchKernelEx(&cfg, k_sweep_fused<2, kSrcPhilox>, ra, fa));
+  else CUDA_TRY(cudaLaunchKernelEx(&cfg, k_sweep_fused<2, kSrcXoshiro>, ra, fa));
   return MSB_OK;
 }
 }  // namespace
@@ -1287,7 +1410,8 @@ int msb_rng_planes(const msb_geom* g, const msb_sweep_params* p, int32_t colour,
   if (colour < -1 || colour > 1) return fail(MSB_ERR_ARG, "colour must be -1 (both), 0 or 1");
   if (!planes) return fail(MSB_ERR_ARG, "null planes buffer");
   if (ext_draws && (g->ghost || colour < 0)) return fail(MSB_ERR_UNSUPPORTED, "external draws: one colour of a whole lattice");
-  if (!ext_draws && (!states || !p->jump)) return fail(MSB_ERR_ARG, "null RNG state or jump table");
+  if (!ext_draws && p->rng == MSB_RNG_XOSHIRO && (!states || !p->jump))
+    return fail(MSB_ERR_ARG, "null RNG state or jump table");
   return rng_planes(g, p, colour, states, ext_draws, planes, as_stream(stream));
 }
 
@@ -1312,23 +1436,30 @@ int msb_sweep(const msb_geom* g, const msb_sweep_params* p, uint32_t* spins, uin
   if (int r = check_geom(g)) return r;
   if (int r = check_params(p)) return r;
   if (n_sweeps < 0) return fail(MSB_ERR_ARG, "sweep count must be non-negative");
-  if (!spins || !states || !planes || !flips || !p->jump) return fail(MSB_ERR_ARG, "null buffer");
+  if (!spins || !planes || !flips) return fail(MSB_ERR_ARG, "null buffer");
+  if (p->rng == MSB_RNG_XOSHIRO && (!states || !p->jump)) return fail(MSB_ERR_ARG, "null RNG state or jump table");
   if (g->ghost) return fail(MSB_ERR_UNSUPPORTED, "msb_sweep runs whole lattices; slabs use the per-phase calls");
   if ((flags & (MSB_SWEEP_AHEAD_IN | MSB_SWEEP_AHEAD_OUT)) && !cur_io)
     return fail(MSB_ERR_ARG, "lookahead flags need cur_io");
   cudaStream_t st = as_stream(stream);
   const int64_t pw = msb_plane_words(g, p->n_planes);
+  // p->block: stream block of the red phase of the first sweep whose planes
+  // this call generates (Philox); advanced by 2 per generated sweep
+  msb_sweep_params q = *p;
+  p = &q;
   int cur = (flags & MSB_SWEEP_AHEAD_IN) ? (*cur_io & 1) : 0;
   const bool fused_ok = p->mode != MSB_MODE_GENERIC && !(flags & MSB_SWEEP_SERIAL);
   if (n_sweeps == 0) {
     if ((flags & MSB_SWEEP_AHEAD_OUT) && !(flags & MSB_SWEEP_AHEAD_IN)) {
       if (int r = rng_planes(g, p, -1, states, nullptr, planes + (size_t)cur * pw, st)) return r;
+      q.block += 2;
     }
     if (cur_io) *cur_io = cur;
     return MSB_OK;
   }
   if (!(flags & MSB_SWEEP_AHEAD_IN)) {
     if (int r = rng_planes(g, p, -1, states, nullptr, planes + (size_t)cur * pw, st)) return r;
+    q.block += 2;
   }
   for (int k = 0; k < n_sweeps; k++) {
     uint32_t* bc = planes + (size_t)cur * pw;
@@ -1339,11 +1470,13 @@ int msb_sweep(const msb_geom* g, const msb_sweep_params* p, uint32_t* spins, uin
       if (int r = flip(g, p, 1, spins, bc, flips, st)) return r;
     } else if (fused_ok) {
       if (int r = fused_sweep(g, p, spins, states, bc, bn, flips, st)) return r;
+      q.block += 2;
       cur = 1 - cur;
     } else {
       if (int r = flip(g, p, 0, spins, bc, flips, st)) return r;
       if (int r = flip(g, p, 1, spins, bc, flips, st)) return r;
       if (int r = rng_planes(g, p, -1, states, nullptr, bn, st)) return r;
+      q.block += 2;
       cur = 1 - cur;
     }
   }
@@ -1362,15 +1495,20 @@ int msb_observe(const msb_geom* g, const uint32_t* spins, int64_t* ups, int64_t*
   return MSB_OK;
 }
 
-int msb_draws(const msb_geom* g, int32_t kg, int32_t phase, const uint32_t* states, uint32_t* out, void* stream) {
+int msb_draws(const msb_geom* g, const msb_sweep_params* p, int32_t phase, const uint32_t* states, uint32_t* out,
+              void* stream) {
   if (int r = check_geom(g)) return r;
   if (g->ghost) return fail(MSB_ERR_UNSUPPORTED, "draw export needs a whole lattice");
+  if (!p) return fail(MSB_ERR_ARG, "null parameters");
+  const int kg = p->kg;
   if (kg != 1 && kg != 2 && kg != 4 && kg != 8 && kg != 16) return fail(MSB_ERR_ARG, "kg must be 1, 2, 4, 8 or 16");
   if (phase != 0 && phase != 1) return fail(MSB_ERR_ARG, "phase must be 0 or 1");
-  if (!states || !out) return fail(MSB_ERR_ARG, "null buffer");
+  if (!out || (p->rng == MSB_RNG_XOSHIRO && !states)) return fail(MSB_ERR_ARG, "null buffer");
   const Geo G = make_geo(g);
   const long long np = (long long)g->n_sim * g->rows * kg;
-  k_draws<<<blocks_for(np, 128), 128, 0, as_stream(stream)>>>(G, phase, kg, 16 / kg, np, states, out);
+  k_draws<<<blocks_for(np, 128), 128, 0, as_stream(stream)>>>(G, phase, kg, 16 / kg, np, states,
+                                                              p->rng == MSB_RNG_PHILOX, (uint32_t)p->seed,
+                                                              (uint32_t)(p->seed >> 32), p->block, out);
   CUDA_TRY(cudaGetLastError());
   return MSB_OK;
 }

@@ -36,13 +36,13 @@ from concurrent.futures import ThreadPoolExecutor
 import numpy as np
 
 from . import _lib
-from ._lib import (call, geom, SweepParams, MSB_FLIP_SLOTS, MSB_MAX_PLANES, MSB_SWEEP_AHEAD_IN,
-                   MSB_SWEEP_AHEAD_OUT, MSB_SWEEP_SERIAL)
+from ._lib import (call, geom, SweepParams, MSB_FLIP_SLOTS, MSB_MAX_PLANES, MSB_RNG_PHILOX, MSB_RNG_XOSHIRO,
+                   MSB_SWEEP_AHEAD_IN, MSB_SWEEP_AHEAD_OUT, MSB_SWEEP_SERIAL)
 from .layout import (
     ALL_CODES, ArrayCode, LatticeDims, PackedArrays, check_spins, halo_audit_index, unpack,
 )
 from .observables import Trajectory
-from .rng import DeviceStreams
+from .rng import DeviceStreams, PhiloxStreams
 
 __all__ = ["FLIP_RED", "FLIP_BLUE", "build_exp_table", "Engine", "run_simulations"]
 
@@ -145,12 +145,17 @@ class Engine:
     """Packed checkerboard Metropolis over ``n_sim`` replicas on one GPU.
 
     Extra keyword-only arguments beyond the reference signature:
-    ``device`` (CUDA device; default current) and ``kg`` (stream pieces per
-    target row, 1/2/4/8/16; default chosen by the library).
+    ``device`` (CUDA device; default current), ``kg`` (stream pieces per
+    target row, 1/2/4/8/16; default chosen by the library) and ``stream``:
+    "xoshiro" (default) draws the reference's own xoshiro256++ streams;
+    "philox" draws the counter-based ``rng.PhiloxStreams``, which
+    the reference Engine reproduces bit-exactly when handed the same object
+    as its ``streams``.
     """
 
     def __init__(self, dims: LatticeDims, temperatures, seed: int, init: str = "random",
-                 coupling: float = 1.0, sim_offset: int = 0, *, device=None, kg: int | None = None):
+                 coupling: float = 1.0, sim_offset: int = 0, *, device=None, kg: int | None = None,
+                 stream: str = "xoshiro"):
         self.dims = dims
         self.temperatures = tuple(float(t) for t in temperatures)
         if not self.temperatures:
@@ -163,6 +168,9 @@ class Engine:
         self._tables = np.stack([build_exp_table(t, coupling) for t in self.temperatures])
         if init not in ("random", "all-up"):
             raise ValueError(f"unknown init mode {init!r} (expected 'random' or 'all-up')")
+        if stream not in ("xoshiro", "philox"):
+            raise ValueError(f"unknown stream {stream!r} (expected 'xoshiro' or 'philox')")
+        self.stream = stream
 
         torch = _torch()
         self.device = _resolve_device(device)
@@ -190,6 +198,8 @@ class Engine:
         self._params.jump = self._jump.data_ptr()
         self._params.thr9 = self._thr.data_ptr()
         self._params.work = self._work.data_ptr()
+        self._params.rng = MSB_RNG_PHILOX if stream == "philox" else MSB_RNG_XOSHIRO
+        self._params.seed = self.seed & _M64
         self._tab_key = None
         self.fault = 0  # test-only adder corruption (selftest seam, cli.py:467-480)
         self.overlap = True  # run the next sweep's RNG concurrently with this sweep's flips
@@ -203,9 +213,13 @@ class Engine:
             del scratch
         else:
             call("msb_init_const", ctypes.byref(self._g), 1, _p(self._spins), self._cs)
-        call("msb_rng_init", ctypes.byref(self._g), ctypes.c_uint64(self.seed & _M64), self.kg,
-             ctypes.c_uint64(0), -1, _p(self._pow), _p(self._states), self._cs)
-        self.streams = DeviceStreams(self.seed, self.n_sim * dims.cells, self.sim_offset * dims.cells)
+        if stream == "xoshiro":
+            call("msb_rng_init", ctypes.byref(self._g), ctypes.c_uint64(self.seed & _M64), self.kg,
+                 ctypes.c_uint64(0), -1, _p(self._pow), _p(self._states), self._cs)
+            self.streams = DeviceStreams(self.seed, self.n_sim * dims.cells, self.sim_offset * dims.cells)
+        else:
+            self.streams = PhiloxStreams(self.seed, self.n_sim * dims.cells, self.sim_offset * dims.cells)
+        self._own_streams = self.streams
         self._blocks = 0        # stream blocks consumed (one per colour phase)
         self._pos = [0, 1]      # block each colour's pieces are positioned at
         self._ahead = False     # next sweep's accept planes already generated (states one sweep on)
@@ -364,7 +378,8 @@ class Engine:
         d = self.dims
         with torch.cuda.stream(self._stream):
             out = torch.empty(self.n_sim * d.cells * 64 * d.words, dtype=torch.int32, device=self.device)
-        call("msb_draws", ctypes.byref(self._g), self.kg, phase, _p(self._states), _p(out), self._cs)
+        call("msb_draws", ctypes.byref(self._g), ctypes.byref(self._params), phase, _p(self._states), _p(out),
+             self._cs)
         self._stream.synchronize()
         draws = out.cpu().numpy().view(np.uint32).reshape(self.n_sim, d.cells, 4, 16, d.words)
         quarters = FLIP_RED if phase == 0 else FLIP_BLUE
@@ -378,8 +393,9 @@ class Engine:
         """Discard pre-generated planes: put the stream pieces back at the
         logical position (the next unconsumed block)."""
         if self._ahead:
-            call("msb_rng_init", ctypes.byref(self._g), ctypes.c_uint64(self.seed & _M64), self.kg,
-                 ctypes.c_uint64(self._blocks), -1, _p(self._pow), _p(self._states), self._cs)
+            if self.stream == "xoshiro":
+                call("msb_rng_init", ctypes.byref(self._g), ctypes.c_uint64(self.seed & _M64), self.kg,
+                     ctypes.c_uint64(self._blocks), -1, _p(self._pow), _p(self._states), self._cs)
             self._pos = [self._blocks, self._blocks + 1]
             self._ahead = False
 
@@ -390,11 +406,12 @@ class Engine:
         self._params.fault = int(bool(self.fault))
         h = self._blocks
         ext = None
-        if not isinstance(self.streams, DeviceStreams):
+        self._params.block = h
+        if self.streams is not self._own_streams:
             ext = self._host_draws(phase)
             self._pos[phase] = None
         else:
-            if self._pos[phase] != h:
+            if self.stream == "xoshiro" and self._pos[phase] != h:
                 call("msb_rng_init", ctypes.byref(self._g), ctypes.c_uint64(self.seed & _M64), self.kg,
                      ctypes.c_uint64(h), phase, _p(self._pow), _p(self._states), self._cs)
             if self.recorder is not None:
@@ -431,7 +448,7 @@ class Engine:
         for name in ("sweep", "flip_red", "flip_blue", "update_red_bc", "update_blue_bc"):
             if name in self.__dict__ or getattr(cls, name) is not getattr(Engine, name):
                 return False
-        return (self.recorder is None and isinstance(self.streams, DeviceStreams)
+        return (self.recorder is None and self.streams is self._own_streams
                 and self._pos == [self._blocks, self._blocks + 1])
 
     def _sweeps(self, k: int) -> None:
@@ -457,6 +474,7 @@ class Engine:
         if not self.overlap:
             flags |= MSB_SWEEP_SERIAL
         cur = ctypes.c_int32(self._cur)
+        self._params.block = self._blocks + (2 if self._ahead else 0)
         call("msb_sweep", ctypes.byref(self._g), ctypes.byref(self._params), _p(self._spins),
              _p(self._states), _p(self._planes), k, flags, ctypes.byref(cur), _p(self._flips_dev), self._cs)
         self._cur = cur.value

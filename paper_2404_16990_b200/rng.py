@@ -11,7 +11,8 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["Xoshiro256pp", "XoshiroStreams", "stream_state", "shape_unit_float", "DeviceStreams"]
+__all__ = ["Xoshiro256pp", "XoshiroStreams", "stream_state", "shape_unit_float", "DeviceStreams",
+           "philox4x32_10", "PhiloxStreams"]
 
 _M64 = (1 << 64) - 1
 _PHI = 0x9E3779B97F4B7C15
@@ -139,3 +140,74 @@ class DeviceStreams:
     def __repr__(self) -> str:
         return (f"DeviceStreams(master_seed={self.master_seed}, n_streams={self.n_streams}, "
                 f"first_stream={self.first_stream})")
+
+
+# ---------------------------------------------------------------------------
+# Counter-based stream
+# ---------------------------------------------------------------------------
+
+_PM0, _PM1, _PW0, _PW1 = 0xD2511F53, 0xCD9E8D57, 0x9E3779B9, 0xBB67AE85
+
+
+def philox4x32_10(c0, c1, c2, c3, k0, k1):
+    """Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11) on numpy uint32
+    arrays (or ints); returns the four output words."""
+    u32 = np.uint32
+    c0, c1, c2, c3 = (np.asarray(v, dtype=np.uint64) for v in (c0, c1, c2, c3))
+    k0 = np.uint64(int(k0) & 0xFFFFFFFF)
+    k1 = np.uint64(int(k1) & 0xFFFFFFFF)
+    m32 = np.uint64(0xFFFFFFFF)
+    for _ in range(10):
+        p0 = c0 * np.uint64(_PM0)
+        p1 = c2 * np.uint64(_PM1)
+        n0 = (p1 >> np.uint64(32)) ^ c1 ^ k0
+        n2 = (p0 >> np.uint64(32)) ^ c3 ^ k1
+        c1 = p1 & m32
+        c3 = p0 & m32
+        c0, c2 = n0 & m32, n2 & m32
+        k0 = (k0 + np.uint64(_PW0)) & m32
+        k1 = (k1 + np.uint64(_PW1)) & m32
+    return tuple(v.astype(u32) for v in (c0, c1, c2, c3))
+
+
+class PhiloxStreams:
+    """Counter-based replacement for ``XoshiroStreams`` (rng.py:150-220).
+
+    Draw d of stream S (= first_stream + column) is the low 23 bits of word
+    d & 3 of Philox4x32-10 with counter (d >> 2 as 64 bits, S as 64 bits)
+    and key = master_seed (64 bits), shaped to k * 2**-23 like every
+    reference draw (rng.py:180-183).  ``unit_block(count)`` has the
+    reference's semantics: every stream advances by ``count`` draws, so the
+    reference ``Engine`` accepts it as ``engine.streams`` unchanged; the GPU
+    kernels generate the same draws from (seed, stream, draw index) alone.
+    """
+
+    def __init__(self, master_seed: int, n_streams: int, first_stream: int = 0, position: int = 0):
+        if n_streams < 1:
+            raise ValueError("need at least one stream")
+        self.master_seed = int(master_seed) & ((1 << 64) - 1)
+        self.n_streams = int(n_streams)
+        self.first_stream = int(first_stream)
+        self.position = int(position)
+
+    def raw_block(self, count: int) -> np.ndarray:
+        """(count, n_streams) uint32: the 32-bit Philox output word of each draw."""
+        d = self.position + np.arange(count, dtype=np.uint64)[:, None]
+        sid = (self.first_stream + np.arange(self.n_streams, dtype=np.uint64))[None, :]
+        c = d >> np.uint64(2)
+        shape = np.broadcast_shapes(d.shape, sid.shape)
+        m32 = np.uint64(0xFFFFFFFF)
+        words = philox4x32_10(np.broadcast_to(c & m32, shape), np.broadcast_to(c >> np.uint64(32), shape),
+                              np.broadcast_to(sid & m32, shape), np.broadcast_to(sid >> np.uint64(32), shape),
+                              self.master_seed & 0xFFFFFFFF, self.master_seed >> 32)
+        e = np.broadcast_to((d & np.uint64(3)).astype(np.intp), shape)
+        out = np.choose(e, words)
+        self.position += count
+        return out.astype(np.uint32)
+
+    def unit_block(self, count: int) -> np.ndarray:
+        return (self.raw_block(count) & np.uint32(0x7FFFFF)).astype(np.float64) * 2.0 ** -23
+
+    def __repr__(self) -> str:
+        return (f"PhiloxStreams(master_seed={self.master_seed}, n_streams={self.n_streams}, "
+                f"first_stream={self.first_stream}, position={self.position})")

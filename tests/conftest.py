@@ -29,4 +29,5 @@ def golden():
     z = np.load(ROOT / "tests" / "golden" / "reference_runs.npz")
     data = {k: z[k] for k in z.files}
     data["_manifest"] = json.loads(bytes(data.pop("manifest")).decode())
+    data["_philox"] = json.loads(bytes(data.pop("philox_manifest")).decode())
     return data

@@ -45,6 +45,16 @@ ENGINE_CASES = [
 ]
 
 
+# (name, m, n, temperatures, seed, init, coupling, sim_offset, n_sweeps, measure_interval)
+PHILOX_CASES = [
+    ("px_12x96", 12, 96, [2.0], 31, "random", 1.0, 0, 30, 1),
+    ("px_128x128", 128, 128, [2.269], 2024, "random", 1.0, 0, 50, 5),
+    ("px_multi", 16, 256, [1.5, 2.269, 3.0], 7, "random", 1.0, 3, 12, 4),
+    ("px_anti", 8, 64, [1.5], 11, "random", -1.0, 0, 10, 5),
+    ("px_bigseed", 4, 32, [2.0], (1 << 64) - 3, "all-up", 1.0, 0, 10, 10),
+]
+
+
 def main() -> None:
     sys.path.insert(0, REF)
     from multispin import Engine, LatticeDims, Xoshiro256pp
@@ -97,6 +107,26 @@ def main() -> None:
     data["fromlat/abs_m"] = traj.abs_m
     data["fromlat/energy"] = traj.energy
     data["fromlat/flips"] = np.array([eng.flips], np.int64)
+
+    # Counter-based stream: the reference Engine itself, handed a
+    # PhiloxStreams as its duck-typed `streams` (engine.py:259-261, 336).
+    sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
+    from paper_2404_16990_b200.rng import PhiloxStreams
+    philox_manifest = []
+    for (name, m, n, temps, seed, init, J, off, sweeps, mi) in PHILOX_CASES:
+        dims = LatticeDims(m, n)
+        eng = Engine(dims, temps, seed, init=init, coupling=J, sim_offset=off)
+        eng.streams = PhiloxStreams(seed, len(temps) * dims.cells, off * dims.cells)
+        traj = eng.run(sweeps, measure_interval=mi)
+        final = np.stack([eng.lattice(s) for s in range(eng.n_sim)])
+        data[f"{name}/final"] = np.packbits(final > 0, axis=-1)
+        data[f"{name}/abs_m"] = traj.abs_m
+        data[f"{name}/energy"] = traj.energy
+        data[f"{name}/flips"] = np.array([eng.flips], np.int64)
+        philox_manifest.append(dict(name=name, m=m, n=n, temperatures=temps, seed=str(seed), init=init,
+                                    coupling=J, sim_offset=off, n_sweeps=sweeps, measure_interval=mi))
+        print(f"{name}: flips={eng.flips}", flush=True)
+    data["philox_manifest"] = np.frombuffer(json.dumps(philox_manifest).encode(), np.uint8)
 
     data["manifest"] = np.frombuffer(json.dumps(manifest).encode(), np.uint8)
     np.savez_compressed(OUT, **data)

@@ -168,3 +168,52 @@ def test_forced_tables():
     e.sweep()
     assert (e.lattice(0) == -spins).all()
     assert e.flips == dims.sites
+
+
+# ---- counter-based stream ------------------------------------------
+
+def test_philox_reference_runs_bit_exact(golden):
+    """Engine(stream="philox") == the reference Engine fed PhiloxStreams."""
+    from paper_2404_16990_b200 import Engine, LatticeDims
+    for c in golden["_philox"]:
+        name = c["name"]
+        e = Engine(LatticeDims(c["m"], c["n"]), c["temperatures"], int(c["seed"]), init=c["init"],
+                   coupling=c["coupling"], sim_offset=c["sim_offset"], stream="philox")
+        traj = e.run(c["n_sweeps"], c["measure_interval"])
+        assert (e.lattices() == unpack_lattice(golden[f"{name}/final"], c["n"])).all(), name
+        assert (traj.abs_m == golden[f"{name}/abs_m"]).all() and (traj.energy == golden[f"{name}/energy"]).all()
+        assert e.flips == int(golden[f"{name}/flips"][0]), name
+
+
+@pytest.mark.parametrize("m,n,n_sim,sweeps", [(64, 1024, 2, 3), (1024, 1024, 2, 2), (96, 14336, 1, 2),
+                                              (36, 96, 3, 5), (20, 160, 2, 4)])
+def test_philox_vs_oracle_shapes(m, n, n_sim, sweeps):
+    from oracle import oracle as orc
+    from paper_2404_16990_b200 import Engine, LatticeDims
+    temps = list(np.linspace(1.8, 3.0, n_sim))
+    e = Engine(LatticeDims(m, n), temps, seed=77, sim_offset=2, stream="philox")
+    o = orc.OracleEngine(m, n, temps, 77, sim_offset=2, stream="philox")
+    e.run(sweeps, measure_interval=1)
+    o.sweep(sweeps)
+    assert (e.lattices() == o.spins).all()
+    assert e.flips == o.flips
+    assert (e.energy_per_spin() == o.energy_per_spin()).all()
+
+
+def test_philox_phase_by_phase_and_external_streams():
+    """Manual phases, the recorder and an external PhiloxStreams object (host
+    draws through the duck-typed seam) all agree with the fused path."""
+    from paper_2404_16990_b200 import Engine, LatticeDims
+    from paper_2404_16990_b200.rng import PhiloxStreams
+    dims = LatticeDims(32, 128)
+    a = Engine(dims, [2.1, 2.6], seed=5, stream="philox")
+    b = Engine(dims, [2.1, 2.6], seed=5, stream="philox")
+    c = Engine(dims, [2.1, 2.6], seed=5)             # xoshiro engine, streams swapped
+    c.streams = PhiloxStreams(5, 2 * dims.cells, 0)
+    a.run(6, measure_interval=3)
+    for _ in range(6):
+        b.flip_red()
+        b.flip_blue()
+        c.sweep()
+    assert (a.lattices() == b.lattices()).all() and (a.lattices() == c.lattices()).all()
+    assert a.flips == b.flips == c.flips

@@ -71,3 +71,26 @@ def test_from_lattices_case(golden):
     assert (abs_m == golden["fromlat/abs_m"]).all()
     assert (energy == golden["fromlat/energy"]).all()
     assert e.flips == int(golden["fromlat/flips"][0])
+
+
+def test_philox_oracle_matches_reference_with_philox_streams(golden):
+    """The reference Engine fed PhiloxStreams (tests/golden) == the oracle's
+    Philox path, bit for bit."""
+    for c in golden["_philox"]:
+        name = c["name"]
+        e = orc.OracleEngine(c["m"], c["n"], c["temperatures"], int(c["seed"]), init=c["init"],
+                             coupling=c["coupling"], sim_offset=c["sim_offset"], stream="philox")
+        _, abs_m, energy = e.run(c["n_sweeps"], c["measure_interval"])
+        assert (e.spins == unpack_lattice(golden[f"{name}/final"], c["n"])).all(), name
+        assert (abs_m == golden[f"{name}/abs_m"]).all() and (energy == golden[f"{name}/energy"]).all(), name
+        assert e.flips == int(golden[f"{name}/flips"][0]), name
+
+
+def test_philox_host_stream_matches_oracle():
+    import numpy as np
+    from paper_2404_16990_b200.rng import PhiloxStreams
+    ps = PhiloxStreams(123, 4, 10, position=37)
+    blk = ps.raw_block(9) & 0x7FFFFF
+    for j in range(4):
+        for r in range(9):
+            assert blk[r, j] == orc.lib().orc_philox_draw(123, 10 + j, 37 + r)

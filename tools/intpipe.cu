@@ -176,6 +176,48 @@ __global__ void kxo2(uint32_t* out, uint32_t seed, int nsteps) {
   if ((acc0 ^ acc1) == 0x12345678u) out[0] = acc0 ^ a0 ^ b1 ^ c0 ^ d1;
 }
 
+// VAR 8: VAR 5 + 64-bit adds through IMAD.WIDE with a dead pair addend and a
+// runtime multiplier of 1 (state update computed first so s0/s3 die there)
+template <int VAR>
+__global__ void kxo3(uint32_t* out, uint32_t seed, int nsteps, const uint32_t* onep) {
+  uint64_t s0 = 0x9E3779B97F4B7C15ull * (blockIdx.x * blockDim.x + threadIdx.x + 1) ^ seed;
+  uint64_t s1 = s0 * 3 + 1, s2 = s0 ^ 0xdeadbeef12345ull, s3 = s1 * 7 + 11;
+  uint32_t acc0 = 0, acc1 = 0, K0 = 0x300000u << 9, K1 = 0x80000u << 9;
+  const uint32_t one = onep[threadIdx.x & 7];
+  uint32_t a0 = (uint32_t)s0, a1 = s0 >> 32, b0 = (uint32_t)s1, b1 = s1 >> 32;
+  uint32_t c0 = (uint32_t)s2, c1 = s2 >> 32, d0 = (uint32_t)s3, d1 = s3 >> 32;
+#pragma unroll 8
+  for (int i = 0; i < nsteps; i++) {
+    uint32_t t0, t1;
+    { uint32_t wh; wide_pow2<17>(b0, t0, wh); t1 = b1 * (1u << 17) + wh; }
+    const uint32_t nc0 = lop3x(c0, a0, t0), nc1 = lop3x(c1, a1, t1);
+    const uint32_t nd0 = d0 ^ b0, nd1 = d1 ^ b1;
+    const uint32_t nb0 = lop3x(b0, c0, a0), nb1 = lop3x(b1, c1, a1);
+    const uint32_t na0 = lop3x(a0, d0, b0), na1 = lop3x(a1, d1, b1);
+    // x = s0 + s3 (old values), addend pair d dies here
+    uint64_t xd = ((uint64_t)d1 << 32) | d0;
+    uint64_t x;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(x) : "r"(a0), "r"(one), "l"(xd));
+    const uint32_t x0 = (uint32_t)x, x1 = (uint32_t)(x >> 32) + a1;
+    const uint32_t r1 = fsl(x0, x1, 23), r0 = fsl(x1, x0, 23);
+    uint32_t o1;
+    if (VAR >= 9) {
+      uint64_t ap = ((uint64_t)a1 << 32) | a0, o;
+      asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(o) : "r"(r0), "r"(one), "l"(ap));
+      o1 = (uint32_t)(o >> 32) + r1;
+    } else {
+      asm("{.reg .b32 t; add.cc.u32 t, %1, %2;\n\taddc.u32 %0, %3, %4;}" : "=r"(o1) : "r"(r0), "r"(a0), "r"(r1), "r"(a1));
+    }
+    const uint32_t hi9 = o1 << 9;
+    asm("{.reg .b32 t; sub.cc.u32 t, %1, %2;\n\taddc.u32 %0, %0, %0;}" : "+r"(acc0) : "r"(hi9), "r"(K0));
+    asm("{.reg .b32 t; sub.cc.u32 t, %1, %2;\n\taddc.u32 %0, %0, %0;}" : "+r"(acc1) : "r"(hi9), "r"(K1));
+    a0 = na0; a1 = na1; b0 = nb0; b1 = nb1; c0 = nc0; c1 = nc1;
+    d1 = fsl(nd1, nd0, 13);
+    d0 = fsl(nd0, nd1, 13);
+  }
+  if ((acc0 ^ acc1) == 0x12345678u) out[0] = acc0 ^ a0 ^ b1 ^ c0 ^ d1;
+}
+
 int main() {
   uint32_t* d; cudaMalloc(&d, 4096);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
@@ -230,6 +272,19 @@ int main() {
         case 6: kxo2<6><<<bl, 256>>>(d, 3, ns); break;
         case 7: kxo2<7><<<bl, 256>>>(d, 3, ns); break;
       }
+    };
+    launch();
+    cudaEventRecord(e0); launch(); cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    printf("xoshiro VAR %d blocks=%d: %.3f ms  %.3f T draws/s\n", var, bl, ms, (double)bl * 256 * ns / ms / 1e9);
+  }
+  uint32_t* onep; cudaMalloc(&onep, 64);
+  { uint32_t h[8] = {1,1,1,1,1,1,1,1}; cudaMemcpy(onep, h, 32, cudaMemcpyHostToDevice); }
+  for (int var = 8; var < 10; var++)
+  for (int bl : {148 * 4, 148 * 8}) {
+    int ns = 1 << 13;
+    auto launch = [&]() {
+      if (var == 8) kxo3<8><<<bl, 256>>>(d, 3, ns, onep); else kxo3<9><<<bl, 256>>>(d, 3, ns, onep);
     };
     launch();
     cudaEventRecord(e0); launch(); cudaEventRecord(e1); cudaEventSynchronize(e1);
