@@ -52,9 +52,14 @@ CONFIGS = {
     "cfg3": dict(m=512, n=512, n_sim=754, init="all-up", seed=2024,
                  temps=lambda n: np.random.default_rng(2024).uniform(2.0, 2.6, n),
                  desc="cfg3: 754 replicas x 512x512, periodic, J=1, T~U[2.0,2.6] from seed, all-up init"),
-    "cfg4": dict(m=14336, n=14336, n_sim=1, init="random", seed=2024,
+    "cfg4": dict(m=14336, n=14336, n_sim=1, init="random", seed=2024, slab="strong",
                  temps=lambda n: np.full(n, 2.269),
-                 desc="cfg4: one 14336x14336 lattice, periodic, J=1, T=2.269, random init"),
+                 desc="cfg4: one 14336x14336 lattice, periodic, J=1, T=2.269, random init; row slabs over the "
+                      "GPUs, one ghost row per colour exchanged per half-sweep (strong scaling)"),
+    "cfg5": dict(m=32768, n=32768, n_sim=1, init="random", seed=2024, slab="weak", measure=10,
+                 temps=lambda n: np.full(n, 2.0),
+                 desc="cfg5: (32768*N)x32768 periodic lattice, 32768 rows per GPU, J=1, T=2.0, random init; "
+                      "ghost exchange per half-sweep, |M| and E all-reduced every 10 sweeps (weak scaling)"),
 }
 
 
@@ -320,6 +325,78 @@ def run_ours(args, cfg):
     return 0
 
 
+def run_slab(args, cfg):
+    """cfg4 / cfg5: one lattice in row slabs, one per rank."""
+    import torch
+    import torch.distributed as dist
+    from paper_2404_16990_b200 import LatticeDims
+    from paper_2404_16990_b200.slab import DistExchange, LocalExchange, SlabLattice, SlabRun, slab_bounds
+
+    ws, rank, local = dist_info()
+    if ws > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    m = cfg["m"] * (ws if cfg["slab"] == "weak" else 1)
+    n = cfg["n"]
+    a, b = slab_bounds(m, ws)[rank]
+    slab = SlabLattice(LatticeDims(m, n), list(cfg["temps"](1)), cfg["seed"], a, b - a, init=cfg["init"],
+                       device=dev, kg=args.kg, stream=args.stream)
+    run = SlabRun([slab], DistExchange() if ws > 1 else LocalExchange())
+    every = cfg.get("measure", 0)
+    peak = int_peak_tops(slab._stream)
+    run.sweep(args.warmup)
+    torch.cuda.synchronize()
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    K = args.steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
+    if ws > 1:
+        dist.barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.02)
+    for k in range(K):
+        with slab.stream_ctx():
+            flush.zero_()
+        evs[k][0].record(slab._stream)
+        run.sweep(1)
+        if every and (k + 1) % every == 0:
+            ups, uns = run.observables()
+            if ws > 1:
+                t = torch.tensor(np.concatenate([ups, uns]), device=dev)
+                with slab.stream_ctx():
+                    dist.all_reduce(t)
+        evs[k][1].record(slab._stream)
+    torch.cuda.synchronize()
+    sampler.stop()
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
+    total_ms = float(sum(step_ms))
+    if ws > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    attempts_step = m * n
+    value = attempts_step * K / (total_ms * 1e-3)
+    if rank == 0:
+        achieved = A_INT * (b - a) * n / (statistics.mean(step_ms) * 1e-3) / 1e12
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": args.warmup,
+            "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": cfg["slab"], "vs_baseline": None,
+            "dtype": "u32", "data": "synthetic (random +/-1 initial spins from the reference init stream)",
+            "config": {"workload": cfg["desc"], "m": m, "n": n, "rows_per_gpu": b - a,
+                       "parallelism": f"row slabs over {ws} GPU(s), NCCL ring exchange of ghost rows",
+                       "l2": f"flushed between timed steps ({L2_FLUSH_BYTES >> 20} MiB write, outside the events)",
+                       "stream": args.stream, "kg": slab.kg},
+            "roofline": {"bound": "int32", "achieved": achieved, "peak": peak, "unit": "Tops/s",
+                         "frac": achieved / peak, "traffic": None, "kernel": "k_rng_planes + k_flip (slab path)"},
+            "e2e": None, "gpu_launches": 3 * K + (4 * K if ws > 1 else 6 * K), "clocks": sampler.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
@@ -337,6 +414,8 @@ def main():
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if cfg.get("slab"):
+        return run_slab(args, cfg)
     return run_ours(args, cfg)
 
 

@@ -355,9 +355,10 @@ __device__ __forceinline__ void finish_warp(unsigned* work, unsigned total_warps
 // One producer warp's share of a sweep's accept planes.  `role_warp` /
 // `role_warps` number the producer warps of the grid; their first unit is
 // static (interleaved across CTAs), later ones come from work[0].
-template <int NPMAX, int SRC>
+template <int NPMAX, int SRC, bool FULL>
 __device__ __forceinline__ void rng_produce(const RngArgs& a, const uint4* __restrict__ jt, int role_warp,
                                             int role_warps) {
+  // FULL: n/32 is a multiple of 32, so every chunk holds 32 draws
   constexpr bool EXT = SRC == kSrcExt;
   constexpr bool XO = SRC == kSrcXoshiro;
   const Geo& G = a.G;
@@ -412,8 +413,23 @@ __device__ __forceinline__ void rng_produce(const RngArgs& a, const uint4* __res
     for (int kk = 0; kk < a.kr; kk++) {
       const int k = kgi * a.kr + kk;
       const int t = t_of_k(k);
+      uint32_t* outk = out + t;
+      if (FULL && XO) {
+        // fast path: whole chunks, reverse + invert straight into the plane words
+        for (int ch = 0; ch < G.nch; ch++) {
+          uint32_t acc0 = 0, acc1 = 0;
+#pragma unroll kChunkUnroll
+          for (int i = 0; i < 32; i++) {
+            const uint32_t h9 = xstep(st) << 9;
+            acc_reject(acc0, h9, key[0]);
+            if (np > 1) acc_reject(acc1, h9, key[NPMAX > 1 ? 1 : 0]);
+          }
+          outk[ch * 16] = ~__brev(acc0);
+          if (np > 1) outk[pstride + ch * 16] = ~__brev(acc1);
+        }
+      } else
       for (int ch = 0; ch < G.nch; ch++) {
-        const int L = chunk_bits(G, ch);
+        const int L = FULL ? 32 : chunk_bits(G, ch);
         uint32_t acc[NPMAX];
 #pragma unroll
         for (int p = 0; p < NPMAX; p++) acc[p] = 0;
@@ -454,6 +470,11 @@ __device__ __forceinline__ void rng_produce(const RngArgs& a, const uint4* __res
               for (int p = 0; p < NPMAX; p++)
                 if (p < np) acc_reject(acc[p], h9, key[p]);
             }
+            // full chunk: reverse + invert straight into the plane words
+#pragma unroll
+            for (int p = 0; p < NPMAX; p++)
+              if (p < np) outk[p * pstride + ch * 16] = ~__brev(acc[p]);
+            continue;
           } else {
             for (int i = 0; i < L; i++) {
               const uint32_t h9 = xstep(st) << 9;
@@ -480,11 +501,14 @@ __device__ __forceinline__ void rng_produce(const RngArgs& a, const uint4* __res
       // at a time, XORs paired into 3-input LOP3s
       if (XO && ((kk + 1) * lk) % 8 == 0) {
         for (int wcount = (kk + 1) * lk / 8 - nib / 8; wcount > 0; wcount--) {
-          const uint4* e = jt + nib * 32;
+          // entry (position nib+j, value v) lives at byte (nib+j)*512 + v*32
+          const char* e = reinterpret_cast<const char*>(jt) + nib * 512;
 #pragma unroll
           for (int j = 0; j < 8; j += 2) {
-            const uint4* ea = e + j * 32 + ((jw0 >> (4 * j)) & 15u) * 2;
-            const uint4* eb = e + (j + 1) * 32 + ((jw0 >> (4 * j + 4)) & 15u) * 2;
+            const uint32_t oa = j == 0 ? ((jw0 << 5) & 0x1E0u) : ((jw0 >> (4 * j - 5)) & 0x1E0u);
+            const uint32_t ob = j == 0 ? ((jw0 << 1) & 0x1E0u) : ((jw0 >> (4 * j - 1)) & 0x1E0u);
+            const uint4* ea = reinterpret_cast<const uint4*>(e + j * 512 + oa);
+            const uint4* eb = reinterpret_cast<const uint4*>(e + (j + 1) * 512 + ob);
             const uint4 la = ea[0], ha = ea[1], lb = eb[0], hb = eb[1];
             r0 = xor3(r0, la.x, lb.x); r1 = xor3(r1, la.y, lb.y); r2 = xor3(r2, la.z, lb.z); r3 = xor3(r3, la.w, lb.w);
             r4 = xor3(r4, ha.x, hb.x); r5 = xor3(r5, ha.y, hb.y); r6 = xor3(r6, ha.z, hb.z); r7 = xor3(r7, ha.w, hb.w);
@@ -506,14 +530,14 @@ __device__ __forceinline__ void rng_produce(const RngArgs& a, const uint4* __res
   }
 }
 
-template <int NPMAX, int SRC>
+template <int NPMAX, int SRC, bool FULL>
 __global__ void __launch_bounds__(kRngThreads, 1) k_rng_planes(const RngArgs a) {
   extern __shared__ uint4 jt[];  // nibble table of A^(4n), 32 KiB
   if (SRC == kSrcXoshiro) {
     for (int i = threadIdx.x; i < kJumpWords / 4; i += blockDim.x) jt[i] = a.jump[i];
     __syncthreads();
   }
-  rng_produce<NPMAX, SRC>(a, jt, threadIdx.x >> 5, blockDim.x >> 5);
+  rng_produce<NPMAX, SRC, FULL>(a, jt, threadIdx.x >> 5, blockDim.x >> 5);
   finish_warp(a.work, gridDim.x * (blockDim.x >> 5));
 }
 
@@ -569,11 +593,8 @@ __device__ __forceinline__ uint32_t flip_word(const FlipArgs& a, bool generic, u
 // (h_second).  COHERENT: other-colour words were written earlier in the same
 // kernel by other SMs, so read them through L2 (ld.global.cg).
 template <bool GENERIC, bool COHERENT>
-__device__ __forceinline__ unsigned flip_quad(const FlipArgs& a, unsigned i, int X) {
+__device__ __forceinline__ unsigned flip_quad_at(const FlipArgs& a, int s, int lr, unsigned qq, int X) {
   const Geo& G = a.G;
-  const unsigned quads = (unsigned)G.Wp >> 2;
-  const unsigned gr = G.quads_div.div(i), qq = i - gr * quads;
-  const int s = (int)G.rows_div.div(gr), lr = (int)(gr - (unsigned)s * G.rows);
   const int c = G.row0 + lr, br = lr + G.ghost;
   const int ch = (int)(qq >> 2), t0 = 4 * (int)(qq & 3);
   const int w0 = ch * 16 + t0;
@@ -638,6 +659,136 @@ __device__ __forceinline__ unsigned flip_quad(const FlipArgs& a, unsigned i, int
   return cnt;
 }
 
+template <bool GENERIC, bool COHERENT>
+__device__ __forceinline__ unsigned flip_quad(const FlipArgs& a, unsigned i, int X) {
+  const Geo& G = a.G;
+  const unsigned quads = (unsigned)G.Wp >> 2;
+  const unsigned gr = G.quads_div.div(i), qq = i - gr * quads;
+  const int s = (int)G.rows_div.div(gr), lr = (int)(gr - (unsigned)s * G.rows);
+  return flip_quad_at<GENERIC, COHERENT>(a, s, lr, qq, X);
+}
+
+// FERRO/ANTI flip of one whole 16-word chunk (t = 0..15 of chunk ch) of row
+// (s, lr), colour X.  The other colour's same-row words stay in registers, so
+// every t+-1 neighbour -- and, when the row is one chunk, the t = 0/15 wraps
+// -- comes from registers; address math happens once per chunk.
+template <bool COHERENT>
+__device__ __forceinline__ unsigned flip_chunk_at(const FlipArgs& a, int s, int lr, int ch, int X) {
+  const Geo& G = a.G;
+  const int c = G.row0 + lr, br = lr + G.ghost;
+  int bu, bd;
+  vert_rows(G, br, bu, bd);
+  const int w0 = ch * 16;
+  uint32_t* own = a.spins + row_off(G, s, X, br) + w0;
+  const uint32_t* ycr = a.spins + row_off(G, s, 1 - X, br);
+  const uint32_t* yu = a.spins + row_off(G, s, 1 - X, bu) + w0;
+  const uint32_t* yd = a.spins + row_off(G, s, 1 - X, bd) + w0;
+  const size_t pstride = (size_t)G.n_sim * G.rows * G.Wp;
+  const uint32_t* pl = a.planes + plane_off(G, a.np, X, 0, s, lr) + w0;
+  auto ld4 = [](const uint32_t* q) {
+    return COHERENT ? __ldcg(reinterpret_cast<const uint4*>(q)) : __ldg(reinterpret_cast<const uint4*>(q));
+  };
+  auto ld1 = [](const uint32_t* q) { return COHERENT ? __ldcg(q) : __ldg(q); };
+  uint32_t y[16];
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const uint4 v = ld4(ycr + w0 + 4 * q);
+    y[4 * q] = v.x; y[4 * q + 1] = v.y; y[4 * q + 2] = v.z; y[4 * q + 3] = v.w;
+  }
+  const int p = (c + X) & 1;
+  const int vb = chunk_bits(G, ch);
+  const uint32_t vm = chunk_mask(G, ch);
+  // the wrap word: p=1 -> t=15 needs bit 0 of the next chunk's t=0 word;
+  // p=0 -> t=0 needs the top valid bit of the previous chunk's t=15 word
+  uint32_t wrapn;
+  if (p) {
+    const int chn = ch + 1 < G.nch ? ch + 1 : 0;
+    const uint32_t nx = chn == ch ? y[0] : ld1(ycr + chn * 16);
+    wrapn = (y[0] >> 1) | ((nx & 1u) << (vb - 1));
+  } else {
+    uint32_t carry;
+    if (ch > 0) carry = ld1(ycr + (ch - 1) * 16 + 15) >> 31;
+    else carry = ((G.nch == 1 ? y[15] : ld1(ycr + (G.nch - 1) * 16 + 15)) >> (chunk_bits(G, G.nch - 1) - 1)) & 1u;
+    wrapn = ((y[15] << 1) | carry) & vm;
+  }
+  unsigned cnt = 0;
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const uint4 O = *reinterpret_cast<const uint4*>(own + 4 * q);
+    const uint4 U = ld4(yu + 4 * q), D = ld4(yd + 4 * q);
+    const uint4 P4 = __ldg(reinterpret_cast<const uint4*>(pl + 4 * q));
+    const uint4 P8 = __ldg(reinterpret_cast<const uint4*>(pl + pstride + 4 * q));
+    const uint32_t o[4] = {O.x, O.y, O.z, O.w}, u4[4] = {U.x, U.y, U.z, U.w}, d4[4] = {D.x, D.y, D.z, D.w};
+    const uint32_t a4[4] = {P4.x, P4.y, P4.z, P4.w}, a8[4] = {P8.x, P8.y, P8.z, P8.w};
+    uint32_t res[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const int t = 4 * q + k;
+      const uint32_t n4 = p ? (t < 15 ? y[t + 1] : wrapn) : (t > 0 ? y[t - 1] : wrapn);
+      const uint32_t f = flip_word(a, false, o[k], u4[k], d4[k], y[t], n4, nullptr, 0, a4[k], a8[k]) & vm;
+      res[k] = o[k] ^ f;
+      cnt += __popc(f);
+    }
+    *reinterpret_cast<uint4*>(own + 4 * q) = make_uint4(res[0], res[1], res[2], res[3]);
+  }
+  return cnt;
+}
+
+// A consumer warp's contiguous run of chunks [i0, i1) (lanes take
+// consecutive chunks), walked with incremental (replica, row, chunk) state.
+template <bool COHERENT>
+__device__ __forceinline__ unsigned flip_run_chunks(const FlipArgs& a, unsigned i0, unsigned i1, int X) {
+  const Geo& G = a.G;
+  if (i0 >= i1) return 0;
+  const unsigned nch = (unsigned)G.nch;
+  unsigned gr = i0 / nch, ch = i0 - gr * nch;
+  int s = (int)G.rows_div.div(gr), lr = (int)(gr - (unsigned)s * G.rows);
+  const unsigned dr = 32u / nch, dc = 32u - dr * nch;
+  unsigned cnt = 0;
+  for (unsigned i = i0; i < i1; i += 32) {
+    cnt += flip_chunk_at<COHERENT>(a, s, lr, (int)ch, X);
+    ch += dc;
+    lr += (int)dr;
+    if (ch >= nch) {
+      ch -= nch;
+      lr++;
+    }
+    while (lr >= G.rows) {
+      lr -= G.rows;
+      s++;
+    }
+  }
+  return cnt;
+}
+
+// A consumer warp's contiguous run of quads [i0, i1) of one colour, walked
+// with incremental (replica, row, quad) bookkeeping: lanes take consecutive
+// quads, each step advances all lanes by 32 quads (dr rows + dq quads).
+template <bool COHERENT>
+__device__ __forceinline__ unsigned flip_run(const FlipArgs& a, unsigned i0, unsigned i1, int X) {
+  const Geo& G = a.G;
+  const unsigned quads = (unsigned)G.Wp >> 2;
+  if (i0 >= i1) return 0;
+  unsigned gr = G.quads_div.div(i0), qq = i0 - gr * quads;
+  int s = (int)G.rows_div.div(gr), lr = (int)(gr - (unsigned)s * G.rows);
+  const unsigned dr = G.quads_div.div(32u), dq = 32u - dr * quads;
+  unsigned cnt = 0;
+  for (unsigned i = i0; i < i1; i += 32) {
+    cnt += flip_quad_at<false, COHERENT>(a, s, lr, qq, X);
+    qq += dq;
+    lr += (int)dr;
+    if (qq >= quads) {
+      qq -= quads;
+      lr++;
+    }
+    while (lr >= G.rows) {
+      lr -= G.rows;
+      s++;
+    }
+  }
+  return cnt;
+}
+
 __device__ __forceinline__ void add_flips(unsigned long long* flips, unsigned cnt) {
   cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
   if ((threadIdx.x & 31) == 0 && cnt)
@@ -670,7 +821,7 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   return v;
 }
 
-template <int NPMAX, int SRC>
+template <int NPMAX, int SRC, bool FULL>
 __global__ void __launch_bounds__(kRngThreads, 1) k_sweep_fused(const RngArgs ra, const FlipArgs fa) {
   const int kFlipWarps = fa.cwarps;
   const int kProducerWarps = (kRngThreads >> 5) - kFlipWarps;
@@ -682,18 +833,20 @@ __global__ void __launch_bounds__(kRngThreads, 1) k_sweep_fused(const RngArgs ra
   const int warp = threadIdx.x >> 5;
   const unsigned total_warps = gridDim.x * (blockDim.x >> 5);
   if (warp < kProducerWarps) {
-    rng_produce<NPMAX, SRC>(ra, jt, warp, kProducerWarps);
+    rng_produce<NPMAX, SRC, FULL>(ra, jt, warp, kProducerWarps);
   } else {
-    const unsigned quads = (unsigned)fa.G.Wp >> 2;
-    const unsigned total = (unsigned)fa.G.n_sim * (unsigned)fa.G.rows * quads;
-    const unsigned stride = gridDim.x * kFlipWarps * 32;
-    const unsigned first = ((warp - kProducerWarps) * gridDim.x + blockIdx.x) * 32 + (threadIdx.x & 31);
+    const unsigned total = (unsigned)fa.G.n_sim * (unsigned)fa.G.rows * (unsigned)fa.G.nch;  // chunks
+    const unsigned nc = gridDim.x * kFlipWarps;
+    const unsigned cw = (warp - kProducerWarps) * gridDim.x + blockIdx.x;
+    const unsigned per = ((total + nc - 1) / nc + 31) & ~31u;  // chunks per consumer warp
+    const unsigned lo = min(total, cw * per), hi = min(total, lo + per);
+    const unsigned i0 = lo + (threadIdx.x & 31);
     unsigned cnt = 0;
     for (int X = 0; X < 2; X++) {
       if (X == 0) {
-        for (unsigned i = first; i < total; i += stride) cnt += flip_quad<false, false>(fa, i, 0);
+        cnt += flip_run_chunks<false>(fa, i0, hi, 0);
       } else {
-        for (unsigned i = first; i < total; i += stride) cnt += flip_quad<false, true>(fa, i, 1);
+        cnt += flip_run_chunks<true>(fa, i0, hi, 1);
       }
       if (X == 0) {  // grid barrier among the flip warps
         __syncwarp();
@@ -1091,22 +1244,24 @@ int rng_planes(const msb_geom* g, const msb_sweep_params* p, int colour, uint32_
   (void)per_cta;
   const unsigned grid = (unsigned)std::max(1LL, std::min<long long>(sms, units));
   const size_t smem = (ext || p->rng == MSB_RNG_PHILOX) ? 0 : (size_t)kJumpWords * 4;
-#define MSB_LAUNCH_RNG(NP, SRC)                                               \
+#define MSB_LAUNCH_RNG(NP, SRC, FULL)                                         \
   do {                                                                        \
     static std::once_flag o;                                                  \
     static cudaError_t e;                                                     \
-    if (int r = set_smem_attr(k_rng_planes<NP, SRC>, o, e)) return r;         \
-    k_rng_planes<NP, SRC><<<grid, kRngThreads, smem, st>>>(a);                \
+    if (int r = set_smem_attr(k_rng_planes<NP, SRC, FULL>, o, e)) return r;   \
+    k_rng_planes<NP, SRC, FULL><<<grid, kRngThreads, smem, st>>>(a);          \
   } while (0)
   const int src = ext ? kSrcExt : (p->rng == MSB_RNG_PHILOX ? kSrcPhilox : kSrcXoshiro);
+  const bool full = (a.G.words % 32) == 0;
   if (p->mode != MSB_MODE_GENERIC) {
-    if (src == kSrcExt) MSB_LAUNCH_RNG(2, kSrcExt);
-    else if (src == kSrcPhilox) MSB_LAUNCH_RNG(2, kSrcPhilox);
-    else MSB_LAUNCH_RNG(2, kSrcXoshiro);
+    if (src == kSrcExt) MSB_LAUNCH_RNG(2, kSrcExt, false);
+    else if (src == kSrcPhilox) MSB_LAUNCH_RNG(2, kSrcPhilox, false);
+    else if (full) MSB_LAUNCH_RNG(2, kSrcXoshiro, true);
+    else MSB_LAUNCH_RNG(2, kSrcXoshiro, false);
   } else {
-    if (src == kSrcExt) MSB_LAUNCH_RNG(MSB_MAX_PLANES, kSrcExt);
-    else if (src == kSrcPhilox) MSB_LAUNCH_RNG(MSB_MAX_PLANES, kSrcPhilox);
-    else MSB_LAUNCH_RNG(MSB_MAX_PLANES, kSrcXoshiro);
+    if (src == kSrcExt) MSB_LAUNCH_RNG(MSB_MAX_PLANES, kSrcExt, false);
+    else if (src == kSrcPhilox) MSB_LAUNCH_RNG(MSB_MAX_PLANES, kSrcPhilox, false);
+    else MSB_LAUNCH_RNG(MSB_MAX_PLANES, kSrcXoshiro, false);
   }
 #undef MSB_LAUNCH_RNG
   CUDA_TRY(cudaGetLastError());
@@ -1159,10 +1314,12 @@ int fused_sweep(const msb_geom* g, const msb_sweep_params* p, uint32_t* spins, u
   CUDA_TRY(cudaGetDevice(&dev));
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const bool philox = p->rng == MSB_RNG_PHILOX;
-  static std::once_flag o, o2;
-  static cudaError_t e, e2;
-  if (int r = set_smem_attr(k_sweep_fused<2, kSrcXoshiro>, o, e)) return r;
-  if (int r = set_smem_attr(k_sweep_fused<2, kSrcPhilox>, o2, e2)) return r;
+  const bool full = (fa.G.words % 32) == 0;
+  static std::once_flag o, o2, o3;
+  static cudaError_t e, e2, e3;
+  if (int r = set_smem_attr(k_sweep_fused<2, kSrcXoshiro, false>, o, e)) return r;
+  if (int r = set_smem_attr(k_sweep_fused<2, kSrcPhilox, false>, o2, e2)) return r;
+  if (int r = set_smem_attr(k_sweep_fused<2, kSrcXoshiro, true>, o3, e3)) return r;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)sms);
   cfg.blockDim = dim3(kRngThreads);
@@ -1173,8 +1330,9 @@ int fused_sweep(const msb_geom* g, const msb_sweep_params* p, uint32_t* spins, u
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (philox) CUDA_TRY(cudaLaunchKernelEx(&cfg, k_sweep_fused<2, kSrcPhilox>, ra, fa));
-  else CUDA_TRY(cudaLaunchKernelEx(&cfg, k_sweep_fused<2, kSrcXoshiro>, ra, fa));
+  if (philox) CUDA_TRY(cudaLaunchKernelEx(&cfg, k_sweep_fused<2, kSrcPhilox, false>, ra, fa));
+  else if (full) CUDA_TRY(cudaLaunchKernelEx(&cfg, k_sweep_fused<2, kSrcXoshiro, true>, ra, fa));
+  else CUDA_TRY(cudaLaunchKernelEx(&cfg, k_sweep_fused<2, kSrcXoshiro, false>, ra, fa));
   return MSB_OK;
 }
 }  // namespace

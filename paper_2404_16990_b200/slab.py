@@ -27,7 +27,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from ._lib import call, geom, SweepParams, MSB_FLIP_SLOTS, MSB_MAX_PLANES
+from ._lib import call, geom, SweepParams, MSB_FLIP_SLOTS, MSB_MAX_PLANES, MSB_RNG_PHILOX, MSB_RNG_XOSHIRO
 from .engine import _M64, _p, _pow_tables, _sweep_jump_table, _torch, build_exp_table
 from .layout import LatticeDims
 
@@ -51,7 +51,8 @@ class SlabLattice:
     accept-plane buffer."""
 
     def __init__(self, dims: LatticeDims, temperatures, seed: int, row0: int, rows: int, init: str = "random",
-                 coupling: float = 1.0, sim_offset: int = 0, device=None, kg: int | None = None):
+                 coupling: float = 1.0, sim_offset: int = 0, device=None, kg: int | None = None,
+                 stream: str = "xoshiro"):
         torch = _torch()
         self.dims = dims
         self.temperatures = tuple(float(t) for t in temperatures)
@@ -92,6 +93,11 @@ class SlabLattice:
         p.mode, p.n_planes = mode.value, npl.value
         p.code_plane[:] = list(codes)
         p.thr9, p.kg, p.jump, p.work = self._thr.data_ptr(), self.kg, self._jump.data_ptr(), self._work.data_ptr()
+        if stream not in ("xoshiro", "philox"):
+            raise ValueError(f"unknown stream {stream!r}")
+        self.stream = stream
+        p.rng = MSB_RNG_PHILOX if stream == "philox" else MSB_RNG_XOSHIRO
+        p.seed = self.seed & _M64
         self._params = p
         if init == "random":
             with torch.cuda.stream(self._stream):
@@ -103,8 +109,9 @@ class SlabLattice:
             call("msb_init_const", ctypes.byref(self._g), 1, _p(self._spins), self._cs)
         else:
             raise ValueError(f"unknown init mode {init!r}")
-        call("msb_rng_init", ctypes.byref(self._g), ctypes.c_uint64(self.seed & _M64), self.kg,
-             ctypes.c_uint64(0), -1, _p(self._pow), _p(self._states), self._cs)
+        if stream == "xoshiro":
+            call("msb_rng_init", ctypes.byref(self._g), ctypes.c_uint64(self.seed & _M64), self.kg,
+                 ctypes.c_uint64(0), -1, _p(self._pow), _p(self._states), self._cs)
         self.sweeps_done = 0
 
     # -- halo plumbing ---------------------------------------------------------
@@ -121,6 +128,7 @@ class SlabLattice:
     # -- compute ---------------------------------------------------------------
 
     def rng_planes(self) -> None:
+        self._params.block = 2 * self.sweeps_done
         call("msb_rng_planes", ctypes.byref(self._g), ctypes.byref(self._params), -1, _p(self._states), None,
              _p(self._planes), self._cs)
 

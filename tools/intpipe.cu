@@ -278,6 +278,15 @@ int main() {
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     printf("xoshiro VAR %d blocks=%d: %.3f ms  %.3f T draws/s\n", var, bl, ms, (double)bl * 256 * ns / ms / 1e9);
   }
+  for (int wps : {2, 3, 4, 6, 8, 16, 32}) {   // warps per SM for VAR 5
+    int ns = 1 << 13;
+    int threads = wps * 32;                         // 1 block per SM
+    int bl = 148;
+    kxo2<5><<<bl, threads>>>(d, 3, ns);
+    cudaEventRecord(e0); kxo2<5><<<bl, threads>>>(d, 3, ns); cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    printf("VAR5 warps/SM=%d: %.3f T draws/s\n", wps, (double)bl * threads * ns / ms / 1e9);
+  }
   uint32_t* onep; cudaMalloc(&onep, 64);
   { uint32_t h[8] = {1,1,1,1,1,1,1,1}; cudaMemcpy(onep, h, 32, cudaMemcpyHostToDevice); }
   for (int var = 8; var < 10; var++)
