@@ -1297,11 +1297,9 @@ int fused_sweep(const msb_geom* g, const msb_sweep_params* p, uint32_t* spins, u
     // proportion to the work: a flip quad costs ~1/16 of a piece's draws per
     // word, but is latency-bound, so weight it up
     static const int env_cw = [] { const char* e = getenv("MSB_FLIP_WARPS"); return e ? atoi(e) : 0; }();
-    const Geo G = make_geo(g);
-    const double draws = 2.0 * g->n_sim * g->rows * (double)(g->n / 2);
-    const double quads = 2.0 * g->n_sim * g->rows * (G.Wp / 4);
-    int cw = (int)std::lround(32.0 * (quads * 48.0) / (draws + quads * 48.0));
-    cw = std::max(4, std::min(12, cw));
+    // 6 flip warps per CTA measured best for flip-heavy shapes (cfg3/cfg4);
+    // fewer when that keeps every producer warp to one unit (cfg2)
+    int cw = 6;
     // never add a producer round: keep ceil(units / (SMs * producers)) minimal
     const long long units = (2LL * g->n_sim * g->rows * p->kg + 31) / 32;
     const int sms_est = 148;
