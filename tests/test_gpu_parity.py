@@ -217,3 +217,22 @@ def test_philox_phase_by_phase_and_external_streams():
         c.sweep()
     assert (a.lattices() == b.lattices()).all() and (a.lattices() == c.lattices()).all()
     assert a.flips == b.flips == c.flips
+
+
+def test_fault_injection_is_detected():
+    """The selftest seam (cli.py:460-484): corrupting the neighbour adder must
+    make the engine diverge from the oracle, in both flip modes."""
+    from oracle import oracle as orc
+    from paper_2404_16990_b200 import Engine, LatticeDims
+    for generic in (False, True):
+        e = Engine(LatticeDims(12, 96), [2.0], seed=20260808)
+        o = orc.OracleEngine(12, 96, [2.0], 20260808)
+        if generic:  # break the ferro structure: (own=0, u=1) gets its own threshold
+            e._tables[:, 1] = 0.3
+            o.tables[:, 1] = 0.3
+            assert e.flip_mode == 2
+        e.fault = 1
+        e.run(5, measure_interval=5)
+        o.sweep(5)
+        assert (e.lattices() != o.spins).any(), f"fault not visible (generic={generic})"
+        e.fault = 0
