@@ -367,7 +367,6 @@ __device__ __forceinline__ void rng_produce(const RngArgs& a, const uint4* __res
   const long long total = a.npieces * a.ncol;
   const long long units = (total + 31) / 32;
   const size_t pstride = (size_t)G.n_sim * G.rows * G.Wp;
-  const int lk = 64 / a.kr;  // jump lookups per k-segment (multiple of 4)
   const long long nwarps = (long long)role_warps * gridDim.x;
   long long u = (long long)role_warp * gridDim.x + blockIdx.x;
   for (;;) {
@@ -497,10 +496,11 @@ __device__ __forceinline__ void rng_produce(const RngArgs& a, const uint4* __res
         for (int p = 0; p < NPMAX; p++)
           if (p < np) out[p * pstride + ch * 16 + t] = (~__brev(acc[p])) >> (32 - L);
       }
-      // jump lookups: 64/KR per k-segment, one 32-bit state word (8 nibbles)
-      // at a time, XORs paired into 3-input LOP3s
-      if (XO && ((kk + 1) * lk) % 8 == 0) {
-        for (int wcount = (kk + 1) * lk / 8 - nib / 8; wcount > 0; wcount--) {
+      // jump lookups: one 32-bit state word (8 nibbles, 64 lookups in all)
+      // after every second k-segment when kr == 16, else 8/kr words per segment
+      if (XO) {
+        const int nwords = a.kr >= 16 ? (kk & 1) : 8 / a.kr;
+        for (int wcount = 0; wcount < nwords; wcount++) {
           // entry (position nib+j, value v) lives at byte (nib+j)*512 + v*32
           const char* e = reinterpret_cast<const char*>(jt) + nib * 512;
 #pragma unroll
@@ -854,7 +854,7 @@ __global__ void __launch_bounds__(kRngThreads, 1) k_sweep_fused(const RngArgs ra
           __threadfence();
           atomicAdd(ra.work + 1, 1u);
           const unsigned need = gridDim.x * kFlipWarps;
-          while (ld_acquire(ra.work + 1) < need) __nanosleep(64);
+          while (ld_acquire(ra.work + 1) < need) __nanosleep(1000);
         }
         __syncwarp();
         __threadfence();
