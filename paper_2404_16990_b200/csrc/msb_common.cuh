@@ -1,0 +1,292 @@
+// Shared device code of libmsb200 (sm_100a): the reference RNG restated for
+// the GPU, the colour-split row geometry and the host-side argument checks.
+// Included by msb_sweep.cu (hot path), msb_state.cu (state/layout kernels)
+// and msb_host.cu (host-only ABI).  See include/msb200.h for the ABI and
+// DESIGN.md for the layout / roofline discussion.
+//
+// Reference algorithm being reproduced bit-exactly (pkg/src/multispin/...):
+//   stream seeding       rng.py:53-82     splitmix64 -> xoshiro256 state
+//   xoshiro256++ step    rng.py:93-105
+//   23-bit shaping       rng.py:113-115, 180-183
+//   draw consumption     engine.py:334-343 (quarter, k = 4i+ii, word)
+//   bit gated by draw    engine.py:321-331 (bit 4ii+i of the target word)
+//   quarter targets      engine.py:57-68  (FLIP_RED / FLIP_BLUE)
+//   Metropolis test      engine.py:78-94, 325-330 (float64 u < table[code])
+//   observables          engine.py:372-386
+//
+// Layout here is NOT the reference's eight folded uint16 arrays: spins are
+// split by checkerboard colour into rows of 32 same-colour sites per uint32
+// (include/msb200.h).  The fold/moat/halo structure of the WSE mapping is an
+// interop format only (msb_to_ref16 / msb_from_ref16).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/msb200.h"
+#include "gf2_jump.h"
+
+namespace msbk {
+
+constexpr uint64_t kGolden = 0x9E3779B97F4B7C15ULL;
+constexpr int kJumpWords = 8192;  // one nibble table = 32 KiB
+constexpr uint32_t kKeyAlways = 0xFFFFFFFFu;
+
+// error reporting (msb_last_error), defined in msb_host.cu
+int fail(int code, const std::string& why);
+int check_geom(const msb_geom* g);
+int check_params(const msb_sweep_params* p);
+
+#define CUDA_TRY(expr)                                                                 \
+  do {                                                                                 \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess) return fail(MSB_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline unsigned blocks_for(long long n, int bt) { return (unsigned)((n + bt - 1) / bt); }
+
+// ---------------------------------------------------------------------------
+// device: RNG
+// ---------------------------------------------------------------------------
+
+struct XState {
+  uint32_t a0, a1, b0, b1, c0, c1, d0, d1;  // s0..s3 as (lo, hi) halves
+};
+
+__device__ __forceinline__ uint32_t xor3(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+// One xoshiro256++ step (rng.py:93-105); returns the HIGH 32 bits of the
+// output, the only bits the reference shapes into a draw (rng.py:115).
+// 64-bit adds are carry chains (IADD3 + IMAD.X), rotations funnel shifts,
+// the XOR network four 3-input LOP3 pairs.
+__device__ __forceinline__ uint32_t xstep(XState& s) {
+  uint32_t x0, x1, o1;
+  asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, %5;"
+      : "=r"(x0), "=r"(x1)
+      : "r"(s.a0), "r"(s.d0), "r"(s.a1), "r"(s.d1));
+  const uint32_t r1 = __funnelshift_l(x0, x1, 23), r0 = __funnelshift_l(x1, x0, 23);
+  asm("{.reg .b32 t;\n\tadd.cc.u32 t, %1, %2;\n\taddc.u32 %0, %3, %4;}"
+      : "=r"(o1)
+      : "r"(r0), "r"(s.a0), "r"(r1), "r"(s.a1));
+  // t = s1 << 17 through IMAD.WIDE (FMA pipe): lo = b0 << 17, hi = b0 >> 15
+  uint64_t w17;
+  asm("mul.wide.u32 %0, %1, 131072;" : "=l"(w17) : "r"(s.b0));
+  const uint32_t t0 = (uint32_t)w17, t1 = s.b1 * 131072u + (uint32_t)(w17 >> 32);
+  const uint32_t nc0 = xor3(s.c0, s.a0, t0), nc1 = xor3(s.c1, s.a1, t1);
+  const uint32_t nd0 = s.d0 ^ s.b0, nd1 = s.d1 ^ s.b1;
+  const uint32_t nb0 = xor3(s.b0, s.c0, s.a0), nb1 = xor3(s.b1, s.c1, s.a1);
+  const uint32_t na0 = xor3(s.a0, s.d0, s.b0), na1 = xor3(s.a1, s.d1, s.b1);
+  s.a0 = na0; s.a1 = na1; s.b0 = nb0; s.b1 = nb1; s.c0 = nc0; s.c1 = nc1;
+  s.d1 = __funnelshift_l(nd1, nd0, 13);  // rotl64(nd, 45)
+  s.d0 = __funnelshift_l(nd0, nd1, 13);
+  return o1;
+}
+
+// acc = 2*acc + [h9 >= key]  (h9 = draw << 9): one carry-out compare plus
+// one carry-in add.  [h9 >= key] is the REJECT bit of u23 < K (key = K<<9,
+// or 0xFFFFFFFF when K == 2^23).
+__device__ __forceinline__ void acc_reject(uint32_t& acc, uint32_t h9, uint32_t key) {
+  asm("{.reg .b32 t;\n\tsub.cc.u32 t, %1, %2;\n\taddc.u32 %0, %0, %0;}" : "+r"(acc) : "r"(h9), "r"(key));
+}
+
+// Philox4x32-10 (Salmon et al., SC'11), the counter-based stream of
+// paper_2404_16990_b200.rng.PhiloxStreams: counter (c0..c3), key (k0, k1).
+// Each round is two IMAD.WIDE (FMA pipe) and two 3-input XORs (ALU); the
+// round keys are warp-uniform.
+__device__ __forceinline__ void philox10(uint32_t& c0, uint32_t& c1, uint32_t& c2, uint32_t& c3, uint32_t k0,
+                                         uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; r++) {
+    const uint64_t p0 = (uint64_t)c0 * 0xD2511F53u, p1 = (uint64_t)c2 * 0xCD9E8D57u;
+    const uint32_t n0 = xor3((uint32_t)(p1 >> 32), c1, k0), n2 = xor3((uint32_t)(p0 >> 32), c3, k1);
+    c1 = (uint32_t)p1;
+    c3 = (uint32_t)p0;
+    c0 = n0;
+    c2 = n2;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {  // rng.py:53-58
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ XState stream_state(uint64_t seed, uint64_t stream) {  // rng.py:71-82
+  uint64_t z = mix64(seed + (stream + 1) * kGolden);
+  uint64_t s[4];
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    z += kGolden;
+    s[i] = mix64(z);
+  }
+  if (!(s[0] | s[1] | s[2] | s[3])) s[0] = kGolden;
+  XState x;
+  x.a0 = (uint32_t)s[0]; x.a1 = (uint32_t)(s[0] >> 32);
+  x.b0 = (uint32_t)s[1]; x.b1 = (uint32_t)(s[1] >> 32);
+  x.c0 = (uint32_t)s[2]; x.c1 = (uint32_t)(s[2] >> 32);
+  x.d0 = (uint32_t)s[3]; x.d1 = (uint32_t)(s[3] >> 32);
+  return x;
+}
+
+// s <- M s with M given as a nibble table T[64][16][8 words] (uint4 pairs).
+__device__ __forceinline__ XState jump_apply(const XState& s, const uint4* __restrict__ T) {
+  const uint32_t w[8] = {s.a0, s.a1, s.b0, s.b1, s.c0, s.c1, s.d0, s.d1};
+  uint32_t r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+  for (int q = 0; q < 8; q++) {
+#pragma unroll
+    for (int nib = 0; nib < 8; nib++) {
+      const int p = q * 8 + nib;
+      const uint32_t v = (w[q] >> (4 * nib)) & 15u;
+      const uint4 lo = T[(p * 16 + v) * 2], hi = T[(p * 16 + v) * 2 + 1];
+      r[0] ^= lo.x; r[1] ^= lo.y; r[2] ^= lo.z; r[3] ^= lo.w;
+      r[4] ^= hi.x; r[5] ^= hi.y; r[6] ^= hi.z; r[7] ^= hi.w;
+    }
+  }
+  XState o;
+  o.a0 = r[0]; o.a1 = r[1]; o.b0 = r[2]; o.b1 = r[3];
+  o.c0 = r[4]; o.c1 = r[5]; o.d0 = r[6]; o.d1 = r[7];
+  return o;
+}
+
+__device__ __forceinline__ XState jump_by(XState s, uint64_t J, const uint4* __restrict__ pow) {
+  for (int b = 0; b < 64; b++)
+    if ((J >> b) & 1) s = jump_apply(s, pow + (size_t)b * (kJumpWords / 4));
+  return s;
+}
+
+__device__ __forceinline__ void load_state(XState& s, const uint32_t* st, long long np, long long gp) {
+  s.a0 = st[0 * np + gp]; s.a1 = st[1 * np + gp]; s.b0 = st[2 * np + gp]; s.b1 = st[3 * np + gp];
+  s.c0 = st[4 * np + gp]; s.c1 = st[5 * np + gp]; s.d0 = st[6 * np + gp]; s.d1 = st[7 * np + gp];
+}
+__device__ __forceinline__ void store_state(const XState& s, uint32_t* st, long long np, long long gp) {
+  st[0 * np + gp] = s.a0; st[1 * np + gp] = s.a1; st[2 * np + gp] = s.b0; st[3 * np + gp] = s.b1;
+  st[4 * np + gp] = s.c0; st[5 * np + gp] = s.c1; st[6 * np + gp] = s.d0; st[7 * np + gp] = s.d1;
+}
+
+// ---------------------------------------------------------------------------
+// device: geometry of the reference stream <-> colour-split rows
+// ---------------------------------------------------------------------------
+
+// For lattice row c and colour X: the reference cell (1-based gamma) whose
+// stream gates it and the quarter q (position of the target array in
+// FLIP_RED / FLIP_BLUE, engine.py:57-68).  Targets: (F,E)->0, (B,O)->1,
+// (B,E)->2, (F,O)->3 for both colours, E/O = parity of the rows r of the
+// colour's sites, (c+X)&1 (lattice.py:156-175).
+struct RowStream {
+  int gamma, q;
+};
+__device__ __host__ __forceinline__ RowStream row_stream(int m, int c, int X) {
+  const bool fwd = c < m / 2;
+  const int odd = (c + X) & 1;
+  RowStream r;
+  r.gamma = fwd ? c / 2 + 1 : (m - 1 - c) / 2 + 1;
+  r.q = fwd ? (odd ? 3 : 0) : (odd ? 1 : 2);
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// device: the interleaved colour-split layout
+// ---------------------------------------------------------------------------
+//
+// Row (c, X) holds the n/2 sites of colour X (X = 0 red: (c+r) even), site
+// index i = r >> 1, split as i = 16 w + t (w < n/32, t < 16) -- exactly the
+// reference's packing of a column vector into uint16 words, word w bit t
+// (lattice.py:199-202).  Our uint32 word (ch, t) of the row holds bit t of
+// the reference words w = 32 ch + b, b = 0..31: a 32-way transpose of the
+// reference words, so the draws a stream consumes for one k (= one t, every
+// w in order, engine.py:321-330) accumulate straight into one word per
+// chunk.  Row pitch Wp = 16 * nch words, nch = ceil((n/32) / 32).
+
+// Division by a run-time invariant 32-bit divisor with a multiply-high
+// (round-up method): q = (t + ((x - t) >> s1)) >> s2, t = umulhi(x, m).
+struct FastDiv {
+  uint32_t d, m, s1, s2;
+  __host__ void init(uint32_t div) {
+    d = div;
+    uint32_t l = 0;
+    while (l < 32 && (1ull << l) < div) l++;
+    m = (uint32_t)(((1ull << 32) * ((1ull << l) - div)) / div + 1);
+    s1 = l < 1 ? l : 1;
+    s2 = l > 0 ? l - 1 : 0;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t x) const {
+    const uint32_t t = __umulhi(x, m);
+    return (t + ((x - t) >> s1)) >> s2;
+  }
+};
+
+struct Geo {
+  int n_sim, m, n, rows, row0, ghost, R, Wp, words, nch;
+  long long sim_offset;
+  FastDiv rows_div, quads_div;
+};
+
+__host__ inline Geo make_geo(const msb_geom* g) {
+  Geo o;
+  o.n_sim = g->n_sim; o.m = g->m; o.n = g->n; o.rows = g->rows; o.row0 = g->row0; o.ghost = g->ghost;
+  o.R = g->rows + 2 * g->ghost;
+  o.words = g->n / 32;
+  o.nch = (o.words + 31) / 32;
+  o.Wp = 16 * o.nch;
+  o.sim_offset = g->sim_offset;
+  o.rows_div.init((uint32_t)o.rows);
+  o.quads_div.init((uint32_t)(o.Wp / 4));
+  return o;
+}
+
+// valid bits of chunk ch (w = 32 ch + b < n/32)
+__device__ __forceinline__ int chunk_bits(const Geo& G, int ch) {
+  const int b = G.words - 32 * ch;
+  return b >= 32 ? 32 : b;
+}
+__device__ __forceinline__ uint32_t chunk_mask(const Geo& G, int ch) {
+  const int b = chunk_bits(G, ch);
+  return b >= 32 ? 0xFFFFFFFFu : ((1u << b) - 1u);
+}
+__device__ __forceinline__ size_t row_off(const Geo& G, int s, int X, int br) {
+  return ((size_t)(s * 2 + X) * G.R + br) * G.Wp;
+}
+// buffer rows of the vertical neighbours (c-1, c+1) of buffer row br
+__device__ __forceinline__ void vert_rows(const Geo& G, int br, int& bu, int& bd) {
+  if (G.ghost) {
+    bu = br - 1; bd = br + 1;
+  } else {
+    bu = br == 0 ? G.R - 1 : br - 1;
+    bd = br + 1 == G.R ? 0 : br + 1;
+  }
+}
+
+// The second horizontal neighbour (site i+1 when p=1, i-1 when p=0, periodic
+// in n/2) of word (ch, t), read from the other colour's row y.  Interior t
+// just uses word t+-1; t = 15 / t = 0 wrap into the next / previous w.
+__device__ __forceinline__ uint32_t h_second(const Geo& G, const uint32_t* y, int ch, int t, int p) {
+  if (p) {
+    if (t < 15) return y[ch * 16 + t + 1];
+    const int chn = ch + 1 < G.nch ? ch + 1 : 0;
+    return (y[ch * 16] >> 1) | ((y[chn * 16] & 1u) << (chunk_bits(G, ch) - 1));
+  }
+  if (t > 0) return y[ch * 16 + t - 1];
+  const uint32_t carry = ch > 0 ? (y[(ch - 1) * 16 + 15] >> 31)
+                                : ((y[(G.nch - 1) * 16 + 15] >> (chunk_bits(G, G.nch - 1) - 1)) & 1u);
+  return ((y[ch * 16 + 15] << 1) | carry) & chunk_mask(G, ch);
+}
+
+
+}  // namespace msbk

@@ -1,7 +1,7 @@
 """Host-side view of the reference RNG stream (pkg/src/multispin/rng.py:53-236).
 
 The sweep kernels generate the reference's xoshiro256++ streams on the GPU
-(csrc/msb_kernels.cu).  This module keeps the host API the reference exports
+(csrc/msb_sweep.cu, csrc/msb_common.cuh).  This module keeps the host API the reference exports
 -- scalar ``Xoshiro256pp``, lock-step ``XoshiroStreams`` and
 ``shape_unit_float`` -- for callers that draw on the host (e.g. custom
 streams handed to ``Engine.streams``).  It is not on the hot path.
