@@ -206,7 +206,7 @@ def load_traffic():
     p = ROOT / "profiles" / "ncu_summary.json"
     try:
         d = json.loads(p.read_text())
-        return d.get("k_sweep_fused", {}).get("dram_bytes_per_launch")
+        return d.get("k_win", {}).get("dram_bytes_per_launch")
     except Exception:
         return None
 
@@ -227,11 +227,12 @@ def run_ours(args, cfg):
     eng = Engine(LatticeDims(cfg["m"], cfg["n"]), temps, cfg["seed"], init=cfg["init"],
                  sim_offset=rank * n_sim, device=dev, kg=args.kg, stream=args.stream)
     st = eng._stream
-    attempts_step = n_sim * cfg["m"] * cfg["n"]
+    S = eng.window                      # one step = one lookahead window of S sweeps = one launch
+    attempts_step = n_sim * cfg["m"] * cfg["n"] * S
     peak = int_peak_tops(st)
 
-    # warm-up (public path)
-    eng._sweeps(args.warmup)
+    # warm-up (public path), whole windows
+    eng._sweeps(args.warmup * S)
     eng.synchronize()
 
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
@@ -247,7 +248,7 @@ def run_ours(args, cfg):
     for k in range(K):
         with torch.cuda.stream(st):
             flush.zero_()          # L2 flush between timed steps (outside the events)
-        eng._timed_sweep(*evs[k])
+        eng._timed_sweeps(S, *evs[k])
     torch.cuda.synchronize()
     t_wall = time.perf_counter() - t_wall
     sampler.stop()
@@ -276,7 +277,7 @@ def run_ours(args, cfg):
         obs = (torch.empty(hi - lo, dtype=torch.int64, pin_memory=True),
                torch.empty(hi - lo, dtype=torch.int64, pin_memory=True))
         g.store_packed(bufs[0])
-        g._sweeps(2)  # warm the group's path
+        g._sweeps(2 * g.window)  # warm the group's path
         groups.append((g, bufs, obs, hi - lo))
     for g, *_ in groups:
         g.synchronize()
@@ -288,10 +289,10 @@ def run_ours(args, cfg):
         g, bufs, (ups, uns), ns = groups[k & 1]
         j = k >> 1
         g.load_packed(bufs[j & 1])
-        g._sweeps(1)
+        g._sweeps(g.window)
         g.store_packed(bufs[(j + 1) & 1])
         g.observe_async(ups, uns)
-        e2e_attempts += ns * cfg["m"] * cfg["n"]
+        e2e_attempts += ns * cfg["m"] * cfg["n"] * g.window
     for g, *_ in groups:
         g.synchronize()
     e2e_s = time.perf_counter() - t0
@@ -314,22 +315,25 @@ def run_ours(args, cfg):
                 "global_replicas": n_sim * ws, "attempts_per_step": attempts_step * ws,
                 "parallelism": f"replicas sharded over {ws} GPU(s), no data-path collective",
                 "l2": f"flushed between timed steps ({L2_FLUSH_BYTES >> 20} MiB write, outside the events)",
-                "stream": "reference xoshiro256++ (bit-exact with multispin.Engine)", "kg": eng.kg,
+                "stream": "reference xoshiro256++ (bit-exact with multispin.Engine)",
+                "step": f"one lookahead window: {S} sweeps in one launch (flips of these {S} sweeps + "
+                        f"accept planes of the next {S})",
+                "sweeps_per_step": S, "window_parts": eng._wP,
             },
             "roofline": {
                 "bound": "int32", "achieved": achieved, "peak": peak, "unit": "Tops/s",
                 "frac": achieved / peak, "traffic": load_traffic(),
-                "kernel": "k_sweep_fused", "per_launch": f"{attempts_step} attempts x {A_INT} int32 ops",
+                "kernel": "k_win", "per_launch": f"{attempts_step} attempts x {A_INT} int32 ops",
                 "peak_source": "msb_bench_int_peak: issue-bound LOP3+IMAD mix, measured in this run",
             },
             "roofline_attempts": {
                 "int_term": peak * 1e12 / A_INT, "hbm_term": 6532.9e9 / A_BYTES,
                 "frac_of_min": value / ws / min(peak * 1e12 / A_INT, 6532.9e9 / A_BYTES),
             },
-            "kernel_ms": {"sweep_fused_mean": statistics.mean(step_ms), "sweep_fused_median": statistics.median(step_ms)},
+            "kernel_ms": {"k_win_mean": statistics.mean(step_ms), "k_win_median": statistics.median(step_ms)},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": nbytes,
                     "d2h_bytes_per_step": nbytes + 16 * half, "steps": Ke,
-                    "path": "per step, one half of the replicas: Engine.load_packed(pinned) -> one sweep -> "
+                    "path": "per step, one half of the replicas: Engine.load_packed(pinned) -> one window of sweeps -> "
                             "Engine.store_packed(pinned) + observables; the two halves alternate on their own "
                             "streams so copies of one overlap the sweep of the other"},
             "gpu_launches": K,

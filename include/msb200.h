@@ -173,6 +173,34 @@ int msb_sweep(const msb_geom *g, const msb_sweep_params *p, uint32_t *spins, uin
               uint32_t *planes, int32_t n_sweeps, int32_t flags, int32_t *cur_io, uint64_t *flips,
               void *stream);
 
+/* ---- lookahead windows: S sweeps of accept planes per launch -------------- */
+/* Steady-state path for FERRO/ANTI whole lattices (replaces the Engine.sweep
+ * loop, engine.py:353-360 / 416-417, S sweeps at a time).  The draws of a
+ * window (sweeps w..w+S-1, stream blocks B..B+2S-1) are produced by pieces
+ * (slot j, part p, stream): the stream's draws of sweep w+j, split into P
+ * contiguous parts (P = 1: the whole sweep, 4n draws).  Each piece runs its
+ * stream contiguously and jumps S*4n ahead once; the jump table passed in
+ * p->jump must be msb_rng_jump_table(S*4n).  A window buffer holds
+ * msb_window_words() uint32 words: [S][2 colours][2 planes][n_sim][m][Wp].
+ * msb_window_pieces: piece count (piece states are 8 uint32 each).
+ * msb_default_window: S and P for a geometry (balanced SM load, bounded
+ * plane memory).
+ * msb_window_init: piece states for a window whose slot 0 starts at stream
+ * block `block` (xoshiro).
+ * msb_window_sweep: flips slots [first, first+count) of window `cur` (red,
+ * blue, red, ... in one cooperative launch) and, if next != NULL, produces
+ * the following window into `next` in the same launch (producer warps
+ * overlap the flips).  For Philox p->block is the block of the produced
+ * window's slot 0.  count == 0 with next != NULL produces only. */
+int msb_default_window(const msb_geom *g, int32_t *S, int32_t *P);
+int64_t msb_window_pieces(const msb_geom *g, int32_t S, int32_t P);
+int64_t msb_window_words(const msb_geom *g, int32_t S);
+int msb_window_init(const msb_geom *g, uint64_t seed, int32_t S, int32_t P, uint64_t block,
+                    const uint32_t *pow_tables, uint32_t *states, void *stream);
+int msb_window_sweep(const msb_geom *g, const msb_sweep_params *p, int32_t S, int32_t P,
+                     uint32_t *spins, uint32_t *states, const uint32_t *cur, int32_t first,
+                     int32_t count, uint32_t *next, uint64_t *flips, void *stream);
+
 /* ---- observables (engine.py:372-386) ------------------------------------- */
 /* Adds, per replica, the number of +1 spins and the number of unsatisfied
  * bonds owned by the held rows (bonds of red sites) into ups[n_sim] and

@@ -201,6 +201,19 @@ __device__ __host__ __forceinline__ RowStream row_stream(int m, int c, int X) {
   return r;
 }
 
+// Inverse of row_stream: the row of colour X that quarter q of cell gamma's
+// stream gates.  Forward quarters (0, 3) gate rows 2(gamma-1) + {0, 1},
+// backward quarters (1, 2) rows m-1-2(gamma-1) - {0, 1}.
+__device__ __host__ __forceinline__ int seg_row(int m, int gamma, int X, int q) {
+  const int g2 = 2 * (gamma - 1);
+  switch (q) {
+    case 0: return g2 + X;
+    case 3: return g2 + 1 - X;
+    case 1: return m - 1 - g2 - X;
+    default: return m - 1 - g2 - (1 - X);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // device: the interleaved colour-split layout
 // ---------------------------------------------------------------------------

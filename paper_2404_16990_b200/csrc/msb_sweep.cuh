@@ -1,0 +1,371 @@
+// Device pieces shared by the per-sweep path (msb_sweep.cu) and the
+// lookahead-window path (msb_window.cu): producer constants and work
+// counters, the flip pass (FERRO/ANTI chunk flips, generic quads), the grid
+// barrier primitive and small host helpers.
+#pragma once
+#include "msb_common.cuh"
+
+namespace msbk {
+namespace {
+
+// draw sources of the producer
+constexpr int kSrcXoshiro = 0;  // persistent per-piece reference streams
+constexpr int kSrcExt = 1;      // host-supplied u23 draws
+constexpr int kSrcPhilox = 2;   // counter-based Philox4x32-10
+
+// reference bit t of a uint16 word is gated by draw k = 4(t%4) + t/4 (the
+// mapping is its own inverse, engine.py:326-330)
+__device__ __forceinline__ int t_of_k(int k) { return 4 * (k & 3) + (k >> 2); }
+
+__device__ __forceinline__ size_t plane_off(const Geo& G, int np, int X, int p, int s, int lr) {
+  return ((((size_t)X * np + p) * G.n_sim + s) * G.rows + lr) * G.Wp;
+}
+
+// Development trace (build with -DMSB_TRACE, tools/trace_producer.py): per
+// warp, globaltimer / clock64 stamps at kernel entry, after the table load,
+// and at the end of its work, plus SM id and the units it processed.
+#ifdef MSB_TRACE
+constexpr int kTraceWarps = 148 * 32;
+__device__ unsigned long long g_trace[kTraceWarps * 8];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_put(int slot, unsigned long long v) {
+  const int w = blockIdx.x * 32 + (threadIdx.x >> 5);
+  if ((threadIdx.x & 31) == 0 && w < kTraceWarps) g_trace[w * 8 + slot] = v;
+}
+#define MSB_TRACE_PUT(slot, v) trace_put(slot, v)
+#else
+#define MSB_TRACE_PUT(slot, v) ((void)0)
+#endif
+
+// Persistent kernel: one 1024-thread CTA per SM shares one copy of the
+// sweep-jump table in shared memory; warps claim 32 consecutive pieces at a
+// time from a self-resetting counter (work[0] = next unit, work[1] = warps
+// done), so SMs stay balanced whatever the piece count.  Each lane runs one
+// piece: it generates the piece's draws (k-range x all w) and, spread through
+// the generation loop, performs the 64 nibble lookups of its jump to the
+// next sweep, so table reads overlap other warps' ALU work.
+constexpr int kRngThreads = 1024;
+#ifndef MSB_CHUNK_UNROLL
+#define MSB_CHUNK_UNROLL 16
+#endif
+constexpr int kChunkUnroll = MSB_CHUNK_UNROLL;
+
+// Work counters (caller-owned, zeroed once, left zeroed by every kernel):
+//   work[0] next dynamic producer unit    work[1] consumer barrier arrivals
+//   work[2] warps finished (last one resets all four)
+__device__ __forceinline__ void finish_warp(unsigned* work, unsigned total_warps) {
+  if ((threadIdx.x & 31) == 0) {
+    __threadfence();
+    if (atomicAdd(work + 2, 1u) == total_warps - 1) {
+      atomicExch(work, 0u);
+      atomicExch(work + 1, 0u);
+      atomicExch(work + 2, 0u);
+    }
+  }
+}
+
+// One producer warp's share of a sweep's accept planes.  `role_warp` /
+// `role_warps` number the producer warps of the grid; their first unit is
+
+// ---------------------------------------------------------------------------
+// device: the flip pass (one colour)
+// ---------------------------------------------------------------------------
+
+struct FlipArgs {
+  Geo G;
+  uint32_t* spins;
+  const uint32_t* planes;
+  unsigned long long* flips;
+  int X, np, cwarps;
+  uint32_t inv;
+  int fault;
+  int8_t code_plane[16];
+};
+
+constexpr int kFlipSlots = 256;
+
+__device__ __forceinline__ uint32_t flip_word(const FlipArgs& a, bool generic, uint32_t o, uint32_t n1, uint32_t n2,
+                                              uint32_t y0, uint32_t n4, const uint32_t* pl, size_t pstride,
+                                              uint32_t A4, uint32_t A8) {
+  if (!generic) {
+    const uint32_t ow = o ^ a.inv;
+    const uint32_t x1 = n1 ^ ow, x2 = n2 ^ ow, x3 = y0 ^ ow;
+    const uint32_t x4 = a.fault ? 0u : (n4 ^ ow);
+    const uint32_t o12 = x1 | x2, a12 = x1 & x2, o34 = x3 | x4, a34 = x3 & x4;
+    const uint32_t ge2 = a12 | a34 | (o12 & o34);  // >= 2 disagreeing neighbours
+    const uint32_t any = o12 | o34;
+    return ge2 | (any & ~ge2 & A4) | (~any & A8);
+  }
+  // neighbour up-count bit planes (bitkernels.py:63-79 restated)
+  const uint32_t s1 = n1 ^ n2, c1 = n1 & n2, s2 = y0 ^ n4, c2 = y0 & n4;
+  uint32_t ones = s1 ^ s2;
+  const uint32_t twos = c1 ^ c2 ^ (s1 & s2), fours = c1 & c2;
+  if (a.fault) ones = s1;
+  uint32_t flip = 0;
+  for (int code = 0; code < 16; code++) {
+    const int pidx = a.code_plane[code];
+    const int u = code & 7;
+    if (pidx == -1 || u > 4) continue;
+    const uint32_t msk = ((code & 8) ? o : ~o) & ((u & 1) ? ones : ~ones) & ((u & 2) ? twos : ~twos) &
+                         ((u & 4) ? fours : ~fours);
+    flip |= pidx == -2 ? msk : (msk & __ldg(pl + pidx * pstride));
+  }
+  return flip;
+}
+
+// One quad of 4 t-words (t0..t0+3 of chunk ch) of row (s, lr) in colour
+// a.X.  Vertical neighbours are the other colour's rows c-1, c+1 (same
+// word); horizontal ones the other colour's row c at sites i and i+-1
+// (h_second).  COHERENT: other-colour words were written earlier in the same
+// kernel by other SMs, so read them through L2 (ld.global.cg).
+template <bool GENERIC, bool COHERENT>
+__device__ __forceinline__ unsigned flip_quad_at(const FlipArgs& a, int s, int lr, unsigned qq, int X) {
+  const Geo& G = a.G;
+  const int c = G.row0 + lr, br = lr + G.ghost;
+  const int ch = (int)(qq >> 2), t0 = 4 * (int)(qq & 3);
+  const int w0 = ch * 16 + t0;
+  int bu, bd;
+  vert_rows(G, br, bu, bd);
+  uint32_t* own = a.spins + row_off(G, s, X, br);
+  const uint32_t* yc = a.spins + row_off(G, s, 1 - X, br);
+  auto ld4 = [](const uint32_t* q) {
+    return COHERENT ? __ldcg(reinterpret_cast<const uint4*>(q)) : __ldg(reinterpret_cast<const uint4*>(q));
+  };
+  auto ld1 = [](const uint32_t* q) { return COHERENT ? __ldcg(q) : __ldg(q); };
+  const uint4 O = *reinterpret_cast<const uint4*>(own + w0);
+  const uint4 Y = ld4(yc + w0);
+  const uint4 U = ld4(a.spins + row_off(G, s, 1 - X, bu) + w0);
+  const uint4 D = ld4(a.spins + row_off(G, s, 1 - X, bd) + w0);
+  const size_t pstride = (size_t)G.n_sim * G.rows * G.Wp;
+  const uint32_t* pl = a.planes + plane_off(G, a.np, X, 0, s, lr) + w0;
+  uint4 P4 = make_uint4(0, 0, 0, 0), P8 = make_uint4(0, 0, 0, 0);
+  if (!GENERIC) {
+    P4 = __ldg(reinterpret_cast<const uint4*>(pl));
+    P8 = __ldg(reinterpret_cast<const uint4*>(pl + pstride));
+  }
+  const int p = (c + X) & 1;
+  const uint32_t y[4] = {Y.x, Y.y, Y.z, Y.w};
+  const uint32_t o[4] = {O.x, O.y, O.z, O.w};
+  const uint32_t u4[4] = {U.x, U.y, U.z, U.w};
+  const uint32_t d4[4] = {D.x, D.y, D.z, D.w};
+  const uint32_t a4[4] = {P4.x, P4.y, P4.z, P4.w};
+  const uint32_t a8[4] = {P8.x, P8.y, P8.z, P8.w};
+  // the neighbour word just outside the quad (t0+4 if p, t0-1 otherwise) or,
+  // at t = 15 / t = 0, the shifted word of the next / previous w
+  uint32_t edge;
+  const int vb = chunk_bits(G, ch);
+  if (p) {
+    if (t0 + 4 < 16) {
+      edge = ld1(yc + w0 + 4);
+    } else {
+      const int chn = ch + 1 < G.nch ? ch + 1 : 0;
+      edge = (ld1(yc + ch * 16) >> 1) | ((ld1(yc + chn * 16) & 1u) << (vb - 1));
+    }
+  } else {
+    if (t0 > 0) {
+      edge = ld1(yc + w0 - 1);
+    } else {
+      const uint32_t carry = ch > 0 ? (ld1(yc + (ch - 1) * 16 + 15) >> 31)
+                                    : ((ld1(yc + (G.nch - 1) * 16 + 15) >> (chunk_bits(G, G.nch - 1) - 1)) & 1u);
+      edge = ((ld1(yc + ch * 16 + 15) << 1) | carry) & chunk_mask(G, ch);
+    }
+  }
+  const uint32_t vm = chunk_mask(G, ch);
+  uint32_t res[4];
+  unsigned cnt = 0;
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    const uint32_t n4 = p ? (k < 3 ? y[k + 1] : edge) : (k > 0 ? y[k - 1] : edge);
+    uint32_t f = flip_word(a, GENERIC, o[k], u4[k], d4[k], y[k], n4, pl + k, pstride, a4[k], a8[k]);
+    f &= vm;
+    res[k] = o[k] ^ f;
+    cnt += __popc(f);
+  }
+  *reinterpret_cast<uint4*>(own + w0) = make_uint4(res[0], res[1], res[2], res[3]);
+  return cnt;
+}
+
+template <bool GENERIC, bool COHERENT>
+__device__ __forceinline__ unsigned flip_quad(const FlipArgs& a, unsigned i, int X) {
+  const Geo& G = a.G;
+  const unsigned quads = (unsigned)G.Wp >> 2;
+  const unsigned gr = G.quads_div.div(i), qq = i - gr * quads;
+  const int s = (int)G.rows_div.div(gr), lr = (int)(gr - (unsigned)s * G.rows);
+  return flip_quad_at<GENERIC, COHERENT>(a, s, lr, qq, X);
+}
+
+// FERRO/ANTI flip of one whole 16-word chunk (t = 0..15 of chunk ch) of row
+// (s, lr), colour X.  The other colour's same-row words stay in registers, so
+// every t+-1 neighbour -- and, when the row is one chunk, the t = 0/15 wraps
+// -- comes from registers; address math happens once per chunk.
+template <bool COHERENT>
+__device__ __forceinline__ unsigned flip_chunk_at(const FlipArgs& a, int s, int lr, int ch, int X) {
+  const Geo& G = a.G;
+  const int c = G.row0 + lr, br = lr + G.ghost;
+  int bu, bd;
+  vert_rows(G, br, bu, bd);
+  const int w0 = ch * 16;
+  uint32_t* own = a.spins + row_off(G, s, X, br) + w0;
+  const uint32_t* ycr = a.spins + row_off(G, s, 1 - X, br);
+  const uint32_t* yu = a.spins + row_off(G, s, 1 - X, bu) + w0;
+  const uint32_t* yd = a.spins + row_off(G, s, 1 - X, bd) + w0;
+  const size_t pstride = (size_t)G.n_sim * G.rows * G.Wp;
+  const uint32_t* pl = a.planes + plane_off(G, a.np, X, 0, s, lr) + w0;
+  auto ld4 = [](const uint32_t* q) {
+    return COHERENT ? __ldcg(reinterpret_cast<const uint4*>(q)) : __ldg(reinterpret_cast<const uint4*>(q));
+  };
+  auto ld1 = [](const uint32_t* q) { return COHERENT ? __ldcg(q) : __ldg(q); };
+  uint32_t y[16];
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const uint4 v = ld4(ycr + w0 + 4 * q);
+    y[4 * q] = v.x; y[4 * q + 1] = v.y; y[4 * q + 2] = v.z; y[4 * q + 3] = v.w;
+  }
+  const int p = (c + X) & 1;
+  const int vb = chunk_bits(G, ch);
+  const uint32_t vm = chunk_mask(G, ch);
+  // the wrap word: p=1 -> t=15 needs bit 0 of the next chunk's t=0 word;
+  // p=0 -> t=0 needs the top valid bit of the previous chunk's t=15 word
+  uint32_t wrapn;
+  if (p) {
+    const int chn = ch + 1 < G.nch ? ch + 1 : 0;
+    const uint32_t nx = chn == ch ? y[0] : ld1(ycr + chn * 16);
+    wrapn = (y[0] >> 1) | ((nx & 1u) << (vb - 1));
+  } else {
+    uint32_t carry;
+    if (ch > 0) carry = ld1(ycr + (ch - 1) * 16 + 15) >> 31;
+    else carry = ((G.nch == 1 ? y[15] : ld1(ycr + (G.nch - 1) * 16 + 15)) >> (chunk_bits(G, G.nch - 1) - 1)) & 1u;
+    wrapn = ((y[15] << 1) | carry) & vm;
+  }
+  unsigned cnt = 0;
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const uint4 O = *reinterpret_cast<const uint4*>(own + 4 * q);
+    const uint4 U = ld4(yu + 4 * q), D = ld4(yd + 4 * q);
+    const uint4 P4 = __ldg(reinterpret_cast<const uint4*>(pl + 4 * q));
+    const uint4 P8 = __ldg(reinterpret_cast<const uint4*>(pl + pstride + 4 * q));
+    const uint32_t o[4] = {O.x, O.y, O.z, O.w}, u4[4] = {U.x, U.y, U.z, U.w}, d4[4] = {D.x, D.y, D.z, D.w};
+    const uint32_t a4[4] = {P4.x, P4.y, P4.z, P4.w}, a8[4] = {P8.x, P8.y, P8.z, P8.w};
+    uint32_t res[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const int t = 4 * q + k;
+      const uint32_t n4 = p ? (t < 15 ? y[t + 1] : wrapn) : (t > 0 ? y[t - 1] : wrapn);
+      const uint32_t f = flip_word(a, false, o[k], u4[k], d4[k], y[t], n4, nullptr, 0, a4[k], a8[k]) & vm;
+      res[k] = o[k] ^ f;
+      cnt += __popc(f);
+    }
+    *reinterpret_cast<uint4*>(own + 4 * q) = make_uint4(res[0], res[1], res[2], res[3]);
+  }
+  return cnt;
+}
+
+// A consumer warp's contiguous run of chunks [i0, i1) (lanes take
+// consecutive chunks), walked with incremental (replica, row, chunk) state.
+template <bool COHERENT>
+__device__ __forceinline__ unsigned flip_run_chunks(const FlipArgs& a, unsigned i0, unsigned i1, int X) {
+  const Geo& G = a.G;
+  if (i0 >= i1) return 0;
+  const unsigned nch = (unsigned)G.nch;
+  unsigned gr = i0 / nch, ch = i0 - gr * nch;
+  int s = (int)G.rows_div.div(gr), lr = (int)(gr - (unsigned)s * G.rows);
+  const unsigned dr = 32u / nch, dc = 32u - dr * nch;
+  unsigned cnt = 0;
+  for (unsigned i = i0; i < i1; i += 32) {
+    cnt += flip_chunk_at<COHERENT>(a, s, lr, (int)ch, X);
+    ch += dc;
+    lr += (int)dr;
+    if (ch >= nch) {
+      ch -= nch;
+      lr++;
+    }
+    while (lr >= G.rows) {
+      lr -= G.rows;
+      s++;
+    }
+  }
+  return cnt;
+}
+
+// A consumer warp's contiguous run of quads [i0, i1) of one colour, walked
+// with incremental (replica, row, quad) bookkeeping: lanes take consecutive
+// quads, each step advances all lanes by 32 quads (dr rows + dq quads).
+template <bool COHERENT>
+__device__ __forceinline__ unsigned flip_run(const FlipArgs& a, unsigned i0, unsigned i1, int X) {
+  const Geo& G = a.G;
+  const unsigned quads = (unsigned)G.Wp >> 2;
+  if (i0 >= i1) return 0;
+  unsigned gr = G.quads_div.div(i0), qq = i0 - gr * quads;
+  int s = (int)G.rows_div.div(gr), lr = (int)(gr - (unsigned)s * G.rows);
+  const unsigned dr = G.quads_div.div(32u), dq = 32u - dr * quads;
+  unsigned cnt = 0;
+  for (unsigned i = i0; i < i1; i += 32) {
+    cnt += flip_quad_at<false, COHERENT>(a, s, lr, qq, X);
+    qq += dq;
+    lr += (int)dr;
+    if (qq >= quads) {
+      qq -= quads;
+      lr++;
+    }
+    while (lr >= G.rows) {
+      lr -= G.rows;
+      s++;
+    }
+  }
+  return cnt;
+}
+
+__device__ __forceinline__ void add_flips(unsigned long long* flips, unsigned cnt) {
+  cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
+  if ((threadIdx.x & 31) == 0 && cnt)
+    atomicAdd(flips + ((blockIdx.x * 32 + (threadIdx.x >> 5)) % kFlipSlots), (unsigned long long)cnt);
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <typename K>
+int set_smem_attr(K kernel, std::once_flag& once, cudaError_t& err) {
+  std::call_once(once, [&] {
+    err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  });
+  if (err != cudaSuccess) return fail(MSB_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(err));
+  return MSB_OK;
+}
+
+inline void fill_flip_args(FlipArgs& a, const msb_geom* g, const msb_sweep_params* p, int colour, uint32_t* spins,
+                    const uint32_t* planes, uint64_t* flips) {
+  a.G = make_geo(g);
+  a.spins = spins;
+  a.planes = planes;
+  a.flips = reinterpret_cast<unsigned long long*>(flips);
+  a.X = colour;
+  a.np = p->n_planes;
+  a.inv = p->mode == MSB_MODE_ANTI ? 0xFFFFFFFFu : 0u;
+  a.fault = p->fault;
+  std::memcpy(a.code_plane, p->code_plane, 16);
+}
+
+// Flip warps per 32-warp CTA of a fused launch: 6 measured best for
+// flip-heavy shapes (cfg3/cfg4); fewer when that keeps every producer warp
+// to one unit on single-round problems (cfg2).  MSB_FLIP_WARPS overrides.
+inline int flip_warps_for(long long units) {
+  static const int env_cw = [] { const char* e = getenv("MSB_FLIP_WARPS"); return e ? atoi(e) : 0; }();
+  if (env_cw > 0) return std::min(28, env_cw);
+  int cw = 6;
+  const int sms_est = 148;
+  auto rounds = [&](int c) { return (units + (long long)sms_est * (32 - c) - 1) / ((long long)sms_est * (32 - c)); };
+  if (rounds(2) == 1)
+    while (cw > 2 && rounds(cw) > 1) cw--;
+  return cw;
+}
+
+}  // namespace
+}  // namespace msbk

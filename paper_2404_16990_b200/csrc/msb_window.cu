@@ -1,0 +1,412 @@
+// libmsb200 lookahead windows: accept planes for S sweeps per launch.
+//
+// The reference consumes each cell stream in sweep order: sweep k takes
+// draws [4n k, 4n (k+1)) of stream (sim_offset+s)*(m/4)+gamma-1 -- block 2k
+// (red) then block 2k+1 (blue), each four quarters of n/2 draws in FLIP_RED /
+// FLIP_BLUE order (engine.py:334-343, 57-68).  The per-sweep path
+// (msb_sweep.cu) gives each stream piece one quarter (or less) and jumps it
+// 4n draws ahead every sweep: one 64-lookup GF(2) jump per n/2 draws.
+//
+// Here a piece is (window slot j, part p, stream): it runs its stream
+// CONTIGUOUSLY through 1/P of sweep j of the window -- P = 1 is the whole
+// sweep, 8 quarter-segments in a row -- and jumps S*4n ahead once, to the same
+// place in the next window.  With S = 8, P = 1 that is one jump per 32 n
+// draws instead of per n/2.  The planes of a window live in one buffer
+// [S][2 colours][2 planes][n_sim][m][Wp] (same per-slot layout as the
+// per-sweep planes), so the flip pass is unchanged.
+//
+// k_win_fused is the steady state: producer warps fill the NEXT window's
+// buffer while consumer warps flip the S sweeps of the CURRENT one (red, grid
+// barrier, blue, grid barrier, ...).  Launch, start-up and tail are paid once
+// per S sweeps.
+#include "msb_sweep.cuh"
+
+namespace msbk {
+namespace {
+
+struct WinArgs {
+  Geo G;
+  uint32_t* states;        // [8][npieces] piece start states (xoshiro)
+  const uint32_t* thr9;    // [2][n_sim] keys (FERRO/ANTI)
+  const uint4* jump;       // nibble table of A^(S*4n)
+  uint32_t* planes;        // window buffer being produced
+  unsigned* work;
+  long long npieces;       // S * P * streams
+  size_t slot_words;       // plane words of one sweep (both colours, both planes)
+  int S, P, pshift, kg, kr, nseg, streams, kit;
+  FastDiv streams_div, cells_div;
+  uint32_t seed_lo, seed_hi;    // Philox key
+  unsigned long long block0;    // stream block of slot 0's first phase
+};
+
+// One 32-bit word of the jump: 8 nibble lookups (paired 3-input XORs) from the
+// piece's start state, consumed 4 bits at a time (jw0 is the current word).
+__device__ __forceinline__ void jump_word(const uint4* __restrict__ jt, int& nib, uint32_t (&jw)[8],
+                                          uint32_t (&r)[8]) {
+  const char* e = reinterpret_cast<const char*>(jt) + nib * 512;
+  const uint32_t w = jw[0];
+#pragma unroll
+  for (int j = 0; j < 8; j += 2) {
+    // entry (position nib+j, value v) lives at byte (nib+j)*512 + v*32
+    const uint32_t oa = j == 0 ? ((w << 5) & 0x1E0u) : ((w >> (4 * j - 5)) & 0x1E0u);
+    const uint32_t ob = j == 0 ? ((w << 1) & 0x1E0u) : ((w >> (4 * j - 1)) & 0x1E0u);
+    const uint4* ea = reinterpret_cast<const uint4*>(e + j * 512 + oa);
+    const uint4* eb = reinterpret_cast<const uint4*>(e + (j + 1) * 512 + ob);
+    const uint4 la = ea[0], ha = ea[1], lb = eb[0], hb = eb[1];
+    r[0] = xor3(r[0], la.x, lb.x); r[1] = xor3(r[1], la.y, lb.y);
+    r[2] = xor3(r[2], la.z, lb.z); r[3] = xor3(r[3], la.w, lb.w);
+    r[4] = xor3(r[4], ha.x, hb.x); r[5] = xor3(r[5], ha.y, hb.y);
+    r[6] = xor3(r[6], ha.z, hb.z); r[7] = xor3(r[7], ha.w, hb.w);
+  }
+  nib += 8;
+#pragma unroll
+  for (int i = 0; i < 7; i++) jw[i] = jw[i + 1];
+}
+
+// Draws of one k of one quarter-segment (all w, in chunks of 32) reduced to
+// the two accept planes.  out points at word t(k) of the row's first plane.
+// Philox: draw d of stream id (st.a1:st.a0) is word d&3 of block (d>>2, id);
+// pd is the stream draw index of this k's first draw.
+template <int SRC, bool FULL>
+__device__ __forceinline__ void win_segment_k(const WinArgs& a, XState& st, uint32_t* outk, uint32_t key0,
+                                              uint32_t key1, size_t pstride, unsigned long long pd) {
+  const Geo& G = a.G;
+  for (int ch = 0; ch < G.nch; ch++) {
+    const int L = FULL ? 32 : chunk_bits(G, ch);
+    uint32_t acc0 = 0, acc1 = 0;
+    if (SRC == kSrcXoshiro) {
+      if (L == 32) {
+#pragma unroll kChunkUnroll
+        for (int i = 0; i < 32; i++) {
+          const uint32_t h9 = xstep(st) << 9;
+          acc_reject(acc0, h9, key0);
+          acc_reject(acc1, h9, key1);
+        }
+      } else {
+        for (int i = 0; i < L; i++) {
+          const uint32_t h9 = xstep(st) << 9;
+          acc_reject(acc0, h9, key0);
+          acc_reject(acc1, h9, key1);
+        }
+      }
+    } else {
+      const unsigned long long d0 = pd + 32ull * ch;
+      if ((d0 & 3) == 0 && (L & 3) == 0) {
+        for (int i = 0; i < L; i += 4) {
+          const unsigned long long c = (d0 + i) >> 2;
+          uint32_t x0 = (uint32_t)c, x1 = (uint32_t)(c >> 32), x2 = st.a0, x3 = st.a1;
+          philox10(x0, x1, x2, x3, a.seed_lo, a.seed_hi);
+          const uint32_t xs[4] = {x0, x1, x2, x3};
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            const uint32_t h9 = xs[q] << 9;
+            acc_reject(acc0, h9, key0);
+            acc_reject(acc1, h9, key1);
+          }
+        }
+      } else {
+        for (int i = 0; i < L; i++) {
+          const unsigned long long d = d0 + i, c = d >> 2;
+          uint32_t x0 = (uint32_t)c, x1 = (uint32_t)(c >> 32), x2 = st.a0, x3 = st.a1;
+          philox10(x0, x1, x2, x3, a.seed_lo, a.seed_hi);
+          const int e = (int)(d & 3);
+          const uint32_t h9 = (e == 0 ? x0 : e == 1 ? x1 : e == 2 ? x2 : x3) << 9;
+          acc_reject(acc0, h9, key0);
+          acc_reject(acc1, h9, key1);
+        }
+      }
+    }
+    // acc holds REJECT bits, newest draw in bit 0: reverse and invert
+    if (FULL) {
+      outk[ch * 16] = ~__brev(acc0);
+      outk[pstride + ch * 16] = ~__brev(acc1);
+    } else {
+      outk[ch * 16] = (~__brev(acc0)) >> (32 - L);
+      outk[pstride + ch * 16] = (~__brev(acc1)) >> (32 - L);
+    }
+  }
+}
+
+// One producer warp's share of a window.  Pieces are numbered
+// ((j * P + p) * streams + stream) so a warp's lanes share (j, p) -- the
+// same segments and k-range -- across 32 consecutive streams.
+template <int SRC, bool FULL>
+__device__ __forceinline__ void win_produce(const WinArgs& a, const uint4* __restrict__ jt, int role_warp,
+                                            int role_warps) {
+  constexpr bool XO = SRC == kSrcXoshiro;
+  const Geo& G = a.G;
+  const int lane = threadIdx.x & 31;
+  const long long units = (a.npieces + 31) / 32;
+  const size_t pstride = (size_t)G.n_sim * G.rows * G.Wp;
+  const long long nwarps = (long long)role_warps * gridDim.x;
+  const int cells = G.m / 4;
+  const unsigned long long n = (unsigned long long)G.n;
+  long long u = (long long)role_warp * gridDim.x + blockIdx.x;
+  for (;;) {
+    if (u >= units) break;
+    const long long gi = u * 32 + lane;
+    if (gi < a.npieces) {
+      const unsigned jp = a.streams_div.div((unsigned)gi);
+      const int sti = (int)((unsigned)gi - jp * (unsigned)a.streams);
+      const int j = (int)(jp >> a.pshift), pp = (int)(jp & (unsigned)(a.P - 1));
+      const int s = (int)a.cells_div.div((unsigned)sti);
+      const int gamma = sti - s * cells + 1;
+      const uint32_t key0 = a.thr9[s], key1 = a.thr9[G.n_sim + s];
+      const int seg0 = a.P <= 8 ? pp * a.nseg : (pp >> (a.pshift - 3));
+      const int k0 = a.P <= 8 ? 0 : (pp & (a.kg - 1)) * a.kr;
+      uint32_t* slot = a.planes + (size_t)j * a.slot_words;
+      XState st;
+      uint32_t jw[8] = {0, 0, 0, 0, 0, 0, 0, 0}, r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      int nib = 0, jacc = 0;
+      if (XO) {
+        load_state(st, a.states, a.npieces, gi);
+        jw[0] = st.a0; jw[1] = st.a1; jw[2] = st.b0; jw[3] = st.b1;
+        jw[4] = st.c0; jw[5] = st.c1; jw[6] = st.d0; jw[7] = st.d1;
+      } else {  // Philox: the stream id rides in st.a0 / st.a1
+        const unsigned long long sid = ((unsigned long long)G.sim_offset + (unsigned long long)s) * cells + gamma - 1;
+        st.a0 = (uint32_t)sid;
+        st.a1 = (uint32_t)(sid >> 32);
+      }
+      for (int sg = 0; sg < a.nseg; sg++) {
+        const int seg = seg0 + sg, X = seg >> 2, q = seg & 3;
+        const int c = seg_row(G.m, gamma, X, q);
+        uint32_t* out = slot + plane_off(G, 2, X, 0, s, c);
+        const unsigned long long pseg = (a.block0 + 2ull * j + X) * 2 * n + (unsigned long long)q * (n / 2);
+        for (int kk = 0; kk < a.kr; kk++) {
+          const int k = k0 + kk;
+          win_segment_k<SRC, FULL>(a, st, out + t_of_k(k), key0, key1, pstride,
+                                   pseg + (unsigned long long)k * G.words);
+          if (XO) {  // the 8 jump words, spread evenly over the piece's kit k-iterations
+            jacc += 8;
+            while (jacc >= a.kit) {
+              jacc -= a.kit;
+              jump_word(jt, nib, jw, r);
+            }
+          }
+        }
+      }
+      if (XO) {
+        XState nx;
+        nx.a0 = r[0]; nx.a1 = r[1]; nx.b0 = r[2]; nx.b1 = r[3];
+        nx.c0 = r[4]; nx.c1 = r[5]; nx.d0 = r[6]; nx.d1 = r[7];
+        store_state(nx, a.states, a.npieces, gi);  // same piece, next window
+      }
+    }
+    long long nu = 0;
+    if (lane == 0) nu = nwarps + (long long)atomicAdd(a.work, 1u);
+    u = __shfl_sync(0xFFFFFFFFu, nu, 0);
+  }
+}
+
+// Window launch: `produce` -> warps [0, 32 - cwarps) fill the next window;
+// the cwarps consumer warps flip slots [first, first + count) of `cur`
+// (red, barrier, blue, barrier, ...).  count == 0: production only.
+template <int SRC, bool FULL>
+__global__ void __launch_bounds__(kRngThreads, 1) k_win(const WinArgs wa, const FlipArgs fa0, const uint32_t* cur,
+                                                        int first, int count, int produce) {
+  extern __shared__ uint4 jt[];
+  const int cwarps = count > 0 ? fa0.cwarps : 0;
+  const int pwarps = produce ? (kRngThreads >> 5) - cwarps : 0;
+  if (SRC == kSrcXoshiro && produce) {
+    for (int i = threadIdx.x; i < kJumpWords / 4; i += blockDim.x) jt[i] = wa.jump[i];
+    __syncthreads();
+  }
+  const int warp = threadIdx.x >> 5;
+  const unsigned total_warps = gridDim.x * (blockDim.x >> 5);
+  if (warp < pwarps) {
+    win_produce<SRC, FULL>(wa, jt, warp, pwarps);
+  } else if (count > 0) {
+    const int nwc = (kRngThreads >> 5) - pwarps;  // consumer warps per CTA
+    const unsigned total = (unsigned)fa0.G.n_sim * (unsigned)fa0.G.rows * (unsigned)fa0.G.nch;  // chunks per colour
+    const unsigned nc = gridDim.x * nwc;
+    const unsigned cw = (warp - pwarps) * gridDim.x + blockIdx.x;
+    const unsigned per = ((total + nc - 1) / nc + 31) & ~31u;
+    const unsigned lo = min(total, cw * per), hi = min(total, lo + per);
+    const unsigned i0 = lo + (threadIdx.x & 31);
+    FlipArgs fa = fa0;
+    unsigned cnt = 0, target = 0;
+    const unsigned need = gridDim.x * nwc;
+    for (int i = 0; i < 2 * count; i++) {
+      const int X = i & 1;
+      fa.planes = cur + (size_t)(first + (i >> 1)) * wa.slot_words;
+      if (i == 0) cnt += flip_run_chunks<false>(fa, i0, hi, X);
+      else cnt += flip_run_chunks<true>(fa, i0, hi, X);
+      if (i + 1 < 2 * count) {  // grid barrier among the consumer warps
+        target += need;
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) {
+          __threadfence();
+          atomicAdd(wa.work + 1, 1u);
+          while (ld_acquire(wa.work + 1) < target) __nanosleep(256);
+        }
+        __syncwarp();
+        __threadfence();
+      }
+    }
+    add_flips(fa.flips, cnt);
+  }
+  finish_warp(wa.work, total_warps);
+}
+
+// Piece start states of a window whose slot 0 starts at stream block
+// `block0`: piece (j, p, stream) starts at draw (block0 + 2j) 2n + p 4n/P.
+__global__ void k_win_init(Geo G, uint64_t seed, int P, int pshift, int streams, FastDiv streams_div,
+                           FastDiv cells_div, long long npieces, uint64_t block0, const uint4* __restrict__ pow,
+                           uint32_t* states) {
+  const long long gi = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi >= npieces) return;
+  const unsigned jp = streams_div.div((unsigned)gi);
+  const int sti = (int)((unsigned)gi - jp * (unsigned)streams);
+  const int j = (int)(jp >> pshift), pp = (int)(jp & (unsigned)(P - 1));
+  const int cells = G.m / 4;
+  const int s = (int)cells_div.div((unsigned)sti);
+  const int gamma = sti - s * cells + 1;
+  const uint64_t n = (uint64_t)G.n;
+  const uint64_t sid = ((uint64_t)G.sim_offset + (uint64_t)s) * (uint64_t)cells + (uint64_t)(gamma - 1);
+  const uint64_t D = (block0 + 2ull * j) * 2 * n + (uint64_t)pp * (4 * n / (uint64_t)P);
+  store_state(jump_by(stream_state(seed, sid), D, pow), states, npieces, gi);
+}
+
+int check_window(const msb_geom* g, int S, int P, long long* npieces) {
+  if (int r = check_geom(g)) return r;
+  if (g->ghost) return fail(MSB_ERR_UNSUPPORTED, "lookahead windows run whole lattices; slabs use the per-phase calls");
+  if (S < 1 || S > 64) return fail(MSB_ERR_ARG, "window length S must be in [1, 64]");
+  if (P < 1 || P > 128 || (P & (P - 1))) return fail(MSB_ERR_ARG, "parts per stream-sweep P must be a power of two <= 128");
+  const long long np = (long long)S * P * g->n_sim * (g->m / 4);
+  if (np >= (1LL << 31)) return fail(MSB_ERR_UNSUPPORTED, "too many window pieces");
+  *npieces = np;
+  return MSB_OK;
+}
+
+size_t slot_words(const msb_geom* g) {
+  const Geo G = make_geo(g);
+  return 2ull * 2 * (size_t)g->n_sim * g->rows * G.Wp;
+}
+
+void fill_win_args(WinArgs& w, const msb_geom* g, const msb_sweep_params* p, int S, int P, long long np,
+                   uint32_t* states, uint32_t* planes) {
+  w.G = make_geo(g);
+  w.states = states;
+  w.thr9 = p->thr9;
+  w.jump = reinterpret_cast<const uint4*>(p->jump);
+  w.planes = planes;
+  w.work = p->work;
+  w.npieces = np;
+  w.slot_words = slot_words(g);
+  w.S = S;
+  w.P = P;
+  w.pshift = 0;
+  while ((1 << w.pshift) < P) w.pshift++;
+  w.kg = P > 8 ? P / 8 : 1;
+  w.kr = 16 / w.kg;
+  w.nseg = P <= 8 ? 8 / P : 1;
+  w.kit = w.nseg * w.kr;
+  w.streams = g->n_sim * (g->m / 4);
+  w.streams_div.init((uint32_t)w.streams);
+  w.cells_div.init((uint32_t)(g->m / 4));
+  w.seed_lo = (uint32_t)p->seed;
+  w.seed_hi = (uint32_t)(p->seed >> 32);
+  w.block0 = p->block;
+}
+
+}  // namespace
+}  // namespace msbk
+
+using namespace msbk;
+
+extern "C" {
+
+int msb_default_window(const msb_geom* g, int32_t* S, int32_t* P) {
+  if (!S || !P) return fail(MSB_ERR_ARG, "null output");
+  long long np = 0;
+  if (int r = check_window(g, 1, 1, &np)) return r;
+  // S = 8 sweeps unless two window buffers would exceed 8 GiB of planes;
+  // P: smallest split giving ~one warp-unit (32 pieces) per producer warp of
+  // every SM (148 SMs x 28 warps), as msb_default_kg.
+  const long long slot_bytes = 4LL * (long long)slot_words(g);
+  int s = 8;
+  while (s > 1 && 2LL * s * slot_bytes > (8LL << 30)) s >>= 1;
+  const long long streams = (long long)g->n_sim * (g->m / 4);
+  int p = 1;
+  while (p < 128 && (long long)s * p * streams < 118000) p *= 2;
+  while (p > 1 && (long long)s * p * streams >= (1LL << 31)) p >>= 1;
+  *S = s;
+  *P = p;
+  return MSB_OK;
+}
+
+int64_t msb_window_pieces(const msb_geom* g, int32_t S, int32_t P) {
+  long long np = 0;
+  if (check_window(g, S, P, &np)) return -1;
+  return np;
+}
+
+int64_t msb_window_words(const msb_geom* g, int32_t S) {
+  long long np = 0;
+  if (check_window(g, S, 1, &np)) return -1;
+  return (int64_t)S * (int64_t)slot_words(g);
+}
+
+int msb_window_init(const msb_geom* g, uint64_t seed, int32_t S, int32_t P, uint64_t block, const uint32_t* pow_tables,
+                    uint32_t* states, void* stream) {
+  long long np = 0;
+  if (int r = check_window(g, S, P, &np)) return r;
+  if (!pow_tables || !states) return fail(MSB_ERR_ARG, "null buffer");
+  int pshift = 0;
+  while ((1 << pshift) < P) pshift++;
+  const int streams = g->n_sim * (g->m / 4);
+  FastDiv sd, cd;
+  sd.init((uint32_t)streams);
+  cd.init((uint32_t)(g->m / 4));
+  k_win_init<<<blocks_for(np, 128), 128, 0, as_stream(stream)>>>(make_geo(g), seed, P, pshift, streams, sd, cd, np,
+                                                                 block, reinterpret_cast<const uint4*>(pow_tables),
+                                                                 states);
+  CUDA_TRY(cudaGetLastError());
+  return MSB_OK;
+}
+
+int msb_window_sweep(const msb_geom* g, const msb_sweep_params* p, int32_t S, int32_t P, uint32_t* spins,
+                     uint32_t* states, const uint32_t* cur, int32_t first, int32_t count, uint32_t* next,
+                     uint64_t* flips, void* stream) {
+  long long np = 0;
+  if (int r = check_window(g, S, P, &np)) return r;
+  if (int r = check_params(p)) return r;
+  if (p->mode == MSB_MODE_GENERIC) return fail(MSB_ERR_UNSUPPORTED, "lookahead windows need FERRO/ANTI tables");
+  if (first < 0 || count < 0 || first + count > S) return fail(MSB_ERR_ARG, "slots [first, first+count) outside the window");
+  if (count > 0 && (!spins || !cur || !flips)) return fail(MSB_ERR_ARG, "null buffer");
+  if (!next && count == 0) return MSB_OK;
+  if (next && p->rng == MSB_RNG_XOSHIRO && (!states || !p->jump)) return fail(MSB_ERR_ARG, "null RNG state or jump table");
+  const bool produce = next != nullptr;
+  WinArgs wa;
+  fill_win_args(wa, g, p, S, P, np, states, next);
+  FlipArgs fa;
+  fill_flip_args(fa, g, p, 0, spins, cur, flips);
+  fa.cwarps = produce ? flip_warps_for((np + 31) / 32) : (kRngThreads >> 5);
+  int dev = 0, sms = 148;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const bool philox = p->rng == MSB_RNG_PHILOX;
+  const bool full = (fa.G.words % 32) == 0;
+  static std::once_flag o1, o2, o3;
+  static cudaError_t e1, e2, e3;
+  if (int r = set_smem_attr(k_win<kSrcXoshiro, true>, o1, e1)) return r;
+  if (int r = set_smem_attr(k_win<kSrcXoshiro, false>, o2, e2)) return r;
+  if (int r = set_smem_attr(k_win<kSrcPhilox, false>, o3, e3)) return r;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)sms);
+  cfg.blockDim = dim3(kRngThreads);
+  cfg.dynamicSmemBytes = (philox || !produce) ? 0 : (size_t)kJumpWords * 4;
+  cfg.stream = as_stream(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = count > 0 ? 1 : 0;  // grid barriers only among consumers
+  const int prod = produce ? 1 : 0;
+  if (philox) CUDA_TRY(cudaLaunchKernelEx(&cfg, k_win<kSrcPhilox, false>, wa, fa, cur, first, count, prod));
+  else if (full) CUDA_TRY(cudaLaunchKernelEx(&cfg, k_win<kSrcXoshiro, true>, wa, fa, cur, first, count, prod));
+  else CUDA_TRY(cudaLaunchKernelEx(&cfg, k_win<kSrcXoshiro, false>, wa, fa, cur, first, count, prod));
+  return MSB_OK;
+}
+
+}  // extern "C"

@@ -36,8 +36,8 @@ from concurrent.futures import ThreadPoolExecutor
 import numpy as np
 
 from . import _lib
-from ._lib import (call, geom, SweepParams, MSB_FLIP_SLOTS, MSB_MAX_PLANES, MSB_RNG_PHILOX, MSB_RNG_XOSHIRO,
-                   MSB_SWEEP_AHEAD_IN, MSB_SWEEP_AHEAD_OUT, MSB_SWEEP_SERIAL)
+from ._lib import (call, geom, MsbError, SweepParams, MSB_FLIP_SLOTS, MSB_MAX_PLANES, MSB_MODE_GENERIC,
+                   MSB_RNG_PHILOX, MSB_RNG_XOSHIRO, MSB_SWEEP_AHEAD_IN, MSB_SWEEP_AHEAD_OUT, MSB_SWEEP_SERIAL)
 from .layout import (
     ALL_CODES, ArrayCode, LatticeDims, PackedArrays, check_spins, halo_audit_index, unpack,
 )
@@ -125,16 +125,21 @@ def _pow_tables(device):
         return _DEV_TABLES[key]
 
 
-def _sweep_jump_table(device, n: int):
-    """Device nibble table of A^(4n): advances a stream piece by one sweep."""
+def _jump_table(device, distance: int):
+    """Device nibble table of A^distance (32 KiB), cached per device."""
     torch = _torch()
     with _TABLE_LOCK:
-        key = ("jump", device.index, n)
+        key = ("jump", device.index, distance)
         if key not in _DEV_TABLES:
             host = np.empty(8192, np.uint32)
-            call("msb_rng_jump_table", ctypes.c_uint64(4 * n), host.ctypes.data_as(ctypes.c_void_p))
+            call("msb_rng_jump_table", ctypes.c_uint64(distance), host.ctypes.data_as(ctypes.c_void_p))
             _DEV_TABLES[key] = torch.from_numpy(host.view(np.int32)).to(device)
         return _DEV_TABLES[key]
+
+
+def _sweep_jump_table(device, n: int):
+    """Device nibble table of A^(4n): advances a stream piece by one sweep."""
+    return _jump_table(device, 4 * n)
 
 
 def _p(t) -> ctypes.c_void_p:
@@ -146,7 +151,10 @@ class Engine:
 
     Extra keyword-only arguments beyond the reference signature:
     ``device`` (CUDA device; default current), ``kg`` (stream pieces per
-    target row, 1/2/4/8/16; default chosen by the library) and ``stream``:
+    target row, 1/2/4/8/16, for the per-phase path; default chosen by the
+    library), ``window`` (sweeps of accept planes generated per launch on the
+    steady-state path, ``msb_window_sweep``; default chosen by the library)
+    and ``stream``:
     "xoshiro" (default) draws the reference's own xoshiro256++ streams;
     "philox" draws the counter-based ``rng.PhiloxStreams``, which
     the reference Engine reproduces bit-exactly when handed the same object
@@ -155,7 +163,7 @@ class Engine:
 
     def __init__(self, dims: LatticeDims, temperatures, seed: int, init: str = "random",
                  coupling: float = 1.0, sim_offset: int = 0, *, device=None, kg: int | None = None,
-                 stream: str = "xoshiro"):
+                 window: int | None = None, stream: str = "xoshiro"):
         self.dims = dims
         self.temperatures = tuple(float(t) for t in temperatures)
         if not self.temperatures:
@@ -203,6 +211,23 @@ class Engine:
         self._tab_key = None
         self.fault = 0  # test-only adder corruption (selftest seam, cli.py:467-480)
         self.overlap = True  # run the next sweep's RNG concurrently with this sweep's flips
+        S, P = ctypes.c_int32(), ctypes.c_int32()
+        call("msb_default_window", ctypes.byref(self._g), ctypes.byref(S), ctypes.byref(P))
+        self.window, self._wP = int(S.value), int(P.value)
+        if window is not None:
+            self.window = int(window)
+            if not 1 <= self.window <= 64:
+                raise ValueError("window must be in [1, 64] sweeps")
+            streams = self.n_sim * dims.cells
+            self._wP = 1
+            while self._wP < 128 and self.window * self._wP * streams < 118000:
+                self._wP *= 2
+        self._wbuf = None       # (states, planes[2], jump table) of the window path, allocated on first use
+        self._wvalid = False    # window buffer _wcur holds slots [_wc, S) of the window at block _wbase
+        self._wcur = 0
+        self._wc = 0
+        self._wbase = 0
+        self._wkey = None
 
         if init == "random":
             with torch.cuda.stream(self._stream):
@@ -392,6 +417,7 @@ class Engine:
     def _drop_ahead(self) -> None:
         """Discard pre-generated planes: put the stream pieces back at the
         logical position (the next unconsumed block)."""
+        self._wvalid = False
         if self._ahead:
             if self.stream == "xoshiro":
                 call("msb_rng_init", ctypes.byref(self._g), ctypes.c_uint64(self.seed & _M64), self.kg,
@@ -448,11 +474,12 @@ class Engine:
         for name in ("sweep", "flip_red", "flip_blue", "update_red_bc", "update_blue_bc"):
             if name in self.__dict__ or getattr(cls, name) is not getattr(Engine, name):
                 return False
-        return (self.recorder is None and self.streams is self._own_streams
-                and self._pos == [self._blocks, self._blocks + 1])
+        return self.recorder is None and self.streams is self._own_streams
 
     def _sweeps(self, k: int) -> None:
-        """k sweeps in one library call (2k kernel launches, no host sync)."""
+        """k sweeps through the library, no host sync: lookahead windows
+        (FERRO/ANTI tables) or the per-sweep fused path (generic tables,
+        ``overlap = False``)."""
         if k <= 0:
             return
         if not self._fast_path_ok():
@@ -462,10 +489,75 @@ class Engine:
         self._push_host_edits()
         self._sync_tables()
         self._params.fault = int(bool(self.fault))
-        self._sweep_call(k)
+        if self.overlap and self._params.mode != MSB_MODE_GENERIC:
+            self._win_sweeps(k)
+        elif self._pos == [self._blocks, self._blocks + 1] or self._ahead:
+            self._sweep_call(k)
+        else:  # per-phase positioning pending (a lone flip_red/flip_blue)
+            for _ in range(k):
+                self.sweep()
+            return
         self.sweeps_done += k
         self.attempts += self.dims.sites * self.n_sim * k
         self._touch()
+
+    # -- lookahead windows (msb_window_sweep) ------------------------------------
+
+    def _win_alloc(self):
+        if self._wbuf is None:
+            torch = _torch()
+            S, P = self.window, self._wP
+            npieces = int(_lib.lib().msb_window_pieces(ctypes.byref(self._g), S, P))
+            words = int(_lib.lib().msb_window_words(ctypes.byref(self._g), S))
+            if npieces < 0 or words < 0:
+                raise MsbError(f"window S={S}, P={P} unsupported: {_lib.lib().msb_last_error().decode()}")
+            with torch.cuda.device(self.device), torch.cuda.stream(self._stream):
+                states = torch.empty(8 * npieces, dtype=torch.int32, device=self.device)
+                planes = torch.empty(2 * words, dtype=torch.int32, device=self.device)
+            jump = _jump_table(self.device, S * 4 * self.dims.n)
+            self._wbuf = (states, planes, words, jump)
+        return self._wbuf
+
+    def _win_launch(self, first: int, count: int, produce: bool) -> None:
+        states, planes, words, jump = self._wbuf
+        cur = planes[self._wcur * words:(self._wcur + 1) * words]
+        nxt = planes[(1 - self._wcur) * words:(2 - self._wcur) * words]
+        if count == 0:      # produce into the current buffer
+            nxt, cur = cur, None
+        self._params.jump = jump.data_ptr()
+        # Philox: block of the produced window's slot 0
+        self._params.block = self._wbase if count == 0 else self._wbase + 2 * self.window
+        call("msb_window_sweep", ctypes.byref(self._g), ctypes.byref(self._params), self.window, self._wP,
+             _p(self._spins), _p(states), _p(cur) if cur is not None else None, first, count,
+             _p(nxt) if produce else None, _p(self._flips_dev), self._cs)
+        self._params.jump = self._jump.data_ptr()
+
+    def _win_sweeps(self, k: int) -> None:
+        self._win_alloc()
+        S = self.window
+        if self._wvalid and (self._wkey != self._tab_key or self._wbase + 2 * self._wc != self._blocks):
+            self._wvalid = False
+        if not self._wvalid:
+            # position the window's pieces at the next unconsumed block and
+            # generate its planes (the per-phase states are left behind)
+            self._wbase, self._wc, self._wcur = self._blocks, 0, 0
+            if self.stream == "xoshiro":
+                call("msb_window_init", ctypes.byref(self._g), ctypes.c_uint64(self.seed & _M64), S, self._wP,
+                     ctypes.c_uint64(self._wbase), _p(self._pow), _p(self._wbuf[0]), self._cs)
+            self._win_launch(0, 0, True)
+            self._wvalid, self._wkey = True, self._tab_key
+        self._ahead = False
+        self._pos = [None, None]   # per-phase pieces must be re-positioned before a lone phase
+        while k > 0:
+            r = min(k, S - self._wc)
+            finish = self._wc + r == S
+            self._win_launch(self._wc, r, finish)
+            self._blocks += 2 * r
+            k -= r
+            if finish:
+                self._wcur, self._wc, self._wbase = 1 - self._wcur, 0, self._wbase + 2 * S
+            else:
+                self._wc += r
 
     def _sweep_call(self, k: int) -> None:
         if self._ahead and self._ahead_key != self._tab_key:
@@ -483,20 +575,23 @@ class Engine:
         self._blocks += 2 * k
         self._pos = [self._blocks, self._blocks + 1]
 
-    def _timed_sweep(self, ev0, ev1) -> None:
-        """One sweep of the fast path bracketed by CUDA events (bench.py):
-        in steady state one fused launch (flips of this sweep + planes of
-        the next)."""
+    def _timed_sweeps(self, k: int, ev0, ev1) -> None:
+        """k sweeps of the fast path bracketed by CUDA events on the engine's
+        stream (bench.py).  With k = window and an aligned window this is one
+        launch: the flips of k sweeps plus the planes of the next k."""
         if not self._fast_path_ok():
             raise RuntimeError("timed sweeps need the engine's own sweep path")
         self._push_host_edits()
         self._sync_tables()
         self._params.fault = int(bool(self.fault))
         ev0.record(self._stream)
-        self._sweep_call(1)
+        if self.overlap and self._params.mode != MSB_MODE_GENERIC:
+            self._win_sweeps(k)
+        else:
+            self._sweep_call(k)
         ev1.record(self._stream)
-        self.sweeps_done += 1
-        self.attempts += self.dims.sites * self.n_sim
+        self.sweeps_done += k
+        self.attempts += self.dims.sites * self.n_sim * k
         self._touch()
 
     def synchronize(self) -> None:
