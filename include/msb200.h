@@ -184,15 +184,18 @@ int msb_sweep(const msb_geom *g, const msb_sweep_params *p, uint32_t *spins, uin
  * msb_window_words() uint32 words: [S][2 colours][2 planes][n_sim][m][Wp].
  * msb_window_pieces: piece count (piece states are 8 uint32 each).
  * msb_default_window: S and P for a geometry (balanced SM load, bounded
- * plane memory).
+ * plane memory, rows being written kept L2-resident); msb_window_parts: P
+ * for a given S.
  * msb_window_init: piece states for a window whose slot 0 starts at stream
  * block `block` (xoshiro).
  * msb_window_sweep: flips slots [first, first+count) of window `cur` (red,
- * blue, red, ... in one cooperative launch) and, if next != NULL, produces
- * the following window into `next` in the same launch (producer warps
- * overlap the flips).  For Philox p->block is the block of the produced
+ * blue, red, ... separated by grid barriers) and, if next != NULL, produces
+ * the following window into `next`, in ONE cooperative launch: producer
+ * warps fill `next` while the remaining warps of every CTA flip (the two
+ * touch disjoint buffers).  For Philox p->block is the block of the produced
  * window's slot 0.  count == 0 with next != NULL produces only. */
 int msb_default_window(const msb_geom *g, int32_t *S, int32_t *P);
+int32_t msb_window_parts(const msb_geom *g, int32_t S);   /* default P for a given S */
 int64_t msb_window_pieces(const msb_geom *g, int32_t S, int32_t P);
 int64_t msb_window_words(const msb_geom *g, int32_t S);
 int msb_window_init(const msb_geom *g, uint64_t seed, int32_t S, int32_t P, uint64_t block,

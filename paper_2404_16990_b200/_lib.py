@@ -69,7 +69,7 @@ EXPORTS = (
     "msb_rng_power_tables", "msb_rng_jump_table", "msb_rng_init", "msb_init_random",
     "msb_init_const", "msb_from_linear", "msb_to_linear", "msb_to_ref16", "msb_from_ref16",
     "msb_plane_words", "msb_rng_planes", "msb_flip", "msb_phase", "msb_sweep",
-    "msb_default_window", "msb_window_pieces", "msb_window_words", "msb_window_init", "msb_window_sweep",
+    "msb_default_window", "msb_window_parts", "msb_window_pieces", "msb_window_words", "msb_window_init", "msb_window_sweep",
     "msb_observe", "msb_draws", "msb_pack_edges", "msb_unpack_ghosts", "msb_bench_int_peak",
 )
 
@@ -121,6 +121,7 @@ def lib() -> ctypes.CDLL:
         "msb_phase": ([G, P, i32, vp, vp, vp, vp, vp, vp], ctypes.c_int),
         "msb_sweep": ([G, P, vp, vp, vp, i32, i32, vp, vp, vp], ctypes.c_int),
         "msb_default_window": ([G, vp, vp], ctypes.c_int),
+        "msb_window_parts": ([G, i32], i32),
         "msb_window_pieces": ([G, i32, i32], i64),
         "msb_window_words": ([G, i32], i64),
         "msb_window_init": ([G, u64, i32, i32, u64, vp, vp, vp], ctypes.c_int),

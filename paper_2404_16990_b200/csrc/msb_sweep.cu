@@ -251,14 +251,6 @@ __global__ void __launch_bounds__(kRngThreads, 1) k_rng_planes(const RngArgs a) 
 }
 
 
-template <bool GENERIC>
-__global__ void __launch_bounds__(256) k_flip(const FlipArgs a) {
-  const unsigned quads = (unsigned)a.G.Wp >> 2;
-  const unsigned total = (unsigned)a.G.n_sim * (unsigned)a.G.rows * quads;
-  const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
-  const unsigned cnt = i < total ? flip_quad<GENERIC, false>(a, i, a.X) : 0u;
-  add_flips(a.flips, cnt);
-}
 
 // ---------------------------------------------------------------------------
 // device: fused sweep -- flips of sweep k overlapped with the planes of k+1
@@ -293,18 +285,18 @@ __global__ void __launch_bounds__(kRngThreads, 1) k_sweep_fused(const RngArgs ra
   if (warp < kProducerWarps) {
     rng_produce<NPMAX, SRC, FULL>(ra, jt, warp, kProducerWarps);
   } else {
-    const unsigned total = (unsigned)fa.G.n_sim * (unsigned)fa.G.rows * (unsigned)fa.G.nch;  // chunks
+    const unsigned total = (unsigned)fa.G.n_sim * (unsigned)fa.G.rows * ((unsigned)fa.G.Wp >> 2);  // quads
     const unsigned nc = gridDim.x * kFlipWarps;
     const unsigned cw = (warp - kProducerWarps) * gridDim.x + blockIdx.x;
-    const unsigned per = ((total + nc - 1) / nc + 31) & ~31u;  // chunks per consumer warp
+    const unsigned per = ((total + nc - 1) / nc + 31) & ~31u;  // quads per consumer warp
     const unsigned lo = min(total, cw * per), hi = min(total, lo + per);
     const unsigned i0 = lo + (threadIdx.x & 31);
     unsigned cnt = 0;
     for (int X = 0; X < 2; X++) {
       if (X == 0) {
-        cnt += flip_run_chunks<false>(fa, i0, hi, 0);
+        cnt += flip_run<false>(fa, i0, hi, 0);
       } else {
-        cnt += flip_run_chunks<true>(fa, i0, hi, 1);
+        cnt += flip_run<true>(fa, i0, hi, 1);
       }
       if (X == 0) {  // grid barrier among the flip warps
         __syncwarp();
@@ -397,20 +389,6 @@ int rng_planes(const msb_geom* g, const msb_sweep_params* p, int colour, uint32_
   return MSB_OK;
 }
 
-int flip(const msb_geom* g, const msb_sweep_params* p, int colour, uint32_t* spins, const uint32_t* planes,
-         uint64_t* flips, cudaStream_t st) {
-  const Geo G = make_geo(g);
-  FlipArgs a;
-  fill_flip_args(a, g, p, colour, spins, planes, flips);
-  const long long total = (long long)g->n_sim * g->rows * (G.Wp / 4);
-  if (total >= (1LL << 31)) return fail(MSB_ERR_UNSUPPORTED, "too many words for one flip launch");
-  if (p->mode == MSB_MODE_GENERIC)
-    k_flip<true><<<blocks_for(total, 256), 256, 0, st>>>(a);
-  else
-    k_flip<false><<<blocks_for(total, 256), 256, 0, st>>>(a);
-  CUDA_TRY(cudaGetLastError());
-  return MSB_OK;
-}
 
 
 // flips of the sweep whose planes are in `cur` + planes of the next sweep

@@ -198,99 +198,6 @@ __device__ __forceinline__ unsigned flip_quad(const FlipArgs& a, unsigned i, int
   return flip_quad_at<GENERIC, COHERENT>(a, s, lr, qq, X);
 }
 
-// FERRO/ANTI flip of one whole 16-word chunk (t = 0..15 of chunk ch) of row
-// (s, lr), colour X.  The other colour's same-row words stay in registers, so
-// every t+-1 neighbour -- and, when the row is one chunk, the t = 0/15 wraps
-// -- comes from registers; address math happens once per chunk.
-template <bool COHERENT>
-__device__ __forceinline__ unsigned flip_chunk_at(const FlipArgs& a, int s, int lr, int ch, int X) {
-  const Geo& G = a.G;
-  const int c = G.row0 + lr, br = lr + G.ghost;
-  int bu, bd;
-  vert_rows(G, br, bu, bd);
-  const int w0 = ch * 16;
-  uint32_t* own = a.spins + row_off(G, s, X, br) + w0;
-  const uint32_t* ycr = a.spins + row_off(G, s, 1 - X, br);
-  const uint32_t* yu = a.spins + row_off(G, s, 1 - X, bu) + w0;
-  const uint32_t* yd = a.spins + row_off(G, s, 1 - X, bd) + w0;
-  const size_t pstride = (size_t)G.n_sim * G.rows * G.Wp;
-  const uint32_t* pl = a.planes + plane_off(G, a.np, X, 0, s, lr) + w0;
-  auto ld4 = [](const uint32_t* q) {
-    return COHERENT ? __ldcg(reinterpret_cast<const uint4*>(q)) : __ldg(reinterpret_cast<const uint4*>(q));
-  };
-  auto ld1 = [](const uint32_t* q) { return COHERENT ? __ldcg(q) : __ldg(q); };
-  uint32_t y[16];
-#pragma unroll
-  for (int q = 0; q < 4; q++) {
-    const uint4 v = ld4(ycr + w0 + 4 * q);
-    y[4 * q] = v.x; y[4 * q + 1] = v.y; y[4 * q + 2] = v.z; y[4 * q + 3] = v.w;
-  }
-  const int p = (c + X) & 1;
-  const int vb = chunk_bits(G, ch);
-  const uint32_t vm = chunk_mask(G, ch);
-  // the wrap word: p=1 -> t=15 needs bit 0 of the next chunk's t=0 word;
-  // p=0 -> t=0 needs the top valid bit of the previous chunk's t=15 word
-  uint32_t wrapn;
-  if (p) {
-    const int chn = ch + 1 < G.nch ? ch + 1 : 0;
-    const uint32_t nx = chn == ch ? y[0] : ld1(ycr + chn * 16);
-    wrapn = (y[0] >> 1) | ((nx & 1u) << (vb - 1));
-  } else {
-    uint32_t carry;
-    if (ch > 0) carry = ld1(ycr + (ch - 1) * 16 + 15) >> 31;
-    else carry = ((G.nch == 1 ? y[15] : ld1(ycr + (G.nch - 1) * 16 + 15)) >> (chunk_bits(G, G.nch - 1) - 1)) & 1u;
-    wrapn = ((y[15] << 1) | carry) & vm;
-  }
-  unsigned cnt = 0;
-#pragma unroll
-  for (int q = 0; q < 4; q++) {
-    const uint4 O = *reinterpret_cast<const uint4*>(own + 4 * q);
-    const uint4 U = ld4(yu + 4 * q), D = ld4(yd + 4 * q);
-    const uint4 P4 = __ldg(reinterpret_cast<const uint4*>(pl + 4 * q));
-    const uint4 P8 = __ldg(reinterpret_cast<const uint4*>(pl + pstride + 4 * q));
-    const uint32_t o[4] = {O.x, O.y, O.z, O.w}, u4[4] = {U.x, U.y, U.z, U.w}, d4[4] = {D.x, D.y, D.z, D.w};
-    const uint32_t a4[4] = {P4.x, P4.y, P4.z, P4.w}, a8[4] = {P8.x, P8.y, P8.z, P8.w};
-    uint32_t res[4];
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-      const int t = 4 * q + k;
-      const uint32_t n4 = p ? (t < 15 ? y[t + 1] : wrapn) : (t > 0 ? y[t - 1] : wrapn);
-      const uint32_t f = flip_word(a, false, o[k], u4[k], d4[k], y[t], n4, nullptr, 0, a4[k], a8[k]) & vm;
-      res[k] = o[k] ^ f;
-      cnt += __popc(f);
-    }
-    *reinterpret_cast<uint4*>(own + 4 * q) = make_uint4(res[0], res[1], res[2], res[3]);
-  }
-  return cnt;
-}
-
-// A consumer warp's contiguous run of chunks [i0, i1) (lanes take
-// consecutive chunks), walked with incremental (replica, row, chunk) state.
-template <bool COHERENT>
-__device__ __forceinline__ unsigned flip_run_chunks(const FlipArgs& a, unsigned i0, unsigned i1, int X) {
-  const Geo& G = a.G;
-  if (i0 >= i1) return 0;
-  const unsigned nch = (unsigned)G.nch;
-  unsigned gr = i0 / nch, ch = i0 - gr * nch;
-  int s = (int)G.rows_div.div(gr), lr = (int)(gr - (unsigned)s * G.rows);
-  const unsigned dr = 32u / nch, dc = 32u - dr * nch;
-  unsigned cnt = 0;
-  for (unsigned i = i0; i < i1; i += 32) {
-    cnt += flip_chunk_at<COHERENT>(a, s, lr, (int)ch, X);
-    ch += dc;
-    lr += (int)dr;
-    if (ch >= nch) {
-      ch -= nch;
-      lr++;
-    }
-    while (lr >= G.rows) {
-      lr -= G.rows;
-      s++;
-    }
-  }
-  return cnt;
-}
-
 // A consumer warp's contiguous run of quads [i0, i1) of one colour, walked
 // with incremental (replica, row, quad) bookkeeping: lanes take consecutive
 // quads, each step advances all lanes by 32 quads (dr rows + dq quads).
@@ -365,6 +272,33 @@ inline int flip_warps_for(long long units) {
   if (rounds(2) == 1)
     while (cw > 2 && rounds(cw) > 1) cw--;
   return cw;
+}
+
+
+// One colour's flip pass as its own launch: a thread per 4-word quad.
+template <bool GENERIC>
+__global__ void __launch_bounds__(256) k_flip(const FlipArgs a) {
+  const unsigned quads = (unsigned)a.G.Wp >> 2;
+  const unsigned total = (unsigned)a.G.n_sim * (unsigned)a.G.rows * quads;
+  const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned cnt = i < total ? flip_quad<GENERIC, false>(a, i, a.X) : 0u;
+  add_flips(a.flips, cnt);
+}
+
+// Launch k_flip for colour `colour` of planes `planes`.
+inline int flip(const msb_geom* g, const msb_sweep_params* p, int colour, uint32_t* spins, const uint32_t* planes,
+         uint64_t* flips, cudaStream_t st) {
+  const Geo G = make_geo(g);
+  FlipArgs a;
+  fill_flip_args(a, g, p, colour, spins, planes, flips);
+  const long long total = (long long)g->n_sim * g->rows * (G.Wp / 4);
+  if (total >= (1LL << 31)) return fail(MSB_ERR_UNSUPPORTED, "too many words for one flip launch");
+  if (p->mode == MSB_MODE_GENERIC)
+    k_flip<true><<<blocks_for(total, 256), 256, 0, st>>>(a);
+  else
+    k_flip<false><<<blocks_for(total, 256), 256, 0, st>>>(a);
+  CUDA_TRY(cudaGetLastError());
+  return MSB_OK;
 }
 
 }  // namespace

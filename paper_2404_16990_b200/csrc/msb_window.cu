@@ -198,16 +198,21 @@ __device__ __forceinline__ void win_produce(const WinArgs& a, const uint4* __res
   }
 }
 
-// Window launch: `produce` -> warps [0, 32 - cwarps) fill the next window;
-// the cwarps consumer warps flip slots [first, first + count) of `cur`
-// (red, barrier, blue, barrier, ...).  count == 0: production only.
+__device__ __forceinline__ void consumer_barrier(unsigned* ctr, unsigned target, int nthreads, bool leader) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+  if (leader) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    while (ld_acquire(ctr) < target) __nanosleep(64);
+    __threadfence();
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
 template <int SRC, bool FULL>
 __global__ void __launch_bounds__(kRngThreads, 1) k_win(const WinArgs wa, const FlipArgs fa0, const uint32_t* cur,
-                                                        int first, int count, int produce) {
+                                                        int first, int count, int pwarps) {
   extern __shared__ uint4 jt[];
-  const int cwarps = count > 0 ? fa0.cwarps : 0;
-  const int pwarps = produce ? (kRngThreads >> 5) - cwarps : 0;
-  if (SRC == kSrcXoshiro && produce) {
+  if (SRC == kSrcXoshiro && pwarps > 0) {
     for (int i = threadIdx.x; i < kJumpWords / 4; i += blockDim.x) jt[i] = wa.jump[i];
     __syncthreads();
   }
@@ -216,32 +221,22 @@ __global__ void __launch_bounds__(kRngThreads, 1) k_win(const WinArgs wa, const 
   if (warp < pwarps) {
     win_produce<SRC, FULL>(wa, jt, warp, pwarps);
   } else if (count > 0) {
-    const int nwc = (kRngThreads >> 5) - pwarps;  // consumer warps per CTA
-    const unsigned total = (unsigned)fa0.G.n_sim * (unsigned)fa0.G.rows * (unsigned)fa0.G.nch;  // chunks per colour
+    const int nwc = (kRngThreads >> 5) - pwarps;
+    const unsigned total = (unsigned)fa0.G.n_sim * (unsigned)fa0.G.rows * ((unsigned)fa0.G.Wp >> 2);  // quads
     const unsigned nc = gridDim.x * nwc;
     const unsigned cw = (warp - pwarps) * gridDim.x + blockIdx.x;
     const unsigned per = ((total + nc - 1) / nc + 31) & ~31u;
     const unsigned lo = min(total, cw * per), hi = min(total, lo + per);
     const unsigned i0 = lo + (threadIdx.x & 31);
     FlipArgs fa = fa0;
-    unsigned cnt = 0, target = 0;
-    const unsigned need = gridDim.x * nwc;
+    unsigned cnt = 0;
+    const bool leader = threadIdx.x == pwarps * 32;
     for (int i = 0; i < 2 * count; i++) {
       const int X = i & 1;
       fa.planes = cur + (size_t)(first + (i >> 1)) * wa.slot_words;
-      if (i == 0) cnt += flip_run_chunks<false>(fa, i0, hi, X);
-      else cnt += flip_run_chunks<true>(fa, i0, hi, X);
-      if (i + 1 < 2 * count) {  // grid barrier among the consumer warps
-        target += need;
-        __syncwarp();
-        if ((threadIdx.x & 31) == 0) {
-          __threadfence();
-          atomicAdd(wa.work + 1, 1u);
-          while (ld_acquire(wa.work + 1) < target) __nanosleep(256);
-        }
-        __syncwarp();
-        __threadfence();
-      }
+      if (i == 0) cnt += flip_run<false>(fa, i0, hi, X);
+      else cnt += flip_run<true>(fa, i0, hi, X);
+      if (i + 1 < 2 * count) consumer_barrier(wa.work + 1, gridDim.x * (unsigned)(i + 1), nwc * 32, leader);
     }
     add_flips(fa.flips, cnt);
   }
@@ -316,22 +311,36 @@ using namespace msbk;
 
 extern "C" {
 
+int32_t msb_window_parts(const msb_geom* g, int32_t S) {
+  long long np = 0;
+  if (check_window(g, S, 1, &np)) return -1;
+  // smallest split giving ~one warp-unit (32 pieces) per producer warp of
+  // every SM (148 SMs x 28 warps), as msb_default_kg
+  const long long streams = (long long)g->n_sim * (g->m / 4);
+  int p = 1;
+  while (p < 128 && (long long)S * p * streams < 118000) p *= 2;
+  // Rows being written concurrently stay L2-resident: a piece completes its
+  // row's plane words one t-word per k, so ~140k pieces in flight write
+  // 140k / max(1, P/8) rows of 8*Wp bytes (P > 8: the P/8 parts of a row run
+  // side by side).  Keep that under ~60 MB.
+  const long long row_bytes = 8LL * make_geo(g).Wp;
+  while (p < 128 && 140000LL / std::max(1, p / 8) * row_bytes > (60LL << 20)) p *= 2;
+  static const int env_p = [] { const char* e = getenv("MSB_WINDOW_PARTS"); return e ? atoi(e) : 0; }();
+  if (env_p > 0 && env_p <= 128 && !(env_p & (env_p - 1))) p = env_p;  // tuning override
+  while (p > 1 && (long long)S * p * streams >= (1LL << 31)) p >>= 1;
+  return p;
+}
+
 int msb_default_window(const msb_geom* g, int32_t* S, int32_t* P) {
   if (!S || !P) return fail(MSB_ERR_ARG, "null output");
   long long np = 0;
   if (int r = check_window(g, 1, 1, &np)) return r;
-  // S = 8 sweeps unless two window buffers would exceed 8 GiB of planes;
-  // P: smallest split giving ~one warp-unit (32 pieces) per producer warp of
-  // every SM (148 SMs x 28 warps), as msb_default_kg.
+  // S = 8 sweeps unless two window buffers would exceed 8 GiB of planes
   const long long slot_bytes = 4LL * (long long)slot_words(g);
   int s = 8;
   while (s > 1 && 2LL * s * slot_bytes > (8LL << 30)) s >>= 1;
-  const long long streams = (long long)g->n_sim * (g->m / 4);
-  int p = 1;
-  while (p < 128 && (long long)s * p * streams < 118000) p *= 2;
-  while (p > 1 && (long long)s * p * streams >= (1LL << 31)) p >>= 1;
   *S = s;
-  *P = p;
+  *P = msb_window_parts(g, s);
   return MSB_OK;
 }
 
@@ -381,10 +390,33 @@ int msb_window_sweep(const msb_geom* g, const msb_sweep_params* p, int32_t S, in
   fill_win_args(wa, g, p, S, P, np, states, next);
   FlipArgs fa;
   fill_flip_args(fa, g, p, 0, spins, cur, flips);
-  fa.cwarps = produce ? flip_warps_for((np + 31) / 32) : (kRngThreads >> 5);
+  // Warp split of the 32-warp CTAs.  A unit (32 pieces) is a whole window's
+  // share of a stream, so an extra producer round costs a full unit: when the
+  // units fit one round, give producers exactly that round and the rest of
+  // the CTA to the flips; otherwise 8 flip warps (flip-heavy shapes gain,
+  // others are insensitive).  Producers are capped so the plane rows being
+  // written stay L2-resident (see msb_window_parts).  MSB_FLIP_WARPS /
+  // MSB_PRODUCER_WARPS override (tuning).
+  static const int env_pw = [] { const char* e = getenv("MSB_PRODUCER_WARPS"); return e ? atoi(e) : 0; }();
+  static const int env_cw = [] { const char* e = getenv("MSB_FLIP_WARPS"); return e ? atoi(e) : 0; }();
   int dev = 0, sms = 148;
   CUDA_TRY(cudaGetDevice(&dev));
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const long long units = (np + 31) / 32;
+  const long long live_per_warp = 32LL * 2 * 4 * fa.G.Wp;  // bytes: 2 plane rows per lane
+  const int cap = (int)std::max(4LL, std::min(32LL, (64LL << 20) / ((long long)sms * live_per_warp)));
+  int pwarps = 0;
+  if (produce) {
+    if (count == 0) {
+      pwarps = cap;
+    } else {
+      const long long one_round = (units + sms - 1) / sms;  // producer warps per CTA for a single round
+      int cw = one_round <= 30 ? (int)(32 - one_round) : 8;
+      if (env_cw > 0) cw = std::min(28, env_cw);
+      pwarps = std::min(cap, 32 - cw);
+    }
+    if (env_pw > 0) pwarps = std::min(32, env_pw);
+  }
   const bool philox = p->rng == MSB_RNG_PHILOX;
   const bool full = (fa.G.words % 32) == 0;
   static std::once_flag o1, o2, o3;
@@ -395,17 +427,16 @@ int msb_window_sweep(const msb_geom* g, const msb_sweep_params* p, int32_t S, in
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)sms);
   cfg.blockDim = dim3(kRngThreads);
-  cfg.dynamicSmemBytes = (philox || !produce) ? 0 : (size_t)kJumpWords * 4;
+  cfg.dynamicSmemBytes = (philox || pwarps == 0) ? 0 : (size_t)kJumpWords * 4;
   cfg.stream = as_stream(stream);
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = count > 0 ? 1 : 0;  // grid barriers only among consumers
-  const int prod = produce ? 1 : 0;
-  if (philox) CUDA_TRY(cudaLaunchKernelEx(&cfg, k_win<kSrcPhilox, false>, wa, fa, cur, first, count, prod));
-  else if (full) CUDA_TRY(cudaLaunchKernelEx(&cfg, k_win<kSrcXoshiro, true>, wa, fa, cur, first, count, prod));
-  else CUDA_TRY(cudaLaunchKernelEx(&cfg, k_win<kSrcXoshiro, false>, wa, fa, cur, first, count, prod));
+  if (philox) CUDA_TRY(cudaLaunchKernelEx(&cfg, k_win<kSrcPhilox, false>, wa, fa, cur, first, count, pwarps));
+  else if (full) CUDA_TRY(cudaLaunchKernelEx(&cfg, k_win<kSrcXoshiro, true>, wa, fa, cur, first, count, pwarps));
+  else CUDA_TRY(cudaLaunchKernelEx(&cfg, k_win<kSrcXoshiro, false>, wa, fa, cur, first, count, pwarps));
   return MSB_OK;
 }
 

@@ -218,10 +218,7 @@ class Engine:
             self.window = int(window)
             if not 1 <= self.window <= 64:
                 raise ValueError("window must be in [1, 64] sweeps")
-            streams = self.n_sim * dims.cells
-            self._wP = 1
-            while self._wP < 128 and self.window * self._wP * streams < 118000:
-                self._wP *= 2
+            self._wP = int(_lib.lib().msb_window_parts(ctypes.byref(self._g), self.window))
         self._wbuf = None       # (states, planes[2], jump table) of the window path, allocated on first use
         self._wvalid = False    # window buffer _wcur holds slots [_wc, S) of the window at block _wbase
         self._wcur = 0
