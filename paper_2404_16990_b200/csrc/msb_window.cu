@@ -127,9 +127,34 @@ __device__ __forceinline__ void win_segment_k(const WinArgs& a, XState& st, uint
   }
 }
 
-// One producer warp's share of a window.  Pieces are numbered
-// ((j * P + p) * streams + stream) so a warp's lanes share (j, p) -- the
-// same segments and k-range -- across 32 consecutive streams.
+// Piece numbering.  P <= 8 (a piece = 8/P whole quarter-segments):
+// gi = (j * P + p) * streams + stream, so a warp's lanes share (j, p) -- the
+// same segments -- across 32 consecutive streams.  P > 8 (a piece = 16/kg
+// k-values of one segment, kg = P/8): gi = ((j * 8 + seg) * streams +
+// stream) * kg + kgi, so the kg parts of a row sit in adjacent lanes and a
+// warp's plane stores land in 32/kg rows (t-words of the same sectors)
+// instead of 32 rows.  Decodes j, stream, first segment and first k.
+__device__ __forceinline__ void win_piece(int P, int pshift, int nseg, int kg, int kr, int streams,
+                                         const FastDiv& streams_div, unsigned gi, int& j, int& sti,
+                                         int& seg0, int& k0) {
+  if (P <= 8) {
+    const unsigned jp = streams_div.div(gi);
+    sti = (int)(gi - jp * (unsigned)streams);
+    j = (int)(jp >> pshift);
+    seg0 = (int)(jp & (unsigned)(P - 1)) * nseg;
+    k0 = 0;
+  } else {
+    const int kgs = pshift - 3;
+    const unsigned rest = gi >> kgs;
+    const unsigned js = streams_div.div(rest);
+    sti = (int)(rest - js * (unsigned)streams);
+    j = (int)(js >> 3);
+    seg0 = (int)(js & 7u);
+    k0 = (int)(gi & (unsigned)(kg - 1)) * kr;
+  }
+}
+
+// One producer warp's share of a window (pieces numbered as win_piece).
 template <int SRC, bool FULL>
 __device__ __forceinline__ void win_produce(const WinArgs& a, const uint4* __restrict__ jt, int role_warp,
                                             int role_warps) {
@@ -146,14 +171,11 @@ __device__ __forceinline__ void win_produce(const WinArgs& a, const uint4* __res
     if (u >= units) break;
     const long long gi = u * 32 + lane;
     if (gi < a.npieces) {
-      const unsigned jp = a.streams_div.div((unsigned)gi);
-      const int sti = (int)((unsigned)gi - jp * (unsigned)a.streams);
-      const int j = (int)(jp >> a.pshift), pp = (int)(jp & (unsigned)(a.P - 1));
+      int j, seg0, k0, sti;
+      win_piece(a.P, a.pshift, a.nseg, a.kg, a.kr, a.streams, a.streams_div, (unsigned)gi, j, sti, seg0, k0);
       const int s = (int)a.cells_div.div((unsigned)sti);
       const int gamma = sti - s * cells + 1;
       const uint32_t key0 = a.thr9[s], key1 = a.thr9[G.n_sim + s];
-      const int seg0 = a.P <= 8 ? pp * a.nseg : (pp >> (a.pshift - 3));
-      const int k0 = a.P <= 8 ? 0 : (pp & (a.kg - 1)) * a.kr;
       uint32_t* slot = a.planes + (size_t)j * a.slot_words;
       XState st;
       uint32_t jw[8] = {0, 0, 0, 0, 0, 0, 0, 0}, r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -244,21 +266,24 @@ __global__ void __launch_bounds__(kRngThreads, 1) k_win(const WinArgs wa, const 
 }
 
 // Piece start states of a window whose slot 0 starts at stream block
-// `block0`: piece (j, p, stream) starts at draw (block0 + 2j) 2n + p 4n/P.
+// `block0`: piece (j, seg0, k0, stream) starts at draw
+// (block0 + 2j) 2n + seg0 n/2 + k0 n/32 (segment = colour block + quarter).
 __global__ void k_win_init(Geo G, uint64_t seed, int P, int pshift, int streams, FastDiv streams_div,
                            FastDiv cells_div, long long npieces, uint64_t block0, const uint4* __restrict__ pow,
                            uint32_t* states) {
   const long long gi = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (gi >= npieces) return;
-  const unsigned jp = streams_div.div((unsigned)gi);
-  const int sti = (int)((unsigned)gi - jp * (unsigned)streams);
-  const int j = (int)(jp >> pshift), pp = (int)(jp & (unsigned)(P - 1));
+  const int kg = P > 8 ? P / 8 : 1, kr = 16 / kg, nseg = P <= 8 ? 8 / P : 1;
+  int j, sti, seg0, k0;
+  win_piece(P, pshift, nseg, kg, kr, streams, streams_div, (unsigned)gi, j, sti, seg0, k0);
+  // offset of the piece's first draw within its stream-sweep (4n draws):
+  // segment seg0 = colour X (block) and quarter q, then k0 * (n/32) draws
   const int cells = G.m / 4;
   const int s = (int)cells_div.div((unsigned)sti);
   const int gamma = sti - s * cells + 1;
   const uint64_t n = (uint64_t)G.n;
   const uint64_t sid = ((uint64_t)G.sim_offset + (uint64_t)s) * (uint64_t)cells + (uint64_t)(gamma - 1);
-  const uint64_t D = (block0 + 2ull * j) * 2 * n + (uint64_t)pp * (4 * n / (uint64_t)P);
+  const uint64_t D = (block0 + 2ull * j) * 2 * n + (uint64_t)seg0 * (n / 2) + (uint64_t)k0 * (n / 32);
   store_state(jump_by(stream_state(seed, sid), D, pow), states, npieces, gi);
 }
 
@@ -403,7 +428,9 @@ int msb_window_sweep(const msb_geom* g, const msb_sweep_params* p, int32_t S, in
   CUDA_TRY(cudaGetDevice(&dev));
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const long long units = (np + 31) / 32;
-  const long long live_per_warp = 32LL * 2 * 4 * fa.G.Wp;  // bytes: 2 plane rows per lane
+  // bytes of plane rows a producer warp has open: 2 rows (planes) per row
+  // being written, 32 / max(1, P/8) rows per warp (win_piece numbering)
+  const long long live_per_warp = 32LL * 2 * 4 * fa.G.Wp / std::max(1, P / 8);
   const int cap = (int)std::max(4LL, std::min(32LL, (64LL << 20) / ((long long)sms * live_per_warp)));
   int pwarps = 0;
   if (produce) {

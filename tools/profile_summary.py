@@ -1,6 +1,6 @@
 """Summarise an ncu launch list + full capture into profiles/*.json.
 
-python tools/profile_summary.py <launches.csv> <capture.ncu-rep> <tag>
+python tools/profile_summary.py <launches.csv> <capture.ncu-rep> <tag> [kernel-key] [attempts-per-launch]
 """
 import collections
 import csv
@@ -10,6 +10,8 @@ import subprocess
 import sys
 
 launches, rep, tag = sys.argv[1], sys.argv[2], sys.argv[3]
+key = sys.argv[4] if len(sys.argv) > 4 else "k_win"
+attempts = int(sys.argv[5]) if len(sys.argv) > 5 else 8 * 64 * 1024 * 1024
 rows = list(csv.reader(open(launches)))
 hdr = None
 tot = collections.defaultdict(lambda: [0, 0.0])
@@ -25,9 +27,9 @@ for r in rows:
         tot[name][0] += 1
         tot[name][1] += float(d["Metric Value"])
 allt = sum(v for c, v in tot.values())
-lsum = {"command": "ncu --metrics gpu__time_duration.sum --clock-control none python bench.py --steps 20 --warmup 3 --no-cpu",
+lsum = {"command": "ncu --metrics gpu__time_duration.sum --clock-control none python bench.py --steps 10 --warmup 3 --no-cpu",
         "unit": "ns",
-        "note": "cold-cache serialised launches; each timed bench step is one k_sweep_fused launch. k_int_peak = INT32 "
+        "note": f"cold-cache serialised launches; each timed bench step is one {key} launch. k_int_peak = INT32 "
                 "peak microbenchmark, FillFunctor<uchar> = L2 flush between steps, linear/observe kernels = e2e leg",
         "kernels": {k: {"launches": c, "total_ns": round(v, 1), "mean_ns": round(v / c, 1), "share": round(v / allt, 4)}
                     for k, (c, v) in sorted(tot.items(), key=lambda x: -x[1][1])}}
@@ -42,7 +44,6 @@ rd, wr = get("dram__bytes_read.sum"), get("dram__bytes_write.sum")
 unit_rd = u[h.index("dram__bytes_read.sum")]
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit_rd]
 insts = get("smsp__inst_executed.sum")
-attempts = 64 * 1024 * 1024
 cap = {
     "kernel": v[h.index("Kernel Name")], "duration_us_cold": dur_us,
     "dram_bytes_read": rd * scale, "dram_bytes_write": wr * scale,
@@ -57,8 +58,8 @@ cap = {
     "inst_executed_warp": insts, "inst_per_attempt": round(insts * 32 / attempts, 2),
 }
 summary = {"round": 1, "tag": tag,
-           "command": "python bench.py --steps 10 --warmup 3 --no-cpu (cfg2 64 x 1024^2, kg=1); ncu --set full "
-                      "--clock-control none -k regex:k_sweep_fused -s 5 -c 1",
-           "k_sweep_fused": cap, "launch_list": f"profiles/launches_{tag}_summary.json"}
+           "command": f"python bench.py --steps 10 --warmup 3 --no-cpu (cfg2 64 x 1024^2); ncu --set full "
+                      f"--clock-control none -k regex:{key} -s 5 -c 1",
+           key: cap, "launch_list": f"profiles/launches_{tag}_summary.json"}
 json.dump(summary, open("profiles/ncu_summary.json", "w"), indent=1)
 print(json.dumps(summary, indent=1))
