@@ -78,7 +78,8 @@ typedef struct msb_sweep_params {
   int32_t fault;                 /* test-only adder corruption (cli.py:467-480 analogue) */
   int32_t block_rows;            /* reserved, 0 */
   uint32_t *work;                /* device: 4 uint32 scratch counters, zeroed once by the caller;
-                                    every kernel leaves them zeroed */
+                                    every kernel leaves them zeroed (one engine/slab per counter
+                                    set: kernels sharing one must be stream-ordered) */
   int32_t rng;                   /* MSB_RNG_XOSHIRO (reference streams) or MSB_RNG_PHILOX */
   uint64_t seed;                 /* Philox key (the engine's master seed) */
   uint64_t block;                /* Philox: stream block (2 per sweep; red = even) of the first
@@ -194,6 +195,27 @@ int msb_sweep(const msb_geom *g, const msb_sweep_params *p, uint32_t *spins, uin
  * warps fill `next` while the remaining warps of every CTA flip (the two
  * touch disjoint buffers).  For Philox p->block is the block of the produced
  * window's slot 0.  count == 0 with next != NULL produces only. */
+/* Row slabs (g->ghost = 1; P must be >= 8 so a piece stays within one row):
+ * the producer generates exactly the slab's rows, and the flips exchange
+ * halos IN the kernel.  Each flip of the first / last owned row is also
+ * stored into the ghost row of the slab above / below (up_spins /
+ * down_spins: their spin buffers, e.g. NVLink peer mappings from symmetric
+ * memory; a single slab ring passes its own buffer).  Between phases the
+ * slabs handshake through monotonic flag counters (system-scope atomics):
+ * after its g-th phase a slab adds 1 to up_flags[1] and down_flags[0];
+ * before its g-th phase it waits until my_flags[0] and my_flags[1] reach g.
+ * phase0 = phases this slab completed in earlier calls; the flags start at
+ * 0 with ghost rows already valid.  A call with count == 0, next == NULL and
+ * a halo waits (on the stream) until both neighbours completed phase0
+ * phases, i.e. the ghost rows are current (before observables). */
+typedef struct msb_halo {
+  uint32_t *up_spins, *down_spins; /* spin buffers of the slabs above / below */
+  int32_t up_R, down_R;            /* their rows per colour (rows + 2) */
+  uint32_t *up_flags, *down_flags; /* their flag pairs */
+  uint32_t *my_flags;              /* ours: [0] from the slab above, [1] from below */
+  uint64_t phase0;
+} msb_halo;
+
 int msb_default_window(const msb_geom *g, int32_t *S, int32_t *P);
 int32_t msb_window_parts(const msb_geom *g, int32_t S);   /* default P for a given S */
 int64_t msb_window_pieces(const msb_geom *g, int32_t S, int32_t P);
@@ -202,7 +224,8 @@ int msb_window_init(const msb_geom *g, uint64_t seed, int32_t S, int32_t P, uint
                     const uint32_t *pow_tables, uint32_t *states, void *stream);
 int msb_window_sweep(const msb_geom *g, const msb_sweep_params *p, int32_t S, int32_t P,
                      uint32_t *spins, uint32_t *states, const uint32_t *cur, int32_t first,
-                     int32_t count, uint32_t *next, uint64_t *flips, void *stream);
+                     int32_t count, uint32_t *next, uint64_t *flips, const msb_halo *halo,
+                     void *stream);
 
 /* ---- observables (engine.py:372-386) ------------------------------------- */
 /* Adds, per replica, the number of +1 spins and the number of unsatisfied

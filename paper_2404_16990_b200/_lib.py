@@ -63,6 +63,16 @@ class SweepParams(ctypes.Structure):
     ]
 
 
+class Halo(ctypes.Structure):
+    """msb_halo: in-kernel halo exchange of a slab window (include/msb200.h)."""
+    _fields_ = [
+        ("up_spins", ctypes.c_void_p), ("down_spins", ctypes.c_void_p),
+        ("up_R", ctypes.c_int32), ("down_R", ctypes.c_int32),
+        ("up_flags", ctypes.c_void_p), ("down_flags", ctypes.c_void_p), ("my_flags", ctypes.c_void_p),
+        ("phase0", ctypes.c_uint64),
+    ]
+
+
 EXPORTS = (
     "msb_status_string", "msb_last_error", "msb_abi_version", "msb_check_geom", "msb_spin_words",
     "msb_row_pitch", "msb_pieces_per_phase", "msb_default_kg", "msb_plan_thresholds",
@@ -125,7 +135,7 @@ def lib() -> ctypes.CDLL:
         "msb_window_pieces": ([G, i32, i32], i64),
         "msb_window_words": ([G, i32], i64),
         "msb_window_init": ([G, u64, i32, i32, u64, vp, vp, vp], ctypes.c_int),
-        "msb_window_sweep": ([G, P, i32, i32, vp, vp, vp, i32, i32, vp, vp, vp], ctypes.c_int),
+        "msb_window_sweep": ([G, P, i32, i32, vp, vp, vp, i32, i32, vp, vp, ctypes.POINTER(Halo), vp], ctypes.c_int),
         "msb_observe": ([G, vp, vp, vp, vp], ctypes.c_int),
         "msb_draws": ([G, P, i32, vp, vp, vp], ctypes.c_int),
         "msb_pack_edges": ([G, i32, vp, vp, vp], ctypes.c_int),

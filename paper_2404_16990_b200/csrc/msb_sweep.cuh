@@ -63,6 +63,7 @@ __device__ __forceinline__ void finish_warp(unsigned* work, unsigned total_warps
     if (atomicAdd(work + 2, 1u) == total_warps - 1) {
       atomicExch(work, 0u);
       atomicExch(work + 1, 0u);
+      atomicExch(work + 3, 0u);
       atomicExch(work + 2, 0u);
     }
   }
@@ -84,6 +85,13 @@ struct FlipArgs {
   uint32_t inv;
   int fault;
   int8_t code_plane[16];
+  // slab halo push (fused slab windows, msb_halo): the first / last owned
+  // row is also stored into the ghost row of the slab above / below, whose
+  // spin buffers (peer memory over NVLink, or this slab itself) have up_R /
+  // down_R rows per colour.  Null: no push.
+  uint32_t* up_spins;
+  uint32_t* down_spins;
+  int up_R, down_R;
 };
 
 constexpr int kFlipSlots = 256;
@@ -185,7 +193,12 @@ __device__ __forceinline__ unsigned flip_quad_at(const FlipArgs& a, int s, int l
     res[k] = o[k] ^ f;
     cnt += __popc(f);
   }
-  *reinterpret_cast<uint4*>(own + w0) = make_uint4(res[0], res[1], res[2], res[3]);
+  const uint4 out = make_uint4(res[0], res[1], res[2], res[3]);
+  *reinterpret_cast<uint4*>(own + w0) = out;
+  if (a.up_spins && lr == 0)  // our first row is the ghost below of the slab above
+    *reinterpret_cast<uint4*>(a.up_spins + (((size_t)s * 2 + X) * a.up_R + a.up_R - 1) * G.Wp + w0) = out;
+  if (a.down_spins && lr == G.rows - 1)  // our last row is the ghost above of the slab below
+    *reinterpret_cast<uint4*>(a.down_spins + ((size_t)s * 2 + X) * a.down_R * G.Wp + w0) = out;
   return cnt;
 }
 
@@ -258,6 +271,8 @@ inline void fill_flip_args(FlipArgs& a, const msb_geom* g, const msb_sweep_param
   a.inv = p->mode == MSB_MODE_ANTI ? 0xFFFFFFFFu : 0u;
   a.fault = p->fault;
   std::memcpy(a.code_plane, p->code_plane, 16);
+  a.up_spins = a.down_spins = nullptr;
+  a.up_R = a.down_R = 0;
 }
 
 // Flip warps per 32-warp CTA of a fused launch: 6 measured best for

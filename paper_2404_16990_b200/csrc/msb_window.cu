@@ -34,7 +34,7 @@ struct WinArgs {
   long long npieces;       // S * P * streams
   size_t slot_words;       // plane words of one sweep (both colours, both planes)
   int S, P, pshift, kg, kr, nseg, streams, kit;
-  FastDiv streams_div, cells_div;
+  FastDiv streams_div, cells_div, sims_div;
   uint32_t seed_lo, seed_hi;    // Philox key
   unsigned long long block0;    // stream block of slot 0's first phase
 };
@@ -127,31 +127,47 @@ __device__ __forceinline__ void win_segment_k(const WinArgs& a, XState& st, uint
   }
 }
 
-// Piece numbering.  P <= 8 (a piece = 8/P whole quarter-segments):
-// gi = (j * P + p) * streams + stream, so a warp's lanes share (j, p) -- the
-// same segments -- across 32 consecutive streams.  P > 8 (a piece = 16/kg
-// k-values of one segment, kg = P/8): gi = ((j * 8 + seg) * streams +
-// stream) * kg + kgi, so the kg parts of a row sit in adjacent lanes and a
-// warp's plane stores land in 32/kg rows (t-words of the same sectors)
-// instead of 32 rows.  Decodes j, stream, first segment and first k.
-__device__ __forceinline__ void win_piece(int P, int pshift, int nseg, int kg, int kr, int streams,
-                                         const FastDiv& streams_div, unsigned gi, int& j, int& sti,
-                                         int& seg0, int& k0) {
-  if (P <= 8) {
-    const unsigned jp = streams_div.div(gi);
-    sti = (int)(gi - jp * (unsigned)streams);
-    j = (int)(jp >> pshift);
-    seg0 = (int)(jp & (unsigned)(P - 1)) * nseg;
-    k0 = 0;
+// Piece numbering.
+//  P < 8 (whole lattices; a piece = 8/P whole quarter-segments of a stream):
+//    gi = (j * P + p) * streams + stream -- a warp's lanes share (j, p), the
+//    same segments, across 32 consecutive streams.
+//  P >= 8 (a piece = 16/kg k-values of ONE quarter-segment, i.e. one row of
+//  one colour; kg = P/8):  gi = (((j * n_sim + s) * 2 + X) * rows + lr) * kg
+//    + kgi over the HELD rows lr -- so a slab generates exactly its own rows,
+//    the kg parts of a row sit in adjacent lanes and a warp's plane stores
+//    land in 32/kg adjacent rows.
+struct WinPiece {
+  int j, s, gamma, seg, k0, lr;  // lr: plane row (held-row index); seg = 4 X + q
+};
+
+__device__ __forceinline__ WinPiece win_piece(const WinArgs& a, unsigned gi) {
+  const Geo& G = a.G;
+  WinPiece w;
+  if (a.P < 8) {
+    const unsigned jp = a.streams_div.div(gi);
+    const int sti = (int)(gi - jp * (unsigned)a.streams);
+    w.j = (int)(jp >> a.pshift);
+    w.seg = (int)(jp & (unsigned)(a.P - 1)) * a.nseg;
+    w.k0 = 0;
+    w.s = (int)a.cells_div.div((unsigned)sti);
+    w.gamma = sti - w.s * (G.m / 4) + 1;
+    w.lr = -1;  // per segment (seg_row)
   } else {
-    const int kgs = pshift - 3;
-    const unsigned rest = gi >> kgs;
-    const unsigned js = streams_div.div(rest);
-    sti = (int)(rest - js * (unsigned)streams);
-    j = (int)(js >> 3);
-    seg0 = (int)(js & 7u);
-    k0 = (int)(gi & (unsigned)(kg - 1)) * kr;
+    const int kgs = a.pshift - 3;
+    const unsigned t = gi >> kgs;
+    const unsigned q1 = G.rows_div.div(t);
+    w.lr = (int)(t - q1 * (unsigned)G.rows);
+    const int X = (int)(q1 & 1u);
+    const unsigned q2 = q1 >> 1;
+    const unsigned jj = a.sims_div.div(q2);
+    w.j = (int)jj;
+    w.s = (int)(q2 - jj * (unsigned)G.n_sim);
+    const RowStream rs = row_stream(G.m, G.row0 + w.lr, X);
+    w.gamma = rs.gamma;
+    w.seg = 4 * X + rs.q;
+    w.k0 = (int)(gi & (unsigned)(a.kg - 1)) * a.kr;
   }
+  return w;
 }
 
 // One producer warp's share of a window (pieces numbered as win_piece).
@@ -171,12 +187,9 @@ __device__ __forceinline__ void win_produce(const WinArgs& a, const uint4* __res
     if (u >= units) break;
     const long long gi = u * 32 + lane;
     if (gi < a.npieces) {
-      int j, seg0, k0, sti;
-      win_piece(a.P, a.pshift, a.nseg, a.kg, a.kr, a.streams, a.streams_div, (unsigned)gi, j, sti, seg0, k0);
-      const int s = (int)a.cells_div.div((unsigned)sti);
-      const int gamma = sti - s * cells + 1;
-      const uint32_t key0 = a.thr9[s], key1 = a.thr9[G.n_sim + s];
-      uint32_t* slot = a.planes + (size_t)j * a.slot_words;
+      const WinPiece w = win_piece(a, (unsigned)gi);
+      const uint32_t key0 = a.thr9[w.s], key1 = a.thr9[G.n_sim + w.s];
+      uint32_t* slot = a.planes + (size_t)w.j * a.slot_words;
       XState st;
       uint32_t jw[8] = {0, 0, 0, 0, 0, 0, 0, 0}, r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       int nib = 0, jacc = 0;
@@ -185,17 +198,18 @@ __device__ __forceinline__ void win_produce(const WinArgs& a, const uint4* __res
         jw[0] = st.a0; jw[1] = st.a1; jw[2] = st.b0; jw[3] = st.b1;
         jw[4] = st.c0; jw[5] = st.c1; jw[6] = st.d0; jw[7] = st.d1;
       } else {  // Philox: the stream id rides in st.a0 / st.a1
-        const unsigned long long sid = ((unsigned long long)G.sim_offset + (unsigned long long)s) * cells + gamma - 1;
+        const unsigned long long sid =
+            ((unsigned long long)G.sim_offset + (unsigned long long)w.s) * cells + w.gamma - 1;
         st.a0 = (uint32_t)sid;
         st.a1 = (uint32_t)(sid >> 32);
       }
       for (int sg = 0; sg < a.nseg; sg++) {
-        const int seg = seg0 + sg, X = seg >> 2, q = seg & 3;
-        const int c = seg_row(G.m, gamma, X, q);
-        uint32_t* out = slot + plane_off(G, 2, X, 0, s, c);
-        const unsigned long long pseg = (a.block0 + 2ull * j + X) * 2 * n + (unsigned long long)q * (n / 2);
+        const int seg = w.seg + sg, X = seg >> 2, q = seg & 3;
+        const int lr = w.lr >= 0 ? w.lr : seg_row(G.m, w.gamma, X, q);
+        uint32_t* out = slot + plane_off(G, 2, X, 0, w.s, lr);
+        const unsigned long long pseg = (a.block0 + 2ull * w.j + X) * 2 * n + (unsigned long long)q * (n / 2);
         for (int kk = 0; kk < a.kr; kk++) {
-          const int k = k0 + kk;
+          const int k = w.k0 + kk;
           win_segment_k<SRC, FULL>(a, st, out + t_of_k(k), key0, key1, pstride,
                                    pseg + (unsigned long long)k * G.words);
           if (XO) {  // the 8 jump words, spread evenly over the piece's kit k-iterations
@@ -220,6 +234,9 @@ __device__ __forceinline__ void win_produce(const WinArgs& a, const uint4* __res
   }
 }
 
+// Grid barrier among the consumer warps: a named CTA barrier (id 1, the
+// consumer warps only), one arrival per CTA on the counter, the CTA leader
+// spins until all CTAs arrived, a second named barrier releases the CTA.
 __device__ __forceinline__ void consumer_barrier(unsigned* ctr, unsigned target, int nthreads, bool leader) {
   asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
   if (leader) {
@@ -230,9 +247,61 @@ __device__ __forceinline__ void consumer_barrier(unsigned* ctr, unsigned target,
   }
   asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
+
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+struct HaloArgs {
+  unsigned *up_flags, *down_flags, *my_flags;
+  unsigned long long phase0;
+  int on;
+};
+
+// Slab-window phase gate (msb_halo).  Ends local phase i (i = -1: launch
+// start) and opens phase i+1 when `open`.  All consumer warps of this GPU
+// arrive (work[1]); the GPU leader (first consumer thread of CTA 0) then
+// signals both neighbours that global phase phase0+i is complete, waits
+// until both neighbours completed phase0+i as well (their halo pushes into
+// our ghost rows have landed, and they no longer read the ghost rows we are
+// about to overwrite), and publishes the release in work[3].
+__device__ __forceinline__ void halo_gate(const HaloArgs& h, unsigned* work, int i, bool open, int nthreads,
+                                          bool cta_leader, bool gpu_leader) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+  if (i >= 0 && cta_leader) {
+    __threadfence();
+    atomicAdd(work + 1, 1u);
+  }
+  if (gpu_leader) {
+    if (i >= 0) {
+      while (ld_acquire(work + 1) < gridDim.x * (unsigned)(i + 1)) __nanosleep(64);
+      __threadfence_system();
+      atomicAdd_system(h.up_flags + 1, 1u);    // we are the lower neighbour of the slab above
+      atomicAdd_system(h.down_flags + 0, 1u);  // and the upper neighbour of the slab below
+    }
+    if (open) {
+      const unsigned need = (unsigned)(h.phase0 + (unsigned long long)(i + 1));
+      while (ld_acquire_sys(h.my_flags + 0) < need || ld_acquire_sys(h.my_flags + 1) < need) __nanosleep(64);
+      __threadfence_system();
+      atomicExch(work + 3, (unsigned)(i + 2));
+    }
+  }
+  if (open && cta_leader) {
+    while (ld_acquire(work + 3) < (unsigned)(i + 2)) __nanosleep(64);
+    __threadfence();
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+// Window launch: warps [0, pwarps) fill the next window (pwarps = 0: no
+// production); the other warps flip slots [first, first + count) of `cur`
+// (red, barrier, blue, barrier, ...).  With a halo (slabs) every phase is
+// gated by halo_gate and all neighbour reads go through L2.
 template <int SRC, bool FULL>
-__global__ void __launch_bounds__(kRngThreads, 1) k_win(const WinArgs wa, const FlipArgs fa0, const uint32_t* cur,
-                                                        int first, int count, int pwarps) {
+__global__ void __launch_bounds__(kRngThreads, 1) k_win(const WinArgs wa, const FlipArgs fa0, const HaloArgs ha,
+                                                        const uint32_t* cur, int first, int count, int pwarps) {
   extern __shared__ uint4 jt[];
   if (SRC == kSrcXoshiro && pwarps > 0) {
     for (int i = threadIdx.x; i < kJumpWords / 4; i += blockDim.x) jt[i] = wa.jump[i];
@@ -253,46 +322,57 @@ __global__ void __launch_bounds__(kRngThreads, 1) k_win(const WinArgs wa, const 
     FlipArgs fa = fa0;
     unsigned cnt = 0;
     const bool leader = threadIdx.x == pwarps * 32;
+    const bool gpu_leader = leader && blockIdx.x == 0;
+    if (ha.on) halo_gate(ha, wa.work, -1, true, nwc * 32, leader, gpu_leader);
     for (int i = 0; i < 2 * count; i++) {
       const int X = i & 1;
       fa.planes = cur + (size_t)(first + (i >> 1)) * wa.slot_words;
-      if (i == 0) cnt += flip_run<false>(fa, i0, hi, X);
+      if (i == 0 && !ha.on) cnt += flip_run<false>(fa, i0, hi, X);
       else cnt += flip_run<true>(fa, i0, hi, X);
-      if (i + 1 < 2 * count) consumer_barrier(wa.work + 1, gridDim.x * (unsigned)(i + 1), nwc * 32, leader);
+      const bool more = i + 1 < 2 * count;
+      if (ha.on) {
+        __threadfence_system();  // this thread's halo pushes (if any) before the neighbours are told
+        halo_gate(ha, wa.work, i, more, nwc * 32, leader, gpu_leader);
+      } else if (more) {
+        consumer_barrier(wa.work + 1, gridDim.x * (unsigned)(i + 1), nwc * 32, leader);
+      }
     }
     add_flips(fa.flips, cnt);
   }
   finish_warp(wa.work, total_warps);
 }
 
+// Halo wait: until both neighbours completed `need` phases (their pushes
+// into our ghost rows landed), e.g. before the observables of a slab.
+__global__ void k_halo_wait(const unsigned* my_flags, unsigned need) {
+  if (threadIdx.x == 0) {
+    while (ld_acquire_sys(my_flags + 0) < need || ld_acquire_sys(my_flags + 1) < need) __nanosleep(128);
+    __threadfence_system();
+  }
+}
+
 // Piece start states of a window whose slot 0 starts at stream block
-// `block0`: piece (j, seg0, k0, stream) starts at draw
-// (block0 + 2j) 2n + seg0 n/2 + k0 n/32 (segment = colour block + quarter).
-__global__ void k_win_init(Geo G, uint64_t seed, int P, int pshift, int streams, FastDiv streams_div,
-                           FastDiv cells_div, long long npieces, uint64_t block0, const uint4* __restrict__ pow,
-                           uint32_t* states) {
+// `block0`: piece (j, segment = 4 X + q, k0, stream) starts at draw
+// (block0 + 2j) 2n + seg n/2 + k0 n/32 of its stream.
+__global__ void k_win_init(const WinArgs a, uint64_t seed, const uint4* __restrict__ pow) {
   const long long gi = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gi >= npieces) return;
-  const int kg = P > 8 ? P / 8 : 1, kr = 16 / kg, nseg = P <= 8 ? 8 / P : 1;
-  int j, sti, seg0, k0;
-  win_piece(P, pshift, nseg, kg, kr, streams, streams_div, (unsigned)gi, j, sti, seg0, k0);
-  // offset of the piece's first draw within its stream-sweep (4n draws):
-  // segment seg0 = colour X (block) and quarter q, then k0 * (n/32) draws
-  const int cells = G.m / 4;
-  const int s = (int)cells_div.div((unsigned)sti);
-  const int gamma = sti - s * cells + 1;
-  const uint64_t n = (uint64_t)G.n;
-  const uint64_t sid = ((uint64_t)G.sim_offset + (uint64_t)s) * (uint64_t)cells + (uint64_t)(gamma - 1);
-  const uint64_t D = (block0 + 2ull * j) * 2 * n + (uint64_t)seg0 * (n / 2) + (uint64_t)k0 * (n / 32);
-  store_state(jump_by(stream_state(seed, sid), D, pow), states, npieces, gi);
+  if (gi >= a.npieces) return;
+  const WinPiece w = win_piece(a, (unsigned)gi);
+  const Geo& G = a.G;
+  const uint64_t n = (uint64_t)G.n, cells = (uint64_t)(G.m / 4);
+  const uint64_t sid = ((uint64_t)G.sim_offset + (uint64_t)w.s) * cells + (uint64_t)(w.gamma - 1);
+  const uint64_t D = (a.block0 + 2ull * w.j) * 2 * n + (uint64_t)w.seg * (n / 2) + (uint64_t)w.k0 * (n / 32);
+  store_state(jump_by(stream_state(seed, sid), D, pow), a.states, a.npieces, gi);
 }
 
 int check_window(const msb_geom* g, int S, int P, long long* npieces) {
   if (int r = check_geom(g)) return r;
-  if (g->ghost) return fail(MSB_ERR_UNSUPPORTED, "lookahead windows run whole lattices; slabs use the per-phase calls");
   if (S < 1 || S > 64) return fail(MSB_ERR_ARG, "window length S must be in [1, 64]");
   if (P < 1 || P > 128 || (P & (P - 1))) return fail(MSB_ERR_ARG, "parts per stream-sweep P must be a power of two <= 128");
-  const long long np = (long long)S * P * g->n_sim * (g->m / 4);
+  if (g->ghost && P < 8) return fail(MSB_ERR_ARG, "slab windows need P >= 8 (one row per piece)");
+  // P >= 8: S * n_sim * 2 colours * held rows * P/8 parts; P < 8: S * P * streams
+  const long long np = P >= 8 ? (long long)S * g->n_sim * 2 * g->rows * (P / 8)
+                              : (long long)S * P * g->n_sim * (g->m / 4);
   if (np >= (1LL << 31)) return fail(MSB_ERR_UNSUPPORTED, "too many window pieces");
   *npieces = np;
   return MSB_OK;
@@ -324,6 +404,7 @@ void fill_win_args(WinArgs& w, const msb_geom* g, const msb_sweep_params* p, int
   w.streams = g->n_sim * (g->m / 4);
   w.streams_div.init((uint32_t)w.streams);
   w.cells_div.init((uint32_t)(g->m / 4));
+  w.sims_div.init((uint32_t)g->n_sim);
   w.seed_lo = (uint32_t)p->seed;
   w.seed_hi = (uint32_t)(p->seed >> 32);
   w.block0 = p->block;
@@ -338,12 +419,13 @@ extern "C" {
 
 int32_t msb_window_parts(const msb_geom* g, int32_t S) {
   long long np = 0;
-  if (check_window(g, S, 1, &np)) return -1;
+  if (check_window(g, S, g && g->ghost ? 8 : 1, &np)) return -1;
   // smallest split giving ~one warp-unit (32 pieces) per producer warp of
-  // every SM (148 SMs x 28 warps), as msb_default_kg
-  const long long streams = (long long)g->n_sim * (g->m / 4);
-  int p = 1;
-  while (p < 128 && (long long)S * p * streams < 118000) p *= 2;
+  // every SM (148 SMs x 28 warps), as msb_default_kg; slabs need P >= 8
+  const long long rows2 = 2LL * g->n_sim * g->rows;  // (replica, colour, row) segments per sweep
+  auto pieces = [&](int p) { return (long long)S * rows2 * p / 8; };
+  int p = g->ghost ? 8 : 1;
+  while (p < 128 && pieces(p) < 118000) p *= 2;
   // Rows being written concurrently stay L2-resident: a piece completes its
   // row's plane words one t-word per k, so ~140k pieces in flight write
   // 140k / max(1, P/8) rows of 8*Wp bytes (P > 8: the P/8 parts of a row run
@@ -351,15 +433,15 @@ int32_t msb_window_parts(const msb_geom* g, int32_t S) {
   const long long row_bytes = 8LL * make_geo(g).Wp;
   while (p < 128 && 140000LL / std::max(1, p / 8) * row_bytes > (60LL << 20)) p *= 2;
   static const int env_p = [] { const char* e = getenv("MSB_WINDOW_PARTS"); return e ? atoi(e) : 0; }();
-  if (env_p > 0 && env_p <= 128 && !(env_p & (env_p - 1))) p = env_p;  // tuning override
-  while (p > 1 && (long long)S * p * streams >= (1LL << 31)) p >>= 1;
+  if (env_p > 0 && env_p <= 128 && !(env_p & (env_p - 1)) && (env_p >= 8 || !g->ghost)) p = env_p;  // tuning
+  while (p > (g->ghost ? 8 : 1) && pieces(p) >= (1LL << 31)) p >>= 1;
   return p;
 }
 
 int msb_default_window(const msb_geom* g, int32_t* S, int32_t* P) {
   if (!S || !P) return fail(MSB_ERR_ARG, "null output");
   long long np = 0;
-  if (int r = check_window(g, 1, 1, &np)) return r;
+  if (int r = check_window(g, 1, g && g->ghost ? 8 : 1, &np)) return r;
   // S = 8 sweeps unless two window buffers would exceed 8 GiB of planes
   const long long slot_bytes = 4LL * (long long)slot_words(g);
   int s = 8;
@@ -377,7 +459,7 @@ int64_t msb_window_pieces(const msb_geom* g, int32_t S, int32_t P) {
 
 int64_t msb_window_words(const msb_geom* g, int32_t S) {
   long long np = 0;
-  if (check_window(g, S, 1, &np)) return -1;
+  if (check_window(g, S, g && g->ghost ? 8 : 1, &np)) return -1;
   return (int64_t)S * (int64_t)slot_words(g);
 }
 
@@ -386,35 +468,55 @@ int msb_window_init(const msb_geom* g, uint64_t seed, int32_t S, int32_t P, uint
   long long np = 0;
   if (int r = check_window(g, S, P, &np)) return r;
   if (!pow_tables || !states) return fail(MSB_ERR_ARG, "null buffer");
-  int pshift = 0;
-  while ((1 << pshift) < P) pshift++;
-  const int streams = g->n_sim * (g->m / 4);
-  FastDiv sd, cd;
-  sd.init((uint32_t)streams);
-  cd.init((uint32_t)(g->m / 4));
-  k_win_init<<<blocks_for(np, 128), 128, 0, as_stream(stream)>>>(make_geo(g), seed, P, pshift, streams, sd, cd, np,
-                                                                 block, reinterpret_cast<const uint4*>(pow_tables),
-                                                                 states);
+  msb_sweep_params p = {};
+  p.block = block;
+  WinArgs wa;
+  fill_win_args(wa, g, &p, S, P, np, states, nullptr);
+  k_win_init<<<blocks_for(np, 128), 128, 0, as_stream(stream)>>>(wa, seed,
+                                                                 reinterpret_cast<const uint4*>(pow_tables));
   CUDA_TRY(cudaGetLastError());
   return MSB_OK;
 }
 
 int msb_window_sweep(const msb_geom* g, const msb_sweep_params* p, int32_t S, int32_t P, uint32_t* spins,
                      uint32_t* states, const uint32_t* cur, int32_t first, int32_t count, uint32_t* next,
-                     uint64_t* flips, void* stream) {
+                     uint64_t* flips, const msb_halo* halo, void* stream) {
   long long np = 0;
   if (int r = check_window(g, S, P, &np)) return r;
   if (int r = check_params(p)) return r;
   if (p->mode == MSB_MODE_GENERIC) return fail(MSB_ERR_UNSUPPORTED, "lookahead windows need FERRO/ANTI tables");
   if (first < 0 || count < 0 || first + count > S) return fail(MSB_ERR_ARG, "slots [first, first+count) outside the window");
   if (count > 0 && (!spins || !cur || !flips)) return fail(MSB_ERR_ARG, "null buffer");
-  if (!next && count == 0) return MSB_OK;
+  if (count > 0 && g->ghost && !halo) return fail(MSB_ERR_ARG, "slab windows flip with an msb_halo (in-kernel exchange)");
+  if (halo && !g->ghost) return fail(MSB_ERR_ARG, "msb_halo needs a slab geometry (ghost = 1)");
+  if (halo && (!halo->up_spins || !halo->down_spins || !halo->up_flags || !halo->down_flags || !halo->my_flags ||
+               halo->up_R < 4 || halo->down_R < 4))
+    return fail(MSB_ERR_ARG, "incomplete msb_halo");
+  if (!next && count == 0) {
+    if (halo) {
+      k_halo_wait<<<1, 32, 0, as_stream(stream)>>>(halo->my_flags, (unsigned)halo->phase0);
+      CUDA_TRY(cudaGetLastError());
+    }
+    return MSB_OK;
+  }
   if (next && p->rng == MSB_RNG_XOSHIRO && (!states || !p->jump)) return fail(MSB_ERR_ARG, "null RNG state or jump table");
   const bool produce = next != nullptr;
   WinArgs wa;
   fill_win_args(wa, g, p, S, P, np, states, next);
   FlipArgs fa;
   fill_flip_args(fa, g, p, 0, spins, cur, flips);
+  HaloArgs ha = {};
+  if (halo && count > 0) {
+    fa.up_spins = halo->up_spins;
+    fa.down_spins = halo->down_spins;
+    fa.up_R = halo->up_R;
+    fa.down_R = halo->down_R;
+    ha.up_flags = halo->up_flags;
+    ha.down_flags = halo->down_flags;
+    ha.my_flags = halo->my_flags;
+    ha.phase0 = halo->phase0;
+    ha.on = 1;
+  }
   // Warp split of the 32-warp CTAs.  A unit (32 pieces) is a whole window's
   // share of a stream, so an extra producer round costs a full unit: when the
   // units fit one round, give producers exactly that round and the rest of
@@ -445,7 +547,7 @@ int msb_window_sweep(const msb_geom* g, const msb_sweep_params* p, int32_t S, in
     if (env_pw > 0) pwarps = std::min(32, env_pw);
   }
   const bool philox = p->rng == MSB_RNG_PHILOX;
-  const bool full = (fa.G.words % 32) == 0;
+  const bool full = (wa.G.words % 32) == 0;
   static std::once_flag o1, o2, o3;
   static cudaError_t e1, e2, e3;
   if (int r = set_smem_attr(k_win<kSrcXoshiro, true>, o1, e1)) return r;
@@ -461,9 +563,9 @@ int msb_window_sweep(const msb_geom* g, const msb_sweep_params* p, int32_t S, in
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = count > 0 ? 1 : 0;  // grid barriers only among consumers
-  if (philox) CUDA_TRY(cudaLaunchKernelEx(&cfg, k_win<kSrcPhilox, false>, wa, fa, cur, first, count, pwarps));
-  else if (full) CUDA_TRY(cudaLaunchKernelEx(&cfg, k_win<kSrcXoshiro, true>, wa, fa, cur, first, count, pwarps));
-  else CUDA_TRY(cudaLaunchKernelEx(&cfg, k_win<kSrcXoshiro, false>, wa, fa, cur, first, count, pwarps));
+  if (philox) CUDA_TRY(cudaLaunchKernelEx(&cfg, k_win<kSrcPhilox, false>, wa, fa, ha, cur, first, count, pwarps));
+  else if (full) CUDA_TRY(cudaLaunchKernelEx(&cfg, k_win<kSrcXoshiro, true>, wa, fa, ha, cur, first, count, pwarps));
+  else CUDA_TRY(cudaLaunchKernelEx(&cfg, k_win<kSrcXoshiro, false>, wa, fa, ha, cur, first, count, pwarps));
   return MSB_OK;
 }
 

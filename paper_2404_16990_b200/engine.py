@@ -526,7 +526,7 @@ class Engine:
         self._params.block = self._wbase if count == 0 else self._wbase + 2 * self.window
         call("msb_window_sweep", ctypes.byref(self._g), ctypes.byref(self._params), self.window, self._wP,
              _p(self._spins), _p(states), _p(cur) if cur is not None else None, first, count,
-             _p(nxt) if produce else None, _p(self._flips_dev), self._cs)
+             _p(nxt) if produce else None, _p(self._flips_dev), None, self._cs)
         self._params.jump = self._jump.data_ptr()
 
     def _win_sweeps(self, k: int) -> None:

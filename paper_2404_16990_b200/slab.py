@@ -17,6 +17,13 @@ Transports:
                  plain device-to-device copies between the phase kernels;
   DistExchange   one slab per torch.distributed rank: batched send/recv of
                  the edge rows (NCCL over NVLink on GPUs, gloo on CPU).
+
+FusedSlabRun drops the host from the loop: one slab per process, lookahead
+windows (msb_window_sweep) whose flip warps store the slab's first/last rows
+straight into the neighbours' ghost rows -- peer memory over NVLink from
+symmetric memory -- and handshake every phase through flag counters in peer
+memory.  One process with one slab is the periodic ring of a single slab
+(its own neighbour), which runs the same kernel path.
 """
 
 from __future__ import annotations
@@ -28,10 +35,11 @@ import numpy as np
 
 from . import _lib
 from ._lib import call, geom, SweepParams, MSB_FLIP_SLOTS, MSB_MAX_PLANES, MSB_RNG_PHILOX, MSB_RNG_XOSHIRO
-from .engine import _M64, _p, _pow_tables, _sweep_jump_table, _torch, build_exp_table
+from .engine import _M64, _jump_table, _p, _pow_tables, _sweep_jump_table, _torch, build_exp_table
 from .layout import LatticeDims
 
-__all__ = ["slab_bounds", "SlabLattice", "LocalExchange", "DistExchange", "SlabRun"]
+__all__ = ["slab_bounds", "ring_plan", "SlabLattice", "LocalExchange", "DistExchange", "SlabRun", "FusedSlabRun",
+           "symmetric_alloc"]
 
 
 def slab_bounds(m: int, parts: int) -> list[tuple[int, int]]:
@@ -52,7 +60,7 @@ class SlabLattice:
 
     def __init__(self, dims: LatticeDims, temperatures, seed: int, row0: int, rows: int, init: str = "random",
                  coupling: float = 1.0, sim_offset: int = 0, device=None, kg: int | None = None,
-                 stream: str = "xoshiro"):
+                 stream: str = "xoshiro", alloc=None):
         torch = _torch()
         self.dims = dims
         self.temperatures = tuple(float(t) for t in temperatures)
@@ -76,8 +84,10 @@ class SlabLattice:
         call("msb_plan_thresholds", tables.ctypes.data_as(ctypes.c_void_p), self.n_sim, ctypes.byref(mode),
              ctypes.byref(npl), codes, thr.ctypes.data_as(ctypes.c_void_p))
         with torch.cuda.device(self.device), torch.cuda.stream(self._stream):
-            self._spins = torch.empty(int(L.msb_spin_words(ctypes.byref(self._g))), dtype=torch.int32,
-                                      device=self.device)
+            nwords = int(L.msb_spin_words(ctypes.byref(self._g)))
+            # alloc: e.g. symmetric_alloc(group) so peers can map the buffer (FusedSlabRun)
+            self._spins = (alloc(nwords, self.device) if alloc is not None
+                           else torch.empty(nwords, dtype=torch.int32, device=self.device))
             self._states = torch.empty(2 * 8 * n_pieces, dtype=torch.int32, device=self.device)
             self._planes = torch.empty(int(L.msb_plane_words(ctypes.byref(self._g), npl.value)),
                                        dtype=torch.int32, device=self.device)
@@ -166,6 +176,28 @@ class SlabLattice:
 
     def synchronize(self) -> None:
         self._stream.synchronize()
+
+
+def ring_plan(m: int, world: int, rank: int) -> dict:
+    """Slab rows of `rank` in a ring of `world` slabs over m rows, and its
+    neighbours: the slab above (rank-1, whose last row is our upper ghost)
+    and below (rank+1), with their buffer rows per colour (rows + 2)."""
+    bounds = slab_bounds(m, world)
+    up, down = (rank - 1) % world, (rank + 1) % world
+    (a, b) = bounds[rank]
+    return {"row0": a, "rows": b - a, "up": up, "down": down,
+            "up_R": bounds[up][1] - bounds[up][0] + 2, "down_R": bounds[down][1] - bounds[down][0] + 2}
+
+
+def symmetric_alloc(group=None):
+    """Allocator for SlabLattice(alloc=...): int32 buffers in torch symmetric
+    memory, so every rank of `group` can map them (FusedSlabRun)."""
+    import torch.distributed._symmetric_memory as symm_mem
+    torch = _torch()
+
+    def alloc(nwords: int, device):
+        return symm_mem.empty(nwords, dtype=torch.int32, device=device)
+    return alloc
 
 
 def _neighbour_ghosts(edges_above, edges_below, n_sim: int, Wp: int):
@@ -261,3 +293,141 @@ class SlabRun:
             ups = u if ups is None else ups + u
             unsat = b if unsat is None else unsat + b
         return ups, unsat
+
+
+class FusedSlabRun:
+    """One slab per process, halos exchanged inside the window kernel.
+
+    Per call of ``sweep(k)`` the slab runs lookahead windows of S sweeps
+    (``msb_window_sweep`` with an ``msb_halo``): producer warps generate the
+    next window's accept planes for the slab's own rows while the flip warps
+    flip the current window phase by phase; every flip of the first / last
+    owned row is also stored into the neighbour's ghost row (peer memory), and
+    the slabs handshake each phase through monotonic flag counters (system-
+    scope atomics on peer memory), so no host synchronisation or separate
+    exchange step remains.
+
+    world 1 (no process group): the slab is its own upper and lower
+    neighbour -- the periodic single-slab ring, same kernel path.  world > 1:
+    build the slab with ``alloc=symmetric_alloc(group)`` and rows from
+    ``ring_plan``; spins and flags are mapped from every peer.
+    """
+
+    def __init__(self, slab: SlabLattice, group=None, window: int | None = None):
+        import torch.distributed as dist
+        torch = _torch()
+        self.slab = slab
+        L = _lib.lib()
+        g = ctypes.byref(slab._g)
+        if slab._params.mode == 2:
+            raise ValueError("fused slab windows need FERRO/ANTI tables")
+        if window is None:
+            S, P = ctypes.c_int32(), ctypes.c_int32()
+            call("msb_default_window", g, ctypes.byref(S), ctypes.byref(P))
+            self.S, self.P = int(S.value), int(P.value)
+        else:
+            self.S = int(window)
+            self.P = int(L.msb_window_parts(g, self.S))
+        npieces = int(L.msb_window_pieces(g, self.S, self.P))
+        self._words = int(L.msb_window_words(g, self.S))
+        if npieces < 0 or self._words < 0:
+            raise _lib.MsbError(f"slab window S={self.S} P={self.P}: {L.msb_last_error().decode()}")
+        self.world = dist.get_world_size(group) if (dist.is_available() and dist.is_initialized()) else 1
+        self.rank = dist.get_rank(group) if self.world > 1 else 0
+        with torch.cuda.device(slab.device), slab.stream_ctx():
+            self._wstates = torch.empty(8 * npieces, dtype=torch.int32, device=slab.device)
+            self._wplanes = torch.empty(2 * self._words, dtype=torch.int32, device=slab.device)
+        self._jump = _jump_table(slab.device, self.S * 4 * slab.dims.n)
+        R = slab.rows + 2
+        h = _lib.Halo()
+        if self.world == 1:
+            with slab.stream_ctx():
+                self._flags = torch.zeros(2, dtype=torch.int32, device=slab.device)
+            sp, fl = slab._spins.data_ptr(), self._flags.data_ptr()
+            h.up_spins = h.down_spins = sp
+            h.up_flags = h.down_flags = h.my_flags = fl
+            h.up_R = h.down_R = R
+            LocalExchange().exchange([slab], 0)
+            LocalExchange().exchange([slab], 1)
+        else:
+            import torch.distributed._symmetric_memory as symm_mem
+            plan = ring_plan(slab.dims.m, self.world, self.rank)
+            if (plan["row0"], plan["rows"]) != (slab.row0, slab.rows):
+                raise ValueError("slab rows must follow ring_plan(m, world, rank)")
+            self._flags = symm_mem.empty(2, dtype=torch.int32, device=slab.device)
+            self._flags.zero_()
+            hs = symm_mem.rendezvous(slab._spins, group)
+            hf = symm_mem.rendezvous(self._flags, group)
+
+            def peer(hdl, t, r):  # peer r's mapping of the same buffer
+                return int(hdl.buffer_ptrs[r]) + (t.data_ptr() - int(hdl.buffer_ptrs[self.rank]))
+            h.up_spins, h.down_spins = peer(hs, slab._spins, plan["up"]), peer(hs, slab._spins, plan["down"])
+            h.up_flags, h.down_flags = peer(hf, self._flags, plan["up"]), peer(hf, self._flags, plan["down"])
+            h.my_flags = self._flags.data_ptr()
+            h.up_R, h.down_R = plan["up_R"], plan["down_R"]
+            DistExchange(group).exchange([slab], 0)
+            DistExchange(group).exchange([slab], 1)
+            torch.cuda.synchronize(slab.device)
+            dist.barrier(group)
+        h.phase0 = 0
+        self._halo = h
+        self._valid = False
+        self._cur = 0
+        self._wc = 0
+        self._wbase = 0
+
+    def _launch(self, first: int, count: int, produce: bool) -> None:
+        s = self.slab
+        w = self._words
+        cur = self._wplanes[self._cur * w:(self._cur + 1) * w]
+        nxt = self._wplanes[(1 - self._cur) * w:(2 - self._cur) * w]
+        if count == 0:
+            nxt, cur = cur, None
+        s._params.jump = self._jump.data_ptr()
+        s._params.block = self._wbase if count == 0 else self._wbase + 2 * self.S
+        call("msb_window_sweep", ctypes.byref(s._g), ctypes.byref(s._params), self.S, self.P, _p(s._spins),
+             _p(self._wstates), _p(cur) if cur is not None else None, first, count,
+             _p(nxt) if produce else None, _p(s._flips), ctypes.byref(self._halo), s._cs)
+        s._params.jump = s._jump.data_ptr()
+
+    def sweep(self, n_sweeps: int = 1) -> None:
+        s = self.slab
+        k = int(n_sweeps)
+        if k <= 0:
+            return
+        if not self._valid:
+            self._wbase, self._wc, self._cur = 2 * s.sweeps_done, 0, 0
+            if s.stream == "xoshiro":
+                call("msb_window_init", ctypes.byref(s._g), ctypes.c_uint64(s.seed & _M64), self.S, self.P,
+                     ctypes.c_uint64(self._wbase), _p(s._pow), _p(self._wstates), s._cs)
+            self._launch(0, 0, True)
+            self._valid = True
+        while k > 0:
+            r = min(k, self.S - self._wc)
+            finish = self._wc + r == self.S
+            self._launch(self._wc, r, finish)
+            self._halo.phase0 += 2 * r
+            s.sweeps_done += r
+            k -= r
+            if finish:
+                self._cur, self._wc, self._wbase = 1 - self._cur, 0, self._wbase + 2 * self.S
+            else:
+                self._wc += r
+
+    def observe_async(self):
+        """Device int64 [2*n_sim] (ups, unsat) of this slab, stream-ordered: a
+        device-side wait until both neighbours finished the phases so far (our
+        ghost rows are current), then msb_observe.  No host synchronisation;
+        callers with world > 1 all-reduce the result."""
+        s = self.slab
+        call("msb_window_sweep", ctypes.byref(s._g), ctypes.byref(s._params), self.S, self.P, None, None, None,
+             0, 0, None, None, ctypes.byref(self._halo), s._cs)
+        return s.observe()
+
+    def observables(self):
+        """(ups, unsat) int64 per replica of this slab (host copies)."""
+        o = self.observe_async()
+        self.slab.synchronize()
+        h = o.cpu().numpy()
+        n = self.slab.n_sim
+        return h[:n].copy(), h[n:].copy()

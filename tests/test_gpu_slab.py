@@ -44,3 +44,47 @@ def test_slabs_large_rows_vs_oracle():
     got = np.concatenate([s.lattice_rows()[0] for s in run.slabs], axis=0)
     assert (got == o.spins[0]).all()
     assert sum(s.flips for s in run.slabs) == o.flips
+
+
+# ---- fused slab windows (in-kernel halo exchange, msb_halo) ---------------------
+
+@pytest.mark.parametrize("m,n,n_sim,stream,window", [
+    (16, 128, 2, "xoshiro", None), (16, 128, 2, "philox", None), (64, 1024, 1, "xoshiro", 3),
+    (12, 96, 3, "xoshiro", 2), (32, 14336, 1, "xoshiro", None),
+])
+def test_fused_slab_single_ring_vs_oracle(m, n, n_sim, stream, window):
+    """One slab that is its own neighbour above and below (the periodic ring
+    of one slab) through the fused window kernel: push of the edge rows into
+    the ghost rows + flag handshake every phase, partial windows included."""
+    from oracle import oracle as orc
+    from paper_2404_16990_b200 import LatticeDims
+    from paper_2404_16990_b200.slab import FusedSlabRun, SlabLattice
+    dims = LatticeDims(m, n)
+    temps = list(np.linspace(1.8, 3.0, n_sim))
+    slab = SlabLattice(dims, temps, 31, 0, m, sim_offset=2, stream=stream)
+    run = FusedSlabRun(slab, window=window)
+    o = orc.OracleEngine(m, n, temps, 31, sim_offset=2, stream=stream)
+    for k in (1, run.S, 2, run.S + 1):
+        run.sweep(k)
+        o.sweep(k)
+        assert (slab.lattice_rows() == o.spins).all(), f"after {k} more sweeps"
+    assert slab.flips == o.flips
+    ups, unsat = run.observables()
+    o_ups, o_bonds = o.observe()
+    assert ups.tolist() == o_ups.tolist()
+    assert (2 * m * n - 2 * unsat).tolist() == o_bonds.tolist()
+
+
+def test_fused_slab_matches_host_exchange_path():
+    """The fused single-slab ring equals the host-driven SlabRun, sweep by sweep."""
+    from paper_2404_16990_b200 import LatticeDims
+    from paper_2404_16990_b200.slab import FusedSlabRun, LocalExchange, SlabLattice, SlabRun
+    dims = LatticeDims(24, 256)
+    a = SlabLattice(dims, [2.1], 8, 0, 24)
+    b = SlabLattice(dims, [2.1], 8, 0, 24)
+    fused, host = FusedSlabRun(a, window=4), SlabRun([b], LocalExchange())
+    for _ in range(6):
+        fused.sweep(1)
+        host.sweep(1)
+        assert (a.lattice_rows() == b.lattice_rows()).all()
+    assert a.flips == b.flips

@@ -74,3 +74,18 @@ def test_halo_audit_and_sources():
     assert canonical_halo_source(ArrayCode.RFE, 0, 1, dims) is None
     with pytest.raises(ValueError):
         canonical_halo_source(ArrayCode.RFE, 1, 1, dims)
+
+
+def test_ring_plan_neighbours():
+    """Slab ring plan (FusedSlabRun): rows cover [0, m) in order, neighbours
+    wrap, and each side's buffer rows match the neighbour's own rows + 2."""
+    from paper_2404_16990_b200.slab import ring_plan
+    for m, world in [(14336, 8), (262144, 8), (12, 3), (16, 1), (64, 5)]:
+        plans = [ring_plan(m, world, r) for r in range(world)]
+        assert plans[0]["row0"] == 0 and sum(p["rows"] for p in plans) == m
+        for r, p in enumerate(plans):
+            assert p["up"] == (r - 1) % world and p["down"] == (r + 1) % world
+            assert p["up_R"] == plans[p["up"]]["rows"] + 2 and p["down_R"] == plans[p["down"]]["rows"] + 2
+            if r + 1 < world:
+                assert plans[r + 1]["row0"] == p["row0"] + p["rows"]
+            assert p["rows"] % 2 == 0 and p["row0"] % 2 == 0
