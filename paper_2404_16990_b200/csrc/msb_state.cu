@@ -61,47 +61,58 @@ __global__ void k_init_linear(Geo G, uint64_t seed, long long words_per_sim, con
   }
 }
 
-// Thread per (s, held row lr, word (ch, t)): both colours' word from the
-// linear row, read as uint32 words (linear bit i -> bit i%32 of word i/32).
-// Sites of word (ch, t): r = 32 w + 2 t + {0, 1}, w = 32 ch + b; the even r
-// belongs to colour c&1, the odd one to (c+1)&1.
-__global__ void k_from_linear(Geo G, const uint32_t* __restrict__ lin, uint32_t* spins) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long total = (long long)G.n_sim * G.rows * G.Wp;
-  if (i >= total) return;
-  const int wd = (int)(i % G.Wp);
-  const long long gr = i / G.Wp;
-  const int s = (int)(gr / G.rows), lr = (int)(gr % G.rows);
-  const int c = G.row0 + lr, br = lr + G.ghost;
-  const int ch = wd >> 4, t = wd & 15;
-  const uint32_t* L = lin + ((size_t)s * G.rows + lr) * (G.n / 32) + 32 * ch;
-  const int nb = chunk_bits(G, ch);
-  uint32_t e = 0, od = 0;
-  for (int b = 0; b < nb; b++) {
-    const uint32_t v = L[b] >> (2 * t);
-    e |= (v & 1u) << b;
-    od |= ((v >> 1) & 1u) << b;
+// 32 x 32 bit transpose across a warp: lane i holds row i (bit j = A[i][j]);
+// afterwards lane j holds column j (bit i = A[i][j]).  Five shuffle stages
+// swap the off-diagonal blocks of size 16, 8, 4, 2, 1.
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x) {
+  const int lane = threadIdx.x & 31;
+  uint32_t m = 0x0000FFFFu;
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1, m ^= m << s) {
+    const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, s);
+    x = (lane & s) ? (((y >> s) & m) | (x & ~m)) : ((x & m) | ((y & m) << s));
   }
-  spins[row_off(G, s, c & 1, br) + wd] = e;
-  spins[row_off(G, s, (c + 1) & 1, br) + wd] = od;
+  return x;
 }
 
-// Thread per linear uint32 word (s, lr, w): sites r = 32 w .. 32 w + 31.
-__global__ void k_to_linear(Geo G, const uint32_t* __restrict__ spins, uint32_t* lin) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long total = (long long)G.n_sim * G.rows * G.words;
-  if (i >= total) return;
-  const int w = (int)(i % G.words);
-  const long long gr = i / G.words;
-  const int s = (int)(gr / G.rows), lr = (int)(gr % G.rows);
+// Linear <-> colour-split, one warp per (replica, row, chunk): the chunk's
+// 32 linear words (1024 sites; lane b holds sites 32b..32b+31, bit k = site
+// 32b + k) and its 2 x 16 colour-split words (bit b of word (X, t) = site
+// 32b + 2t + p, p = (c+X)&1) are one 32 x 32 bit transpose: after it, lane
+// 2t + p holds word t of parity p.  Loads and stores are coalesced rows.
+__global__ void k_from_linear(Geo G, const uint32_t* __restrict__ lin, uint32_t* spins) {
+  // 32-bit index math (64-bit div/mod is emulated)
+  const unsigned wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const unsigned total = (unsigned)G.n_sim * (unsigned)G.rows * (unsigned)G.nch;
+  if (wg >= total) return;  // warp-uniform
+  const unsigned gr = G.nch == 1 ? wg : wg / (unsigned)G.nch;
+  const int ch = (int)(wg - gr * (unsigned)G.nch);
+  const unsigned sq = G.rows_div.div(gr);
+  const int s = (int)sq, lr = (int)(gr - sq * (unsigned)G.rows);
   const int c = G.row0 + lr, br = lr + G.ghost;
-  const int ch = w >> 5, b = w & 31;
-  const uint32_t* E = spins + row_off(G, s, c & 1, br) + ch * 16;
-  const uint32_t* Od = spins + row_off(G, s, (c + 1) & 1, br) + ch * 16;
-  uint32_t v = 0;
-#pragma unroll
-  for (int t = 0; t < 16; t++) v |= (((E[t] >> b) & 1u) << (2 * t)) | (((Od[t] >> b) & 1u) << (2 * t + 1));
-  lin[i] = v;
+  const int nb = chunk_bits(G, ch);
+  const uint32_t L = lane < nb ? lin[((size_t)s * G.rows + lr) * G.words + 32 * ch + lane] : 0u;
+  const uint32_t w = warp_transpose32(L);
+  const int t = lane >> 1, p = lane & 1;
+  spins[row_off(G, s, (c + p) & 1, br) + ch * 16 + t] = w;
+}
+
+__global__ void k_to_linear(Geo G, const uint32_t* __restrict__ spins, uint32_t* lin) {
+  const unsigned wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const unsigned total = (unsigned)G.n_sim * (unsigned)G.rows * (unsigned)G.nch;
+  if (wg >= total) return;  // warp-uniform
+  const unsigned gr = G.nch == 1 ? wg : wg / (unsigned)G.nch;
+  const int ch = (int)(wg - gr * (unsigned)G.nch);
+  const unsigned sq = G.rows_div.div(gr);
+  const int s = (int)sq, lr = (int)(gr - sq * (unsigned)G.rows);
+  const int c = G.row0 + lr, br = lr + G.ghost;
+  const int t = lane >> 1, p = lane & 1;
+  const uint32_t W = spins[row_off(G, s, (c + p) & 1, br) + ch * 16 + t];
+  const uint32_t L = warp_transpose32(W);
+  const int nb = chunk_bits(G, ch);
+  if (lane < nb) lin[((size_t)s * G.rows + lr) * G.words + 32 * ch + lane] = L;
 }
 
 __global__ void k_init_const(Geo G, uint32_t up, uint32_t* spins) {
@@ -181,40 +192,48 @@ __global__ void k_from_ref16(Geo G, const uint16_t* __restrict__ state, uint32_t
 // device: observables (engine.py:372-386)
 // ---------------------------------------------------------------------------
 
-__global__ void k_observe(Geo G, const uint32_t* __restrict__ spins, long long* ups, long long* unsat) {
-  const long long gr = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long total = (long long)G.n_sim * G.rows;
-  int s = -1;
+// Replica s = blockIdx.y; the CTAs along x stride over its rows x Wp words
+// (lanes take consecutive words of a row: coalesced), each thread sums its
+// words, the CTA reduces, and one atomic per CTA per quantity remains.
+__global__ void __launch_bounds__(256) k_observe(Geo G, const uint32_t* __restrict__ spins, long long* ups,
+                                                 long long* unsat) {
+  const int s = blockIdx.y;
+  const unsigned per = (unsigned)G.rows * (unsigned)G.Wp;
   uint32_t u = 0, b = 0;
-  if (gr < total) {
-    s = (int)(gr / G.rows);
-    const int lr = (int)(gr % G.rows);
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < per; i += gridDim.x * blockDim.x) {
+    const unsigned lr_u = i / (unsigned)G.Wp;
+    const int wd = (int)(i - lr_u * (unsigned)G.Wp);
+    const int lr = (int)lr_u;
     const int c = G.row0 + lr, br = lr + G.ghost;
     const int p = c & 1;  // red sites of row c sit at rows r with parity c&1
     int bu, bd;
     vert_rows(G, br, bu, bd);
-    const uint32_t* red = spins + row_off(G, s, 0, br);
     const uint32_t* blu = spins + row_off(G, s, 1, br);
-    const uint32_t* yu = spins + row_off(G, s, 1, bu);
-    const uint32_t* yd = spins + row_off(G, s, 1, bd);
-    for (int ch = 0; ch < G.nch; ch++) {
-      const uint32_t vm = chunk_mask(G, ch);
-      for (int t = 0; t < 16; t++) {
-        const int wd = ch * 16 + t;
-        const uint32_t o = red[wd], y0 = blu[wd];
-        u += __popc(o) + __popc(y0);
-        b += __popc((o ^ yu[wd]) & vm) + __popc((o ^ yd[wd]) & vm) + __popc((o ^ y0) & vm) +
-             __popc((o ^ h_second(G, blu, ch, t, p)) & vm);
-      }
-    }
+    const int ch = wd >> 4, t = wd & 15;
+    const uint32_t vm = chunk_mask(G, ch);
+    const uint32_t o = spins[row_off(G, s, 0, br) + wd], y0 = blu[wd];
+    const uint32_t yu = spins[row_off(G, s, 1, bu) + wd], yd = spins[row_off(G, s, 1, bd) + wd];
+    u += __popc(o) + __popc(y0);
+    b += __popc((o ^ yu) & vm) + __popc((o ^ yd) & vm) + __popc((o ^ y0) & vm) +
+         __popc((o ^ h_second(G, blu, ch, t, p)) & vm);
   }
-  // segmented warp reduction by replica
-  const unsigned lanes = __match_any_sync(0xFFFFFFFFu, s);
-  const uint32_t su = __reduce_add_sync(lanes, u), sb = __reduce_add_sync(lanes, b);
-  const int leader = __ffs(lanes) - 1;
-  if (s >= 0 && (int)(threadIdx.x & 31) == leader) {
-    atomicAdd(reinterpret_cast<unsigned long long*>(ups + s), (unsigned long long)su);
-    atomicAdd(reinterpret_cast<unsigned long long*>(unsat + s), (unsigned long long)sb);
+  u = __reduce_add_sync(0xFFFFFFFFu, u);
+  b = __reduce_add_sync(0xFFFFFFFFu, b);
+  __shared__ unsigned long long su[8], sb[8];
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    su[warp] = u;
+    sb[warp] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long tu = 0, tb = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
+      tu += su[w];
+      tb += sb[w];
+    }
+    atomicAdd(reinterpret_cast<unsigned long long*>(ups + s), tu);
+    atomicAdd(reinterpret_cast<unsigned long long*>(unsat + s), tb);
   }
 }
 
@@ -318,8 +337,8 @@ int msb_from_linear(const msb_geom* g, const uint64_t* lin, uint32_t* spins, voi
   if (int r = check_geom(g)) return r;
   if (!lin || !spins) return fail(MSB_ERR_ARG, "null buffer");
   const Geo G = make_geo(g);
-  const long long total = (long long)G.n_sim * G.rows * G.Wp;
-  k_from_linear<<<blocks_for(total, 256), 256, 0, as_stream(stream)>>>(
+  if (32LL * G.n_sim * G.rows * G.nch >= (1LL << 31)) return fail(MSB_ERR_UNSUPPORTED, "too many chunks for one launch");
+  k_from_linear<<<blocks_for(32LL * G.n_sim * G.rows * G.nch, 256), 256, 0, as_stream(stream)>>>(
       G, reinterpret_cast<const uint32_t*>(lin), spins);
   CUDA_TRY(cudaGetLastError());
   return MSB_OK;
@@ -329,8 +348,9 @@ int msb_to_linear(const msb_geom* g, const uint32_t* spins, uint64_t* lin, void*
   if (int r = check_geom(g)) return r;
   if (!lin || !spins) return fail(MSB_ERR_ARG, "null buffer");
   const Geo G = make_geo(g);
-  const long long total = (long long)G.n_sim * G.rows * G.words;
-  k_to_linear<<<blocks_for(total, 256), 256, 0, as_stream(stream)>>>(G, spins, reinterpret_cast<uint32_t*>(lin));
+  if (32LL * G.n_sim * G.rows * G.nch >= (1LL << 31)) return fail(MSB_ERR_UNSUPPORTED, "too many chunks for one launch");
+  k_to_linear<<<blocks_for(32LL * G.n_sim * G.rows * G.nch, 256), 256, 0, as_stream(stream)>>>(
+      G, spins, reinterpret_cast<uint32_t*>(lin));
   CUDA_TRY(cudaGetLastError());
   return MSB_OK;
 }
@@ -361,8 +381,11 @@ int msb_observe(const msb_geom* g, const uint32_t* spins, int64_t* ups, int64_t*
   if (int r = check_geom(g)) return r;
   if (!spins || !ups || !unsat) return fail(MSB_ERR_ARG, "null buffer");
   const Geo G = make_geo(g);
-  const long long total = (long long)g->n_sim * g->rows;
-  k_observe<<<blocks_for(total, 256), 256, 0, as_stream(stream)>>>(G, spins, reinterpret_cast<long long*>(ups),
+  const long long per = (long long)g->rows * G.Wp;  // words per replica
+  if (per >= (1LL << 32) || g->n_sim > 65535) return fail(MSB_ERR_UNSUPPORTED, "observe launch too large");
+  // ~4 words per thread, at most 64 CTAs per replica
+  const dim3 grid((unsigned)std::max(1LL, std::min(64LL, (per + 1023) / 1024)), (unsigned)g->n_sim);
+  k_observe<<<grid, 256, 0, as_stream(stream)>>>(G, spins, reinterpret_cast<long long*>(ups),
                                                                     reinterpret_cast<long long*>(unsat));
   CUDA_TRY(cudaGetLastError());
   return MSB_OK;

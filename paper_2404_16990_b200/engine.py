@@ -593,6 +593,10 @@ class Engine:
 
     def synchronize(self) -> None:
         self._stream.synchronize()
+        if hasattr(self, "_io"):
+            self._in_stream.synchronize()
+            self._out_stream.synchronize()
+            self._host_out.clear()
 
     @property
     def flips(self) -> int:
@@ -640,58 +644,113 @@ class Engine:
         """Bytes of all replicas' lattices as bit-packed linear sites."""
         return self.n_sim * self.dims.sites // 8
 
+    def _io_slot(self):
+        """Current of two (input, output) device staging buffers for packed
+        host I/O.  Copies in and out run on two copy streams (so a load never
+        queues behind an earlier store's wait for the sweeps), ordered against
+        the engine's stream by events."""
+        torch = _torch()
+        if not hasattr(self, "_io"):
+            words = self.packed_nbytes() // 8
+            with torch.cuda.device(self.device):
+                self._in_stream = torch.cuda.Stream(device=self.device)
+                self._out_stream = torch.cuda.Stream(device=self.device)
+                bufs = [(torch.empty(words, dtype=torch.int64, device=self.device),
+                         torch.empty(words, dtype=torch.int64, device=self.device)) for _ in range(2)]
+            self._io = [{"in": i, "out": o, "in_free": None, "out_full": None} for i, o in bufs]
+            self._io_next = 0
+            self._host_out = {}  # host buffer address -> event of the pending copy into it
+        return self._io[self._io_next]
+
     def load_packed(self, src) -> None:
         """Replace every replica's lattice from bit-packed host (or device)
         memory: bit i%8 of byte i//8 of replica s is site i = c*n + r
-        (np.packbits(lattice > 0, bitorder="little")).  Pinned torch host
-        tensors are copied asynchronously on the engine's stream."""
+        (np.packbits(lattice > 0, bitorder="little")).  A pinned host tensor
+        is copied on the engine's input copy stream into a double-buffered
+        staging area, so the copy overlaps device work already queued (the
+        previous sweeps); the engine's stream waits only for this copy (and
+        the copy waits for any pending ``store_packed`` into ``src``)."""
         torch = _torch()
         self._push_host_edits()
         if isinstance(src, np.ndarray):
             src = torch.from_numpy(np.ascontiguousarray(src).view(np.uint8).reshape(-1))
         if src.numel() * src.element_size() != self.packed_nbytes():
             raise ValueError(f"expected {self.packed_nbytes()} bytes of packed lattices")
-        with torch.cuda.stream(self._stream):
-            if src.device.type != "cuda":
-                if not hasattr(self, "_lin_buf") or self._lin_buf.numel() != self.packed_nbytes() // 8:
-                    self._lin_buf = torch.empty(self.packed_nbytes() // 8, dtype=torch.int64, device=self.device)
-                self._lin_buf.view(torch.uint8).copy_(src.view(torch.uint8).reshape(-1), non_blocking=True)
-                dev = self._lin_buf
-            else:
-                dev = src
-        call("msb_from_linear", ctypes.byref(self._g), _p(dev), _p(self._spins), self._cs)
+        if src.device.type == "cuda":
+            call("msb_from_linear", ctypes.byref(self._g), _p(src), _p(self._spins), self._cs)
+            self._touch()
+            return
+        slot = self._io_slot()
+        with torch.cuda.stream(self._in_stream):
+            if slot["in_free"] is not None:          # its last reader (msb_from_linear) is done
+                self._in_stream.wait_event(slot["in_free"])
+            pending = self._host_out.pop(src.data_ptr(), None)
+            if pending is not None:                  # src is still being written by a store
+                self._in_stream.wait_event(pending)
+            slot["in"].view(torch.uint8).copy_(src.view(torch.uint8).reshape(-1), non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(self._in_stream)
+        self._stream.wait_event(ready)
+        call("msb_from_linear", ctypes.byref(self._g), _p(slot["in"]), _p(self._spins), self._cs)
+        free = torch.cuda.Event()
+        free.record(self._stream)
+        slot["in_free"] = free
         self._touch()
 
     def store_packed(self, dst) -> None:
         """Write every replica's lattice, bit-packed as in ``load_packed``,
-        into ``dst`` (pinned host tensor: asynchronous; call ``synchronize``)."""
+        into ``dst``.  A pinned host destination is filled on the engine's
+        output copy stream (asynchronous: ``synchronize()`` before reading
+        it); the engine's stream continues with the next sweeps meanwhile."""
         torch = _torch()
         self._push_host_edits()
         if dst.numel() * dst.element_size() != self.packed_nbytes():
             raise ValueError(f"expected {self.packed_nbytes()} bytes of packed lattices")
-        with torch.cuda.stream(self._stream):
-            if not hasattr(self, "_lin_buf") or self._lin_buf.numel() != self.packed_nbytes() // 8:
-                self._lin_buf = torch.empty(self.packed_nbytes() // 8, dtype=torch.int64, device=self.device)
-        call("msb_to_linear", ctypes.byref(self._g), _p(self._spins), _p(self._lin_buf), self._cs)
-        with torch.cuda.stream(self._stream):
-            dst.view(torch.uint8).reshape(-1).copy_(self._lin_buf.view(torch.uint8), non_blocking=True)
+        slot = self._io_slot()
+        self._io_next ^= 1
+        if slot["out_full"] is not None:             # its previous copy-out is done
+            self._stream.wait_event(slot["out_full"])
+        call("msb_to_linear", ctypes.byref(self._g), _p(self._spins), _p(slot["out"]), self._cs)
+        written = torch.cuda.Event()
+        written.record(self._stream)
+        with torch.cuda.stream(self._out_stream):
+            self._out_stream.wait_event(written)
+            dst.view(torch.uint8).reshape(-1).copy_(slot["out"].view(torch.uint8), non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(self._out_stream)
+        slot["out_full"] = done
+        if dst.device.type != "cuda":
+            self._host_out[dst.data_ptr()] = done
 
     def observe_async(self, ups_out, unsat_out) -> None:
         """Enqueue the integer observables (ups, unsatisfied bonds per replica)
-        into pinned host int64 tensors without synchronising."""
+        into pinned host int64 tensors without synchronising.  The copies run
+        on the output copy stream, so the engine's stream never waits behind
+        a large lattice copy in the copy engine."""
         torch = _torch()
         self._push_host_edits()
+        self._io_slot()
+        if getattr(self, "_obs_copied", None) is not None:  # previous copy-out of _obs done
+            self._stream.wait_event(self._obs_copied)
         with torch.cuda.stream(self._stream):
             self._obs.zero_()
         call("msb_observe", ctypes.byref(self._g), _p(self._spins), _p(self._obs[: self.n_sim]),
              _p(self._obs[self.n_sim:]), self._cs)
-        with torch.cuda.stream(self._stream):
+        ready = torch.cuda.Event()
+        ready.record(self._stream)
+        with torch.cuda.stream(self._out_stream):
+            self._out_stream.wait_event(ready)
             ups_out.copy_(self._obs[: self.n_sim], non_blocking=True)
             unsat_out.copy_(self._obs[self.n_sim:], non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(self._out_stream)
+        self._obs_copied = done
 
     def _observe(self):
         self._push_host_edits()
         if self._obs_ver != self._ver:
+            if getattr(self, "_obs_copied", None) is not None:  # an observe_async copy-out may be pending
+                self._stream.wait_event(self._obs_copied)
             with _torch().cuda.stream(self._stream):
                 self._obs.zero_()
             ups = self._obs[: self.n_sim]
