@@ -130,7 +130,7 @@ __device__ __forceinline__ uint32_t flip_word(const FlipArgs& a, bool generic, u
 // word); horizontal ones the other colour's row c at sites i and i+-1
 // (h_second).  COHERENT: other-colour words were written earlier in the same
 // kernel by other SMs, so read them through L2 (ld.global.cg).
-template <bool GENERIC, bool COHERENT>
+template <bool GENERIC, bool COHERENT, bool PUSH = false>
 __device__ __forceinline__ unsigned flip_quad_at(const FlipArgs& a, int s, int lr, unsigned qq, int X) {
   const Geo& G = a.G;
   const int c = G.row0 + lr, br = lr + G.ghost;
@@ -195,10 +195,12 @@ __device__ __forceinline__ unsigned flip_quad_at(const FlipArgs& a, int s, int l
   }
   const uint4 out = make_uint4(res[0], res[1], res[2], res[3]);
   *reinterpret_cast<uint4*>(own + w0) = out;
-  if (a.up_spins && lr == 0)  // our first row is the ghost below of the slab above
-    *reinterpret_cast<uint4*>(a.up_spins + (((size_t)s * 2 + X) * a.up_R + a.up_R - 1) * G.Wp + w0) = out;
-  if (a.down_spins && lr == G.rows - 1)  // our last row is the ghost above of the slab below
-    *reinterpret_cast<uint4*>(a.down_spins + ((size_t)s * 2 + X) * a.down_R * G.Wp + w0) = out;
+  if (PUSH) {
+    if (lr == 0)  // our first row is the ghost below of the slab above
+      *reinterpret_cast<uint4*>(a.up_spins + (((size_t)s * 2 + X) * a.up_R + a.up_R - 1) * G.Wp + w0) = out;
+    if (lr == G.rows - 1)  // our last row is the ghost above of the slab below
+      *reinterpret_cast<uint4*>(a.down_spins + ((size_t)s * 2 + X) * a.down_R * G.Wp + w0) = out;
+  }
   return cnt;
 }
 
@@ -214,7 +216,7 @@ __device__ __forceinline__ unsigned flip_quad(const FlipArgs& a, unsigned i, int
 // A consumer warp's contiguous run of quads [i0, i1) of one colour, walked
 // with incremental (replica, row, quad) bookkeeping: lanes take consecutive
 // quads, each step advances all lanes by 32 quads (dr rows + dq quads).
-template <bool COHERENT>
+template <bool COHERENT, bool PUSH = false>
 __device__ __forceinline__ unsigned flip_run(const FlipArgs& a, unsigned i0, unsigned i1, int X) {
   const Geo& G = a.G;
   const unsigned quads = (unsigned)G.Wp >> 2;
@@ -224,7 +226,7 @@ __device__ __forceinline__ unsigned flip_run(const FlipArgs& a, unsigned i0, uns
   const unsigned dr = G.quads_div.div(32u), dq = 32u - dr * quads;
   unsigned cnt = 0;
   for (unsigned i = i0; i < i1; i += 32) {
-    cnt += flip_quad_at<false, COHERENT>(a, s, lr, qq, X);
+    cnt += flip_quad_at<false, COHERENT, PUSH>(a, s, lr, qq, X);
     qq += dq;
     lr += (int)dr;
     if (qq >= quads) {

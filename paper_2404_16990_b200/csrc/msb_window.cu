@@ -299,7 +299,7 @@ __device__ __forceinline__ void halo_gate(const HaloArgs& h, unsigned* work, int
 // production); the other warps flip slots [first, first + count) of `cur`
 // (red, barrier, blue, barrier, ...).  With a halo (slabs) every phase is
 // gated by halo_gate and all neighbour reads go through L2.
-template <int SRC, bool FULL>
+template <int SRC, bool FULL, bool HALO>
 __global__ void __launch_bounds__(kRngThreads, 1) k_win(const WinArgs wa, const FlipArgs fa0, const HaloArgs ha,
                                                         const uint32_t* cur, int first, int count, int pwarps) {
   extern __shared__ uint4 jt[];
@@ -323,14 +323,15 @@ __global__ void __launch_bounds__(kRngThreads, 1) k_win(const WinArgs wa, const 
     unsigned cnt = 0;
     const bool leader = threadIdx.x == pwarps * 32;
     const bool gpu_leader = leader && blockIdx.x == 0;
-    if (ha.on) halo_gate(ha, wa.work, -1, true, nwc * 32, leader, gpu_leader);
+    if (HALO) halo_gate(ha, wa.work, -1, true, nwc * 32, leader, gpu_leader);
     for (int i = 0; i < 2 * count; i++) {
       const int X = i & 1;
       fa.planes = cur + (size_t)(first + (i >> 1)) * wa.slot_words;
-      if (i == 0 && !ha.on) cnt += flip_run<false>(fa, i0, hi, X);
+      if (HALO) cnt += flip_run<true, true>(fa, i0, hi, X);
+      else if (i == 0) cnt += flip_run<false>(fa, i0, hi, X);
       else cnt += flip_run<true>(fa, i0, hi, X);
       const bool more = i + 1 < 2 * count;
-      if (ha.on) {
+      if (HALO) {
         __threadfence_system();  // this thread's halo pushes (if any) before the neighbours are told
         halo_gate(ha, wa.work, i, more, nwc * 32, leader, gpu_leader);
       } else if (more) {
@@ -548,11 +549,14 @@ int msb_window_sweep(const msb_geom* g, const msb_sweep_params* p, int32_t S, in
   }
   const bool philox = p->rng == MSB_RNG_PHILOX;
   const bool full = (wa.G.words % 32) == 0;
-  static std::once_flag o1, o2, o3;
-  static cudaError_t e1, e2, e3;
-  if (int r = set_smem_attr(k_win<kSrcXoshiro, true>, o1, e1)) return r;
-  if (int r = set_smem_attr(k_win<kSrcXoshiro, false>, o2, e2)) return r;
-  if (int r = set_smem_attr(k_win<kSrcPhilox, false>, o3, e3)) return r;
+  static std::once_flag o[6];
+  static cudaError_t e[6];
+  if (int r = set_smem_attr(k_win<kSrcXoshiro, true, false>, o[0], e[0])) return r;
+  if (int r = set_smem_attr(k_win<kSrcXoshiro, false, false>, o[1], e[1])) return r;
+  if (int r = set_smem_attr(k_win<kSrcPhilox, false, false>, o[2], e[2])) return r;
+  if (int r = set_smem_attr(k_win<kSrcXoshiro, true, true>, o[3], e[3])) return r;
+  if (int r = set_smem_attr(k_win<kSrcXoshiro, false, true>, o[4], e[4])) return r;
+  if (int r = set_smem_attr(k_win<kSrcPhilox, false, true>, o[5], e[5])) return r;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)sms);
   cfg.blockDim = dim3(kRngThreads);
@@ -563,9 +567,18 @@ int msb_window_sweep(const msb_geom* g, const msb_sweep_params* p, int32_t S, in
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = count > 0 ? 1 : 0;  // grid barriers only among consumers
-  if (philox) CUDA_TRY(cudaLaunchKernelEx(&cfg, k_win<kSrcPhilox, false>, wa, fa, ha, cur, first, count, pwarps));
-  else if (full) CUDA_TRY(cudaLaunchKernelEx(&cfg, k_win<kSrcXoshiro, true>, wa, fa, ha, cur, first, count, pwarps));
-  else CUDA_TRY(cudaLaunchKernelEx(&cfg, k_win<kSrcXoshiro, false>, wa, fa, ha, cur, first, count, pwarps));
+#define MSB_LAUNCH_WIN(SRC, FULL, HALO) \
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, k_win<SRC, FULL, HALO>, wa, fa, ha, cur, first, count, pwarps))
+  if (ha.on) {
+    if (philox) MSB_LAUNCH_WIN(kSrcPhilox, false, true);
+    else if (full) MSB_LAUNCH_WIN(kSrcXoshiro, true, true);
+    else MSB_LAUNCH_WIN(kSrcXoshiro, false, true);
+  } else {
+    if (philox) MSB_LAUNCH_WIN(kSrcPhilox, false, false);
+    else if (full) MSB_LAUNCH_WIN(kSrcXoshiro, true, false);
+    else MSB_LAUNCH_WIN(kSrcXoshiro, false, false);
+  }
+#undef MSB_LAUNCH_WIN
   return MSB_OK;
 }
 
