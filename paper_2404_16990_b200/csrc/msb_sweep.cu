@@ -395,6 +395,7 @@ int rng_planes(const msb_geom* g, const msb_sweep_params* p, int colour, uint32_
 // into `next`, one cooperative launch (FERRO/ANTI whole lattices).
 int fused_sweep(const msb_geom* g, const msb_sweep_params* p, uint32_t* spins, uint32_t* states, const uint32_t* cur,
                 uint32_t* next, uint64_t* flips, cudaStream_t st) {
+  if (int r = check_flip_extent(g, p->n_planes)) return r;
   RngArgs ra;
   fill_rng_args(ra, g, p, -1, states, nullptr, next);
   FlipArgs fa;

@@ -138,18 +138,24 @@ __device__ __forceinline__ unsigned flip_quad_at(const FlipArgs& a, int s, int l
   const int w0 = ch * 16 + t0;
   int bu, bd;
   vert_rows(G, br, bu, bd);
-  uint32_t* own = a.spins + row_off(G, s, X, br);
-  const uint32_t* yc = a.spins + row_off(G, s, 1 - X, br);
+  // 32-bit word offsets (buffers < 2^32 words, checked by check_flip_extent):
+  // the 64-bit offset chains were a third of the quad's instructions
+  const unsigned R = (unsigned)G.R, Wp = (unsigned)G.Wp;
+  const unsigned oth = (unsigned)s * 2u + (unsigned)(1 - X);
+  uint32_t* own = a.spins + (((unsigned)s * 2u + (unsigned)X) * R + (unsigned)br) * Wp;
+  const uint32_t* yc = a.spins + (oth * R + (unsigned)br) * Wp;
   auto ld4 = [](const uint32_t* q) {
     return COHERENT ? __ldcg(reinterpret_cast<const uint4*>(q)) : __ldg(reinterpret_cast<const uint4*>(q));
   };
   auto ld1 = [](const uint32_t* q) { return COHERENT ? __ldcg(q) : __ldg(q); };
   const uint4 O = *reinterpret_cast<const uint4*>(own + w0);
   const uint4 Y = ld4(yc + w0);
-  const uint4 U = ld4(a.spins + row_off(G, s, 1 - X, bu) + w0);
-  const uint4 D = ld4(a.spins + row_off(G, s, 1 - X, bd) + w0);
-  const size_t pstride = (size_t)G.n_sim * G.rows * G.Wp;
-  const uint32_t* pl = a.planes + plane_off(G, a.np, X, 0, s, lr) + w0;
+  const uint4 U = ld4(a.spins + ((oth * R + (unsigned)bu) * Wp + (unsigned)w0));
+  const uint4 D = ld4(a.spins + ((oth * R + (unsigned)bd) * Wp + (unsigned)w0));
+  const unsigned pstride = (unsigned)G.n_sim * (unsigned)G.rows * Wp;
+  const uint32_t* pl =
+      a.planes + ((((unsigned)X * (unsigned)a.np) * (unsigned)G.n_sim + (unsigned)s) * (unsigned)G.rows +
+                  (unsigned)lr) * Wp + (unsigned)w0;
   uint4 P4 = make_uint4(0, 0, 0, 0), P8 = make_uint4(0, 0, 0, 0);
   if (!GENERIC) {
     P4 = __ldg(reinterpret_cast<const uint4*>(pl));
@@ -302,9 +308,20 @@ __global__ void __launch_bounds__(256) k_flip(const FlipArgs a) {
   add_flips(a.flips, cnt);
 }
 
+// The flip path indexes spins and planes with 32-bit word offsets.
+inline int check_flip_extent(const msb_geom* g, int n_planes) {
+  const Geo G = make_geo(g);
+  const long long spin_words = (long long)G.n_sim * 2 * G.R * G.Wp;
+  const long long plane_words = 2LL * std::max(n_planes, 1) * G.n_sim * G.rows * G.Wp;
+  if (spin_words >= (1LL << 32) || plane_words >= (1LL << 32))
+    return fail(MSB_ERR_UNSUPPORTED, "spin or plane buffer of 2^32 words or more: split the replicas");
+  return MSB_OK;
+}
+
 // Launch k_flip for colour `colour` of planes `planes`.
 inline int flip(const msb_geom* g, const msb_sweep_params* p, int colour, uint32_t* spins, const uint32_t* planes,
          uint64_t* flips, cudaStream_t st) {
+  if (int r = check_flip_extent(g, p->n_planes)) return r;
   const Geo G = make_geo(g);
   FlipArgs a;
   fill_flip_args(a, g, p, colour, spins, planes, flips);

@@ -489,6 +489,8 @@ int msb_window_sweep(const msb_geom* g, const msb_sweep_params* p, int32_t S, in
   if (first < 0 || count < 0 || first + count > S) return fail(MSB_ERR_ARG, "slots [first, first+count) outside the window");
   if (count > 0 && (!spins || !cur || !flips)) return fail(MSB_ERR_ARG, "null buffer");
   if (count > 0 && g->ghost && !halo) return fail(MSB_ERR_ARG, "slab windows flip with an msb_halo (in-kernel exchange)");
+  if (count > 0)
+    if (int r = check_flip_extent(g, 2)) return r;
   if (halo && !g->ghost) return fail(MSB_ERR_ARG, "msb_halo needs a slab geometry (ghost = 1)");
   if (halo && (!halo->up_spins || !halo->down_spins || !halo->up_flags || !halo->down_flags || !halo->my_flags ||
                halo->up_R < 4 || halo->down_R < 4))
