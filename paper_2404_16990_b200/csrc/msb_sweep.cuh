@@ -92,6 +92,10 @@ struct FlipArgs {
   uint32_t* up_spins;
   uint32_t* down_spins;
   int up_R, down_R;
+  // band walk (flip_band_run): rows of QPR <= 32 quads (QPR | 32); a warp
+  // group covers band_gb bands of band_h rows, lanes = (band, quad).  0: off.
+  int band_h, band_gb;
+  unsigned band_groups;  // groups per colour phase (all replicas)
 };
 
 constexpr int kFlipSlots = 256;
@@ -222,6 +226,94 @@ __device__ __forceinline__ unsigned flip_quad(const FlipArgs& a, unsigned i, int
 // A consumer warp's contiguous run of quads [i0, i1) of one colour, walked
 // with incremental (replica, row, quad) bookkeeping: lanes take consecutive
 // quads, each step advances all lanes by 32 quads (dr rows + dq quads).
+// FERRO/ANTI flip of one colour over band groups [g0, g1) (one warp): each
+// lane walks band_h consecutive rows of one quad column.  The other colour's
+// rows above and at the current row stay in registers (U, Y), so a step loads
+// the row below (D), the own quad (O) and the two plane quads; the horizontal
+// neighbour word at the quad edge comes from the lane holding it (shuffle),
+// including the one-bit chunk wraps of the interleaved layout.
+template <bool COHERENT, bool PUSH = false>
+__device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0, unsigned g1, int X) {
+  const Geo& G = a.G;
+  const int lane = threadIdx.x & 31;
+  const int qpr = G.Wp >> 2;             // quads per row (divides 32)
+  const int H = a.band_h, gb = a.band_gb;
+  const int bi = lane / qpr, q = lane - bi * qpr, base = bi * qpr;
+  const int ch = q >> 2, t0 = 4 * (q & 3), w0 = q * 4;
+  const int vb = chunk_bits(G, ch);
+  const uint32_t vm = chunk_mask(G, ch);
+  const int lastbits = chunk_bits(G, G.nch - 1);
+  const unsigned R = (unsigned)G.R, Wp = (unsigned)G.Wp;
+  const unsigned pstride = (unsigned)G.n_sim * (unsigned)G.rows * Wp;
+  const unsigned groups_per_sim = (unsigned)G.rows / (unsigned)(gb * H);
+  // shuffle sources (fixed per lane): next quad, this chunk's first and last
+  // quads, previous quad (the previous chunk's last / the row's last quad)
+  const int s_next = base + (q + 1) % qpr, s_first = base + (q & ~3), s_last = base + (q | 3),
+            s_prev = base + (q + qpr - 1) % qpr;
+  auto ld4 = [](const uint32_t* p) {
+    return COHERENT ? __ldcg(reinterpret_cast<const uint4*>(p)) : __ldg(reinterpret_cast<const uint4*>(p));
+  };
+  unsigned cnt = 0;
+  for (unsigned g = g0; g < g1; g++) {
+    const unsigned s = g / groups_per_sim;
+    const int lr0 = (int)(g - s * groups_per_sim) * gb * H + bi * H;  // this lane's band
+    const uint32_t* ybase = a.spins + ((s * 2u + (unsigned)(1 - X)) * R) * Wp + w0;
+    uint32_t* obase = a.spins + ((s * 2u + (unsigned)X) * R) * Wp + w0;
+    const uint32_t* pbase = a.planes + ((((unsigned)X * (unsigned)a.np) * (unsigned)G.n_sim + s) * (unsigned)G.rows) * Wp + w0;
+    int br = lr0 + G.ghost, bu, bd;
+    vert_rows(G, br, bu, bd);
+    uint4 U = ld4(ybase + (unsigned)bu * Wp), Y = ld4(ybase + (unsigned)br * Wp);
+    for (int h = 0; h < H; h++) {
+      const int lr = lr0 + h;
+      if (h > 0) {
+        br = lr + G.ghost;
+        vert_rows(G, br, bu, bd);
+      }
+      const uint4 D = ld4(ybase + (unsigned)bd * Wp);
+      const uint4 O = *reinterpret_cast<const uint4*>(obase + (unsigned)br * Wp);
+      const uint4 P4 = __ldg(reinterpret_cast<const uint4*>(pbase + (unsigned)lr * Wp));
+      const uint4 P8 = __ldg(reinterpret_cast<const uint4*>(pbase + pstride + (unsigned)lr * Wp));
+      const int p = (G.row0 + lr + X) & 1;  // warp-uniform (H even, bands even-aligned)
+      uint32_t edge;
+      if (p) {  // word t0+4, or the chunk wrap: (first word >> 1) | (next chunk's bit 0 << vb-1)
+        const uint32_t xa = __shfl_sync(0xFFFFFFFFu, Y.x, s_next);
+        const uint32_t xb = __shfl_sync(0xFFFFFFFFu, Y.x, s_first);
+        edge = (q & 3) != 3 ? xa : ((xb >> 1) | ((xa & 1u) << (vb - 1)));
+      } else {  // word t0-1, or the chunk wrap: ((last word << 1) | carry) & mask
+        const uint32_t wa = __shfl_sync(0xFFFFFFFFu, Y.w, s_prev);
+        const uint32_t wb = __shfl_sync(0xFFFFFFFFu, Y.w, s_last);
+        const uint32_t carry = ch > 0 ? (wa >> 31) : ((wa >> (lastbits - 1)) & 1u);
+        edge = (q & 3) != 0 ? wa : (((wb << 1) | carry) & vm);
+      }
+      const uint32_t y[4] = {Y.x, Y.y, Y.z, Y.w};
+      const uint32_t o[4] = {O.x, O.y, O.z, O.w};
+      const uint32_t u4[4] = {U.x, U.y, U.z, U.w};
+      const uint32_t d4[4] = {D.x, D.y, D.z, D.w};
+      const uint32_t a4[4] = {P4.x, P4.y, P4.z, P4.w};
+      const uint32_t a8[4] = {P8.x, P8.y, P8.z, P8.w};
+      uint32_t res[4];
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const uint32_t n4 = p ? (k < 3 ? y[k + 1] : edge) : (k > 0 ? y[k - 1] : edge);
+        const uint32_t f = flip_word(a, false, o[k], u4[k], d4[k], y[k], n4, nullptr, 0, a4[k], a8[k]) & vm;
+        res[k] = o[k] ^ f;
+        cnt += __popc(f);
+      }
+      const uint4 out = make_uint4(res[0], res[1], res[2], res[3]);
+      *reinterpret_cast<uint4*>(obase + (unsigned)br * Wp) = out;
+      if (PUSH) {
+        if (lr == 0)
+          *reinterpret_cast<uint4*>(a.up_spins + (((size_t)s * 2 + X) * a.up_R + a.up_R - 1) * Wp + w0) = out;
+        if (lr == G.rows - 1)
+          *reinterpret_cast<uint4*>(a.down_spins + ((size_t)s * 2 + X) * a.down_R * Wp + w0) = out;
+      }
+      U = Y;
+      Y = D;
+    }
+  }
+  return cnt;
+}
+
 template <bool COHERENT, bool PUSH = false>
 __device__ __forceinline__ unsigned flip_run(const FlipArgs& a, unsigned i0, unsigned i1, int X) {
   const Geo& G = a.G;
@@ -281,6 +373,21 @@ inline void fill_flip_args(FlipArgs& a, const msb_geom* g, const msb_sweep_param
   std::memcpy(a.code_plane, p->code_plane, 16);
   a.up_spins = a.down_spins = nullptr;
   a.up_R = a.down_R = 0;
+  // band walk geometry: lanes cover whole rows (QPR quads, QPR | 32), bands
+  // of H rows never cross a replica (H | rows / gb), H even (uniform parity)
+  a.band_h = a.band_gb = 0;
+  a.band_groups = 0;
+  const int qpr = a.G.Wp / 4;
+  if (p->mode != MSB_MODE_GENERIC && qpr <= 32 && 32 % qpr == 0) {
+    const int gb = 32 / qpr;
+    for (int h = 16; h >= 2; h >>= 1)
+      if (g->rows % (gb * h) == 0) {
+        a.band_h = h;
+        a.band_gb = gb;
+        a.band_groups = (unsigned)((long long)g->n_sim * g->rows / (gb * h));
+        break;
+      }
+  }
 }
 
 // Flip warps per 32-warp CTA of a fused launch: 6 measured best for

@@ -303,20 +303,30 @@ template <int SRC, bool FULL, bool HALO>
 __global__ void __launch_bounds__(kRngThreads, 1) k_win(const WinArgs wa, const FlipArgs fa0, const HaloArgs ha,
                                                         const uint32_t* cur, int first, int count, int pwarps) {
   extern __shared__ uint4 jt[];
+#ifdef MSB_TRACE
+  MSB_TRACE_PUT(0, gtimer());
+#endif
   if (SRC == kSrcXoshiro && pwarps > 0) {
     for (int i = threadIdx.x; i < kJumpWords / 4; i += blockDim.x) jt[i] = wa.jump[i];
     __syncthreads();
   }
   const int warp = threadIdx.x >> 5;
   const unsigned total_warps = gridDim.x * (blockDim.x >> 5);
+#ifdef MSB_TRACE
+  MSB_TRACE_PUT(1, gtimer());
+  MSB_TRACE_PUT(3, warp < pwarps ? 0ull : (1ull << 63));
+#endif
   if (warp < pwarps) {
     win_produce<SRC, FULL>(wa, jt, warp, pwarps);
   } else if (count > 0) {
     const int nwc = (kRngThreads >> 5) - pwarps;
-    const unsigned total = (unsigned)fa0.G.n_sim * (unsigned)fa0.G.rows * ((unsigned)fa0.G.Wp >> 2);  // quads
     const unsigned nc = gridDim.x * nwc;
     const unsigned cw = (warp - pwarps) * gridDim.x + blockIdx.x;
-    const unsigned per = ((total + nc - 1) / nc + 31) & ~31u;
+    // band walk: contiguous band groups per warp; else quads, lanes interleaved
+    const bool band = fa0.band_h > 0;
+    const unsigned total = band ? fa0.band_groups
+                                : (unsigned)fa0.G.n_sim * (unsigned)fa0.G.rows * ((unsigned)fa0.G.Wp >> 2);
+    const unsigned per = band ? (total + nc - 1) / nc : (((total + nc - 1) / nc + 31) & ~31u);
     const unsigned lo = min(total, cw * per), hi = min(total, lo + per);
     const unsigned i0 = lo + (threadIdx.x & 31);
     FlipArgs fa = fa0;
@@ -327,19 +337,31 @@ __global__ void __launch_bounds__(kRngThreads, 1) k_win(const WinArgs wa, const 
     for (int i = 0; i < 2 * count; i++) {
       const int X = i & 1;
       fa.planes = cur + (size_t)(first + (i >> 1)) * wa.slot_words;
-      if (HALO) cnt += flip_run<true, true>(fa, i0, hi, X);
-      else if (i == 0) cnt += flip_run<false>(fa, i0, hi, X);
-      else cnt += flip_run<true>(fa, i0, hi, X);
+      if (band) {
+        if (HALO) cnt += flip_band_run<true, true>(fa, lo, hi, X);
+        else if (i == 0) cnt += flip_band_run<false>(fa, lo, hi, X);
+        else cnt += flip_band_run<true>(fa, lo, hi, X);
+      } else {
+        if (HALO) cnt += flip_run<true, true>(fa, i0, hi, X);
+        else if (i == 0) cnt += flip_run<false>(fa, i0, hi, X);
+        else cnt += flip_run<true>(fa, i0, hi, X);
+      }
       const bool more = i + 1 < 2 * count;
       if (HALO) {
         __threadfence_system();  // this thread's halo pushes (if any) before the neighbours are told
         halo_gate(ha, wa.work, i, more, nwc * 32, leader, gpu_leader);
       } else if (more) {
+#ifdef MSB_TRACE
+        if (i == 0) MSB_TRACE_PUT(6, gtimer());  // first phase done (before its barrier)
+#endif
         consumer_barrier(wa.work + 1, gridDim.x * (unsigned)(i + 1), nwc * 32, leader);
       }
     }
     add_flips(fa.flips, cnt);
   }
+#ifdef MSB_TRACE
+  MSB_TRACE_PUT(2, gtimer());
+#endif
   finish_warp(wa.work, total_warps);
 }
 
@@ -417,6 +439,15 @@ void fill_win_args(WinArgs& w, const msb_geom* g, const msb_sweep_params* p, int
 using namespace msbk;
 
 extern "C" {
+
+#ifdef MSB_TRACE
+int msb_debug_trace_win(uint64_t* host_out, int32_t n) {
+  if (n > kTraceWarps * 8) n = kTraceWarps * 8;
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpyFromSymbol(host_out, g_trace, (size_t)n * 8));
+  return MSB_OK;
+}
+#endif
 
 int32_t msb_window_parts(const msb_geom* g, int32_t S) {
   long long np = 0;
