@@ -133,3 +133,21 @@ def test_packed_io_round_trip_and_hazards():
     for k in range(3):
         assert (bufs[k].numpy() == host[k]).all(), k
     assert pipe.flips == ref.flips
+
+
+@pytest.mark.parametrize("m,n,n_sim,stream", [
+    (16, 96, 2, "xoshiro"),     # 4 quads per row, 3-bit chunk (partial): band walk
+    (32, 160, 1, "philox"),     # 5-bit chunk, band walk
+    (32, 2048, 2, "xoshiro"),   # 8 quads per row (2 chunks)
+    (16, 4096, 1, "xoshiro"),   # 16 quads per row
+    (8, 8192, 1, "philox"),     # 32 quads per row, one band per warp
+    (20, 128, 3, "xoshiro"),    # rows do not split into even bands: quad walker
+])
+def test_band_walk_geometries(m, n, n_sim, stream):
+    """The window consumers' band walk (edge words by shuffle, chunk wraps)
+    and its quad-walker fallback, against the oracle."""
+    temps = list(np.linspace(1.9, 2.9, n_sim))
+    e, o = _pair(m, n, temps, 13, stream=stream, window=4)
+    e._sweeps(9)
+    o.sweep(9)
+    _same(e, o)
