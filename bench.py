@@ -40,7 +40,8 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "spin flip attempts/sec (aggregate, device-timed)"
 UNIT = "attempts/s"
-A_INT = 27.5      # int32 ops per attempt, reference xoshiro256++ stream
+A_INT_XOSHIRO = 27.5  # int32 ops per attempt, reference xoshiro256++ stream
+A_INT_PHILOX = 13.5   # counter-based Philox4x32-10 stream
 A_BYTES = 0.375   # algorithmic HBM bytes per attempt
 L2_FLUSH_BYTES = 256 << 20
 
@@ -298,7 +299,8 @@ def run_ours(args, cfg):
 
     if rank == 0:
         kern_avg_s = statistics.mean(step_ms) * 1e-3
-        achieved = A_INT * attempts_step / kern_avg_s / 1e12
+        a_int = A_INT_PHILOX if args.stream == "philox" else A_INT_XOSHIRO
+        achieved = a_int * attempts_step / kern_avg_s / 1e12
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": args.warmup,
             "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -316,12 +318,12 @@ def run_ours(args, cfg):
             "roofline": {
                 "bound": "int32", "achieved": achieved, "peak": peak, "unit": "Tops/s",
                 "frac": achieved / peak, "traffic": load_traffic(),
-                "kernel": "k_win", "per_launch": f"{attempts_step} attempts x {A_INT} int32 ops",
+                "kernel": "k_win", "per_launch": f"{attempts_step} attempts x {a_int} int32 ops",
                 "peak_source": "msb_bench_int_peak: issue-bound LOP3+IMAD mix, measured in this run",
             },
             "roofline_attempts": {
-                "int_term": peak * 1e12 / A_INT, "hbm_term": 6532.9e9 / A_BYTES,
-                "frac_of_min": value / ws / min(peak * 1e12 / A_INT, 6532.9e9 / A_BYTES),
+                "int_term": peak * 1e12 / a_int, "hbm_term": 6532.9e9 / A_BYTES,
+                "frac_of_min": value / ws / min(peak * 1e12 / a_int, 6532.9e9 / A_BYTES),
             },
             "kernel_ms": {"k_win_mean": statistics.mean(step_ms), "k_win_median": statistics.median(step_ms)},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": nbytes,
@@ -402,7 +404,8 @@ def run_slab(args, cfg):
     attempts_step = m * n * S
     value = attempts_step * K / (total_ms * 1e-3)
     if rank == 0:
-        achieved = A_INT * (b - a) * n * S / (statistics.mean(step_ms) * 1e-3) / 1e12
+        a_int = A_INT_PHILOX if args.stream == "philox" else A_INT_XOSHIRO
+        achieved = a_int * (b - a) * n * S / (statistics.mean(step_ms) * 1e-3) / 1e12
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": args.warmup,
             "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": cfg["slab"], "vs_baseline": None,
