@@ -67,17 +67,24 @@ __device__ __forceinline__ void jump_word(const uint4* __restrict__ jt, int& nib
 // the two accept planes.  out points at word t(k) of the row's first plane.
 // Philox: draw d of stream id (st.a1:st.a0) is word d&3 of block (d>>2, id);
 // pd is the stream draw index of this k's first draw.
-template <int SRC, bool FULL>
+template <int SRC, int CB>
 __device__ __forceinline__ void win_segment_k(const WinArgs& a, XState& st, uint32_t* outk, uint32_t key0,
                                               uint32_t key1, size_t pstride, unsigned long long pd) {
   const Geo& G = a.G;
   for (int ch = 0; ch < G.nch; ch++) {
-    const int L = FULL ? 32 : chunk_bits(G, ch);
+    const int L = CB ? CB : chunk_bits(G, ch);  // CB: compile-time chunk width (32, 16) or 0
     uint32_t acc0 = 0, acc1 = 0;
     if (SRC == kSrcXoshiro) {
       if (L == 32) {
 #pragma unroll kChunkUnroll
         for (int i = 0; i < 32; i++) {
+          const uint32_t h9 = xstep(st) << 9;
+          acc_reject(acc0, h9, key0);
+          acc_reject(acc1, h9, key1);
+        }
+      } else if (CB == 16) {  // n = 512: one 16-draw chunk per k
+#pragma unroll
+        for (int i = 0; i < 16; i++) {
           const uint32_t h9 = xstep(st) << 9;
           acc_reject(acc0, h9, key0);
           acc_reject(acc1, h9, key1);
@@ -92,6 +99,7 @@ __device__ __forceinline__ void win_segment_k(const WinArgs& a, XState& st, uint
     } else {
       const unsigned long long d0 = pd + 32ull * ch;
       if ((d0 & 3) == 0 && (L & 3) == 0) {
+#pragma unroll 1  // one block in flight per thread measured best (register pressure)
         for (int i = 0; i < L; i += 4) {
           const unsigned long long c = (d0 + i) >> 2;
           uint32_t x0 = (uint32_t)c, x1 = (uint32_t)(c >> 32), x2 = st.a0, x3 = st.a1;
@@ -117,7 +125,7 @@ __device__ __forceinline__ void win_segment_k(const WinArgs& a, XState& st, uint
       }
     }
     // acc holds REJECT bits, newest draw in bit 0: reverse and invert
-    if (FULL) {
+    if (CB == 32) {
       outk[ch * 16] = ~__brev(acc0);
       outk[pstride + ch * 16] = ~__brev(acc1);
     } else {
@@ -171,7 +179,7 @@ __device__ __forceinline__ WinPiece win_piece(const WinArgs& a, unsigned gi) {
 }
 
 // One producer warp's share of a window (pieces numbered as win_piece).
-template <int SRC, bool FULL>
+template <int SRC, int CB>
 __device__ __forceinline__ void win_produce(const WinArgs& a, const uint4* __restrict__ jt, int role_warp,
                                             int role_warps) {
   constexpr bool XO = SRC == kSrcXoshiro;
@@ -210,7 +218,7 @@ __device__ __forceinline__ void win_produce(const WinArgs& a, const uint4* __res
         const unsigned long long pseg = (a.block0 + 2ull * w.j + X) * 2 * n + (unsigned long long)q * (n / 2);
         for (int kk = 0; kk < a.kr; kk++) {
           const int k = w.k0 + kk;
-          win_segment_k<SRC, FULL>(a, st, out + t_of_k(k), key0, key1, pstride,
+          win_segment_k<SRC, CB>(a, st, out + t_of_k(k), key0, key1, pstride,
                                    pseg + (unsigned long long)k * G.words);
           if (XO) {  // the 8 jump words, spread evenly over the piece's kit k-iterations
             jacc += 8;
@@ -299,7 +307,7 @@ __device__ __forceinline__ void halo_gate(const HaloArgs& h, unsigned* work, int
 // production); the other warps flip slots [first, first + count) of `cur`
 // (red, barrier, blue, barrier, ...).  With a halo (slabs) every phase is
 // gated by halo_gate and all neighbour reads go through L2.
-template <int SRC, bool FULL, bool HALO>
+template <int SRC, int CB, bool HALO>
 __global__ void __launch_bounds__(kRngThreads, 1) k_win(const WinArgs wa, const FlipArgs fa0, const HaloArgs ha,
                                                         const uint32_t* cur, int first, int count, int pwarps) {
   extern __shared__ uint4 jt[];
@@ -317,7 +325,7 @@ __global__ void __launch_bounds__(kRngThreads, 1) k_win(const WinArgs wa, const 
   MSB_TRACE_PUT(3, warp < pwarps ? 0ull : (1ull << 63));
 #endif
   if (warp < pwarps) {
-    win_produce<SRC, FULL>(wa, jt, warp, pwarps);
+    win_produce<SRC, CB>(wa, jt, warp, pwarps);
   } else if (count > 0) {
     const int nwc = (kRngThreads >> 5) - pwarps;
     const unsigned nc = gridDim.x * nwc;
@@ -581,15 +589,9 @@ int msb_window_sweep(const msb_geom* g, const msb_sweep_params* p, int32_t S, in
     if (env_pw > 0) pwarps = std::min(32, env_pw);
   }
   const bool philox = p->rng == MSB_RNG_PHILOX;
-  const bool full = (wa.G.words % 32) == 0;
-  static std::once_flag o[6];
-  static cudaError_t e[6];
-  if (int r = set_smem_attr(k_win<kSrcXoshiro, true, false>, o[0], e[0])) return r;
-  if (int r = set_smem_attr(k_win<kSrcXoshiro, false, false>, o[1], e[1])) return r;
-  if (int r = set_smem_attr(k_win<kSrcPhilox, false, false>, o[2], e[2])) return r;
-  if (int r = set_smem_attr(k_win<kSrcXoshiro, true, true>, o[3], e[3])) return r;
-  if (int r = set_smem_attr(k_win<kSrcXoshiro, false, true>, o[4], e[4])) return r;
-  if (int r = set_smem_attr(k_win<kSrcPhilox, false, true>, o[5], e[5])) return r;
+  // compile-time chunk width: every chunk 32 draws (n/32 % 32 == 0), a
+  // single 16-draw chunk (n = 512), or generic
+  const int cb = (wa.G.words % 32) == 0 ? 32 : (wa.G.words == 16 ? 16 : 0);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)sms);
   cfg.blockDim = dim3(kRngThreads);
@@ -600,17 +602,27 @@ int msb_window_sweep(const msb_geom* g, const msb_sweep_params* p, int32_t S, in
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = count > 0 ? 1 : 0;  // grid barriers only among consumers
-#define MSB_LAUNCH_WIN(SRC, FULL, HALO) \
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, k_win<SRC, FULL, HALO>, wa, fa, ha, cur, first, count, pwarps))
+#define MSB_LAUNCH_WIN(SRC, CB, HALO)                                                            \
+  do {                                                                                           \
+    static std::once_flag o_;                                                                    \
+    static cudaError_t e_;                                                                       \
+    if (int r = set_smem_attr(k_win<SRC, CB, HALO>, o_, e_)) return r;                          \
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, k_win<SRC, CB, HALO>, wa, fa, ha, cur, first, count, pwarps)); \
+  } while (0)
+#define MSB_LAUNCH_WIN_CB(SRC, HALO)                  \
+  do {                                                \
+    if (cb == 32) MSB_LAUNCH_WIN(SRC, 32, HALO);      \
+    else if (cb == 16) MSB_LAUNCH_WIN(SRC, 16, HALO); \
+    else MSB_LAUNCH_WIN(SRC, 0, HALO);                \
+  } while (0)
   if (ha.on) {
-    if (philox) MSB_LAUNCH_WIN(kSrcPhilox, false, true);
-    else if (full) MSB_LAUNCH_WIN(kSrcXoshiro, true, true);
-    else MSB_LAUNCH_WIN(kSrcXoshiro, false, true);
+    if (philox) MSB_LAUNCH_WIN_CB(kSrcPhilox, true);
+    else MSB_LAUNCH_WIN_CB(kSrcXoshiro, true);
   } else {
-    if (philox) MSB_LAUNCH_WIN(kSrcPhilox, false, false);
-    else if (full) MSB_LAUNCH_WIN(kSrcXoshiro, true, false);
-    else MSB_LAUNCH_WIN(kSrcXoshiro, false, false);
+    if (philox) MSB_LAUNCH_WIN_CB(kSrcPhilox, false);
+    else MSB_LAUNCH_WIN_CB(kSrcXoshiro, false);
   }
+#undef MSB_LAUNCH_WIN_CB
 #undef MSB_LAUNCH_WIN
   return MSB_OK;
 }
