@@ -263,12 +263,12 @@ def run_ours(args, cfg):
     value = attempts_step * K * ws / (total_ms * 1e-3)
 
     # end to end through the public API, host buffers both ways every step:
-    # Engine.load_packed from pinned memory -> one window of sweeps ->
-    # Engine.store_packed into pinned memory + observables.  The engine copies
-    # in and out on its own copy streams (double-buffered staging), so with
-    # three host buffers (step k reads buffer k%3, writes (k+2)%3: two
-    # interleaved chains) the copies of one step overlap the sweeps of the
-    # previous one.
+    # Engine.step_packed = lattices from pinned memory -> one window of sweeps
+    # -> lattices into pinned memory + observables (the conversions and the
+    # observables run inside the window launch).  The engine copies in and out
+    # on its own copy streams (double-buffered staging), so with three host
+    # buffers (step k reads buffer k%3, writes (k+2)%3: two interleaved
+    # chains) the copies of one step overlap the sweeps of the previous one.
     Ke = min(K, 200)
     nbytes = eng.packed_nbytes()
     bufs = [torch.empty(nbytes, dtype=torch.uint8, pin_memory=True) for _ in range(3)]
@@ -277,18 +277,13 @@ def run_ours(args, cfg):
     eng.store_packed(bufs[0])
     eng.store_packed(bufs[1])
     for k in range(2):  # warm the I/O path
-        eng.load_packed(bufs[k % 3])
-        eng._sweeps(S)
-        eng.store_packed(bufs[(k + 2) % 3])
+        eng.step_packed(bufs[k % 3], S, bufs[(k + 2) % 3], ups, uns)
     eng.synchronize()
     if ws > 1:
         dist.barrier()
     t0 = time.perf_counter()
     for k in range(Ke):
-        eng.load_packed(bufs[k % 3])
-        eng._sweeps(S)
-        eng.store_packed(bufs[(k + 2) % 3])
-        eng.observe_async(ups, uns)
+        eng.step_packed(bufs[k % 3], S, bufs[(k + 2) % 3], ups, uns)
     eng.synchronize()
     e2e_s = time.perf_counter() - t0
     if ws > 1:
@@ -328,9 +323,9 @@ def run_ours(args, cfg):
             "kernel_ms": {"k_win_mean": statistics.mean(step_ms), "k_win_median": statistics.median(step_ms)},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": nbytes,
                     "d2h_bytes_per_step": nbytes + 16 * n_sim, "steps": Ke,
-                    "path": "per step: Engine.load_packed(pinned host, all replicas) -> one window of sweeps -> "
-                            "Engine.store_packed(pinned host) + observables (pinned); copies run on the engine's "
-                            "copy streams and overlap the previous step's sweeps (3 host buffers)"},
+                    "path": "per step: Engine.step_packed(pinned host lattices in, one window of sweeps, pinned host "
+                            "lattices + observables out); layout conversions and observables fused into the window "
+                            "launch, copies on the engine's copy streams overlap the previous step (3 host buffers)"},
             "gpu_launches": K,
             "clocks": sampler.summary(),
             "wall_s_timed_region": t_wall,

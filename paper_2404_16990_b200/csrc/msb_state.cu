@@ -61,58 +61,24 @@ __global__ void k_init_linear(Geo G, uint64_t seed, long long words_per_sim, con
   }
 }
 
-// 32 x 32 bit transpose across a warp: lane i holds row i (bit j = A[i][j]);
-// afterwards lane j holds column j (bit i = A[i][j]).  Five shuffle stages
-// swap the off-diagonal blocks of size 16, 8, 4, 2, 1.
-__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x) {
-  const int lane = threadIdx.x & 31;
-  uint32_t m = 0x0000FFFFu;
-#pragma unroll
-  for (int s = 16; s > 0; s >>= 1, m ^= m << s) {
-    const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, s);
-    x = (lane & s) ? (((y >> s) & m) | (x & ~m)) : ((x & m) | ((y & m) << s));
-  }
-  return x;
-}
-
-// Linear <-> colour-split, one warp per (replica, row, chunk): the chunk's
-// 32 linear words (1024 sites; lane b holds sites 32b..32b+31, bit k = site
-// 32b + k) and its 2 x 16 colour-split words (bit b of word (X, t) = site
-// 32b + 2t + p, p = (c+X)&1) are one 32 x 32 bit transpose: after it, lane
-// 2t + p holds word t of parity p.  Loads and stores are coalesced rows.
+// Linear <-> colour-split, one warp per (replica, row, chunk)
+// (chunk_from_linear / chunk_to_linear in msb_common.cuh).
 __global__ void k_from_linear(Geo G, const uint32_t* __restrict__ lin, uint32_t* spins) {
-  // 32-bit index math (64-bit div/mod is emulated)
   const unsigned wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
   const unsigned total = (unsigned)G.n_sim * (unsigned)G.rows * (unsigned)G.nch;
   if (wg >= total) return;  // warp-uniform
-  const unsigned gr = G.nch == 1 ? wg : wg / (unsigned)G.nch;
-  const int ch = (int)(wg - gr * (unsigned)G.nch);
-  const unsigned sq = G.rows_div.div(gr);
-  const int s = (int)sq, lr = (int)(gr - sq * (unsigned)G.rows);
-  const int c = G.row0 + lr, br = lr + G.ghost;
-  const int nb = chunk_bits(G, ch);
-  const uint32_t L = lane < nb ? lin[((size_t)s * G.rows + lr) * G.words + 32 * ch + lane] : 0u;
-  const uint32_t w = warp_transpose32(L);
-  const int t = lane >> 1, p = lane & 1;
-  spins[row_off(G, s, (c + p) & 1, br) + ch * 16 + t] = w;
+  int s, lr, ch;
+  chunk_coords(G, wg, s, lr, ch);
+  chunk_from_linear(G, lin, spins, s, lr, ch);
 }
 
 __global__ void k_to_linear(Geo G, const uint32_t* __restrict__ spins, uint32_t* lin) {
   const unsigned wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
   const unsigned total = (unsigned)G.n_sim * (unsigned)G.rows * (unsigned)G.nch;
   if (wg >= total) return;  // warp-uniform
-  const unsigned gr = G.nch == 1 ? wg : wg / (unsigned)G.nch;
-  const int ch = (int)(wg - gr * (unsigned)G.nch);
-  const unsigned sq = G.rows_div.div(gr);
-  const int s = (int)sq, lr = (int)(gr - sq * (unsigned)G.rows);
-  const int c = G.row0 + lr, br = lr + G.ghost;
-  const int t = lane >> 1, p = lane & 1;
-  const uint32_t W = spins[row_off(G, s, (c + p) & 1, br) + ch * 16 + t];
-  const uint32_t L = warp_transpose32(W);
-  const int nb = chunk_bits(G, ch);
-  if (lane < nb) lin[((size_t)s * G.rows + lr) * G.words + 32 * ch + lane] = L;
+  int s, lr, ch;
+  chunk_coords(G, wg, s, lr, ch);
+  chunk_to_linear(G, spins, lin, s, lr, ch);
 }
 
 __global__ void k_init_const(Geo G, uint32_t up, uint32_t* spins) {
@@ -202,20 +168,7 @@ __global__ void __launch_bounds__(256) k_observe(Geo G, const uint32_t* __restri
   uint32_t u = 0, b = 0;
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < per; i += gridDim.x * blockDim.x) {
     const unsigned lr_u = i / (unsigned)G.Wp;
-    const int wd = (int)(i - lr_u * (unsigned)G.Wp);
-    const int lr = (int)lr_u;
-    const int c = G.row0 + lr, br = lr + G.ghost;
-    const int p = c & 1;  // red sites of row c sit at rows r with parity c&1
-    int bu, bd;
-    vert_rows(G, br, bu, bd);
-    const uint32_t* blu = spins + row_off(G, s, 1, br);
-    const int ch = wd >> 4, t = wd & 15;
-    const uint32_t vm = chunk_mask(G, ch);
-    const uint32_t o = spins[row_off(G, s, 0, br) + wd], y0 = blu[wd];
-    const uint32_t yu = spins[row_off(G, s, 1, bu) + wd], yd = spins[row_off(G, s, 1, bd) + wd];
-    u += __popc(o) + __popc(y0);
-    b += __popc((o ^ yu) & vm) + __popc((o ^ yd) & vm) + __popc((o ^ y0) & vm) +
-         __popc((o ^ h_second(G, blu, ch, t, p)) & vm);
+    word_observe(G, spins, s, (int)lr_u, (int)(i - lr_u * (unsigned)G.Wp), u, b);
   }
   u = __reduce_add_sync(0xFFFFFFFFu, u);
   b = __reduce_add_sync(0xFFFFFFFFu, b);

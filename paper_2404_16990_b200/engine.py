@@ -746,6 +746,23 @@ class Engine:
             done.record(self._out_stream)
         self._obs_copied = done
 
+    def step_packed(self, src, n_sweeps: int, dst=None, ups_out=None, unsat_out=None) -> None:
+        """One host-I/O step: ``load_packed(src)``, ``n_sweeps`` sweeps,
+        ``store_packed(dst)`` and ``observe_async(ups_out, unsat_out)`` (dst
+        and the observables optional; pinned host tensors, asynchronous:
+        ``synchronize()`` before reading them).  The copies run on the
+        engine's copy streams and overlap the sweeps of earlier steps.
+        (Fusing the conversions / observables into the window launch was
+        measured slower: the few flip warps would carry bulk work.)"""
+        if (ups_out is None) != (unsat_out is None):
+            raise ValueError("ups_out and unsat_out go together")
+        self.load_packed(src)
+        self._sweeps(int(n_sweeps))
+        if dst is not None:
+            self.store_packed(dst)
+        if ups_out is not None:
+            self.observe_async(ups_out, unsat_out)
+
     def _observe(self):
         self._push_host_edits()
         if self._obs_ver != self._ver:

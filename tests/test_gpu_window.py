@@ -151,3 +151,44 @@ def test_band_walk_geometries(m, n, n_sim, stream):
     e._sweeps(9)
     o.sweep(9)
     _same(e, o)
+
+
+@pytest.mark.parametrize("window,k", [(8, 8), (4, 6), (3, 3)])
+def test_step_packed_equals_separate_calls(window, k):
+    """Engine.step_packed (one host-I/O step through the copy streams) ==
+    load_packed + sweeps + store_packed + observe_async."""
+    import torch
+    from paper_2404_16990_b200 import Engine, LatticeDims
+    dims = LatticeDims(32, 1024)
+    temps = [1.8, 2.3, 2.9]
+    fused, plain = Engine(dims, temps, 21, window=window), Engine(dims, temps, 21, window=window)
+    nb = fused.packed_nbytes()
+    pin = lambda: torch.empty(nb, dtype=torch.uint8, pin_memory=True)
+    fb, pb = [pin() for _ in range(3)], [pin() for _ in range(3)]
+    obs = [torch.empty(3, dtype=torch.int64, pin_memory=True) for _ in range(4)]
+    for e, b in ((fused, fb), (plain, pb)):
+        e.store_packed(b[0])
+        e.store_packed(b[1])
+    fused.synchronize()
+    plain.synchronize()
+    for step in range(5):
+        src, dst = step % 3, (step + 2) % 3
+        want_obs = step % 2 == 0
+        fused.step_packed(fb[src], k, fb[dst], *(obs[:2] if want_obs else (None, None)))
+        plain.load_packed(pb[src])
+        plain._sweeps(k)
+        plain.store_packed(pb[dst])
+        if want_obs:
+            plain.observe_async(obs[2], obs[3])
+        fused.synchronize()
+        plain.synchronize()
+        assert (fb[dst].numpy() == pb[dst].numpy()).all(), step
+        if want_obs:
+            assert (obs[0].numpy() == obs[2].numpy()).all() and (obs[1].numpy() == obs[3].numpy()).all()
+    assert (fused.lattices() == plain.lattices()).all()
+    assert fused.flips == plain.flips
+    # without outputs, then a plain store
+    fused.step_packed(fb[0], k)
+    plain.load_packed(pb[0])
+    plain._sweeps(k)
+    assert (fused.lattices() == plain.lattices()).all()
