@@ -469,9 +469,10 @@ int32_t msb_window_parts(const msb_geom* g, int32_t S) {
   // Rows being written concurrently stay L2-resident: a piece completes its
   // row's plane words one t-word per k, so ~140k pieces in flight write
   // 140k / max(1, P/8) rows of 8*Wp bytes (P > 8: the P/8 parts of a row run
-  // side by side).  Keep that under ~60 MB.
+  // side by side).  Keep that under ~100 MB (measured: cfg4 best at P = 32,
+  // the 32768-wide cfg5 rows at P = 32-64; P = 8 cost 9-19%).
   const long long row_bytes = 8LL * make_geo(g).Wp;
-  while (p < 128 && 140000LL / std::max(1, p / 8) * row_bytes > (60LL << 20)) p *= 2;
+  while (p < 128 && 140000LL / std::max(1, p / 8) * row_bytes > (100LL << 20)) p *= 2;
   static const int env_p = [] { const char* e = getenv("MSB_WINDOW_PARTS"); return e ? atoi(e) : 0; }();
   if (env_p > 0 && env_p <= 128 && !(env_p & (env_p - 1)) && (env_p >= 8 || !g->ghost)) p = env_p;  // tuning
   while (p > (g->ghost ? 8 : 1) && pieces(p) >= (1LL << 31)) p >>= 1;
@@ -575,7 +576,7 @@ int msb_window_sweep(const msb_geom* g, const msb_sweep_params* p, int32_t S, in
   // bytes of plane rows a producer warp has open: 2 rows (planes) per row
   // being written, 32 / max(1, P/8) rows per warp (win_piece numbering)
   const long long live_per_warp = 32LL * 2 * 4 * fa.G.Wp / std::max(1, P / 8);
-  const int cap = (int)std::max(4LL, std::min(32LL, (64LL << 20) / ((long long)sms * live_per_warp)));
+  const int cap = (int)std::max(4LL, std::min(32LL, (100LL << 20) / ((long long)sms * live_per_warp)));
   int pwarps = 0;
   if (produce) {
     if (count == 0) {

@@ -10,8 +10,9 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--m", type=int, default=1024); ap.add_argument("--n", type=int, default=1024)
 ap.add_argument("--n-sim", type=int, default=64); ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--window", type=int, default=None)
+ap.add_argument("--stream", default="xoshiro")
 a = ap.parse_args()
-e = Engine(LatticeDims(a.m, a.n), list(np.linspace(1.5, 3.5, a.n_sim)), 7, window=a.window)
+e = Engine(LatticeDims(a.m, a.n), list(np.linspace(1.5, 3.5, a.n_sim)), 7, window=a.window, stream=a.stream)
 S = e.window
 e._sweeps(2 * S); e.synchronize()
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
