@@ -336,8 +336,13 @@ int msb_observe(const msb_geom* g, const uint32_t* spins, int64_t* ups, int64_t*
   const Geo G = make_geo(g);
   const long long per = (long long)g->rows * G.Wp;  // words per replica
   if (per >= (1LL << 32) || g->n_sim > 65535) return fail(MSB_ERR_UNSUPPORTED, "observe launch too large");
-  // ~4 words per thread, at most 64 CTAs per replica
-  const dim3 grid((unsigned)std::max(1LL, std::min(64LL, (per + 1023) / 1024)), (unsigned)g->n_sim);
+  // ~4+ words per thread; enough CTAs in all to fill the GPU (~8 per SM)
+  // however few replicas, few enough per replica to keep the atomics cheap
+  int dev = 0, sms = 148;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const long long want = std::max(1LL, (8LL * sms + g->n_sim - 1) / g->n_sim);
+  const dim3 grid((unsigned)std::max(1LL, std::min(want, (per + 1023) / 1024)), (unsigned)g->n_sim);
   k_observe<<<grid, 256, 0, as_stream(stream)>>>(G, spins, reinterpret_cast<long long*>(ups),
                                                                     reinterpret_cast<long long*>(unsat));
   CUDA_TRY(cudaGetLastError());
