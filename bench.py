@@ -173,11 +173,12 @@ def run_reference(args, cfg):
     attempts = replicas * cfg["m"] * cfg["n"] * args.steps
     value = attempts / dt
     line = {
-        "impl": "reference", "metric": METRIC.replace("device-timed", "host-timed"), "value": value,
+        "impl": "reference", "metric": METRIC, "value": value,
         "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u64 (xoshiro) / i8 spins / f64 compare", "data": "synthetic",
-        "config": {"workload": cfg["desc"], "replicas_timed": replicas},
+        "config": {"workload": cfg["desc"], "m": cfg["m"], "n": cfg["n"], "replicas_per_gpu": cfg["n_sim"],
+                   "replicas_timed": replicas, "timing": "host wall clock over the timed sweeps (CPU path)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"each step = 1 sweep of {replicas} of the {cfg['n_sim']} replicas on "
                                    f"{threads} threads (oracle/msb_oracle.c, the C restatement of the "
