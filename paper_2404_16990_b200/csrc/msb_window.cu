@@ -15,10 +15,12 @@
 // [S][2 colours][2 planes][n_sim][m][Wp] (same per-slot layout as the
 // per-sweep planes), so the flip pass is unchanged.
 //
-// k_win_fused is the steady state: producer warps fill the NEXT window's
-// buffer while consumer warps flip the S sweeps of the CURRENT one (red, grid
-// barrier, blue, grid barrier, ...).  Launch, start-up and tail are paid once
-// per S sweeps.
+// k_win is the steady state, one cooperative launch per window: producer
+// warps fill the NEXT window's buffer while the consumer warps of every CTA
+// flip the S sweeps of the CURRENT one (red, grid barrier, blue, grid
+// barrier, ...; band walk or quad walk, msb_sweep.cuh).  Launch, start-up and
+// tail are paid once per S sweeps.  Row slabs (msb_halo) additionally push
+// their edge rows into the neighbours' ghost rows and handshake every phase.
 #include "msb_sweep.cuh"
 
 namespace msbk {

@@ -194,9 +194,10 @@ class Engine:
             self._states = torch.empty(2 * 8 * n_pieces, dtype=torch.int32, device=self.device)
             self._thr = torch.zeros(MSB_MAX_PLANES * self.n_sim, dtype=torch.int32, device=self.device)
             self._flips_dev = torch.zeros(MSB_FLIP_SLOTS, dtype=torch.int64, device=self.device)
-            pw = int(_lib.lib().msb_plane_words(ctypes.byref(self._g), MSB_MAX_PLANES))
-            self._plane_words = pw
-            self._planes = torch.empty(2 * pw, dtype=torch.int32, device=self.device)
+            # per-phase / per-sweep path planes (2 buffers of up to 10 planes):
+            # allocated on first use, the window path has its own
+            self._plane_words = int(_lib.lib().msb_plane_words(ctypes.byref(self._g), MSB_MAX_PLANES))
+            self._planes_t = None
             self._work = torch.zeros(4, dtype=torch.int32, device=self.device)
             self._obs = torch.zeros(2 * self.n_sim, dtype=torch.int64, device=self.device)
         self._pow = _pow_tables(self.device)
@@ -260,6 +261,14 @@ class Engine:
         self.recorder = None
         self.update_red_bc()
         self.update_blue_bc()
+
+    @property
+    def _planes(self):
+        if self._planes_t is None:
+            torch = _torch()
+            with torch.cuda.device(self.device), torch.cuda.stream(self._stream):
+                self._planes_t = torch.empty(2 * self._plane_words, dtype=torch.int32, device=self.device)
+        return self._planes_t
 
     # -- construction from explicit lattices (engine.py:284-300) -------------
 
