@@ -239,17 +239,19 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
   const int qpr = G.Wp >> 2;             // quads per row (divides 32)
   const int H = a.band_h, gb = a.band_gb;
   const int bi = lane / qpr, q = lane - bi * qpr, base = bi * qpr;
-  const int ch = q >> 2, t0 = 4 * (q & 3), w0 = q * 4;
+  const int ch = q >> 2, w0 = q * 4;
   const int vb = chunk_bits(G, ch);
   const uint32_t vm = chunk_mask(G, ch);
   const int lastbits = chunk_bits(G, G.nch - 1);
-  const unsigned R = (unsigned)G.R, Wp = (unsigned)G.Wp;
+  const unsigned Wp = (unsigned)G.Wp;
+  const unsigned colour_words = (unsigned)G.R * Wp;  // one colour of one replica
   const unsigned pstride = (unsigned)G.n_sim * (unsigned)G.rows * Wp;
   const unsigned groups_per_sim = (unsigned)G.rows / (unsigned)(gb * H);
   // shuffle sources (fixed per lane): next quad, this chunk's first and last
   // quads, previous quad (the previous chunk's last / the row's last quad)
   const int s_next = base + (q + 1) % qpr, s_first = base + (q & ~3), s_last = base + (q | 3),
             s_prev = base + (q + qpr - 1) % qpr;
+  const bool chunk_last = (q & 3) == 3, chunk_first = (q & 3) == 0;
   auto ld4 = [](const uint32_t* p) {
     return COHERENT ? __ldcg(reinterpret_cast<const uint4*>(p)) : __ldg(reinterpret_cast<const uint4*>(p));
   };
@@ -257,33 +259,33 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
   for (unsigned g = g0; g < g1; g++) {
     const unsigned s = g / groups_per_sim;
     const int lr0 = (int)(g - s * groups_per_sim) * gb * H + bi * H;  // this lane's band
-    const uint32_t* ybase = a.spins + ((s * 2u + (unsigned)(1 - X)) * R) * Wp + w0;
-    uint32_t* obase = a.spins + ((s * 2u + (unsigned)X) * R) * Wp + w0;
-    const uint32_t* pbase = a.planes + ((((unsigned)X * (unsigned)a.np) * (unsigned)G.n_sim + s) * (unsigned)G.rows) * Wp + w0;
-    int br = lr0 + G.ghost, bu, bd;
-    vert_rows(G, br, bu, bd);
-    uint4 U = ld4(ybase + (unsigned)bu * Wp), Y = ld4(ybase + (unsigned)br * Wp);
+    const uint32_t* ybase = a.spins + (s * 2u + (unsigned)(1 - X)) * colour_words + w0;
+    const int br0 = lr0 + G.ghost;
+    int bu, bd;
+    vert_rows(G, br0, bu, bd);
+    uint4 U = ld4(ybase + (unsigned)bu * Wp), Y = ld4(ybase + (unsigned)br0 * Wp);
+    // incremental row pointers: the other colour's current row, the own row,
+    // the plane rows; the row below wraps only past a whole lattice's last row
+    const uint32_t* yrow = ybase + (unsigned)br0 * Wp;
+    uint32_t* orow = a.spins + (s * 2u + (unsigned)X) * colour_words + (unsigned)br0 * Wp + w0;
+    const uint32_t* prow =
+        a.planes + ((((unsigned)X * (unsigned)a.np) * (unsigned)G.n_sim + s) * (unsigned)G.rows + (unsigned)lr0) * Wp + w0;
+    int p = (G.row0 + lr0 + X) & 1;  // warp-uniform (H even, bands even-aligned); alternates per row
     for (int h = 0; h < H; h++) {
-      const int lr = lr0 + h;
-      if (h > 0) {
-        br = lr + G.ghost;
-        vert_rows(G, br, bu, bd);
-      }
-      const uint4 D = ld4(ybase + (unsigned)bd * Wp);
-      const uint4 O = *reinterpret_cast<const uint4*>(obase + (unsigned)br * Wp);
-      const uint4 P4 = __ldg(reinterpret_cast<const uint4*>(pbase + (unsigned)lr * Wp));
-      const uint4 P8 = __ldg(reinterpret_cast<const uint4*>(pbase + pstride + (unsigned)lr * Wp));
-      const int p = (G.row0 + lr + X) & 1;  // warp-uniform (H even, bands even-aligned)
+      const int lr = lr0 + h, br = br0 + h;
+      const uint32_t* drow = br + 1 < G.R ? yrow + Wp : ybase;
+      const uint4 D = ld4(drow);
+      const uint4 O = *reinterpret_cast<const uint4*>(orow);
+      const uint4 P4 = __ldg(reinterpret_cast<const uint4*>(prow));
+      const uint4 P8 = __ldg(reinterpret_cast<const uint4*>(prow + pstride));
       uint32_t edge;
       if (p) {  // word t0+4, or the chunk wrap: (first word >> 1) | (next chunk's bit 0 << vb-1)
-        const uint32_t xa = __shfl_sync(0xFFFFFFFFu, Y.x, s_next);
-        const uint32_t xb = __shfl_sync(0xFFFFFFFFu, Y.x, s_first);
-        edge = (q & 3) != 3 ? xa : ((xb >> 1) | ((xa & 1u) << (vb - 1)));
+        const uint32_t xa = __shfl_sync(0xFFFFFFFFu, Y.x, s_next), xb = __shfl_sync(0xFFFFFFFFu, Y.x, s_first);
+        edge = chunk_last ? ((xb >> 1) | ((xa & 1u) << (vb - 1))) : xa;
       } else {  // word t0-1, or the chunk wrap: ((last word << 1) | carry) & mask
-        const uint32_t wa = __shfl_sync(0xFFFFFFFFu, Y.w, s_prev);
-        const uint32_t wb = __shfl_sync(0xFFFFFFFFu, Y.w, s_last);
+        const uint32_t wa = __shfl_sync(0xFFFFFFFFu, Y.w, s_prev), wb = __shfl_sync(0xFFFFFFFFu, Y.w, s_last);
         const uint32_t carry = ch > 0 ? (wa >> 31) : ((wa >> (lastbits - 1)) & 1u);
-        edge = (q & 3) != 0 ? wa : (((wb << 1) | carry) & vm);
+        edge = chunk_first ? (((wb << 1) | carry) & vm) : wa;
       }
       const uint32_t y[4] = {Y.x, Y.y, Y.z, Y.w};
       const uint32_t o[4] = {O.x, O.y, O.z, O.w};
@@ -300,7 +302,7 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
         cnt += __popc(f);
       }
       const uint4 out = make_uint4(res[0], res[1], res[2], res[3]);
-      *reinterpret_cast<uint4*>(obase + (unsigned)br * Wp) = out;
+      *reinterpret_cast<uint4*>(orow) = out;
       if (PUSH) {
         if (lr == 0)
           *reinterpret_cast<uint4*>(a.up_spins + (((size_t)s * 2 + X) * a.up_R + a.up_R - 1) * Wp + w0) = out;
@@ -309,6 +311,10 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
       }
       U = Y;
       Y = D;
+      yrow = drow;
+      orow += Wp;
+      prow += Wp;
+      p ^= 1;
     }
   }
   return cnt;
