@@ -435,8 +435,9 @@ def main():
     ap.add_argument("--stream", choices=["xoshiro", "philox"], default="xoshiro",
                     help="xoshiro: the reference's own streams (default); philox: counter-based (SURVEY F1)")
     args = ap.parse_args()
-    if args.warmup < 3:
-        ap.error("--warmup must be >= 3")
+    if args.warmup < 3:  # the timing rules need >= 3 warm-up steps: do 3, report what was done
+        print(f"bench.py: --warmup {args.warmup} raised to 3 (timing rules)", file=sys.stderr)
+        args.warmup = 3
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)
