@@ -234,6 +234,12 @@ int msb_window_sweep(const msb_geom *g, const msb_sweep_params *p, int32_t S, in
  * E/N = -J (2N - 2 unsat)/N, evaluated on the host like the reference. */
 int msb_observe(const msb_geom *g, const uint32_t *spins, int64_t *ups, int64_t *unsat,
                 void *stream);
+/* msb_to_linear and msb_observe in one pass over the spins (either output
+ * may be NULL; ups and unsat go together).  The layout transpose already
+ * holds both colours of a row, so the observables cost only the neighbour
+ * rows.  msb_to_linear / msb_observe are this call with one output. */
+int msb_export(const msb_geom *g, const uint32_t *spins, uint64_t *lin, int64_t *ups,
+               int64_t *unsat, void *stream);
 
 /* ---- record/replay support (reference.py:179-208) ------------------------ */
 /* The u23 draws the next `phase` would consume, in the reference block order

@@ -307,8 +307,7 @@ __device__ __forceinline__ uint32_t h_second(const Geo& G, const uint32_t* y, in
 
 
 // ---------------------------------------------------------------------------
-// device: layout conversion and observables of one chunk / word (shared by
-// msb_state.cu's kernels and the window kernel's I/O prologue / epilogue)
+// device: layout conversion helpers (msb_state.cu)
 // ---------------------------------------------------------------------------
 
 // 32 x 32 bit transpose across a warp: lane i holds row i (bit j = A[i][j]);
@@ -334,50 +333,10 @@ __device__ __forceinline__ void chunk_coords(const Geo& G, unsigned wg, int& s, 
   lr = (int)(gr - sq * (unsigned)G.rows);
 }
 
-// Linear <-> colour-split for one chunk, whole warp: the chunk's 32 linear
-// words (1024 sites; lane b holds sites 32b..32b+31, bit k = site 32b + k)
-// and its 2 x 16 colour-split words (bit b of word (X, t) = site 32b + 2t + p,
-// p = (c+X)&1) are one 32 x 32 bit transpose: after it, lane 2t + p holds word
-// t of parity p.  Loads and stores are coalesced rows.
-__device__ __forceinline__ void chunk_from_linear(const Geo& G, const uint32_t* __restrict__ lin, uint32_t* spins,
-                                                  int s, int lr, int ch) {
-  const int lane = threadIdx.x & 31;
-  const int c = G.row0 + lr, br = lr + G.ghost;
-  const int nb = chunk_bits(G, ch);
-  const uint32_t L = lane < nb ? lin[((size_t)s * G.rows + lr) * G.words + 32 * ch + lane] : 0u;
-  const uint32_t w = warp_transpose32(L);
-  const int t = lane >> 1, p = lane & 1;
-  spins[row_off(G, s, (c + p) & 1, br) + ch * 16 + t] = w;
-}
-
-__device__ __forceinline__ void chunk_to_linear(const Geo& G, const uint32_t* __restrict__ spins, uint32_t* lin,
-                                                int s, int lr, int ch) {
-  const int lane = threadIdx.x & 31;
-  const int c = G.row0 + lr, br = lr + G.ghost;
-  const int t = lane >> 1, p = lane & 1;
-  const uint32_t W = spins[row_off(G, s, (c + p) & 1, br) + ch * 16 + t];
-  const uint32_t L = warp_transpose32(W);
-  const int nb = chunk_bits(G, ch);
-  if (lane < nb) lin[((size_t)s * G.rows + lr) * G.words + 32 * ch + lane] = L;
-}
-
-// Observables of word wd of held row lr (engine.py:372-386): +1 spins of
-// both colours, and unsatisfied bonds of its red sites (4 neighbours each),
-// accumulated into u and b.
-__device__ __forceinline__ void word_observe(const Geo& G, const uint32_t* __restrict__ spins, int s, int lr, int wd,
-                                             uint32_t& u, uint32_t& b) {
-  const int c = G.row0 + lr, br = lr + G.ghost;
-  const int p = c & 1;  // red sites of row c sit at rows r with parity c&1
-  int bu, bd;
-  vert_rows(G, br, bu, bd);
-  const uint32_t* blu = spins + row_off(G, s, 1, br);
-  const int ch = wd >> 4, t = wd & 15;
-  const uint32_t vm = chunk_mask(G, ch);
-  const uint32_t o = spins[row_off(G, s, 0, br) + wd], y0 = blu[wd];
-  const uint32_t yu = spins[row_off(G, s, 1, bu) + wd], yd = spins[row_off(G, s, 1, bd) + wd];
-  u += __popc(o) + __popc(y0);
-  b += __popc((o ^ yu) & vm) + __popc((o ^ yd) & vm) + __popc((o ^ y0) & vm) +
-       __popc((o ^ h_second(G, blu, ch, t, p)) & vm);
-}
+// Linear <-> colour-split for one chunk is a whole-warp 32 x 32 bit transpose:
+// the chunk's 32 linear words (1024 sites; lane b holds sites 32b..32b+31,
+// bit k = site 32b + k) and its 2 x 16 colour-split words (bit b of word
+// (X, t) = site 32b + 2t + p, p = (c+X)&1) are transposes of each other, and
+// lane 2t + p holds word t of parity p (k_from_linear / k_export).
 
 }  // namespace msbk

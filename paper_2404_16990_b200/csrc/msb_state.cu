@@ -61,24 +61,116 @@ __global__ void k_init_linear(Geo G, uint64_t seed, long long words_per_sim, con
   }
 }
 
-// Linear <-> colour-split, one warp per (replica, row, chunk)
-// (chunk_from_linear / chunk_to_linear in msb_common.cuh).
-__global__ void k_from_linear(Geo G, const uint32_t* __restrict__ lin, uint32_t* spins) {
-  const unsigned wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const unsigned total = (unsigned)G.n_sim * (unsigned)G.rows * (unsigned)G.nch;
-  if (wg >= total) return;  // warp-uniform
-  int s, lr, ch;
-  chunk_coords(G, wg, s, lr, ch);
-  chunk_from_linear(G, lin, spins, s, lr, ch);
+// Linear <-> colour-split, one warp per CPW consecutive chunks (replica, row,
+// chunk), all of one replica (CPW divides rows * nch).  A chunk is one warp
+// transpose (msb_common.cuh); a warp issues all its chunks' loads before the
+// first transpose, so CPW 128-byte requests per warp are in flight (one per
+// warp left these kernels at ~1.5 TB/s, latency-bound).
+constexpr int kConvThreads = 256;
+
+__device__ __forceinline__ void next_chunk(const Geo& G, int& lr, int& ch) {
+  if (++ch == G.nch) {
+    ch = 0;
+    ++lr;
+  }
 }
 
-__global__ void k_to_linear(Geo G, const uint32_t* __restrict__ spins, uint32_t* lin) {
-  const unsigned wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const unsigned total = (unsigned)G.n_sim * (unsigned)G.rows * (unsigned)G.nch;
-  if (wg >= total) return;  // warp-uniform
-  int s, lr, ch;
-  chunk_coords(G, wg, s, lr, ch);
-  chunk_to_linear(G, spins, lin, s, lr, ch);
+template <int CPW>
+__global__ void __launch_bounds__(kConvThreads) k_from_linear(Geo G, const uint32_t* __restrict__ lin,
+                                                               uint32_t* __restrict__ spins, unsigned nwarps) {
+  const unsigned wq = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (wq >= nwarps) return;  // warp-uniform
+  const int lane = threadIdx.x & 31, t = lane >> 1, p = lane & 1;
+  int s, lr0, ch0;
+  chunk_coords(G, wq * CPW, s, lr0, ch0);
+  uint32_t L[CPW];
+  int lr = lr0, ch = ch0;
+#pragma unroll
+  for (int j = 0; j < CPW; j++, next_chunk(G, lr, ch))
+    L[j] = lane < chunk_bits(G, ch) ? __ldcs(lin + ((size_t)s * G.rows + lr) * G.words + 32 * ch + lane) : 0u;
+  lr = lr0;
+  ch = ch0;
+#pragma unroll
+  for (int j = 0; j < CPW; j++, next_chunk(G, lr, ch)) {
+    const int c = G.row0 + lr;
+    spins[row_off(G, s, (c + p) & 1, lr + G.ghost) + ch * 16 + t] = warp_transpose32(L[j]);
+  }
+}
+
+// Colour-split -> linear and/or the observables (engine.py:372-386), one
+// pass: the warp holds both colours' words of its chunk for the transpose, so
+// the observables add only the blue rows above and below.  ups gets the +1
+// spins of both colours; unsat the unsatisfied bonds of the red sites (4
+// neighbours each, every bond once).  Red lane 2t+p0 (p0 = c&1) takes its
+// blue word t from lane ^ 1 and the second horizontal neighbour (h_second)
+// from lane +-1, or at the chunk's edge word from lane 0 / 31 plus one bit of
+// the adjacent chunk (a load).  One atomic per warp and quantity.
+template <int CPW, bool LIN, bool OBS>
+__global__ void __launch_bounds__(kConvThreads) k_export(Geo G, const uint32_t* __restrict__ spins,
+                                                          uint32_t* __restrict__ lin, long long* ups,
+                                                          long long* unsat, unsigned nwarps) {
+  const unsigned wq = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (wq >= nwarps) return;  // warp-uniform
+  const int lane = threadIdx.x & 31, t = lane >> 1, p = lane & 1;
+  int s, lr0, ch0;
+  chunk_coords(G, wq * CPW, s, lr0, ch0);
+  uint32_t W[CPW], Yu[CPW], Yd[CPW], E[CPW];
+  int lr = lr0, ch = ch0;
+#pragma unroll
+  for (int j = 0; j < CPW; j++, next_chunk(G, lr, ch)) {
+    const int c = G.row0 + lr, br = lr + G.ghost, wd = ch * 16 + t;
+    W[j] = spins[row_off(G, s, (c + p) & 1, br) + wd];
+    if (OBS) {
+      const int p0 = c & 1;
+      const bool red = p == p0;
+      int bu, bd;
+      vert_rows(G, br, bu, bd);
+      const uint32_t* blu = spins + row_off(G, s, 1, br);
+      Yu[j] = red ? spins[row_off(G, s, 1, bu) + wd] : 0u;
+      Yd[j] = red ? spins[row_off(G, s, 1, bd) + wd] : 0u;
+      // the adjacent chunk's word that supplies the edge bit
+      E[j] = 0u;
+      if (red && p0 && t == 15) E[j] = blu[(ch + 1 < G.nch ? ch + 1 : 0) * 16];
+      if (red && !p0 && t == 0) E[j] = blu[(ch > 0 ? ch - 1 : G.nch - 1) * 16 + 15];
+    }
+  }
+  uint32_t u = 0, b = 0;
+  lr = lr0;
+  ch = ch0;
+#pragma unroll
+  for (int j = 0; j < CPW; j++, next_chunk(G, lr, ch)) {
+    if (LIN) {
+      const uint32_t L = warp_transpose32(W[j]);
+      if (lane < chunk_bits(G, ch)) __stcs(lin + ((size_t)s * G.rows + lr) * G.words + 32 * ch + lane, L);
+    }
+    if (OBS) {
+      const int p0 = (G.row0 + lr) & 1;
+      const int nb = chunk_bits(G, ch);
+      const uint32_t vm = chunk_mask(G, ch);
+      const uint32_t y0 = __shfl_xor_sync(0xFFFFFFFFu, W[j], 1);
+      const uint32_t yi = __shfl_sync(0xFFFFFFFFu, W[j], p0 ? (lane + 1) & 31 : (lane + 31) & 31);
+      const uint32_t ye = __shfl_sync(0xFFFFFFFFu, W[j], p0 ? 0 : 31);
+      uint32_t hs = yi;
+      if (p0 && t == 15) hs = (ye >> 1) | ((E[j] & 1u) << (nb - 1));
+      if (!p0 && t == 0) {
+        const uint32_t carry = ch > 0 ? E[j] >> 31 : (E[j] >> (chunk_bits(G, G.nch - 1) - 1)) & 1u;
+        hs = ((ye << 1) | carry) & vm;
+      }
+      u += __popc(W[j]);
+      if (p == p0) {
+        const uint32_t o = W[j];
+        b += __popc((o ^ Yu[j]) & vm) + __popc((o ^ Yd[j]) & vm) + __popc((o ^ y0) & vm) + __popc((o ^ hs) & vm);
+      }
+    }
+  }
+  if (OBS) {
+    u = __reduce_add_sync(0xFFFFFFFFu, u);
+    b = __reduce_add_sync(0xFFFFFFFFu, b);
+    if (lane == 0) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(ups + s), (unsigned long long)u);
+      atomicAdd(reinterpret_cast<unsigned long long*>(unsat + s), (unsigned long long)b);
+    }
+  }
 }
 
 __global__ void k_init_const(Geo G, uint32_t up, uint32_t* spins) {
@@ -158,37 +250,7 @@ __global__ void k_from_ref16(Geo G, const uint16_t* __restrict__ state, uint32_t
 // device: observables (engine.py:372-386)
 // ---------------------------------------------------------------------------
 
-// Replica s = blockIdx.y; the CTAs along x stride over its rows x Wp words
-// (lanes take consecutive words of a row: coalesced), each thread sums its
-// words, the CTA reduces, and one atomic per CTA per quantity remains.
-__global__ void __launch_bounds__(256) k_observe(Geo G, const uint32_t* __restrict__ spins, long long* ups,
-                                                 long long* unsat) {
-  const int s = blockIdx.y;
-  const unsigned per = (unsigned)G.rows * (unsigned)G.Wp;
-  uint32_t u = 0, b = 0;
-  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < per; i += gridDim.x * blockDim.x) {
-    const unsigned lr_u = i / (unsigned)G.Wp;
-    word_observe(G, spins, s, (int)lr_u, (int)(i - lr_u * (unsigned)G.Wp), u, b);
-  }
-  u = __reduce_add_sync(0xFFFFFFFFu, u);
-  b = __reduce_add_sync(0xFFFFFFFFu, b);
-  __shared__ unsigned long long su[8], sb[8];
-  const int warp = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0) {
-    su[warp] = u;
-    sb[warp] = b;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long tu = 0, tb = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
-      tu += su[w];
-      tb += sb[w];
-    }
-    atomicAdd(reinterpret_cast<unsigned long long*>(ups + s), tu);
-    atomicAdd(reinterpret_cast<unsigned long long*>(unsat + s), tb);
-  }
-}
+// (observables: k_export above)
 
 // ---------------------------------------------------------------------------
 // device: record/replay, slab halos, INT microbenchmark
@@ -237,6 +299,44 @@ __global__ void k_unpack_ghosts(Geo G, int X, const uint32_t* __restrict__ ghost
   const int j = i % G.Wp, which = (i / G.Wp) % 2, s = i / (2 * G.Wp);
   const int br = which == 0 ? 0 : G.R - 1;
   spins[row_off(G, s, X, br) + j] = ghost_rows[i];
+}
+
+
+// Chunks per warp of the conversion kernels: the largest of 8, 4, 2, 1 that
+// divides a replica's chunk count, so a warp never spans two replicas.
+int conv_cpw(const Geo& G) {
+  const long long per = (long long)G.rows * G.nch;
+  return per % 8 == 0 ? 8 : per % 4 == 0 ? 4 : per % 2 == 0 ? 2 : 1;
+}
+
+int check_conv(const Geo& G) {
+  if (32LL * G.n_sim * G.rows * G.nch >= (1LL << 31)) return fail(MSB_ERR_UNSUPPORTED, "too many chunks for one launch");
+  return MSB_OK;
+}
+
+template <int CPW>
+void launch_from_linear(const Geo& G, const uint32_t* lin, uint32_t* spins, cudaStream_t st) {
+  const unsigned nw = (unsigned)((long long)G.n_sim * G.rows * G.nch / CPW);
+  k_from_linear<CPW><<<blocks_for(32LL * nw, kConvThreads), kConvThreads, 0, st>>>(G, lin, spins, nw);
+}
+
+template <int CPW, bool LIN, bool OBS>
+void launch_export(const Geo& G, const uint32_t* spins, uint32_t* lin, long long* ups, long long* unsat,
+                          cudaStream_t st) {
+  const unsigned nw = (unsigned)((long long)G.n_sim * G.rows * G.nch / CPW);
+  k_export<CPW, LIN, OBS><<<blocks_for(32LL * nw, kConvThreads), kConvThreads, 0, st>>>(G, spins, lin, ups, unsat,
+                                                                                        nw);
+}
+
+template <bool LIN, bool OBS>
+void export_cpw(const Geo& G, const uint32_t* spins, uint32_t* lin, long long* ups, long long* unsat,
+                       cudaStream_t st) {
+  switch (conv_cpw(G)) {
+    case 8: launch_export<8, LIN, OBS>(G, spins, lin, ups, unsat, st); break;
+    case 4: launch_export<4, LIN, OBS>(G, spins, lin, ups, unsat, st); break;
+    case 2: launch_export<2, LIN, OBS>(G, spins, lin, ups, unsat, st); break;
+    default: launch_export<1, LIN, OBS>(G, spins, lin, ups, unsat, st); break;
+  }
 }
 
 
@@ -290,22 +390,39 @@ int msb_from_linear(const msb_geom* g, const uint64_t* lin, uint32_t* spins, voi
   if (int r = check_geom(g)) return r;
   if (!lin || !spins) return fail(MSB_ERR_ARG, "null buffer");
   const Geo G = make_geo(g);
-  if (32LL * G.n_sim * G.rows * G.nch >= (1LL << 31)) return fail(MSB_ERR_UNSUPPORTED, "too many chunks for one launch");
-  k_from_linear<<<blocks_for(32LL * G.n_sim * G.rows * G.nch, 256), 256, 0, as_stream(stream)>>>(
-      G, reinterpret_cast<const uint32_t*>(lin), spins);
+  if (int r = check_conv(G)) return r;
+  const uint32_t* l = reinterpret_cast<const uint32_t*>(lin);
+  switch (conv_cpw(G)) {
+    case 8: launch_from_linear<8>(G, l, spins, as_stream(stream)); break;
+    case 4: launch_from_linear<4>(G, l, spins, as_stream(stream)); break;
+    case 2: launch_from_linear<2>(G, l, spins, as_stream(stream)); break;
+    default: launch_from_linear<1>(G, l, spins, as_stream(stream)); break;
+  }
+  CUDA_TRY(cudaGetLastError());
+  return MSB_OK;
+}
+
+int msb_export(const msb_geom* g, const uint32_t* spins, uint64_t* lin, int64_t* ups, int64_t* unsat,
+               void* stream) {
+  if (int r = check_geom(g)) return r;
+  if (!spins) return fail(MSB_ERR_ARG, "null buffer");
+  if ((ups == nullptr) != (unsat == nullptr)) return fail(MSB_ERR_ARG, "ups and unsat go together");
+  const Geo G = make_geo(g);
+  if (int r = check_conv(G)) return r;
+  uint32_t* l = reinterpret_cast<uint32_t*>(lin);
+  long long *u = reinterpret_cast<long long*>(ups), *b = reinterpret_cast<long long*>(unsat);
+  const cudaStream_t st = as_stream(stream);
+  if (lin && ups) export_cpw<true, true>(G, spins, l, u, b, st);
+  else if (lin) export_cpw<true, false>(G, spins, l, u, b, st);
+  else if (ups) export_cpw<false, true>(G, spins, l, u, b, st);
+  else return MSB_OK;
   CUDA_TRY(cudaGetLastError());
   return MSB_OK;
 }
 
 int msb_to_linear(const msb_geom* g, const uint32_t* spins, uint64_t* lin, void* stream) {
-  if (int r = check_geom(g)) return r;
-  if (!lin || !spins) return fail(MSB_ERR_ARG, "null buffer");
-  const Geo G = make_geo(g);
-  if (32LL * G.n_sim * G.rows * G.nch >= (1LL << 31)) return fail(MSB_ERR_UNSUPPORTED, "too many chunks for one launch");
-  k_to_linear<<<blocks_for(32LL * G.n_sim * G.rows * G.nch, 256), 256, 0, as_stream(stream)>>>(
-      G, spins, reinterpret_cast<uint32_t*>(lin));
-  CUDA_TRY(cudaGetLastError());
-  return MSB_OK;
+  if (!lin) return fail(MSB_ERR_ARG, "null buffer");
+  return msb_export(g, spins, lin, nullptr, nullptr, stream);
 }
 
 int msb_to_ref16(const msb_geom* g, const uint32_t* spins, uint16_t* state, void* stream) {
@@ -331,22 +448,8 @@ int msb_from_ref16(const msb_geom* g, const uint16_t* state, uint32_t* spins, vo
 }
 
 int msb_observe(const msb_geom* g, const uint32_t* spins, int64_t* ups, int64_t* unsat, void* stream) {
-  if (int r = check_geom(g)) return r;
-  if (!spins || !ups || !unsat) return fail(MSB_ERR_ARG, "null buffer");
-  const Geo G = make_geo(g);
-  const long long per = (long long)g->rows * G.Wp;  // words per replica
-  if (per >= (1LL << 32) || g->n_sim > 65535) return fail(MSB_ERR_UNSUPPORTED, "observe launch too large");
-  // ~4+ words per thread; enough CTAs in all to fill the GPU (~8 per SM)
-  // however few replicas, few enough per replica to keep the atomics cheap
-  int dev = 0, sms = 148;
-  CUDA_TRY(cudaGetDevice(&dev));
-  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const long long want = std::max(1LL, (8LL * sms + g->n_sim - 1) / g->n_sim);
-  const dim3 grid((unsigned)std::max(1LL, std::min(want, (per + 1023) / 1024)), (unsigned)g->n_sim);
-  k_observe<<<grid, 256, 0, as_stream(stream)>>>(G, spins, reinterpret_cast<long long*>(ups),
-                                                                    reinterpret_cast<long long*>(unsat));
-  CUDA_TRY(cudaGetLastError());
-  return MSB_OK;
+  if (!ups || !unsat) return fail(MSB_ERR_ARG, "null buffer");
+  return msb_export(g, spins, nullptr, ups, unsat, stream);
 }
 
 int msb_draws(const msb_geom* g, const msb_sweep_params* p, int32_t phase, const uint32_t* states, uint32_t* out,

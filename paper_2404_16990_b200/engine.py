@@ -711,66 +711,77 @@ class Engine:
         into ``dst``.  A pinned host destination is filled on the engine's
         output copy stream (asynchronous: ``synchronize()`` before reading
         it); the engine's stream continues with the next sweeps meanwhile."""
-        torch = _torch()
-        self._push_host_edits()
-        if dst.numel() * dst.element_size() != self.packed_nbytes():
-            raise ValueError(f"expected {self.packed_nbytes()} bytes of packed lattices")
-        slot = self._io_slot()
-        self._io_next ^= 1
-        if slot["out_full"] is not None:             # its previous copy-out is done
-            self._stream.wait_event(slot["out_full"])
-        call("msb_to_linear", ctypes.byref(self._g), _p(self._spins), _p(slot["out"]), self._cs)
-        written = torch.cuda.Event()
-        written.record(self._stream)
-        with torch.cuda.stream(self._out_stream):
-            self._out_stream.wait_event(written)
-            dst.view(torch.uint8).reshape(-1).copy_(slot["out"].view(torch.uint8), non_blocking=True)
-            done = torch.cuda.Event()
-            done.record(self._out_stream)
-        slot["out_full"] = done
-        if dst.device.type != "cuda":
-            self._host_out[dst.data_ptr()] = done
+        self._export(dst, None, None)
 
     def observe_async(self, ups_out, unsat_out) -> None:
         """Enqueue the integer observables (ups, unsatisfied bonds per replica)
         into pinned host int64 tensors without synchronising.  The copies run
         on the output copy stream, so the engine's stream never waits behind
         a large lattice copy in the copy engine."""
-        torch = _torch()
-        self._push_host_edits()
-        self._io_slot()
-        if getattr(self, "_obs_copied", None) is not None:  # previous copy-out of _obs done
-            self._stream.wait_event(self._obs_copied)
-        with torch.cuda.stream(self._stream):
-            self._obs.zero_()
-        call("msb_observe", ctypes.byref(self._g), _p(self._spins), _p(self._obs[: self.n_sim]),
-             _p(self._obs[self.n_sim:]), self._cs)
-        ready = torch.cuda.Event()
-        ready.record(self._stream)
-        with torch.cuda.stream(self._out_stream):
-            self._out_stream.wait_event(ready)
-            ups_out.copy_(self._obs[: self.n_sim], non_blocking=True)
-            unsat_out.copy_(self._obs[self.n_sim:], non_blocking=True)
-            done = torch.cuda.Event()
-            done.record(self._out_stream)
-        self._obs_copied = done
+        self._export(None, ups_out, unsat_out)
 
     def step_packed(self, src, n_sweeps: int, dst=None, ups_out=None, unsat_out=None) -> None:
         """One host-I/O step: ``load_packed(src)``, ``n_sweeps`` sweeps,
         ``store_packed(dst)`` and ``observe_async(ups_out, unsat_out)`` (dst
         and the observables optional; pinned host tensors, asynchronous:
         ``synchronize()`` before reading them).  The copies run on the
-        engine's copy streams and overlap the sweeps of earlier steps.
+        engine's copy streams and overlap the sweeps of earlier steps; the
+        lattice export and the observables are one kernel (``msb_export``).
         (Fusing the conversions / observables into the window launch was
         measured slower: the few flip warps would carry bulk work.)"""
         if (ups_out is None) != (unsat_out is None):
             raise ValueError("ups_out and unsat_out go together")
         self.load_packed(src)
         self._sweeps(int(n_sweeps))
+        self._export(dst, ups_out, unsat_out)
+
+    def _export(self, dst, ups_out, unsat_out) -> None:
+        """``msb_export`` of the lattice (into the current output staging
+        slot, then ``dst``) and/or the observables (into ``_obs``, then
+        ups_out / unsat_out), copied out on the output copy stream.  The copy
+        stream runs copies only: a kernel queued there (e.g. clearing
+        ``_obs``) waits behind the next cooperative window launch, and every
+        later host-buffer wait would move past that window."""
+        torch = _torch()
+        if (ups_out is None) != (unsat_out is None):
+            raise ValueError("ups_out and unsat_out go together")
+        if dst is None and ups_out is None:
+            return
+        self._push_host_edits()
+        if dst is not None and dst.numel() * dst.element_size() != self.packed_nbytes():
+            raise ValueError(f"expected {self.packed_nbytes()} bytes of packed lattices")
+        slot = self._io_slot()
+        lin = ctypes.c_void_p(None)
         if dst is not None:
-            self.store_packed(dst)
+            self._io_next ^= 1
+            if slot["out_full"] is not None:         # its previous copy-out is done
+                self._stream.wait_event(slot["out_full"])
+            lin = _p(slot["out"])
+        ups = uns = ctypes.c_void_p(None)
         if ups_out is not None:
-            self.observe_async(ups_out, unsat_out)
+            if getattr(self, "_obs_copied", None) is not None:  # previous copy-out of _obs done
+                self._stream.wait_event(self._obs_copied)
+            with torch.cuda.stream(self._stream):
+                self._obs.zero_()
+            ups, uns = _p(self._obs[: self.n_sim]), _p(self._obs[self.n_sim:])
+        call("msb_export", ctypes.byref(self._g), _p(self._spins), lin, ups, uns, self._cs)
+        written = torch.cuda.Event()
+        written.record(self._stream)
+        with torch.cuda.stream(self._out_stream):
+            self._out_stream.wait_event(written)
+            if dst is not None:
+                dst.view(torch.uint8).reshape(-1).copy_(slot["out"].view(torch.uint8), non_blocking=True)
+            if ups_out is not None:
+                ups_out.copy_(self._obs[: self.n_sim], non_blocking=True)
+                unsat_out.copy_(self._obs[self.n_sim:], non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(self._out_stream)
+        if dst is not None:
+            slot["out_full"] = done
+            if dst.device.type != "cuda":
+                self._host_out[dst.data_ptr()] = done
+        if ups_out is not None:
+            self._obs_copied = done
 
     def _observe(self):
         self._push_host_edits()

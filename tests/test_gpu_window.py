@@ -192,3 +192,30 @@ def test_step_packed_equals_separate_calls(window, k):
     plain.load_packed(pb[0])
     plain._sweeps(k)
     assert (fused.lattices() == plain.lattices()).all()
+
+
+@pytest.mark.parametrize("m,n,n_sim", [(16, 96, 2), (20, 96, 3), (36, 160, 2), (32, 2048, 2), (8, 8192, 1)])
+def test_export_one_pass(m, n, n_sim):
+    """msb_export (linear lattice + observables in one kernel; chunk-edge
+    horizontal bonds, partial chunks, 1-8 chunks per warp) against the oracle
+    lattice and a numpy count of up spins and unsatisfied bonds."""
+    import ctypes
+    import torch
+    from paper_2404_16990_b200._lib import call
+    temps = list(np.linspace(1.8, 3.0, n_sim))
+    e, o = _pair(m, n, temps, 17, window=4)
+    e._sweeps(5)
+    o.sweep(5)
+    _same(e, o)
+    p = lambda t: ctypes.c_void_p(t.data_ptr())
+    lin = torch.empty(e.packed_nbytes() // 8, dtype=torch.int64, device=e._spins.device)
+    obs = torch.zeros(2 * n_sim, dtype=torch.int64, device=e._spins.device)
+    call("msb_export", ctypes.byref(e._g), p(e._spins), p(lin), p(obs[:n_sim]), p(obs[n_sim:]), e._cs)
+    e._stream.synchronize()
+    bits = np.unpackbits(lin.cpu().numpy().view(np.uint8), bitorder="little").reshape(n_sim, m, n)
+    assert (np.where(bits == 1, 1, -1) == o.spins).all()
+    sp = o.spins
+    unsat = (sp != np.roll(sp, 1, axis=1)).sum(axis=(1, 2)) + (sp != np.roll(sp, 1, axis=2)).sum(axis=(1, 2))
+    host = obs.cpu().numpy()
+    assert (host[:n_sim] == (sp > 0).sum(axis=(1, 2))).all()
+    assert (host[n_sim:] == unsat).all()
