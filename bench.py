@@ -265,8 +265,8 @@ def run_ours(args, cfg):
 
     # end to end through the public API, host buffers both ways every step:
     # Engine.step_packed = lattices from pinned memory -> one window of sweeps
-    # -> lattices into pinned memory + observables (msb_from_linear before the
-    # window launch, one msb_export kernel after it).  The engine copies in and out
+    # -> lattices into pinned memory + observables (the layout conversions and
+    # the observables run inside the window launch, msb_window_io).  The engine copies in and out
     # on its own copy streams (double-buffered staging), so with three host
     # buffers (step k reads buffer k%3, writes (k+2)%3: two interleaved
     # chains) the copies of one step overlap the sweeps of the previous one.
@@ -325,8 +325,8 @@ def run_ours(args, cfg):
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": nbytes,
                     "d2h_bytes_per_step": nbytes + 16 * n_sim, "steps": Ke,
                     "path": "per step: Engine.step_packed(pinned host lattices in, one window of sweeps, pinned host "
-                            "lattices + observables out); msb_from_linear + one k_win launch + msb_export (lattice and "
-                            "observables in one kernel) on the engine's stream, copies on the engine's copy streams overlap the previous step (3 host buffers)"},
+                            "lattices + observables out); one k_win launch per step: every warp converts the loaded lattice "
+                            "first, the flip warps export lattice + observables after the last phase (msb_window_io), copies on the engine's copy streams overlap the previous step (3 host buffers)"},
             "gpu_launches": K,
             "clocks": sampler.summary(),
             "wall_s_timed_region": t_wall,

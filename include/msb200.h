@@ -215,6 +215,19 @@ typedef struct msb_halo {
   uint32_t *my_flags;              /* ours: [0] from the slab above, [1] from below */
   uint64_t phase0;
 } msb_halo;
+/* Host I/O fused into a flip launch (whole lattices: no halo, count > 0).
+ * lin_in: every warp of the launch first converts this linear lattice into
+ * `spins` (msb_from_linear; all its SMs share the 8 MiB of cfg2 in a few us),
+ * then the flips start.  lin_out and/or ups + unsat: after the last flip
+ * phase the flip warps export the lattice / the observables (msb_export)
+ * inside their slack behind the producers; ups and unsat are WRITTEN (zeroed
+ * in the launch), not added.  Any member may be NULL (ups and unsat go
+ * together).  Chunk groups of 4 chunks: m * ceil(n/1024) % 4 == 0. */
+typedef struct msb_window_io {
+  const uint64_t *lin_in;
+  uint64_t *lin_out;
+  int64_t *ups, *unsat;
+} msb_window_io;
 
 int msb_default_window(const msb_geom *g, int32_t *S, int32_t *P);
 int32_t msb_window_parts(const msb_geom *g, int32_t S);   /* default P for a given S */
@@ -225,7 +238,7 @@ int msb_window_init(const msb_geom *g, uint64_t seed, int32_t S, int32_t P, uint
 int msb_window_sweep(const msb_geom *g, const msb_sweep_params *p, int32_t S, int32_t P,
                      uint32_t *spins, uint32_t *states, const uint32_t *cur, int32_t first,
                      int32_t count, uint32_t *next, uint64_t *flips, const msb_halo *halo,
-                     void *stream);
+                     const msb_window_io *io, void *stream);
 
 /* ---- observables (engine.py:372-386) ------------------------------------- */
 /* Adds, per replica, the number of +1 spins and the number of unsatisfied

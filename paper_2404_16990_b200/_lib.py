@@ -73,6 +73,14 @@ class Halo(ctypes.Structure):
     ]
 
 
+class WindowIO(ctypes.Structure):
+    """msb_window_io: host I/O fused into a window flip launch (include/msb200.h)."""
+    _fields_ = [
+        ("lin_in", ctypes.c_void_p), ("lin_out", ctypes.c_void_p),
+        ("ups", ctypes.c_void_p), ("unsat", ctypes.c_void_p),
+    ]
+
+
 EXPORTS = (
     "msb_status_string", "msb_last_error", "msb_abi_version", "msb_check_geom", "msb_spin_words",
     "msb_row_pitch", "msb_pieces_per_phase", "msb_default_kg", "msb_plan_thresholds",
@@ -135,7 +143,8 @@ def lib() -> ctypes.CDLL:
         "msb_window_pieces": ([G, i32, i32], i64),
         "msb_window_words": ([G, i32], i64),
         "msb_window_init": ([G, u64, i32, i32, u64, vp, vp, vp], ctypes.c_int),
-        "msb_window_sweep": ([G, P, i32, i32, vp, vp, vp, i32, i32, vp, vp, ctypes.POINTER(Halo), vp], ctypes.c_int),
+        "msb_window_sweep": ([G, P, i32, i32, vp, vp, vp, i32, i32, vp, vp, ctypes.POINTER(Halo),
+                              ctypes.POINTER(WindowIO), vp], ctypes.c_int),
         "msb_observe": ([G, vp, vp, vp, vp], ctypes.c_int),
         "msb_export": ([G, vp, vp, vp, vp, vp], ctypes.c_int),
         "msb_draws": ([G, P, i32, vp, vp, vp], ctypes.c_int),

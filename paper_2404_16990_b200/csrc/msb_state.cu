@@ -1,7 +1,7 @@
 // libmsb200 state kernels: stream positioning, lattice initialisation,
 // layout conversions (linear / reference interop), observables, draw export
 // and slab halo packing, with their ABI entry points.
-#include "msb_common.cuh"
+#include "msb_io.cuh"
 
 namespace msbk {
 namespace {
@@ -61,114 +61,60 @@ __global__ void k_init_linear(Geo G, uint64_t seed, long long words_per_sim, con
   }
 }
 
-// Linear <-> colour-split, one warp per CPW consecutive chunks (replica, row,
-// chunk), all of one replica (CPW divides rows * nch).  A chunk is one warp
-// transpose (msb_common.cuh); a warp issues all its chunks' loads before the
-// first transpose, so CPW 128-byte requests per warp are in flight (one per
-// warp left these kernels at ~1.5 TB/s, latency-bound).
+// Linear <-> colour-split and the observables, one warp per group of CPW
+// consecutive chunks (msb_io.cuh).
 constexpr int kConvThreads = 256;
-
-__device__ __forceinline__ void next_chunk(const Geo& G, int& lr, int& ch) {
-  if (++ch == G.nch) {
-    ch = 0;
-    ++lr;
-  }
-}
 
 template <int CPW>
 __global__ void __launch_bounds__(kConvThreads) k_from_linear(Geo G, const uint32_t* __restrict__ lin,
                                                                uint32_t* __restrict__ spins, unsigned nwarps) {
   const unsigned wq = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (wq >= nwarps) return;  // warp-uniform
-  const int lane = threadIdx.x & 31, t = lane >> 1, p = lane & 1;
-  int s, lr0, ch0;
-  chunk_coords(G, wq * CPW, s, lr0, ch0);
-  uint32_t L[CPW];
-  int lr = lr0, ch = ch0;
-#pragma unroll
-  for (int j = 0; j < CPW; j++, next_chunk(G, lr, ch))
-    L[j] = lane < chunk_bits(G, ch) ? __ldcs(lin + ((size_t)s * G.rows + lr) * G.words + 32 * ch + lane) : 0u;
-  lr = lr0;
-  ch = ch0;
-#pragma unroll
-  for (int j = 0; j < CPW; j++, next_chunk(G, lr, ch)) {
-    const int c = G.row0 + lr;
-    spins[row_off(G, s, (c + p) & 1, lr + G.ghost) + ch * 16 + t] = warp_transpose32(L[j]);
-  }
+  if (wq < nwarps) from_linear_group<CPW>(G, lin, spins, wq);  // warp-uniform
 }
 
-// Colour-split -> linear and/or the observables (engine.py:372-386), one
-// pass: the warp holds both colours' words of its chunk for the transpose, so
-// the observables add only the blue rows above and below.  ups gets the +1
-// spins of both colours; unsat the unsatisfied bonds of the red sites (4
-// neighbours each, every bond once).  Red lane 2t+p0 (p0 = c&1) takes its
-// blue word t from lane ^ 1 and the second horizontal neighbour (h_second)
-// from lane +-1, or at the chunk's edge word from lane 0 / 31 plus one bit of
-// the adjacent chunk (a load).  One atomic per warp and quantity.
+// The observables are reduced per warp, then per CTA: one atomic per CTA and
+// replica run (a CTA's warps are consecutive chunk groups, so it spans one
+// replica or the boundary of two).  Per-warp atomics on the n_sim counters
+// serialised (35 us at 2 chunks per warp for cfg2).
 template <int CPW, bool LIN, bool OBS>
 __global__ void __launch_bounds__(kConvThreads) k_export(Geo G, const uint32_t* __restrict__ spins,
                                                           uint32_t* __restrict__ lin, long long* ups,
                                                           long long* unsat, unsigned nwarps) {
   const unsigned wq = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (wq >= nwarps) return;  // warp-uniform
-  const int lane = threadIdx.x & 31, t = lane >> 1, p = lane & 1;
-  int s, lr0, ch0;
-  chunk_coords(G, wq * CPW, s, lr0, ch0);
-  uint32_t W[CPW], Yu[CPW], Yd[CPW], E[CPW];
-  int lr = lr0, ch = ch0;
-#pragma unroll
-  for (int j = 0; j < CPW; j++, next_chunk(G, lr, ch)) {
-    const int c = G.row0 + lr, br = lr + G.ghost, wd = ch * 16 + t;
-    W[j] = spins[row_off(G, s, (c + p) & 1, br) + wd];
-    if (OBS) {
-      const int p0 = c & 1;
-      const bool red = p == p0;
-      int bu, bd;
-      vert_rows(G, br, bu, bd);
-      const uint32_t* blu = spins + row_off(G, s, 1, br);
-      Yu[j] = red ? spins[row_off(G, s, 1, bu) + wd] : 0u;
-      Yd[j] = red ? spins[row_off(G, s, 1, bd) + wd] : 0u;
-      // the adjacent chunk's word that supplies the edge bit
-      E[j] = 0u;
-      if (red && p0 && t == 15) E[j] = blu[(ch + 1 < G.nch ? ch + 1 : 0) * 16];
-      if (red && !p0 && t == 0) E[j] = blu[(ch > 0 ? ch - 1 : G.nch - 1) * 16 + 15];
-    }
-  }
+  int s = -1;
   uint32_t u = 0, b = 0;
-  lr = lr0;
-  ch = ch0;
-#pragma unroll
-  for (int j = 0; j < CPW; j++, next_chunk(G, lr, ch)) {
-    if (LIN) {
-      const uint32_t L = warp_transpose32(W[j]);
-      if (lane < chunk_bits(G, ch)) __stcs(lin + ((size_t)s * G.rows + lr) * G.words + 32 * ch + lane, L);
-    }
-    if (OBS) {
-      const int p0 = (G.row0 + lr) & 1;
-      const int nb = chunk_bits(G, ch);
-      const uint32_t vm = chunk_mask(G, ch);
-      const uint32_t y0 = __shfl_xor_sync(0xFFFFFFFFu, W[j], 1);
-      const uint32_t yi = __shfl_sync(0xFFFFFFFFu, W[j], p0 ? (lane + 1) & 31 : (lane + 31) & 31);
-      const uint32_t ye = __shfl_sync(0xFFFFFFFFu, W[j], p0 ? 0 : 31);
-      uint32_t hs = yi;
-      if (p0 && t == 15) hs = (ye >> 1) | ((E[j] & 1u) << (nb - 1));
-      if (!p0 && t == 0) {
-        const uint32_t carry = ch > 0 ? E[j] >> 31 : (E[j] >> (chunk_bits(G, G.nch - 1) - 1)) & 1u;
-        hs = ((ye << 1) | carry) & vm;
-      }
-      u += __popc(W[j]);
-      if (p == p0) {
-        const uint32_t o = W[j];
-        b += __popc((o ^ Yu[j]) & vm) + __popc((o ^ Yd[j]) & vm) + __popc((o ^ y0) & vm) + __popc((o ^ hs) & vm);
-      }
-    }
-  }
+  if (wq < nwarps) s = export_group<CPW, LIN, OBS, false>(G, spins, lin, wq, u, b);  // warp-uniform
   if (OBS) {
     u = __reduce_add_sync(0xFFFFFFFFu, u);
     b = __reduce_add_sync(0xFFFFFFFFu, b);
-    if (lane == 0) {
-      atomicAdd(reinterpret_cast<unsigned long long*>(ups + s), (unsigned long long)u);
-      atomicAdd(reinterpret_cast<unsigned long long*>(unsat + s), (unsigned long long)b);
+    constexpr int kW = kConvThreads / 32;
+    __shared__ int ss[kW];
+    __shared__ uint32_t su[kW], sb[kW];
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+      ss[w] = s;
+      su[w] = u;
+      sb[w] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int cur = -1;
+      unsigned long long tu = 0, tb = 0;
+      for (int i = 0; i <= kW; i++) {
+        const int si = i < kW ? ss[i] : -1;
+        if (si != cur) {
+          if (cur >= 0) {
+            atomicAdd(reinterpret_cast<unsigned long long*>(ups + cur), tu);
+            atomicAdd(reinterpret_cast<unsigned long long*>(unsat + cur), tb);
+          }
+          cur = si;
+          tu = tb = 0;
+        }
+        if (i < kW) {
+          tu += su[i];
+          tb += sb[i];
+        }
+      }
     }
   }
 }
@@ -304,9 +250,11 @@ __global__ void k_unpack_ghosts(Geo G, int X, const uint32_t* __restrict__ ghost
 
 // Chunks per warp of the conversion kernels: the largest of 8, 4, 2, 1 that
 // divides a replica's chunk count, so a warp never spans two replicas.
-int conv_cpw(const Geo& G) {
+int conv_cpw(const Geo& G, int cap) {
   const long long per = (long long)G.rows * G.nch;
-  return per % 8 == 0 ? 8 : per % 4 == 0 ? 4 : per % 2 == 0 ? 2 : 1;
+  for (int c = cap; c > 1; c >>= 1)
+    if (per % c == 0) return c;
+  return 1;
 }
 
 int check_conv(const Geo& G) {
@@ -331,8 +279,7 @@ void launch_export(const Geo& G, const uint32_t* spins, uint32_t* lin, long long
 template <bool LIN, bool OBS>
 void export_cpw(const Geo& G, const uint32_t* spins, uint32_t* lin, long long* ups, long long* unsat,
                        cudaStream_t st) {
-  switch (conv_cpw(G)) {
-    case 8: launch_export<8, LIN, OBS>(G, spins, lin, ups, unsat, st); break;
+  switch (conv_cpw(G, 4)) {  // 4 beats 8 with the observables (registers: 40 vs 80)
     case 4: launch_export<4, LIN, OBS>(G, spins, lin, ups, unsat, st); break;
     case 2: launch_export<2, LIN, OBS>(G, spins, lin, ups, unsat, st); break;
     default: launch_export<1, LIN, OBS>(G, spins, lin, ups, unsat, st); break;
@@ -392,7 +339,7 @@ int msb_from_linear(const msb_geom* g, const uint64_t* lin, uint32_t* spins, voi
   const Geo G = make_geo(g);
   if (int r = check_conv(G)) return r;
   const uint32_t* l = reinterpret_cast<const uint32_t*>(lin);
-  switch (conv_cpw(G)) {
+  switch (conv_cpw(G, 8)) {
     case 8: launch_from_linear<8>(G, l, spins, as_stream(stream)); break;
     case 4: launch_from_linear<4>(G, l, spins, as_stream(stream)); break;
     case 2: launch_from_linear<2>(G, l, spins, as_stream(stream)); break;

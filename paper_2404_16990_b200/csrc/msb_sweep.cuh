@@ -360,7 +360,11 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
 template <typename K>
 int set_smem_attr(K kernel, std::once_flag& once, cudaError_t& err) {
   std::call_once(once, [&] {
-    err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncAttributes fa = {};  // the 227 KiB per CTA include the kernel's static shared memory
+    err = cudaFuncGetAttributes(&fa, kernel);
+    if (err == cudaSuccess)
+      err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 227 * 1024 - (int)fa.sharedSizeBytes);
   });
   if (err != cudaSuccess) return fail(MSB_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(err));
   return MSB_OK;

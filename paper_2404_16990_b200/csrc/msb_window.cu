@@ -22,6 +22,7 @@
 // tail are paid once per S sweeps.  Row slabs (msb_halo) additionally push
 // their edge rows into the neighbours' ghost rows and handshake every phase.
 #include "msb_sweep.cuh"
+#include "msb_io.cuh"
 
 namespace msbk {
 namespace {
@@ -305,13 +306,70 @@ __device__ __forceinline__ void halo_gate(const HaloArgs& h, unsigned* work, int
   asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
 
+// Host I/O of a flip launch (msb_window_io): chunk groups of kIoCpw chunks.
+struct WinIO {
+  const uint32_t* lin_in;
+  uint32_t* lin_out;
+  long long *ups, *unsat;
+  unsigned ngroups;  // groups of kIoCpw chunks
+  int load16;        // rows * nch % 16 == 0: the prologue loads 16 chunks per batch
+};
+
+// Prologue share of warp w of nw (every warp of the grid): groups of CPW
+// chunks.  With CPW = 16 a cfg2 lattice is fewer groups than warps, so each
+// warp has at most one group, i.e. 16 loads in flight, and the conversion
+// takes ~the latency of one load batch.
+template <int CPW>
+__device__ __forceinline__ void win_load(const Geo& G, uint32_t* spins, const WinIO& io, unsigned w, unsigned nw) {
+  const unsigned ng = io.ngroups / (CPW / kIoCpw);
+  for (unsigned q = w; q < ng; q += nw) from_linear_group<CPW>(G, io.lin_in, spins, q);
+}
+
+// Epilogue of one flip warp (cw of nc): export its contiguous range of chunk
+// groups; observables summed per replica run, one atomic per run and warp.
+template <bool LIN, bool OBS>
+__device__ __forceinline__ void win_export(const Geo& G, const uint32_t* spins, const WinIO& io, unsigned cw,
+                                           unsigned nc) {
+  const unsigned per = (io.ngroups + nc - 1) / nc;
+  const unsigned lo = min(io.ngroups, cw * per), hi = min(io.ngroups, lo + per);
+  int cs = -1;
+  uint32_t u = 0, b = 0;
+  auto flush = [&]() {
+    if (!OBS || cs < 0) return;
+    const uint32_t tu = __reduce_add_sync(0xFFFFFFFFu, u), tb = __reduce_add_sync(0xFFFFFFFFu, b);
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(io.ups + cs), (unsigned long long)tu);
+      atomicAdd(reinterpret_cast<unsigned long long*>(io.unsat + cs), (unsigned long long)tb);
+    }
+  };
+  for (unsigned q = lo; q < hi; q++) {
+    uint32_t du = 0, db = 0;
+    const int s = export_group<kIoCpw, LIN, OBS, true>(G, spins, io.lin_out, q, du, db);
+    if (OBS && s != cs) {
+      flush();
+      cs = s;
+      u = b = 0;
+    }
+    u += du;
+    b += db;
+  }
+  flush();
+}
+
 // Window launch: warps [0, pwarps) fill the next window (pwarps = 0: no
 // production); the other warps flip slots [first, first + count) of `cur`
 // (red, barrier, blue, barrier, ...).  With a halo (slabs) every phase is
-// gated by halo_gate and all neighbour reads go through L2.
+// gated by halo_gate and all neighbour reads go through L2.  Host I/O (io,
+// whole lattices): every warp of the grid first converts io.lin_in into the
+// spins (16-chunk groups: a few us; each CTA then arrives on work[1] and only
+// the flip warps wait for all arrivals, the producers go on), and after the
+// last phase the flip warps export io.lin_out / the observables in their
+// slack behind the producers.  (The flip warps alone took ~190 us to
+// convert beside 28 producer warps per SM, and became the critical path.)
 template <int SRC, int CB, bool HALO>
 __global__ void __launch_bounds__(kRngThreads, 1) k_win(const WinArgs wa, const FlipArgs fa0, const HaloArgs ha,
-                                                        const uint32_t* cur, int first, int count, int pwarps) {
+                                                        const WinIO io, const uint32_t* cur, int first, int count,
+                                                        int pwarps) {
   extern __shared__ uint4 jt[];
 #ifdef MSB_TRACE
   MSB_TRACE_PUT(0, gtimer());
@@ -326,6 +384,31 @@ __global__ void __launch_bounds__(kRngThreads, 1) k_win(const WinArgs wa, const 
   MSB_TRACE_PUT(1, gtimer());
   MSB_TRACE_PUT(3, warp < pwarps ? 0ull : (1ull << 63));
 #endif
+  const bool pro = !HALO && io.lin_in != nullptr;
+#ifdef MSB_TRACE
+  MSB_TRACE_PUT(5, 0ull);
+#endif
+  if (pro) {
+    // each warp converts its share and reports it; the CTA's last warp posts
+    // the CTA's arrival, so a producer waits for nothing but its own share
+    __shared__ unsigned pro_done;
+    if (threadIdx.x == 0) pro_done = 0;
+    __syncthreads();
+    const unsigned w = (unsigned)warp * gridDim.x + blockIdx.x, nw = gridDim.x * (blockDim.x >> 5);
+    if (io.load16) win_load<16>(fa0.G, fa0.spins, io, w, nw);
+    else win_load<kIoCpw>(fa0.G, fa0.spins, io, w, nw);
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+      __threadfence();
+      if (atomicAdd(&pro_done, 1u) == (blockDim.x >> 5) - 1) {
+        __threadfence();
+        atomicAdd(wa.work + 1, 1u);
+      }
+    }
+#ifdef MSB_TRACE
+    MSB_TRACE_PUT(5, gtimer());  // prologue done (this CTA)
+#endif
+  }
   if (warp < pwarps) {
     win_produce<SRC, CB>(wa, jt, warp, pwarps);
   } else if (count > 0) {
@@ -344,16 +427,27 @@ __global__ void __launch_bounds__(kRngThreads, 1) k_win(const WinArgs wa, const 
     const bool leader = threadIdx.x == pwarps * 32;
     const bool gpu_leader = leader && blockIdx.x == 0;
     if (HALO) halo_gate(ha, wa.work, -1, true, nwc * 32, leader, gpu_leader);
+    const unsigned base = pro ? gridDim.x : 0u;  // the prologue's arrivals on work[1]
+    const bool epi = !HALO && (io.lin_out != nullptr || io.ups != nullptr);
+    if (!HALO && io.ups != nullptr && blockIdx.x == 0)  // written, not added (ordered by the barriers below)
+      for (int j = threadIdx.x - pwarps * 32; j < fa0.G.n_sim; j += nwc * 32) io.ups[j] = io.unsat[j] = 0;
+    if (pro) {
+      if (leader) {
+        while (ld_acquire(wa.work + 1) < base) __nanosleep(64);
+        __threadfence();
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(nwc * 32) : "memory");
+    }
     for (int i = 0; i < 2 * count; i++) {
       const int X = i & 1;
       fa.planes = cur + (size_t)(first + (i >> 1)) * wa.slot_words;
       if (band) {
         if (HALO) cnt += flip_band_run<true, true>(fa, lo, hi, X);
-        else if (i == 0) cnt += flip_band_run<false>(fa, lo, hi, X);
+        else if (i == 0 && !pro) cnt += flip_band_run<false>(fa, lo, hi, X);
         else cnt += flip_band_run<true>(fa, lo, hi, X);
       } else {
         if (HALO) cnt += flip_run<true, true>(fa, i0, hi, X);
-        else if (i == 0) cnt += flip_run<false>(fa, i0, hi, X);
+        else if (i == 0 && !pro) cnt += flip_run<false>(fa, i0, hi, X);
         else cnt += flip_run<true>(fa, i0, hi, X);
       }
       const bool more = i + 1 < 2 * count;
@@ -364,10 +458,19 @@ __global__ void __launch_bounds__(kRngThreads, 1) k_win(const WinArgs wa, const 
 #ifdef MSB_TRACE
         if (i == 0) MSB_TRACE_PUT(6, gtimer());  // first phase done (before its barrier)
 #endif
-        consumer_barrier(wa.work + 1, gridDim.x * (unsigned)(i + 1), nwc * 32, leader);
+        consumer_barrier(wa.work + 1, base + gridDim.x * (unsigned)(i + 1), nwc * 32, leader);
       }
     }
     add_flips(fa.flips, cnt);
+#ifdef MSB_TRACE
+    MSB_TRACE_PUT(7, gtimer());  // flips done (before the epilogue)
+#endif
+    if (epi) {  // every flip of the launch is done before any export read
+      consumer_barrier(wa.work + 1, base + gridDim.x * (unsigned)(2 * count), nwc * 32, leader);
+      if (io.lin_out && io.ups) win_export<true, true>(fa0.G, fa0.spins, io, cw, nc);
+      else if (io.lin_out) win_export<true, false>(fa0.G, fa0.spins, io, cw, nc);
+      else win_export<false, true>(fa0.G, fa0.spins, io, cw, nc);
+    }
   }
 #ifdef MSB_TRACE
   MSB_TRACE_PUT(2, gtimer());
@@ -523,7 +626,7 @@ int msb_window_init(const msb_geom* g, uint64_t seed, int32_t S, int32_t P, uint
 
 int msb_window_sweep(const msb_geom* g, const msb_sweep_params* p, int32_t S, int32_t P, uint32_t* spins,
                      uint32_t* states, const uint32_t* cur, int32_t first, int32_t count, uint32_t* next,
-                     uint64_t* flips, const msb_halo* halo, void* stream) {
+                     uint64_t* flips, const msb_halo* halo, const msb_window_io* io, void* stream) {
   long long np = 0;
   if (int r = check_window(g, S, P, &np)) return r;
   if (int r = check_params(p)) return r;
@@ -537,6 +640,21 @@ int msb_window_sweep(const msb_geom* g, const msb_sweep_params* p, int32_t S, in
   if (halo && (!halo->up_spins || !halo->down_spins || !halo->up_flags || !halo->down_flags || !halo->my_flags ||
                halo->up_R < 4 || halo->down_R < 4))
     return fail(MSB_ERR_ARG, "incomplete msb_halo");
+  WinIO wio = {};
+  if (io && (io->lin_in || io->lin_out || io->ups || io->unsat)) {
+    if (count == 0 || halo || g->ghost) return fail(MSB_ERR_ARG, "msb_window_io needs a flip launch of a whole lattice");
+    if ((io->ups == nullptr) != (io->unsat == nullptr)) return fail(MSB_ERR_ARG, "ups and unsat go together");
+    const Geo G = make_geo(g);
+    const long long chunks = (long long)g->n_sim * g->rows * G.nch;
+    if (((long long)g->rows * G.nch) % kIoCpw) return fail(MSB_ERR_UNSUPPORTED, "msb_window_io needs rows * chunks % 4 == 0");
+    if (32LL * chunks >= (1LL << 31)) return fail(MSB_ERR_UNSUPPORTED, "too many chunks for msb_window_io");
+    wio.lin_in = reinterpret_cast<const uint32_t*>(io->lin_in);
+    wio.lin_out = reinterpret_cast<uint32_t*>(io->lin_out);
+    wio.ups = reinterpret_cast<long long*>(io->ups);
+    wio.unsat = reinterpret_cast<long long*>(io->unsat);
+    wio.ngroups = (unsigned)(chunks / kIoCpw);
+    wio.load16 = ((long long)g->rows * G.nch) % 16 == 0;
+  }
   if (!next && count == 0) {
     if (halo) {
       k_halo_wait<<<1, 32, 0, as_stream(stream)>>>(halo->my_flags, (unsigned)halo->phase0);
@@ -610,7 +728,7 @@ int msb_window_sweep(const msb_geom* g, const msb_sweep_params* p, int32_t S, in
     static std::once_flag o_;                                                                    \
     static cudaError_t e_;                                                                       \
     if (int r = set_smem_attr(k_win<SRC, CB, HALO>, o_, e_)) return r;                          \
-    CUDA_TRY(cudaLaunchKernelEx(&cfg, k_win<SRC, CB, HALO>, wa, fa, ha, cur, first, count, pwarps)); \
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, k_win<SRC, CB, HALO>, wa, fa, ha, wio, cur, first, count, pwarps)); \
   } while (0)
 #define MSB_LAUNCH_WIN_CB(SRC, HALO)                  \
   do {                                                \

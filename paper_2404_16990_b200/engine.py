@@ -36,7 +36,7 @@ from concurrent.futures import ThreadPoolExecutor
 import numpy as np
 
 from . import _lib
-from ._lib import (call, geom, MsbError, SweepParams, MSB_FLIP_SLOTS, MSB_MAX_PLANES, MSB_MODE_GENERIC,
+from ._lib import (call, geom, MsbError, SweepParams, WindowIO, MSB_FLIP_SLOTS, MSB_MAX_PLANES, MSB_MODE_GENERIC,
                    MSB_RNG_PHILOX, MSB_RNG_XOSHIRO, MSB_SWEEP_AHEAD_IN, MSB_SWEEP_AHEAD_OUT, MSB_SWEEP_SERIAL)
 from .layout import (
     ALL_CODES, ArrayCode, LatticeDims, PackedArrays, check_spins, halo_audit_index, unpack,
@@ -482,12 +482,15 @@ class Engine:
                 return False
         return self.recorder is None and self.streams is self._own_streams
 
-    def _sweeps(self, k: int) -> None:
+    def _sweeps(self, k: int, io=None) -> None:
         """k sweeps through the library, no host sync: lookahead windows
         (FERRO/ANTI tables) or the per-sweep fused path (generic tables,
-        ``overlap = False``)."""
+        ``overlap = False``).  ``io``: a WindowIO for the window path
+        (step_packed; the caller checked ``_window_route``)."""
         if k <= 0:
             return
+        if io is not None and not self._window_route():
+            raise RuntimeError("msb_window_io outside the window path")
         if not self._fast_path_ok():
             for _ in range(k):
                 self.sweep()
@@ -496,7 +499,7 @@ class Engine:
         self._sync_tables()
         self._params.fault = int(bool(self.fault))
         if self.overlap and self._params.mode != MSB_MODE_GENERIC:
-            self._win_sweeps(k)
+            self._win_sweeps(k, io)
         elif self._pos == [self._blocks, self._blocks + 1] or self._ahead:
             self._sweep_call(k)
         else:  # per-phase positioning pending (a lone flip_red/flip_blue)
@@ -524,7 +527,12 @@ class Engine:
             self._wbuf = (states, planes, words, jump)
         return self._wbuf
 
-    def _win_launch(self, first: int, count: int, produce: bool) -> None:
+    @property
+    def _io_groups_ok(self) -> bool:
+        """msb_window_io works in groups of 4 chunks of 1024 sites."""
+        return (self.dims.m * -(-self.dims.n // 1024)) % 4 == 0
+
+    def _win_launch(self, first: int, count: int, produce: bool, io=None) -> None:
         states, planes, words, jump = self._wbuf
         cur = planes[self._wcur * words:(self._wcur + 1) * words]
         nxt = planes[(1 - self._wcur) * words:(2 - self._wcur) * words]
@@ -535,10 +543,11 @@ class Engine:
         self._params.block = self._wbase if count == 0 else self._wbase + 2 * self.window
         call("msb_window_sweep", ctypes.byref(self._g), ctypes.byref(self._params), self.window, self._wP,
              _p(self._spins), _p(states), _p(cur) if cur is not None else None, first, count,
-             _p(nxt) if produce else None, _p(self._flips_dev), None, self._cs)
+             _p(nxt) if produce else None, _p(self._flips_dev), None,
+             ctypes.byref(io) if io is not None else None, self._cs)
         self._params.jump = self._jump.data_ptr()
 
-    def _win_sweeps(self, k: int) -> None:
+    def _win_sweeps(self, k: int, io=None) -> None:
         self._win_alloc()
         S = self.window
         if self._wvalid and (self._wkey != self._tab_key or self._wbase + 2 * self._wc != self._blocks):
@@ -554,10 +563,17 @@ class Engine:
             self._wvalid, self._wkey = True, self._tab_key
         self._ahead = False
         self._pos = [None, None]   # per-phase pieces must be re-positioned before a lone phase
+        first_launch = True
         while k > 0:
             r = min(k, S - self._wc)
             finish = self._wc + r == S
-            self._win_launch(self._wc, r, finish)
+            lio = None
+            if io is not None:  # the load goes with the first flip launch, the export with the last
+                lio = WindowIO(io.lin_in if first_launch else None, None, None, None)
+                if r == k:
+                    lio.lin_out, lio.ups, lio.unsat = io.lin_out, io.ups, io.unsat
+            first_launch = False
+            self._win_launch(self._wc, r, finish, lio)
             self._blocks += 2 * r
             k -= r
             if finish:
@@ -679,19 +695,32 @@ class Engine:
         staging area, so the copy overlaps device work already queued (the
         previous sweeps); the engine's stream waits only for this copy (and
         the copy waits for any pending ``store_packed`` into ``src``)."""
-        torch = _torch()
         self._push_host_edits()
-        if isinstance(src, np.ndarray):
-            src = torch.from_numpy(np.ascontiguousarray(src).view(np.uint8).reshape(-1))
-        if src.numel() * src.element_size() != self.packed_nbytes():
-            raise ValueError(f"expected {self.packed_nbytes()} bytes of packed lattices")
+        src = self._packed_src(src)
         if src.device.type == "cuda":
             call("msb_from_linear", ctypes.byref(self._g), _p(src), _p(self._spins), self._cs)
             self._touch()
             return
+        slot = self._stage_in(src)
+        call("msb_from_linear", ctypes.byref(self._g), _p(slot["in"]), _p(self._spins), self._cs)
+        self._in_done(slot)
+        self._touch()
+
+    def _packed_src(self, src):
+        torch = _torch()
+        if isinstance(src, np.ndarray):
+            src = torch.from_numpy(np.ascontiguousarray(src).view(np.uint8).reshape(-1))
+        if src.numel() * src.element_size() != self.packed_nbytes():
+            raise ValueError(f"expected {self.packed_nbytes()} bytes of packed lattices")
+        return src
+
+    def _stage_in(self, src):
+        """Copy host ``src`` into the current staging slot on the input copy
+        stream; the engine's stream waits for it.  Returns the slot."""
+        torch = _torch()
         slot = self._io_slot()
         with torch.cuda.stream(self._in_stream):
-            if slot["in_free"] is not None:          # its last reader (msb_from_linear) is done
+            if slot["in_free"] is not None:          # its last reader is done
                 self._in_stream.wait_event(slot["in_free"])
             pending = self._host_out.pop(src.data_ptr(), None)
             if pending is not None:                  # src is still being written by a store
@@ -700,11 +729,13 @@ class Engine:
             ready = torch.cuda.Event()
             ready.record(self._in_stream)
         self._stream.wait_event(ready)
-        call("msb_from_linear", ctypes.byref(self._g), _p(slot["in"]), _p(self._spins), self._cs)
-        free = torch.cuda.Event()
+        return slot
+
+    def _in_done(self, slot) -> None:
+        """The engine's stream has enqueued the last reader of slot["in"]."""
+        free = _torch().cuda.Event()
         free.record(self._stream)
         slot["in_free"] = free
-        self._touch()
 
     def store_packed(self, dst) -> None:
         """Write every replica's lattice, bit-packed as in ``load_packed``,
@@ -725,23 +756,85 @@ class Engine:
         ``store_packed(dst)`` and ``observe_async(ups_out, unsat_out)`` (dst
         and the observables optional; pinned host tensors, asynchronous:
         ``synchronize()`` before reading them).  The copies run on the
-        engine's copy streams and overlap the sweeps of earlier steps; the
-        lattice export and the observables are one kernel (``msb_export``).
-        (Fusing the conversions / observables into the window launch was
-        measured slower: the few flip warps would carry bulk work.)"""
+        engine's copy streams and overlap the sweeps of earlier steps.  On
+        the window path the layout conversions and the observables run inside
+        the window launches (``msb_window_io``): every warp converts the
+        loaded lattice before the first flip, and the flip warps export the
+        lattice and the observables after the last one, in their slack
+        behind the producers.  Otherwise ``msb_from_linear`` and one
+        ``msb_export`` kernel run beside the sweeps."""
         if (ups_out is None) != (unsat_out is None):
             raise ValueError("ups_out and unsat_out go together")
-        self.load_packed(src)
-        self._sweeps(int(n_sweeps))
-        self._export(dst, ups_out, unsat_out)
+        n_sweeps = int(n_sweeps)
+        self._push_host_edits()
+        src = self._packed_src(src)
+        if dst is not None and dst.numel() * dst.element_size() != self.packed_nbytes():
+            raise ValueError(f"expected {self.packed_nbytes()} bytes of packed lattices")
+        if not (n_sweeps > 0 and src.device.type != "cuda" and self._window_route()):
+            self.load_packed(src)
+            self._sweeps(n_sweeps)
+            self._export(dst, ups_out, unsat_out)
+            return
+        slot = self._stage_in(src)
+        out = self._out_begin(dst, ups_out is not None)
+        io = WindowIO(_p(slot["in"]).value, out[1].value, out[2].value, out[3].value)
+        self._touch()
+        self._sweeps(n_sweeps, io)
+        self._in_done(slot)
+        self._out_end(out[0], dst, ups_out, unsat_out)
+
+    def _window_route(self) -> bool:
+        """Whether ``_sweeps`` runs on lookahead windows (msb_window_io)."""
+        self._sync_tables()
+        return (self._fast_path_ok() and self.overlap and self._params.mode != MSB_MODE_GENERIC
+                and self._io_groups_ok)
+
+    def _out_begin(self, dst, want_obs):
+        """Waits and pointers for an export into the current output staging
+        slot (dst) and/or ``_obs``: (slot, lin, ups, unsat) pointers."""
+        slot = None
+        lin = ups = uns = ctypes.c_void_p(None)
+        if dst is not None:
+            slot = self._io_slot()
+            self._io_next ^= 1
+            if slot["out_full"] is not None:         # its previous copy-out is done
+                self._stream.wait_event(slot["out_full"])
+            lin = _p(slot["out"])
+        if want_obs:
+            if getattr(self, "_obs_copied", None) is not None:  # previous copy-out of _obs done
+                self._stream.wait_event(self._obs_copied)
+            ups, uns = _p(self._obs[: self.n_sim]), _p(self._obs[self.n_sim:])
+        return slot, lin, ups, uns
+
+    def _out_end(self, slot, dst, ups_out, unsat_out) -> None:
+        """Copy the exported lattice / observables out on the output copy
+        stream once the engine's stream has produced them.  The copy stream
+        runs copies only: a kernel queued there waits behind the next
+        cooperative window launch, and every later host-buffer wait would
+        move past that window."""
+        torch = _torch()
+        written = torch.cuda.Event()
+        written.record(self._stream)
+        with torch.cuda.stream(self._out_stream):
+            self._out_stream.wait_event(written)
+            if ups_out is not None:  # first: the next step's kernel waits for it, not for the lattice copy
+                ups_out.copy_(self._obs[: self.n_sim], non_blocking=True)
+                unsat_out.copy_(self._obs[self.n_sim:], non_blocking=True)
+                self._obs_copied = torch.cuda.Event()
+                self._obs_copied.record(self._out_stream)
+            if dst is not None:
+                dst.view(torch.uint8).reshape(-1).copy_(slot["out"].view(torch.uint8), non_blocking=True)
+                done = torch.cuda.Event()
+                done.record(self._out_stream)
+                slot["out_full"] = done
+                if dst.device.type != "cuda":
+                    self._host_out[dst.data_ptr()] = done
 
     def _export(self, dst, ups_out, unsat_out) -> None:
         """``msb_export`` of the lattice (into the current output staging
         slot, then ``dst``) and/or the observables (into ``_obs``, then
-        ups_out / unsat_out), copied out on the output copy stream.  The copy
-        stream runs copies only: a kernel queued there (e.g. clearing
-        ``_obs``) waits behind the next cooperative window launch, and every
-        later host-buffer wait would move past that window."""
+        ups_out / unsat_out): one kernel on the engine's stream, copies on
+        the output copy stream."""
         torch = _torch()
         if (ups_out is None) != (unsat_out is None):
             raise ValueError("ups_out and unsat_out go together")
@@ -750,38 +843,12 @@ class Engine:
         self._push_host_edits()
         if dst is not None and dst.numel() * dst.element_size() != self.packed_nbytes():
             raise ValueError(f"expected {self.packed_nbytes()} bytes of packed lattices")
-        slot = self._io_slot()
-        lin = ctypes.c_void_p(None)
-        if dst is not None:
-            self._io_next ^= 1
-            if slot["out_full"] is not None:         # its previous copy-out is done
-                self._stream.wait_event(slot["out_full"])
-            lin = _p(slot["out"])
-        ups = uns = ctypes.c_void_p(None)
+        slot, lin, ups, uns = self._out_begin(dst, ups_out is not None)
         if ups_out is not None:
-            if getattr(self, "_obs_copied", None) is not None:  # previous copy-out of _obs done
-                self._stream.wait_event(self._obs_copied)
             with torch.cuda.stream(self._stream):
                 self._obs.zero_()
-            ups, uns = _p(self._obs[: self.n_sim]), _p(self._obs[self.n_sim:])
         call("msb_export", ctypes.byref(self._g), _p(self._spins), lin, ups, uns, self._cs)
-        written = torch.cuda.Event()
-        written.record(self._stream)
-        with torch.cuda.stream(self._out_stream):
-            self._out_stream.wait_event(written)
-            if dst is not None:
-                dst.view(torch.uint8).reshape(-1).copy_(slot["out"].view(torch.uint8), non_blocking=True)
-            if ups_out is not None:
-                ups_out.copy_(self._obs[: self.n_sim], non_blocking=True)
-                unsat_out.copy_(self._obs[self.n_sim:], non_blocking=True)
-            done = torch.cuda.Event()
-            done.record(self._out_stream)
-        if dst is not None:
-            slot["out_full"] = done
-            if dst.device.type != "cuda":
-                self._host_out[dst.data_ptr()] = done
-        if ups_out is not None:
-            self._obs_copied = done
+        self._out_end(slot, dst, ups_out, unsat_out)
 
     def _observe(self):
         self._push_host_edits()

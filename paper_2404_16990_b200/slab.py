@@ -387,7 +387,7 @@ class FusedSlabRun:
         s._params.block = self._wbase if count == 0 else self._wbase + 2 * self.S
         call("msb_window_sweep", ctypes.byref(s._g), ctypes.byref(s._params), self.S, self.P, _p(s._spins),
              _p(self._wstates), _p(cur) if cur is not None else None, first, count,
-             _p(nxt) if produce else None, _p(s._flips), ctypes.byref(self._halo), s._cs)
+             _p(nxt) if produce else None, _p(s._flips), ctypes.byref(self._halo), None, s._cs)
         s._params.jump = s._jump.data_ptr()
 
     def sweep(self, n_sweeps: int = 1) -> None:
@@ -421,7 +421,7 @@ class FusedSlabRun:
         callers with world > 1 all-reduce the result."""
         s = self.slab
         call("msb_window_sweep", ctypes.byref(s._g), ctypes.byref(s._params), self.S, self.P, None, None, None,
-             0, 0, None, None, ctypes.byref(self._halo), s._cs)
+             0, 0, None, None, ctypes.byref(self._halo), None, s._cs)
         return s.observe()
 
     def observables(self):

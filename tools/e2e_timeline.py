@@ -22,9 +22,8 @@ for k in range(K):
     ev[k][1].record(e._stream)
     e._sweeps(e.window)
     ev[k][2].record(e._stream)
-    e.store_packed(hb[(k + 2) % 3])
+    e._export(hb[(k + 2) % 3], ups, uns)   # step_packed's fused store + observe
     ev[k][3].record(e._stream)
-    e.observe_async(ups, uns)
     ev[k][4].record(e._stream)
     cpu.append((time.perf_counter() - c0) * 1e6)
 e.synchronize()
@@ -33,5 +32,4 @@ st = lambda a, b: float(np.median([ev[k][a].elapsed_time(ev[k][b]) * 1000 for k 
 gap = float(np.median([ev[k][4].elapsed_time(ev[k + 1][0]) * 1000 for k in range(5, K - 1)]))
 step = float(np.median([ev[k][0].elapsed_time(ev[k + 1][0]) * 1000 for k in range(5, K - 1)]))
 print(json.dumps({"wall_us_per_step": wall, "cpu_us_per_step_enqueue": float(np.median(cpu)),
-                  "gpu_step_us": step, "load_us": st(0, 1), "window_us": st(1, 2), "store_us": st(2, 3),
-                  "observe_us": st(3, 4), "gap_to_next_us": gap}))
+                  "gpu_step_us": step, "load_us": st(0, 1), "window_us": st(1, 2), "export_us": st(2, 3), "gap_to_next_us": gap}))

@@ -1,0 +1,38 @@
+"""Device time of one cfg2 window launch with each part of msb_window_io
+(development tool): none, lin_in only, lin_out only, observables only, all."""
+import json
+import numpy as np
+import torch
+from paper_2404_16990_b200 import Engine, LatticeDims
+from paper_2404_16990_b200._lib import WindowIO
+
+e = Engine(LatticeDims(1024, 1024), list(np.linspace(1.5, 3.5, 64)), 2024)
+S = e.window
+words = e.packed_nbytes() // 8
+lin_in = torch.empty(words, dtype=torch.int64, device=e._spins.device)
+lin_out = torch.empty_like(lin_in)
+obs = torch.zeros(128, dtype=torch.int64, device=e._spins.device)
+e._sweeps(2 * S)
+torch.cuda.synchronize()
+from paper_2404_16990_b200.engine import _p
+e.store_packed(torch.empty(e.packed_nbytes(), dtype=torch.uint8, device=e._spins.device))
+call_lin = lambda: None
+variants = {
+    "none": None,
+    "in": WindowIO(lin_in.data_ptr(), None, None, None),
+    "out": WindowIO(None, lin_out.data_ptr(), None, None),
+    "obs": WindowIO(None, None, obs[:64].data_ptr(), obs[64:].data_ptr()),
+    "all": WindowIO(lin_in.data_ptr(), lin_out.data_ptr(), obs[:64].data_ptr(), obs[64:].data_ptr()),
+}
+res = {}
+for name, io in variants.items():
+    ts = []
+    for it in range(12):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(e._stream)
+        e._sweeps(S, io)
+        b.record(e._stream)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) * 1000)
+    res[name] = round(float(np.median(ts[2:])), 1)
+print(json.dumps(res))
