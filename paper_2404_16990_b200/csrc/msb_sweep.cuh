@@ -5,6 +5,8 @@
 #pragma once
 #include "msb_common.cuh"
 
+#include <type_traits>
+
 namespace msbk {
 namespace {
 
@@ -270,8 +272,11 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
     uint32_t* orow = a.spins + (s * 2u + (unsigned)X) * colour_words + (unsigned)br0 * Wp + w0;
     const uint32_t* prow =
         a.planes + ((((unsigned)X * (unsigned)a.np) * (unsigned)G.n_sim + s) * (unsigned)G.rows + (unsigned)lr0) * Wp + w0;
-    int p = (G.row0 + lr0 + X) & 1;  // warp-uniform (H even, bands even-aligned); alternates per row
-    for (int h = 0; h < H; h++) {
+    // one row; the parity P of its red sites is a compile-time constant: bands
+    // are even-aligned with even H, so rows alternate P, !P from the band's
+    // first row and the loop below steps two rows at a time
+    auto step = [&](auto PC, int h) {
+      constexpr int P = decltype(PC)::value;
       const int lr = lr0 + h, br = br0 + h;
       const uint32_t* drow = br + 1 < G.R ? yrow + Wp : ybase;
       const uint4 D = ld4(drow);
@@ -279,7 +284,7 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
       const uint4 P4 = __ldg(reinterpret_cast<const uint4*>(prow));
       const uint4 P8 = __ldg(reinterpret_cast<const uint4*>(prow + pstride));
       uint32_t edge;
-      if (p) {  // word t0+4, or the chunk wrap: (first word >> 1) | (next chunk's bit 0 << vb-1)
+      if (P) {  // word t0+4, or the chunk wrap: (first word >> 1) | (next chunk's bit 0 << vb-1)
         const uint32_t xa = __shfl_sync(0xFFFFFFFFu, Y.x, s_next), xb = __shfl_sync(0xFFFFFFFFu, Y.x, s_first);
         edge = chunk_last ? ((xb >> 1) | ((xa & 1u) << (vb - 1))) : xa;
       } else {  // word t0-1, or the chunk wrap: ((last word << 1) | carry) & mask
@@ -296,7 +301,7 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
       uint32_t res[4];
 #pragma unroll
       for (int k = 0; k < 4; k++) {
-        const uint32_t n4 = p ? (k < 3 ? y[k + 1] : edge) : (k > 0 ? y[k - 1] : edge);
+        const uint32_t n4 = P ? (k < 3 ? y[k + 1] : edge) : (k > 0 ? y[k - 1] : edge);
         const uint32_t f = flip_word(a, false, o[k], u4[k], d4[k], y[k], n4, nullptr, 0, a4[k], a8[k]) & vm;
         res[k] = o[k] ^ f;
         cnt += __popc(f);
@@ -314,7 +319,19 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
       yrow = drow;
       orow += Wp;
       prow += Wp;
-      p ^= 1;
+    };
+    using P0 = std::integral_constant<int, 0>;
+    using P1 = std::integral_constant<int, 1>;
+    if ((G.row0 + lr0 + X) & 1) {  // warp-uniform
+      for (int h = 0; h < H; h += 2) {
+        step(P1(), h);
+        step(P0(), h + 1);
+      }
+    } else {
+      for (int h = 0; h < H; h += 2) {
+        step(P0(), h);
+        step(P1(), h + 1);
+      }
     }
   }
   return cnt;
