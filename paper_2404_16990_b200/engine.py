@@ -770,7 +770,7 @@ class Engine:
         src = self._packed_src(src)
         if dst is not None and dst.numel() * dst.element_size() != self.packed_nbytes():
             raise ValueError(f"expected {self.packed_nbytes()} bytes of packed lattices")
-        if not (n_sweeps > 0 and src.device.type != "cuda" and self._window_route()):
+        if not (n_sweeps > 0 and src.device.type != "cuda" and self._window_route() and self._io_fused_ok):
             self.load_packed(src)
             self._sweeps(n_sweeps)
             self._export(dst, ups_out, unsat_out)
@@ -784,10 +784,24 @@ class Engine:
         self._out_end(out[0], dst, ups_out, unsat_out)
 
     def _window_route(self) -> bool:
-        """Whether ``_sweeps`` runs on lookahead windows (msb_window_io)."""
+        """Whether ``_sweeps`` runs on lookahead windows."""
         self._sync_tables()
-        return (self._fast_path_ok() and self.overlap and self._params.mode != MSB_MODE_GENERIC
-                and self._io_groups_ok)
+        return self._fast_path_ok() and self.overlap and self._params.mode != MSB_MODE_GENERIC
+
+    @property
+    def _io_fused_ok(self) -> bool:
+        """Whether step_packed moves its I/O into the window launch
+        (msb_window_io): chunk groups fit, and the window's producer units
+        fit one round (the library's warp split then leaves the flip warps
+        slack behind the producers for the export).  Multi-round shapes have
+        no such slack: cfg3's fused launch measured 2092 vs 1988 us for the
+        separate kernels; cfg2's 611 vs 615 us."""
+        if not hasattr(self, "_io_fused"):
+            torch = _torch()
+            units = -(-int(_lib.lib().msb_window_pieces(ctypes.byref(self._g), self.window, self._wP)) // 32)
+            sms = torch.cuda.get_device_properties(self.device).multi_processor_count
+            self._io_fused = self._io_groups_ok and -(-units // sms) <= 30
+        return self._io_fused
 
     def _out_begin(self, dst, want_obs):
         """Waits and pointers for an export into the current output staging
