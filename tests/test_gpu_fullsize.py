@@ -1,0 +1,114 @@
+"""BASELINE.json's configurations at their full per-GPU sizes, bit-exact
+against the CPU oracle (multithreaded, so every case finishes in seconds):
+
+* cfg2: 64 replicas x 1024^2, lookahead windows vs the per-sweep ABI path vs
+  the oracle, across a partial and a full window;
+* cfg3: 754 replicas x 512^2 (many producer unit rounds per window);
+* cfg4: one 14336^2 lattice, through the whole-lattice engine and through the
+  fused slab ring (the bench's slab path, in-kernel halo exchange);
+* cfg5: one 32768^2 lattice (1.07e9 sites) through the fused slab ring.
+
+Lattices, flip counts and the integer observables are compared; the large
+lattices in row blocks to bound host memory."""
+import numpy as np
+import pytest
+
+from tests.conftest import cuda_available
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_available(), reason="needs a CUDA device")]
+
+
+def _same_rows(get_rows, want, block=2048):
+    """get_rows(): the full int8 lattice [m, n] (or [n_sim, m, n]); compared
+    with the oracle's block by block."""
+    got = get_rows()
+    assert got.shape == want.shape
+    flat_g, flat_w = got.reshape(-1, got.shape[-1]), want.reshape(-1, want.shape[-1])
+    for r in range(0, flat_g.shape[0], block):
+        assert np.array_equal(flat_g[r:r + block], flat_w[r:r + block]), f"rows {r}..{r + block}"
+
+
+def _observables_match(ups, unsat, o, sites):
+    o_ups, o_bonds = o.observe()
+    assert np.asarray(ups).tolist() == o_ups.tolist()
+    assert (2 * sites - 2 * np.asarray(unsat)).tolist() == o_bonds.tolist()
+
+
+def test_cfg2_full_size():
+    from oracle import oracle as orc
+    from paper_2404_16990_b200 import Engine, LatticeDims
+    temps = list(np.linspace(1.5, 3.5, 64))
+    dims = LatticeDims(1024, 1024)
+    win = Engine(dims, temps, 2024)
+    per = Engine(dims, temps, 2024)
+    per.overlap = False                       # msb_sweep, one launch per sweep
+    o = orc.OracleEngine(1024, 1024, temps, 2024)
+    for k in (3, win.window):                 # a partial window, then a full one
+        win._sweeps(k)
+        per._sweeps(k)
+        o.sweep(k)
+    assert win.flips == per.flips == o.flips
+    _same_rows(win.lattices, o.spins)
+    assert np.array_equal(per.lattices(), win.lattices())
+    _observables_match(*win._observe(), o, dims.sites)
+
+
+def test_cfg3_full_size():
+    from oracle import oracle as orc
+    from paper_2404_16990_b200 import Engine, LatticeDims
+    temps = list(np.random.default_rng(2024).uniform(2.0, 2.6, 754))
+    e = Engine(LatticeDims(512, 512), temps, 2024, init="all-up")
+    o = orc.OracleEngine(512, 512, temps, 2024, init="all-up")
+    e._sweeps(2)
+    o.sweep(2)
+    assert e.flips == o.flips
+    _same_rows(e.lattices, o.spins)
+    _observables_match(*e._observe(), o, 512 * 512)
+
+
+def test_cfg4_full_size_engine_and_slab_ring():
+    from oracle import oracle as orc
+    from paper_2404_16990_b200 import Engine, LatticeDims
+    from paper_2404_16990_b200.slab import FusedSlabRun, SlabLattice
+    dims = LatticeDims(14336, 14336)
+    o = orc.OracleEngine(14336, 14336, [2.269], 2024)
+    o.sweep(2)
+    e = Engine(dims, [2.269], 2024)
+    e._sweeps(2)
+    assert e.flips == o.flips
+    _same_rows(lambda: e.lattice(0), o.spins[0])
+    del e
+    slab = SlabLattice(dims, [2.269], 2024, 0, 14336)
+    run = FusedSlabRun(slab)
+    run.sweep(2)
+    assert slab.flips == o.flips
+    _same_rows(lambda: slab.lattice_rows()[0], o.spins[0])
+    _observables_match(*run.observables(), o, dims.sites)
+
+
+def test_cfg5_full_size_slab_ring():
+    from oracle import oracle as orc
+    from paper_2404_16990_b200 import LatticeDims
+    from paper_2404_16990_b200.slab import FusedSlabRun, SlabLattice
+    dims = LatticeDims(32768, 32768)
+    slab = SlabLattice(dims, [2.0], 2024, 0, 32768)
+    run = FusedSlabRun(slab)
+    run.sweep(1)
+    o = orc.OracleEngine(32768, 32768, [2.0], 2024)
+    o.sweep(1)
+    assert slab.flips == o.flips
+    _same_rows(lambda: slab.lattice_rows()[0], o.spins[0])
+    _observables_match(*run.observables(), o, dims.sites)
+
+
+def test_cfg2_full_size_philox():
+    """The counter-based stream mode at cfg2's full size (a partial window)."""
+    from oracle import oracle as orc
+    from paper_2404_16990_b200 import Engine, LatticeDims
+    temps = list(np.linspace(1.5, 3.5, 64))
+    e = Engine(LatticeDims(1024, 1024), temps, 2024, stream="philox")
+    o = orc.OracleEngine(1024, 1024, temps, 2024, stream="philox")
+    e._sweeps(2)
+    o.sweep(2)
+    assert e.flips == o.flips
+    _same_rows(e.lattices, o.spins)
