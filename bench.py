@@ -415,7 +415,11 @@ def run_slab(args, cfg):
                                                                        else "")},
             "roofline": {"bound": "int32", "achieved": achieved, "peak": peak, "unit": "Tops/s",
                          "frac": achieved / peak, "traffic": None, "kernel": "k_win (slab, in-kernel halo exchange)"},
-            "e2e": None, "gpu_launches": K * (1 + (1 if every else 0)), "clocks": sampler.summary(),
+            "e2e": None,
+            "e2e_note": "none for the slab configurations: the lattice is generated on the device from the seed "
+                        "(init='random') and stays resident; a step's only host traffic is the observables. The "
+                        "end-to-end leg (host lattices in and out every step) is the cfg2 line's.",
+            "gpu_launches": K * (1 + (1 if every else 0)), "clocks": sampler.summary(),
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
