@@ -97,7 +97,8 @@ struct FlipArgs {
   // band walk (flip_band_run): rows of QPR <= 32 quads (QPR | 32); a warp
   // group covers band_gb bands of band_h rows, lanes = (band, quad).  0: off.
   int band_h, band_gb;
-  unsigned band_groups;  // groups per colour phase (all replicas)
+  int band_sq, band_nseg;  // quads per row segment (divides 32), segments per row
+  unsigned band_groups;    // groups per colour phase (all replicas)
 };
 
 constexpr int kFlipSlots = 256;
@@ -233,17 +234,17 @@ __device__ __forceinline__ unsigned flip_quad(const FlipArgs& a, unsigned i, int
 // rows above and at the current row stay in registers (U, Y), so a step loads
 // the row below (D), the own quad (O) and the two plane quads; the horizontal
 // neighbour word at the quad edge comes from the lane holding it (shuffle),
-// including the one-bit chunk wraps of the interleaved layout.
-template <bool COHERENT, bool PUSH = false>
+// including the one-bit chunk wraps of the interleaved layout.  A row is
+// band_nseg segments of band_sq quads (band_sq | 32): lanes = (band, quad of
+// the segment); when a row has several segments, the lanes at a segment's
+// edges read their outer neighbour word from the row instead (one load).
+template <bool COHERENT, bool PUSH = false, bool SEG = false>
 __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0, unsigned g1, int X) {
   const Geo& G = a.G;
   const int lane = threadIdx.x & 31;
-  const int qpr = G.Wp >> 2;             // quads per row (divides 32)
-  const int H = a.band_h, gb = a.band_gb;
-  const int bi = lane / qpr, q = lane - bi * qpr, base = bi * qpr;
-  const int ch = q >> 2, w0 = q * 4;
-  const int vb = chunk_bits(G, ch);
-  const uint32_t vm = chunk_mask(G, ch);
+  const int sq = a.band_sq, nseg = SEG ? a.band_nseg : 1;  // quads per segment, segments per row (SEG: > 1)
+  const int H = a.band_h, gb = a.band_gb;        // rows per band, bands per warp (32 / sq)
+  const int bi = lane / sq, q = lane - bi * sq, base = bi * sq;
   const int lastbits = chunk_bits(G, G.nch - 1);
   const unsigned Wp = (unsigned)G.Wp;
   const unsigned colour_words = (unsigned)G.R * Wp;  // one colour of one replica
@@ -251,16 +252,26 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
   const unsigned groups_per_sim = (unsigned)G.rows / (unsigned)(gb * H);
   // shuffle sources (fixed per lane): next quad, this chunk's first and last
   // quads, previous quad (the previous chunk's last / the row's last quad)
-  const int s_next = base + (q + 1) % qpr, s_first = base + (q & ~3), s_last = base + (q | 3),
-            s_prev = base + (q + qpr - 1) % qpr;
+  const int s_next = base + (q + 1) % sq, s_first = base + (q & ~3), s_last = base + (q | 3),
+            s_prev = base + (q + sq - 1) % sq;
   const bool chunk_last = (q & 3) == 3, chunk_first = (q & 3) == 0;
+  const bool seg_last = SEG && q == sq - 1, seg_first = SEG && q == 0;
   auto ld4 = [](const uint32_t* p) {
     return COHERENT ? __ldcg(reinterpret_cast<const uint4*>(p)) : __ldg(reinterpret_cast<const uint4*>(p));
   };
+  auto ld1 = [](const uint32_t* p) { return COHERENT ? __ldcg(p) : __ldg(p); };
   unsigned cnt = 0;
   for (unsigned g = g0; g < g1; g++) {
-    const unsigned s = g / groups_per_sim;
-    const int lr0 = (int)(g - s * groups_per_sim) * gb * H + bi * H;  // this lane's band
+    const unsigned gr = SEG ? g / (unsigned)nseg : g;
+    const int seg = (int)(g - gr * (unsigned)nseg);
+    const unsigned s = gr / groups_per_sim;
+    const int lr0 = (int)(gr - s * groups_per_sim) * gb * H + bi * H;  // this lane's band
+    const int qg = seg * sq + q;  // quad of the row
+    const int ch = qg >> 2, w0 = qg * 4;
+    const int vb = chunk_bits(G, ch);
+    const uint32_t vm = chunk_mask(G, ch);
+    // a segment-edge lane's outer neighbour word, relative to its quad
+    const int off_next = (w0 + 4 == (int)Wp ? 0 : w0 + 4) - w0, off_prev = (w0 == 0 ? (int)Wp - 1 : w0 - 1) - w0;
     const uint32_t* ybase = a.spins + (s * 2u + (unsigned)(1 - X)) * colour_words + w0;
     const int br0 = lr0 + G.ghost;
     int bu, bd;
@@ -285,10 +296,14 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
       const uint4 P8 = __ldg(reinterpret_cast<const uint4*>(prow + pstride));
       uint32_t edge;
       if (P) {  // word t0+4, or the chunk wrap: (first word >> 1) | (next chunk's bit 0 << vb-1)
-        const uint32_t xa = __shfl_sync(0xFFFFFFFFu, Y.x, s_next), xb = __shfl_sync(0xFFFFFFFFu, Y.x, s_first);
+        uint32_t xa = __shfl_sync(0xFFFFFFFFu, Y.x, s_next);
+        const uint32_t xb = __shfl_sync(0xFFFFFFFFu, Y.x, s_first);
+        if (SEG && seg_last) xa = ld1(yrow + off_next);
         edge = chunk_last ? ((xb >> 1) | ((xa & 1u) << (vb - 1))) : xa;
       } else {  // word t0-1, or the chunk wrap: ((last word << 1) | carry) & mask
-        const uint32_t wa = __shfl_sync(0xFFFFFFFFu, Y.w, s_prev), wb = __shfl_sync(0xFFFFFFFFu, Y.w, s_last);
+        uint32_t wa = __shfl_sync(0xFFFFFFFFu, Y.w, s_prev);
+        const uint32_t wb = __shfl_sync(0xFFFFFFFFu, Y.w, s_last);
+        if (SEG && seg_first) wa = ld1(yrow + off_prev);
         const uint32_t carry = ch > 0 ? (wa >> 31) : ((wa >> (lastbits - 1)) & 1u);
         edge = chunk_first ? (((wb << 1) | carry) & vm) : wa;
       }
@@ -400,18 +415,26 @@ inline void fill_flip_args(FlipArgs& a, const msb_geom* g, const msb_sweep_param
   std::memcpy(a.code_plane, p->code_plane, 16);
   a.up_spins = a.down_spins = nullptr;
   a.up_R = a.down_R = 0;
-  // band walk geometry: lanes cover whole rows (QPR quads, QPR | 32), bands
-  // of H rows never cross a replica (H | rows / gb), H even (uniform parity)
+  // band walk geometry: lanes cover row segments of SQ quads (SQ | 32, the
+  // largest power of two dividing the row's quads: a whole row when it has
+  // at most 32), bands of H rows never cross a replica (H | rows / gb), H
+  // even (uniform parity)
   a.band_h = a.band_gb = 0;
+  a.band_sq = a.band_nseg = 0;
   a.band_groups = 0;
-  const int qpr = a.G.Wp / 4;
-  if (p->mode != MSB_MODE_GENERIC && qpr <= 32 && 32 % qpr == 0) {
-    const int gb = 32 / qpr;
+  const int qpr = a.G.Wp / 4;  // 4 * chunks: a multiple of 4
+  if (p->mode != MSB_MODE_GENERIC) {
+    int sq = 32;
+    while (sq > 4 && qpr % sq) sq >>= 1;
+    if (qpr < sq) sq = qpr;
+    const int gb = 32 / sq, nseg = qpr / sq;
     for (int h = 16; h >= 2; h >>= 1)
       if (g->rows % (gb * h) == 0) {
         a.band_h = h;
         a.band_gb = gb;
-        a.band_groups = (unsigned)((long long)g->n_sim * g->rows / (gb * h));
+        a.band_sq = sq;
+        a.band_nseg = nseg;
+        a.band_groups = (unsigned)((long long)g->n_sim * g->rows / (gb * h) * nseg);
         break;
       }
   }

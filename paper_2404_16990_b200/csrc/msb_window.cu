@@ -442,9 +442,15 @@ __global__ void __launch_bounds__(kRngThreads, 1) k_win(const WinArgs wa, const 
       const int X = i & 1;
       fa.planes = cur + (size_t)(first + (i >> 1)) * wa.slot_words;
       if (band) {
-        if (HALO) cnt += flip_band_run<true, true>(fa, lo, hi, X);
-        else if (i == 0 && !pro) cnt += flip_band_run<false>(fa, lo, hi, X);
-        else cnt += flip_band_run<true>(fa, lo, hi, X);
+        if (fa.band_nseg > 1) {  // wide rows (cfg4, cfg5): segment-edge words from memory
+          if (HALO) cnt += flip_band_run<true, true, true>(fa, lo, hi, X);
+          else if (i == 0 && !pro) cnt += flip_band_run<false, false, true>(fa, lo, hi, X);
+          else cnt += flip_band_run<true, false, true>(fa, lo, hi, X);
+        } else {
+          if (HALO) cnt += flip_band_run<true, true>(fa, lo, hi, X);
+          else if (i == 0 && !pro) cnt += flip_band_run<false>(fa, lo, hi, X);
+          else cnt += flip_band_run<true>(fa, lo, hi, X);
+        }
       } else {
         if (HALO) cnt += flip_run<true, true>(fa, i0, hi, X);
         else if (i == 0 && !pro) cnt += flip_run<false>(fa, i0, hi, X);

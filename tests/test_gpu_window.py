@@ -142,6 +142,11 @@ def test_packed_io_round_trip_and_hazards():
     (16, 4096, 1, "xoshiro"),   # 16 quads per row
     (8, 8192, 1, "philox"),     # 32 quads per row, one band per warp
     (20, 128, 3, "xoshiro"),    # rows do not split into even bands: quad walker
+    (16, 3072, 2, "xoshiro"),   # 12 quads per row: 3 segments of 4 (edge words loaded)
+    (8, 14336, 1, "philox"),    # 56 quads per row: 7 segments of 8 (cfg4 rows)
+    (8, 16384, 1, "xoshiro"),   # 64 quads per row: 2 segments of 32
+    (4, 32768, 1, "xoshiro"),   # 128 quads per row: 4 segments of 32 (cfg5 rows)
+    (16, 2080, 1, "xoshiro"),   # 3 chunks, the last one partial (1 bit): 12 quads in segments of 4
 ])
 def test_band_walk_geometries(m, n, n_sim, stream):
     """The window consumers' band walk (edge words by shuffle, chunk wraps)
