@@ -162,3 +162,35 @@ def test_power_tables_are_powers_of_two_jumps():
         one = np.empty(8192, np.uint32)
         call("msb_rng_jump_table", ctypes.c_uint64(1 << b), one.ctypes.data_as(ctypes.c_void_p))
         assert (pw[b * 8192:(b + 1) * 8192] == one).all()
+
+
+def test_window_io_argument_errors():
+    """msb_window_sweep rejects a malformed msb_window_io before any device
+    work (host-side checks only; no GPU needed)."""
+    from paper_2404_16990_b200._lib import Halo, SweepParams, WindowIO, MSB_MODE_FERRO, MSB_RNG_XOSHIRO
+    L = _lib.lib()
+    dummy = np.zeros(64, np.uint32)
+    ptr = dummy.ctypes.data
+    p = SweepParams(mode=MSB_MODE_FERRO, n_planes=2, thr9=ptr, kg=1, jump=ptr, work=ptr, rng=MSB_RNG_XOSHIRO)
+    g = geom(2, 64, 1024)
+
+    def sweep(g, first, count, io, halo=None, spins=ptr):
+        P = 8 if g.ghost else 1  # slab windows need a row per piece
+        return L.msb_window_sweep(ctypes.byref(g), ctypes.byref(p), 8, P, spins, ptr, ptr, first, count, ptr, ptr,
+                                  ctypes.byref(halo) if halo is not None else None,
+                                  ctypes.byref(io) if io is not None else None, None)
+
+    cases = [
+        (g, 0, 0, WindowIO(ptr, None, None, None), None, "needs a flip launch"),
+        (g, 0, 8, WindowIO(None, ptr, ptr, None), None, "ups and unsat go together"),
+        (geom(1, 64, 1024, row0=0, rows=16, ghost=1), 0, 8, WindowIO(ptr, None, None, None), None,
+         "flip with an msb_halo"),
+        (g, 0, 9, WindowIO(ptr, None, None, None), None, "outside the window"),
+        (g, 0, 8, None, Halo(), "msb_halo needs a slab geometry"),
+        (geom(1, 64, 1024, row0=0, rows=16, ghost=1), 0, 8, WindowIO(ptr, None, None, None),
+         Halo(up_spins=ptr, down_spins=ptr, up_R=18, down_R=18, up_flags=ptr, down_flags=ptr, my_flags=ptr),
+         "needs a flip launch of a whole lattice"),
+    ]
+    for gg, first, count, io, halo, text in cases:
+        assert sweep(gg, first, count, io, halo) == -1, text
+        assert text in L.msb_last_error().decode()
