@@ -311,15 +311,23 @@ __device__ __forceinline__ uint32_t h_second(const Geo& G, const uint32_t* y, in
 // ---------------------------------------------------------------------------
 
 // 32 x 32 bit transpose across a warp: lane i holds row i (bit j = A[i][j]);
-// afterwards lane j holds column j (bit i = A[i][j]).  Five shuffle stages
-// swap the off-diagonal blocks of size 16, 8, 4, 2, 1.
+// afterwards lane j holds column j (bit i = A[i][j]).  Five butterfly stages
+// swap the off-diagonal blocks of size s = 16, 8, 4, 2, 1 (masks m = low s
+// bits of every 2s-bit block).  A lane with bit s clear keeps x & m and takes
+// (y << s) & ~m, one with it set keeps x & ~m and takes (y >> s) & m, where y
+// is the partner's word: both are a rotation of y (by s, or by 32 - s) whose
+// wrapped bits land in the discarded positions, so a stage is SHFL + one
+// funnel rotate + one LOP3 select.
 __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x) {
   const int lane = threadIdx.x & 31;
   uint32_t m = 0x0000FFFFu;
 #pragma unroll
   for (int s = 16; s > 0; s >>= 1, m ^= m << s) {
     const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, s);
-    x = (lane & s) ? (((y >> s) & m) | (x & ~m)) : ((x & m) | ((y & m) << s));
+    const bool up = (lane & s) != 0;
+    const uint32_t keep = up ? ~m : m;
+    const uint32_t r = __funnelshift_l(y, y, up ? 32 - s : s);
+    x = (x & keep) | (r & ~keep);
   }
   return x;
 }

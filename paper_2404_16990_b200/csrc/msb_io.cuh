@@ -19,32 +19,50 @@ namespace msbk {
 
 constexpr int kIoCpw = 4;
 
-__device__ __forceinline__ void next_chunk(const Geo& G, int& lr, int& ch) {
-  if (++ch == G.nch) {
-    ch = 0;
-    ++lr;
+// Walks the consecutive chunks of one replica with 32-bit word offsets
+// (every buffer a conversion touches is < 2^31 words, msb_state.cu's
+// check_conv): lrow = linear row start, srow = colour-0 spin row start (the
+// colour-1 row is cstride further), c = lattice row, ch = chunk of the row.
+struct ChunkWalk {
+  unsigned lrow, srow;
+  int s, c, ch, br;
+  __device__ __forceinline__ ChunkWalk(const Geo& G, unsigned q, int cpw) {
+    int lr;
+    chunk_coords(G, q * (unsigned)cpw, s, lr, ch);
+    c = G.row0 + lr;
+    br = lr + G.ghost;
+    lrow = ((unsigned)s * (unsigned)G.rows + (unsigned)lr) * (unsigned)G.words;
+    srow = ((unsigned)s * 2u * (unsigned)G.R + (unsigned)br) * (unsigned)G.Wp;
   }
-}
+  __device__ __forceinline__ void next(const Geo& G) {
+    if (++ch == G.nch) {
+      ch = 0;
+      ++c;
+      ++br;
+      lrow += (unsigned)G.words;
+      srow += (unsigned)G.Wp;
+    }
+  }
+  // valid linear words of the current chunk (only a row's last chunk is partial)
+  __device__ __forceinline__ int bits(const Geo& G) const { return chunk_bits(G, ch); }
+};
 
 // Linear -> colour-split for chunk group q (engine.py:285-300 layout).
 template <int CPW>
 __device__ __forceinline__ void from_linear_group(const Geo& G, const uint32_t* __restrict__ lin,
                                                   uint32_t* __restrict__ spins, unsigned q) {
   const int lane = threadIdx.x & 31, t = lane >> 1, p = lane & 1;
-  int s, lr0, ch0;
-  chunk_coords(G, q * CPW, s, lr0, ch0);
+  const unsigned cstride = (unsigned)G.R * (unsigned)G.Wp;
+  const ChunkWalk w0(G, q, CPW);
   uint32_t L[CPW];
-  int lr = lr0, ch = ch0;
+  ChunkWalk w = w0;
 #pragma unroll
-  for (int j = 0; j < CPW; j++, next_chunk(G, lr, ch))
-    L[j] = lane < chunk_bits(G, ch) ? __ldcs(lin + ((size_t)s * G.rows + lr) * G.words + 32 * ch + lane) : 0u;
-  lr = lr0;
-  ch = ch0;
+  for (int j = 0; j < CPW; j++, w.next(G))
+    L[j] = lane < w.bits(G) ? __ldcs(lin + (w.lrow + 32u * (unsigned)w.ch + (unsigned)lane)) : 0u;
+  w = w0;
 #pragma unroll
-  for (int j = 0; j < CPW; j++, next_chunk(G, lr, ch)) {
-    const int c = G.row0 + lr;
-    spins[row_off(G, s, (c + p) & 1, lr + G.ghost) + ch * 16 + t] = warp_transpose32(L[j]);
-  }
+  for (int j = 0; j < CPW; j++, w.next(G))
+    spins[w.srow + (((w.c + p) & 1) ? cstride : 0u) + 16u * (unsigned)w.ch + (unsigned)t] = warp_transpose32(L[j]);  // unsigned index
 }
 
 // Colour-split -> linear (LIN) and/or the observables (OBS; engine.py:372-386)
@@ -63,38 +81,39 @@ __device__ __forceinline__ int export_group(const Geo& G, const uint32_t* __rest
                                             uint32_t* __restrict__ lin, unsigned q, uint32_t& u, uint32_t& b) {
   const int lane = threadIdx.x & 31, t = lane >> 1, p = lane & 1;
   auto ld = [](const uint32_t* a) { return COHERENT ? __ldcg(a) : *a; };
-  int s, lr0, ch0;
-  chunk_coords(G, q * CPW, s, lr0, ch0);
+  const unsigned Wp = (unsigned)G.Wp, cstride = (unsigned)G.R * Wp;
+  const ChunkWalk w0(G, q, CPW);
   uint32_t W[CPW], V[CPW], E[CPW];
-  int lr = lr0, ch = ch0;
+  ChunkWalk w = w0;
 #pragma unroll
-  for (int j = 0; j < CPW; j++, next_chunk(G, lr, ch)) {
-    const int c = G.row0 + lr, br = lr + G.ghost, wd = ch * 16 + t;
-    W[j] = ld(spins + row_off(G, s, (c + p) & 1, br) + wd);
+  for (int j = 0; j < CPW; j++, w.next(G)) {
+    const unsigned wd = 16u * (unsigned)w.ch + (unsigned)t;
+    W[j] = ld(spins + (w.srow + (((w.c + p) & 1) ? cstride : 0u) + wd));
     if (OBS) {
-      const int p0 = c & 1;
+      const int p0 = w.c & 1;
       const bool red = p == p0;
       int bu, bd;
-      vert_rows(G, br, bu, bd);
-      const uint32_t* blu = spins + row_off(G, s, 1, br);
-      V[j] = ld(spins + row_off(G, s, 1, red ? bu : bd) + wd);
+      vert_rows(G, w.br, bu, bd);
+      const unsigned blu = w.srow + cstride;  // the blue row of c
+      // blue word t of the row above (red lanes) / below (their blue partners)
+      // (32-bit offset arithmetic first: the row delta may be negative)
+      V[j] = ld(spins + (blu + (unsigned)((red ? bu : bd) - w.br) * Wp + wd));
       E[j] = 0u;  // the adjacent chunk's word that supplies the edge bit
-      if (red && p0 && t == 15) E[j] = ld(blu + (ch + 1 < G.nch ? ch + 1 : 0) * 16);
-      if (red && !p0 && t == 0) E[j] = ld(blu + (ch > 0 ? ch - 1 : G.nch - 1) * 16 + 15);
+      if (red && p0 && t == 15) E[j] = ld(spins + (blu + 16u * (unsigned)(w.ch + 1 < G.nch ? w.ch + 1 : 0)));
+      if (red && !p0 && t == 0) E[j] = ld(spins + (blu + 16u * (unsigned)(w.ch > 0 ? w.ch - 1 : G.nch - 1) + 15u));
     }
   }
-  lr = lr0;
-  ch = ch0;
+  w = w0;
 #pragma unroll
-  for (int j = 0; j < CPW; j++, next_chunk(G, lr, ch)) {
+  for (int j = 0; j < CPW; j++, w.next(G)) {
     if (LIN) {
       const uint32_t L = warp_transpose32(W[j]);
-      if (lane < chunk_bits(G, ch)) __stcs(lin + ((size_t)s * G.rows + lr) * G.words + 32 * ch + lane, L);
+      if (lane < w.bits(G)) __stcs(lin + (w.lrow + 32u * (unsigned)w.ch + (unsigned)lane), L);
     }
     if (OBS) {
-      const int p0 = (G.row0 + lr) & 1;
-      const int nb = chunk_bits(G, ch);
-      const uint32_t vm = chunk_mask(G, ch);
+      const int p0 = w.c & 1;
+      const int nb = w.bits(G);
+      const uint32_t vm = nb >= 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u);
       const uint32_t y0 = __shfl_xor_sync(0xFFFFFFFFu, W[j], 1);
       const uint32_t yd = __shfl_xor_sync(0xFFFFFFFFu, V[j], 1);
       const uint32_t yi = __shfl_sync(0xFFFFFFFFu, W[j], p0 ? (lane + 1) & 31 : (lane + 31) & 31);
@@ -102,7 +121,7 @@ __device__ __forceinline__ int export_group(const Geo& G, const uint32_t* __rest
       uint32_t hs = yi;
       if (p0 && t == 15) hs = (ye >> 1) | ((E[j] & 1u) << (nb - 1));
       if (!p0 && t == 0) {
-        const uint32_t carry = ch > 0 ? E[j] >> 31 : (E[j] >> (chunk_bits(G, G.nch - 1) - 1)) & 1u;
+        const uint32_t carry = w.ch > 0 ? E[j] >> 31 : (E[j] >> (chunk_bits(G, G.nch - 1) - 1)) & 1u;
         hs = ((ye << 1) | carry) & vm;
       }
       u += __popc(W[j]);
@@ -112,7 +131,7 @@ __device__ __forceinline__ int export_group(const Geo& G, const uint32_t* __rest
       }
     }
   }
-  return s;
+  return w0.s;
 }
 
 }  // namespace msbk
