@@ -224,3 +224,35 @@ def test_export_one_pass(m, n, n_sim):
     host = obs.cpu().numpy()
     assert (host[:n_sim] == (sp > 0).sum(axis=(1, 2))).all()
     assert (host[n_sim:] == unsat).all()
+
+
+def test_step_packed_fused_edge_cases():
+    """The fused path (msb_window_io) with device-side destinations, after a
+    table change (window invalid: production-only launch first), and a sweep
+    count spanning three launches; each step against the plain calls."""
+    import torch
+    from paper_2404_16990_b200 import Engine, LatticeDims
+    dims = LatticeDims(32, 2048)
+    temps = [1.9, 2.6]
+    fused, plain = Engine(dims, temps, 5, window=4), Engine(dims, temps, 5, window=4)
+    nb = fused.packed_nbytes()
+    src = torch.empty(nb, dtype=torch.uint8, pin_memory=True)
+    plain.store_packed(src)
+    plain.synchronize()
+    dev_dst = torch.empty(nb, dtype=torch.uint8, device=fused._spins.device)
+    ups = torch.zeros(2, dtype=torch.int64, device=fused._spins.device)
+    uns = torch.zeros(2, dtype=torch.int64, device=fused._spins.device)
+    for k in (3, 9, 4):
+        fused._tables[:] = fused._tables[::-1].copy() if k == 9 else fused._tables
+        plain._tables[:] = fused._tables
+        fused.step_packed(src, k, dev_dst, ups, uns)
+        plain.load_packed(src)
+        plain._sweeps(k)
+        fused.synchronize()
+        host = torch.empty(nb, dtype=torch.uint8, pin_memory=True)
+        plain.store_packed(host)
+        plain.synchronize()
+        assert (dev_dst.cpu().numpy() == host.numpy()).all(), k
+        p_ups, p_uns = plain._observe()
+        assert ups.cpu().tolist() == p_ups.tolist() and uns.cpu().tolist() == p_uns.tolist(), k
+        assert fused.flips == plain.flips
