@@ -309,7 +309,31 @@ uint32_t orc_philox_draw(uint64_t seed, uint64_t stream, uint64_t d) {
   return c[d & 3] & 0x7FFFFF;
 }
 
-typedef struct { int m, n, phase; uint64_t seed, sim_offset, block; const double *table; int8_t *spins; } pphase_ctx;
+/* Bit-plane variant (paper_2404_16990_b200.rng.PhiloxBitStreams): group
+ * g = d >> 5 of a stream has 23 plane words, from Philox blocks j = 0..5 with
+ * counter (g lo, (g hi << 3) | j, S lo, S hi | 2^31); draw d = 32g + i is
+ * the u23 whose bit 22-b is bit i of plane b. */
+static void pbits_planes(uint64_t seed, uint64_t stream, uint64_t g, uint32_t pl[24]) {
+  for (int j = 0; j < 6; j++) {
+    uint32_t c[4] = {(uint32_t)g, ((uint32_t)(g >> 32) << 3) | (uint32_t)j, (uint32_t)stream,
+                     (uint32_t)(stream >> 32) | 0x80000000u};
+    philox10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+    for (int e = 0; e < 4; e++) pl[4 * j + e] = c[e];
+  }
+}
+static uint32_t pbits_u23(const uint32_t pl[24], int i) {
+  uint32_t u = 0;
+  for (int b = 0; b < 23; b++) u |= ((pl[b] >> i) & 1u) << (22 - b);
+  return u;
+}
+uint32_t orc_pbits_draw(uint64_t seed, uint64_t stream, uint64_t d) {
+  uint32_t pl[24];
+  pbits_planes(seed, stream, d >> 5, pl);
+  return pbits_u23(pl, (int)(d & 31));
+}
+
+typedef struct { int m, n, phase; uint64_t seed, sim_offset, block; const double *table; int8_t *spins; int bits; }
+    pphase_ctx;
 static void pphase_body(long lo, long hi, void *vctx, uint64_t *acc) {
   pphase_ctx *x = (pphase_ctx *)vctx;
   const int m = x->m, n = x->n, cells = m / 4, words = n / 32, red = x->phase == 0;
@@ -320,6 +344,8 @@ static void pphase_body(long lo, long hi, void *vctx, uint64_t *acc) {
     int8_t *lat = x->spins + (uint64_t)s * sites;
     const double *tab = x->table + 16 * s;
     uint64_t d = x->block * 2 * (uint64_t)n, local = 0;
+    uint32_t pl[24];
+    uint64_t pg = ~0ull;  /* group whose planes pl holds (bit-plane stream) */
     for (int q = 0; q < 4; q++) {
       const int even = Q_EVEN[q];
       const int c = target_column(m, red, Q_FWD[q], even, g);
@@ -329,7 +355,14 @@ static void pphase_body(long lo, long hi, void *vctx, uint64_t *acc) {
       for (int k = 0; k < 16; k++) {
         const int t = 4 * (k % 4) + k / 4;
         for (int w = 0; w < words; w++, d++) {
-          const double u = (double)orc_philox_draw(x->seed, stream, d) * (1.0 / 8388608.0);
+          uint32_t u23;
+          if (x->bits) {
+            if ((d >> 5) != pg) pbits_planes(x->seed, stream, pg = d >> 5, pl);
+            u23 = pbits_u23(pl, (int)(d & 31));
+          } else {
+            u23 = orc_philox_draw(x->seed, stream, d);
+          }
+          const double u = (double)u23 * (1.0 / 8388608.0);
           const int r = 32 * w + 2 * t + p0;
           const int ru = r + 1 == n ? 0 : r + 1, rd = r == 0 ? n - 1 : r - 1;
           const int own = row[r] > 0;
@@ -346,6 +379,11 @@ static void pphase_body(long lo, long hi, void *vctx, uint64_t *acc) {
 }
 void orc_flip_phase_philox(int n_sim, int m, int n, int phase, uint64_t seed, uint64_t sim_offset, uint64_t block,
                            const double *table, int8_t *spins, uint64_t *flips) {
-  pphase_ctx x = {m, n, phase, seed, sim_offset, block, table, spins};
+  pphase_ctx x = {m, n, phase, seed, sim_offset, block, table, spins, 0};
+  *flips += par_for((long)n_sim * (m / 4), pphase_body, &x);
+}
+void orc_flip_phase_philox_bits(int n_sim, int m, int n, int phase, uint64_t seed, uint64_t sim_offset,
+                                uint64_t block, const double *table, int8_t *spins, uint64_t *flips) {
+  pphase_ctx x = {m, n, phase, seed, sim_offset, block, table, spins, 1};
   *flips += par_for((long)n_sim * (m / 4), pphase_body, &x);
 }

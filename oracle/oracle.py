@@ -53,6 +53,9 @@ def lib():
         L.orc_flip_phase_philox.argtypes = [i32, i32, i32, i32, u64, u64, u64, vp, vp, vp]
         L.orc_philox_draw.argtypes = [u64, u64, u64]
         L.orc_philox_draw.restype = ctypes.c_uint32
+        L.orc_flip_phase_philox_bits.argtypes = [i32, i32, i32, i32, u64, u64, u64, vp, vp, vp]
+        L.orc_pbits_draw.argtypes = [u64, u64, u64]
+        L.orc_pbits_draw.restype = ctypes.c_uint32
         L.orc_num_threads.restype = i32
         _lib = L
     return _lib
@@ -147,12 +150,12 @@ class OracleEngine:
 
     def sweep(self, n_sweeps: int = 1) -> None:
         tab = np.ascontiguousarray(self.tables, dtype=np.float64)
-        if self.stream == "philox":
+        if self.stream in ("philox", "philox-bits"):
+            fn = lib().orc_flip_phase_philox if self.stream == "philox" else lib().orc_flip_phase_philox_bits
             for k in range(n_sweeps):
                 for ph in (0, 1):
-                    lib().orc_flip_phase_philox(self.n_sim, self.m, self.n, ph, _u64(self.seed), self.sim_offset,
-                                                2 * (self.sweeps_done + k) + ph, _p(tab), _p(self.spins),
-                                                _p(self._flips))
+                    fn(self.n_sim, self.m, self.n, ph, _u64(self.seed), self.sim_offset,
+                       2 * (self.sweeps_done + k) + ph, _p(tab), _p(self.spins), _p(self._flips))
         else:
             lib().orc_sweeps(self.n_sim, self.m, self.n, int(n_sweeps), _p(self.states), _p(tab),
                              _p(self.spins), _p(self._flips))

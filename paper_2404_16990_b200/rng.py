@@ -12,7 +12,7 @@ from __future__ import annotations
 import numpy as np
 
 __all__ = ["Xoshiro256pp", "XoshiroStreams", "stream_state", "shape_unit_float", "DeviceStreams",
-           "philox4x32_10", "PhiloxStreams"]
+           "philox4x32_10", "PhiloxStreams", "PhiloxBitStreams", "PBITS_PLANES", "PBITS_CALLS"]
 
 _M64 = (1 << 64) - 1
 _PHI = 0x9E3779B97F4B7C15
@@ -210,4 +210,76 @@ class PhiloxStreams:
 
     def __repr__(self) -> str:
         return (f"PhiloxStreams(master_seed={self.master_seed}, n_streams={self.n_streams}, "
+                f"first_stream={self.first_stream}, position={self.position})")
+
+
+PBITS_PLANES = 23   # bit planes of a draw (u23, most significant first)
+PBITS_CALLS = 6     # Philox blocks per 32-draw group: 4 planes each, the 24th word unused
+PBITS_DOMAIN = 0x80000000  # set in the stream's high counter word: separates these blocks from PhiloxStreams'
+
+
+class PhiloxBitStreams:
+    """Counter-based stream defined by bit planes, for lazy comparison on the
+    GPU (SURVEY F1 option).
+
+    Draws come in groups of 32 consecutive draws of a stream: group g holds
+    draws 32g .. 32g+31.  Philox4x32-10 block j (0..5) of group g, with
+    counter (g lo, (g hi << 3) | j, S lo, S hi | 2^31) and key = master_seed,
+    gives four plane words, planes 4j .. 4j+3.  Draw d = 32g + i is the
+    23-bit number whose bit 22-b is bit i of plane b (b = 0..22), shaped to
+    u23 * 2**-23 like every reference draw (rng.py:180-183).
+
+    A Metropolis test u < K reads u from the most significant plane down and
+    stops at the first bit where u and K differ, so 32 draws (one plane word)
+    resolve after ~7 planes instead of 23 bits each.  The GPU generates only
+    the planes its 32 comparisons need (``Engine(stream="philox-bits")``).
+    The comparison results are the same, so this class replays it exactly
+    through the reference ``Engine`` (as ``engine.streams``, like
+    ``PhiloxStreams``).
+    """
+
+    def __init__(self, master_seed: int, n_streams: int, first_stream: int = 0, position: int = 0):
+        if n_streams < 1:
+            raise ValueError("need at least one stream")
+        self.master_seed = int(master_seed) & ((1 << 64) - 1)
+        self.n_streams = int(n_streams)
+        self.first_stream = int(first_stream)
+        self.position = int(position)
+
+    def planes(self, g0: int, groups: int) -> np.ndarray:
+        """(groups, n_streams, 24) uint32 plane words of groups g0 .. g0+groups-1."""
+        g = (int(g0) + np.arange(groups, dtype=np.uint64))[:, None]
+        sid = (self.first_stream + np.arange(self.n_streams, dtype=np.uint64))[None, :]
+        shape = (groups, self.n_streams)
+        m32 = np.uint64(0xFFFFFFFF)
+        out = np.empty(shape + (4 * PBITS_CALLS,), np.uint32)
+        for j in range(PBITS_CALLS):
+            words = philox4x32_10(np.broadcast_to(g & m32, shape),
+                                  np.broadcast_to(((g >> np.uint64(32)) << np.uint64(3)) | np.uint64(j), shape),
+                                  np.broadcast_to(sid & m32, shape),
+                                  np.broadcast_to((sid >> np.uint64(32)) | np.uint64(PBITS_DOMAIN), shape),
+                                  self.master_seed & 0xFFFFFFFF, self.master_seed >> 32)
+            for e in range(4):
+                out[:, :, 4 * j + e] = words[e]
+        return out
+
+    def raw_block(self, count: int) -> np.ndarray:
+        """(count, n_streams) uint32: the 23-bit value of each draw."""
+        d = self.position + np.arange(count, dtype=np.int64)
+        g0 = int(self.position) >> 5
+        groups = ((int(self.position) + count - 1) >> 5) - g0 + 1 if count > 0 else 0
+        pl = self.planes(g0, max(groups, 1))                  # (groups, streams, 24)
+        gi = (d >> 5) - g0
+        bit = (d & 31).astype(np.uint32)
+        u = np.zeros((count, self.n_streams), np.uint32)
+        for b in range(PBITS_PLANES):
+            u |= ((pl[gi, :, b] >> bit[:, None]) & np.uint32(1)) << np.uint32(PBITS_PLANES - 1 - b)
+        self.position += count
+        return u
+
+    def unit_block(self, count: int) -> np.ndarray:
+        return self.raw_block(count).astype(np.float64) * 2.0 ** -23
+
+    def __repr__(self) -> str:
+        return (f"PhiloxBitStreams(master_seed={self.master_seed}, n_streams={self.n_streams}, "
                 f"first_stream={self.first_stream}, position={self.position})")

@@ -30,4 +30,5 @@ def golden():
     data = {k: z[k] for k in z.files}
     data["_manifest"] = json.loads(bytes(data.pop("manifest")).decode())
     data["_philox"] = json.loads(bytes(data.pop("philox_manifest")).decode())
+    data["_pbits"] = json.loads(bytes(data.pop("pbits_manifest")).decode())
     return data

@@ -54,6 +54,17 @@ PHILOX_CASES = [
     ("px_bigseed", 4, 32, [2.0], (1 << 64) - 3, "all-up", 1.0, 0, 10, 10),
 ]
 
+# Bit-plane counter stream (PhiloxBitStreams): full 32-draw chunks, 16-draw
+# chunks (n = 512), and chunks straddling 32-draw groups (n/32 = 3, 5).
+PBITS_CASES = [
+    ("pb_12x96", 12, 96, [2.0], 31, "random", 1.0, 0, 30, 1),
+    ("pb_32x1024", 32, 1024, [1.8, 2.6], 5, "random", 1.0, 1, 12, 4),
+    ("pb_16x512", 16, 512, [2.269], 9, "random", 1.0, 0, 10, 5),
+    ("pb_8x160", 8, 160, [2.5], 3, "random", 1.0, 0, 8, 4),
+    ("pb_anti", 8, 64, [1.5], 11, "random", -1.0, 0, 10, 5),
+    ("pb_bigseed", 4, 32, [2.0], (1 << 64) - 3, "all-up", 1.0, 0, 10, 10),
+]
+
 
 def main() -> None:
     sys.path.insert(0, REF)
@@ -127,6 +138,25 @@ def main() -> None:
                                     coupling=J, sim_offset=off, n_sweeps=sweeps, measure_interval=mi))
         print(f"{name}: flips={eng.flips}", flush=True)
     data["philox_manifest"] = np.frombuffer(json.dumps(philox_manifest).encode(), np.uint8)
+
+    # Bit-plane counter stream, the same way (the reference Engine fed a
+    # PhiloxBitStreams; the GPU compares these draws plane by plane, lazily).
+    from paper_2404_16990_b200.rng import PhiloxBitStreams
+    pbits_manifest = []
+    for (name, m, n, temps, seed, init, J, off, sweeps, mi) in PBITS_CASES:
+        dims = LatticeDims(m, n)
+        eng = Engine(dims, temps, seed, init=init, coupling=J, sim_offset=off)
+        eng.streams = PhiloxBitStreams(seed, len(temps) * dims.cells, off * dims.cells)
+        traj = eng.run(sweeps, measure_interval=mi)
+        final = np.stack([eng.lattice(s) for s in range(eng.n_sim)])
+        data[f"{name}/final"] = np.packbits(final > 0, axis=-1)
+        data[f"{name}/abs_m"] = traj.abs_m
+        data[f"{name}/energy"] = traj.energy
+        data[f"{name}/flips"] = np.array([eng.flips], np.int64)
+        pbits_manifest.append(dict(name=name, m=m, n=n, temperatures=temps, seed=str(seed), init=init,
+                                   coupling=J, sim_offset=off, n_sweeps=sweeps, measure_interval=mi))
+        print(f"{name}: flips={eng.flips}", flush=True)
+    data["pbits_manifest"] = np.frombuffer(json.dumps(pbits_manifest).encode(), np.uint8)
 
     data["manifest"] = np.frombuffer(json.dumps(manifest).encode(), np.uint8)
     np.savez_compressed(OUT, **data)

@@ -94,3 +94,27 @@ def test_philox_host_stream_matches_oracle():
     for j in range(4):
         for r in range(9):
             assert blk[r, j] == orc.lib().orc_philox_draw(123, 10 + j, 37 + r)
+
+
+def test_philox_bits_oracle_matches_reference(golden):
+    """The reference Engine fed PhiloxBitStreams (tests/golden) == the
+    oracle's bit-plane Philox path, bit for bit (16- and 32-draw chunks and
+    chunks straddling 32-draw groups)."""
+    for c in golden["_pbits"]:
+        name = c["name"]
+        e = orc.OracleEngine(c["m"], c["n"], c["temperatures"], int(c["seed"]), init=c["init"],
+                             coupling=c["coupling"], sim_offset=c["sim_offset"], stream="philox-bits")
+        _, abs_m, energy = e.run(c["n_sweeps"], c["measure_interval"])
+        assert (e.spins == unpack_lattice(golden[f"{name}/final"], c["n"])).all(), name
+        assert (abs_m == golden[f"{name}/abs_m"]).all() and (energy == golden[f"{name}/energy"]).all(), name
+        assert e.flips == int(golden[f"{name}/flips"][0]), name
+
+
+def test_philox_bits_host_stream_matches_oracle():
+    from paper_2404_16990_b200.rng import PhiloxBitStreams
+    seed = (1 << 64) - 5
+    ps = PhiloxBitStreams(seed, 4, 10, position=29)
+    blk = ps.raw_block(70)   # spans three 32-draw groups
+    for j in range(4):
+        for r in range(70):
+            assert blk[r, j] == orc.lib().orc_pbits_draw(seed, 10 + j, 29 + r)
