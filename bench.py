@@ -42,6 +42,14 @@ METRIC = "spin flip attempts/sec (aggregate, device-timed)"
 UNIT = "attempts/s"
 A_INT_XOSHIRO = 27.5  # int32 ops per attempt, reference xoshiro256++ stream
 A_INT_PHILOX = 13.5   # counter-based Philox4x32-10 stream
+A_INT_PBITS = 6.0     # bit-plane Philox stream, lazily compared
+A_INT = {"xoshiro": A_INT_XOSHIRO, "philox": A_INT_PHILOX, "philox-bits": A_INT_PBITS}
+STREAM_DESC = {
+    "xoshiro": "reference xoshiro256++ (bit-exact with multispin.Engine)",
+    "philox": "counter-based Philox4x32-10 (rng.PhiloxStreams; bit-exact with multispin.Engine fed that object)",
+    "philox-bits": "counter-based bit-plane Philox4x32-10 (rng.PhiloxBitStreams; bit-exact with multispin.Engine "
+                   "fed that object; the GPU generates only the planes its comparisons need)",
+}
 A_BYTES = 0.375   # algorithmic HBM bytes per attempt
 L2_FLUSH_BYTES = 256 << 20
 
@@ -295,18 +303,19 @@ def run_ours(args, cfg):
 
     if rank == 0:
         kern_avg_s = statistics.mean(step_ms) * 1e-3
-        a_int = A_INT_PHILOX if args.stream == "philox" else A_INT_XOSHIRO
+        a_int = A_INT[args.stream]
         achieved = a_int * attempts_step / kern_avg_s / 1e12
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": args.warmup,
             "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "u32", "data": "synthetic (random +/-1 initial spins from the reference init stream)",
             "config": {
-                "workload": cfg["desc"], "m": cfg["m"], "n": cfg["n"], "replicas_per_gpu": n_sim,
+                "workload": cfg["desc"].replace("reference xoshiro256++", f"{args.stream}")
+                if args.stream != "xoshiro" else cfg["desc"], "m": cfg["m"], "n": cfg["n"], "replicas_per_gpu": n_sim,
                 "global_replicas": n_sim * ws, "attempts_per_step": attempts_step * ws,
                 "parallelism": f"replicas sharded over {ws} GPU(s), no data-path collective",
                 "l2": f"flushed between timed steps ({L2_FLUSH_BYTES >> 20} MiB write, outside the events)",
-                "stream": "reference xoshiro256++ (bit-exact with multispin.Engine)",
+                "stream": STREAM_DESC[args.stream],
                 "step": f"one lookahead window: {S} sweeps in one launch (flips of these {S} sweeps + "
                         f"accept planes of the next {S})",
                 "sweeps_per_step": S, "window_parts": eng._wP,
@@ -400,7 +409,7 @@ def run_slab(args, cfg):
     attempts_step = m * n * S
     value = attempts_step * K / (total_ms * 1e-3)
     if rank == 0:
-        a_int = A_INT_PHILOX if args.stream == "philox" else A_INT_XOSHIRO
+        a_int = A_INT[args.stream]
         achieved = a_int * (b - a) * n * S / (statistics.mean(step_ms) * 1e-3) / 1e12
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": args.warmup,
@@ -436,8 +445,9 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2")
     ap.add_argument("--kg", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--stream", choices=["xoshiro", "philox"], default="xoshiro",
-                    help="xoshiro: the reference's own streams (default); philox: counter-based (SURVEY F1)")
+    ap.add_argument("--stream", choices=sorted(A_INT), default="xoshiro",
+                    help="xoshiro: the reference's own streams (default); philox, philox-bits: counter-based "
+                         "(SURVEY F1)")
     args = ap.parse_args()
     if args.warmup < 3:  # the timing rules need >= 3 warm-up steps: do 3, report what was done
         print(f"bench.py: --warmup {args.warmup} raised to 3 (timing rules)", file=sys.stderr)

@@ -55,9 +55,15 @@ extern "C" {
  * low 23 bits of word d&3 of Philox(counter = (d>>2, S), key = seed); the
  * same stream on the host is paper_2404_16990_b200.rng.PhiloxStreams, which
  * the reference Engine accepts through its duck-typed `streams` seam
- * (engine.py:259-261, 336). */
+ * (engine.py:259-261, 336).  PHILOX_BITS: counter-based, bit-plane form:
+ * draw d = 32g + i of stream S is the u23 whose bit 22-b is bit i of plane
+ * word b (b = 0..22) of group g; plane 4j+e is word e of Philox(counter =
+ * (g lo, (g hi << 3) | j, S lo, S hi | 2^31), key = seed), j = 0..5.  The
+ * device reads only the planes its comparisons need; the host stream is
+ * paper_2404_16990_b200.rng.PhiloxBitStreams. */
 #define MSB_RNG_XOSHIRO 0
 #define MSB_RNG_PHILOX 1
+#define MSB_RNG_PHILOX_BITS 2
 
 typedef struct msb_geom {
   int32_t n_sim;      /* replicas in the buffer */
@@ -80,8 +86,8 @@ typedef struct msb_sweep_params {
   uint32_t *work;                /* device: 4 uint32 scratch counters, zeroed once by the caller;
                                     every kernel leaves them zeroed (one engine/slab per counter
                                     set: kernels sharing one must be stream-ordered) */
-  int32_t rng;                   /* MSB_RNG_XOSHIRO (reference streams) or MSB_RNG_PHILOX */
-  uint64_t seed;                 /* Philox key (the engine's master seed) */
+  int32_t rng;                   /* MSB_RNG_XOSHIRO (reference streams), _PHILOX or _PHILOX_BITS */
+  uint64_t seed;                 /* Philox key (the engine's master seed), both Philox streams */
   uint64_t block;                /* Philox: stream block (2 per sweep; red = even) of the first
                                     phase whose draws the call generates */
 } msb_sweep_params;

@@ -28,6 +28,8 @@ MSB_SWEEP_AHEAD_OUT = 2
 MSB_SWEEP_SERIAL = 4
 MSB_RNG_XOSHIRO = 0
 MSB_RNG_PHILOX = 1
+MSB_RNG_PHILOX_BITS = 2
+RNG_MODES = {"xoshiro": MSB_RNG_XOSHIRO, "philox": MSB_RNG_PHILOX, "philox-bits": MSB_RNG_PHILOX_BITS}
 
 
 class MsbError(RuntimeError):

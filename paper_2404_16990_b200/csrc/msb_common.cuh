@@ -125,6 +125,174 @@ __device__ __forceinline__ void philox10(uint32_t& c0, uint32_t& c1, uint32_t& c
   }
 }
 
+// Round keys of Philox4x32-10 for one master seed, computed on the host
+// (philox_keys): round r uses (k[2r], k[2r+1]).  Kernels take them by value
+// in their parameter block, so every XOR reads its key straight from the
+// constant bank instead of re-deriving it per call.
+struct PhiloxKeys {
+  uint32_t k[20];
+};
+
+inline PhiloxKeys philox_keys(uint64_t seed) {
+  PhiloxKeys K;
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  for (int r = 0; r < 10; r++, k0 += 0x9E3779B9u, k1 += 0xBB67AE85u) {
+    K.k[2 * r] = k0;
+    K.k[2 * r + 1] = k1;
+  }
+  return K;
+}
+
+constexpr uint32_t kPhiloxM0 = 0xD2511F53u, kPhiloxM1 = 0xCD9E8D57u;
+
+__device__ __forceinline__ void philox_round(uint32_t& c0, uint32_t& c1, uint32_t& c2, uint32_t& c3, uint32_t k0,
+                                             uint32_t k1) {
+  // plain XORs (not the asm xor3): the key can stay a constant-bank operand
+  const uint64_t p0 = (uint64_t)c0 * kPhiloxM0, p1 = (uint64_t)c2 * kPhiloxM1;
+  const uint32_t n0 = (uint32_t)(p1 >> 32) ^ k0 ^ c1, n2 = (uint32_t)(p0 >> 32) ^ k1 ^ c3;
+  c1 = (uint32_t)p1;
+  c3 = (uint32_t)p0;
+  c0 = n0;
+  c2 = n2;
+}
+
+// Bit b of the 32-bit key as an all-lanes mask, recomputed at its point of
+// use (volatile: hoisted out of the group loop, the 46 masks spill).
+__device__ __forceinline__ uint32_t key_mask(uint32_t key, int b) {
+  uint32_t m;
+  asm volatile("{.reg .b32 t;\n\tshl.b32 t, %1, %2;\n\tshr.s32 %0, t, 31;}" : "=r"(m) : "r"(key), "r"(b));
+  return m;
+}
+
+// philox10 with host-computed round keys.
+__device__ __forceinline__ void philox10k(uint32_t& c0, uint32_t& c1, uint32_t& c2, uint32_t& c3,
+                                          const PhiloxKeys& K) {
+#pragma unroll
+  for (int r = 0; r < 10; r++) philox_round(c0, c1, c2, c3, K.k[2 * r], K.k[2 * r + 1]);
+}
+
+// Bit-plane Philox stream (paper_2404_16990_b200.rng.PhiloxBitStreams):
+// group g of stream S = draws 32g .. 32g+31; Philox block j (0..5) with
+// counter (g lo, (g hi << 3) | j, S lo, S hi | 2^31) gives planes 4j .. 4j+3;
+// bit i of plane b is bit 22-b of draw 32g+i.  pbits_group resolves the 32
+// comparisons u23 < K_p most significant plane first and stops generating
+// planes once every comparison is decided (~7-8 planes instead of 23 bits
+// per draw).  key[p] = K_p << 9 (kKeyAlways when K_p = 2^23, 0 when K_p = 0);
+// acc[p] bit i = [draw 32g+i < K_p].  A comparison still open after plane 22
+// is u == K: rejected.
+//
+// The six blocks of a group differ only in the low bits of counter word 1,
+// so the first three rounds are largely shared: round 1 entirely (block j
+// only XORs j into its output word 0), round 2's word-2 product and round
+// 3's word-0 product.  A block then costs 16 IMAD.WIDE + 17 LOP3.
+constexpr uint32_t kPbitsDomain = 0x80000000u;
+
+struct PbitsLane {  // per stream: its id words and the stream-constant round-1 product
+  uint32_t s0, s1d, h1, l1;  // s1d = S hi | domain; (h1, l1) = S lo * M1
+};
+
+__device__ __forceinline__ PbitsLane pbits_lane(uint32_t s0, uint32_t s1) {
+  PbitsLane L;
+  L.s0 = s0;
+  L.s1d = s1 | kPbitsDomain;
+  const uint64_t p = (uint64_t)s0 * kPhiloxM1;
+  L.h1 = (uint32_t)(p >> 32);
+  L.l1 = (uint32_t)p;
+  return L;
+}
+
+template <int NPMAX>
+__device__ __forceinline__ void pbits_group(unsigned long long g, const PbitsLane& L, const PhiloxKeys& K,
+                                            const uint32_t (&key)[NPMAX], int np, uint32_t (&acc)[NPMAX]) {
+  uint32_t und[NPMAX], any = 0;
+#pragma unroll
+  for (int p = 0; p < NPMAX; p++) {
+    const bool on = p < np && key[p] != 0xFFFFFFFFu && key[p] != 0u;  // K = 2^23 / K = 0: decided
+    und[p] = on ? 0xFFFFFFFFu : 0u;
+    acc[p] = (p < np && key[p] == 0xFFFFFFFFu) ? 0xFFFFFFFFu : 0u;
+    any |= und[p];
+  }
+  if (!any) return;
+  // round 1 (keys 0, 1): c0 = base ^ j, c1 = l1, c2 = r1c2, c3 = r1c3
+  const uint64_t q0 = (uint64_t)(uint32_t)g * kPhiloxM0;
+  const uint32_t base = L.h1 ^ K.k[0] ^ ((uint32_t)(g >> 32) << 3);
+  const uint32_t r1c2 = (uint32_t)(q0 >> 32) ^ K.k[1] ^ L.s1d, r1c3 = (uint32_t)q0;
+  // round 2, shared half: c0' = hi(r1c2 M1) ^ l1 ^ k2, c1' = lo(r1c2 M1)
+  const uint64_t q1 = (uint64_t)r1c2 * kPhiloxM1;
+  const uint32_t r2c0 = (uint32_t)(q1 >> 32) ^ K.k[2] ^ L.l1, r2c1 = (uint32_t)q1;
+  // round 3, shared product: r2c0 M0
+  const uint64_t q2 = (uint64_t)r2c0 * kPhiloxM0;
+  const uint32_t q2h = (uint32_t)(q2 >> 32), q2l = (uint32_t)q2;
+#pragma unroll
+  for (int j = 0; j < 6; j++) {
+    if (j > 0 && !any) break;
+    // round 2, block half
+    const uint64_t pj = (uint64_t)(base ^ (uint32_t)j) * kPhiloxM0;
+    const uint32_t r2c2 = (uint32_t)(pj >> 32) ^ K.k[3] ^ r1c3, r2c3 = (uint32_t)pj;
+    // round 3
+    const uint64_t p3 = (uint64_t)r2c2 * kPhiloxM1;
+    uint32_t x0 = (uint32_t)(p3 >> 32) ^ K.k[4] ^ r2c1, x1 = (uint32_t)p3;
+    uint32_t x2 = q2h ^ K.k[5] ^ r2c3, x3 = q2l;
+#pragma unroll
+    for (int r = 3; r < 10; r++) philox_round(x0, x1, x2, x3, K.k[2 * r], K.k[2 * r + 1]);
+    const uint32_t xs[4] = {x0, x1, x2, x3};
+    any = 0;
+#pragma unroll
+    for (int p = 0; p < NPMAX; p++) {
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        const int b = 4 * j + e;
+        if (b < 23) {
+          const uint32_t km = key_mask(key[p], b);                       // bit 22-b of K, all lanes
+          acc[p] |= und[p] & ~xs[e] & km;                                // u bit 0, K bit 1: u < K
+          und[p] &= ~(xs[e] ^ km);                                       // still equal
+        }
+      }
+      any |= und[p];
+    }
+  }
+}
+
+// Accept bits of draws [d0, d0 + L) (1 <= L <= 32) of one stream: bit i =
+// draw d0 + i.  Straddles at most two groups.
+template <int NPMAX>
+__device__ __forceinline__ void pbits_chunk(unsigned long long d0, int L, const PbitsLane& S, const PhiloxKeys& K,
+                                            const uint32_t (&key)[NPMAX], int np, uint32_t (&acc)[NPMAX]) {
+  const int o = (int)(d0 & 31);
+  pbits_group<NPMAX>(d0 >> 5, S, K, key, np, acc);
+  if (o) {
+#pragma unroll
+    for (int p = 0; p < NPMAX; p++) acc[p] >>= o;
+    if (o + L > 32) {
+      uint32_t hi[NPMAX];
+      pbits_group<NPMAX>((d0 >> 5) + 1, S, K, key, np, hi);
+#pragma unroll
+      for (int p = 0; p < NPMAX; p++) acc[p] |= hi[p] << (32 - o);
+    }
+  }
+  const uint32_t mask = L >= 32 ? 0xFFFFFFFFu : ((1u << L) - 1u);
+#pragma unroll
+  for (int p = 0; p < NPMAX; p++) acc[p] &= mask;
+}
+
+// u23 of draw d (debug / record path): all 23 planes of its group.
+__device__ __forceinline__ uint32_t pbits_draw(unsigned long long d, uint32_t s0, uint32_t s1, uint32_t k0,
+                                               uint32_t k1) {
+  const unsigned long long g = d >> 5;
+  const int i = (int)(d & 31);
+  uint32_t u = 0;
+  for (int j = 0; j < 6; j++) {
+    uint32_t x0 = (uint32_t)g, x1 = ((uint32_t)(g >> 32) << 3) | (uint32_t)j, x2 = s0, x3 = s1 | kPbitsDomain;
+    philox10(x0, x1, x2, x3, k0, k1);
+    const uint32_t xs[4] = {x0, x1, x2, x3};
+    for (int e = 0; e < 4; e++) {
+      const int b = 4 * j + e;
+      if (b < 23) u |= ((xs[e] >> i) & 1u) << (22 - b);
+    }
+  }
+  return u;
+}
+
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {  // rng.py:53-58
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;

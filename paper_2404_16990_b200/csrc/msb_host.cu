@@ -38,7 +38,7 @@ int check_params(const msb_sweep_params* p) {
   if (p->mode < 0 || p->mode > 2) return fail(MSB_ERR_ARG, "bad mode");
   if (p->n_planes > 0 && !p->thr9) return fail(MSB_ERR_ARG, "null thresholds");
   if (!p->work) return fail(MSB_ERR_ARG, "null work counter (4 zeroed uint32 per engine)");
-  if (p->rng != MSB_RNG_XOSHIRO && p->rng != MSB_RNG_PHILOX) return fail(MSB_ERR_ARG, "unknown rng");
+  if (p->rng != MSB_RNG_XOSHIRO && p->rng != MSB_RNG_PHILOX && p->rng != MSB_RNG_PHILOX_BITS) return fail(MSB_ERR_ARG, "unknown rng");
   return MSB_OK;
 }
 

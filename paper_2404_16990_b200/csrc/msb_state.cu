@@ -221,6 +221,13 @@ __global__ void k_draws(Geo G, int X, int kg, int kr, long long npieces, const u
   const unsigned long long sid = ((unsigned long long)G.sim_offset + s) * (unsigned long long)(G.m / 4) + rs.gamma - 1;
   const unsigned long long n = (unsigned long long)G.n;
   const unsigned long long d0 = block * 2 * n + (unsigned long long)rs.q * (n / 2);
+  if (philox == 2) {  // bit-plane form
+    for (int k = kgi * kr; k < (kgi + 1) * kr; k++)
+      for (int w = 0; w < G.words; w++)
+        o[(size_t)k * G.words + w] =
+            pbits_draw(d0 + (unsigned long long)k * G.words + w, (uint32_t)sid, (uint32_t)(sid >> 32), seed_lo, seed_hi);
+    return;
+  }
   for (int k = kgi * kr; k < (kgi + 1) * kr; k++)
     for (int w = 0; w < G.words; w++) {
       const unsigned long long d = d0 + (unsigned long long)k * G.words + w, cc = d >> 2;
@@ -411,7 +418,7 @@ int msb_draws(const msb_geom* g, const msb_sweep_params* p, int32_t phase, const
   const Geo G = make_geo(g);
   const long long np = (long long)g->n_sim * g->rows * kg;
   k_draws<<<blocks_for(np, 128), 128, 0, as_stream(stream)>>>(G, phase, kg, 16 / kg, np, states,
-                                                              p->rng == MSB_RNG_PHILOX, (uint32_t)p->seed,
+                                                              p->rng == MSB_RNG_PHILOX ? 1 : p->rng == MSB_RNG_PHILOX_BITS ? 2 : 0, (uint32_t)p->seed,
                                                               (uint32_t)(p->seed >> 32), p->block, out);
   CUDA_TRY(cudaGetLastError());
   return MSB_OK;

@@ -31,6 +31,7 @@ struct RngArgs {
   FastDiv pieces_div;
   uint32_t seed_lo, seed_hi;  // Philox key
   unsigned long long block0;  // Philox: stream block of colour0's phase
+  PhiloxKeys pk;              // Philox round keys
 };
 
 // static (interleaved across CTAs), later ones come from work[0].
@@ -121,13 +122,20 @@ __device__ __forceinline__ void rng_produce(const RngArgs& a, const uint4* __res
         uint32_t acc[NPMAX];
 #pragma unroll
         for (int p = 0; p < NPMAX; p++) acc[p] = 0;
-        if (SRC == kSrcPhilox) {
+        if (SRC == kSrcPbits) {  // accept bits straight from the bit planes
+          pbits_chunk<NPMAX>(pd0 + (unsigned long long)k * G.words + 32 * ch, L, pbits_lane(ps0, ps1), a.pk, key, np,
+                             acc);
+#pragma unroll
+          for (int p = 0; p < NPMAX; p++)
+            if (p < np) out[p * pstride + ch * 16 + t] = acc[p];
+          continue;
+        } else if (SRC == kSrcPhilox) {
           const unsigned long long d0 = pd0 + (unsigned long long)k * G.words + 32 * ch;
           if ((d0 & 3) == 0 && (L & 3) == 0) {
             for (int i = 0; i < L; i += 4) {
               const unsigned long long c = (d0 + i) >> 2;
               uint32_t x0 = (uint32_t)c, x1 = (uint32_t)(c >> 32), x2 = ps0, x3 = ps1;
-              philox10(x0, x1, x2, x3, a.seed_lo, a.seed_hi);
+              philox10k(x0, x1, x2, x3, a.pk);
               const uint32_t xs[4] = {x0, x1, x2, x3};
 #pragma unroll
               for (int j = 0; j < 4; j++) {
@@ -141,7 +149,7 @@ __device__ __forceinline__ void rng_produce(const RngArgs& a, const uint4* __res
             for (int i = 0; i < L; i++) {
               const unsigned long long d = d0 + i, c = d >> 2;
               uint32_t x0 = (uint32_t)c, x1 = (uint32_t)(c >> 32), x2 = ps0, x3 = ps1;
-              philox10(x0, x1, x2, x3, a.seed_lo, a.seed_hi);
+              philox10k(x0, x1, x2, x3, a.pk);
               const int e = (int)(d & 3);
               const uint32_t h9 = (e == 0 ? x0 : e == 1 ? x1 : e == 2 ? x2 : x3) << 9;
 #pragma unroll
@@ -349,6 +357,7 @@ void fill_rng_args(RngArgs& a, const msb_geom* g, const msb_sweep_params* p, int
   a.seed_lo = (uint32_t)p->seed;
   a.seed_hi = (uint32_t)(p->seed >> 32);
   a.block0 = p->block;
+  a.pk = philox_keys(p->seed);
 }
 
 
@@ -364,7 +373,7 @@ int rng_planes(const msb_geom* g, const msb_sweep_params* p, int colour, uint32_
   const long long per_cta = kRngThreads / 32;
   (void)per_cta;
   const unsigned grid = (unsigned)std::max(1LL, std::min<long long>(sms, units));
-  const size_t smem = (ext || p->rng == MSB_RNG_PHILOX) ? 0 : (size_t)kJumpWords * 4;
+  const size_t smem = (ext || p->rng != MSB_RNG_XOSHIRO) ? 0 : (size_t)kJumpWords * 4;
 #define MSB_LAUNCH_RNG(NP, SRC, FULL)                                         \
   do {                                                                        \
     static std::once_flag o;                                                  \
@@ -372,16 +381,20 @@ int rng_planes(const msb_geom* g, const msb_sweep_params* p, int colour, uint32_
     if (int r = set_smem_attr(k_rng_planes<NP, SRC, FULL>, o, e)) return r;   \
     k_rng_planes<NP, SRC, FULL><<<grid, kRngThreads, smem, st>>>(a);          \
   } while (0)
-  const int src = ext ? kSrcExt : (p->rng == MSB_RNG_PHILOX ? kSrcPhilox : kSrcXoshiro);
+  const int src = ext ? kSrcExt
+                      : (p->rng == MSB_RNG_PHILOX ? kSrcPhilox
+                                                  : (p->rng == MSB_RNG_PHILOX_BITS ? kSrcPbits : kSrcXoshiro));
   const bool full = (a.G.words % 32) == 0;
   if (p->mode != MSB_MODE_GENERIC) {
     if (src == kSrcExt) MSB_LAUNCH_RNG(2, kSrcExt, false);
     else if (src == kSrcPhilox) MSB_LAUNCH_RNG(2, kSrcPhilox, false);
+    else if (src == kSrcPbits) MSB_LAUNCH_RNG(2, kSrcPbits, false);
     else if (full) MSB_LAUNCH_RNG(2, kSrcXoshiro, true);
     else MSB_LAUNCH_RNG(2, kSrcXoshiro, false);
   } else {
     if (src == kSrcExt) MSB_LAUNCH_RNG(MSB_MAX_PLANES, kSrcExt, false);
     else if (src == kSrcPhilox) MSB_LAUNCH_RNG(MSB_MAX_PLANES, kSrcPhilox, false);
+    else if (src == kSrcPbits) MSB_LAUNCH_RNG(MSB_MAX_PLANES, kSrcPbits, false);
     else MSB_LAUNCH_RNG(MSB_MAX_PLANES, kSrcXoshiro, false);
   }
 #undef MSB_LAUNCH_RNG
@@ -404,17 +417,18 @@ int fused_sweep(const msb_geom* g, const msb_sweep_params* p, uint32_t* spins, u
   int dev = 0, sms = 148;
   CUDA_TRY(cudaGetDevice(&dev));
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const bool philox = p->rng == MSB_RNG_PHILOX;
+  const bool philox = p->rng == MSB_RNG_PHILOX, pbits = p->rng == MSB_RNG_PHILOX_BITS;
   const bool full = (fa.G.words % 32) == 0;
-  static std::once_flag o, o2, o3;
-  static cudaError_t e, e2, e3;
+  static std::once_flag o, o2, o3, o4;
+  static cudaError_t e, e2, e3, e4;
   if (int r = set_smem_attr(k_sweep_fused<2, kSrcXoshiro, false>, o, e)) return r;
   if (int r = set_smem_attr(k_sweep_fused<2, kSrcPhilox, false>, o2, e2)) return r;
   if (int r = set_smem_attr(k_sweep_fused<2, kSrcXoshiro, true>, o3, e3)) return r;
+  if (int r = set_smem_attr(k_sweep_fused<2, kSrcPbits, false>, o4, e4)) return r;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)sms);
   cfg.blockDim = dim3(kRngThreads);
-  cfg.dynamicSmemBytes = philox ? 0 : (size_t)kJumpWords * 4;
+  cfg.dynamicSmemBytes = (philox || pbits) ? 0 : (size_t)kJumpWords * 4;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
@@ -422,6 +436,7 @@ int fused_sweep(const msb_geom* g, const msb_sweep_params* p, uint32_t* spins, u
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (philox) CUDA_TRY(cudaLaunchKernelEx(&cfg, k_sweep_fused<2, kSrcPhilox, false>, ra, fa));
+  else if (pbits) CUDA_TRY(cudaLaunchKernelEx(&cfg, k_sweep_fused<2, kSrcPbits, false>, ra, fa));
   else if (full) CUDA_TRY(cudaLaunchKernelEx(&cfg, k_sweep_fused<2, kSrcXoshiro, true>, ra, fa));
   else CUDA_TRY(cudaLaunchKernelEx(&cfg, k_sweep_fused<2, kSrcXoshiro, false>, ra, fa));
   return MSB_OK;

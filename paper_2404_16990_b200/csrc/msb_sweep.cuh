@@ -14,6 +14,7 @@ namespace {
 constexpr int kSrcXoshiro = 0;  // persistent per-piece reference streams
 constexpr int kSrcExt = 1;      // host-supplied u23 draws
 constexpr int kSrcPhilox = 2;   // counter-based Philox4x32-10
+constexpr int kSrcPbits = 3;    // counter-based Philox4x32-10, bit-plane form (lazy comparisons)
 
 // reference bit t of a uint16 word is gated by draw k = 4(t%4) + t/4 (the
 // mapping is its own inverse, engine.py:326-330)

@@ -40,6 +40,7 @@ struct WinArgs {
   FastDiv streams_div, cells_div, sims_div;
   uint32_t seed_lo, seed_hi;    // Philox key
   unsigned long long block0;    // stream block of slot 0's first phase
+  PhiloxKeys pk;                // Philox round keys
 };
 
 // One 32-bit word of the jump: 8 nibble lookups (paired 3-input XORs) from the
@@ -71,9 +72,20 @@ __device__ __forceinline__ void jump_word(const uint4* __restrict__ jt, int& nib
 // Philox: draw d of stream id (st.a1:st.a0) is word d&3 of block (d>>2, id);
 // pd is the stream draw index of this k's first draw.
 template <int SRC, int CB>
-__device__ __forceinline__ void win_segment_k(const WinArgs& a, XState& st, uint32_t* outk, uint32_t key0,
-                                              uint32_t key1, size_t pstride, unsigned long long pd) {
+__device__ __forceinline__ void win_segment_k(const WinArgs& a, XState& st, const PbitsLane& pl, uint32_t* outk,
+                                              uint32_t key0, uint32_t key1, size_t pstride, unsigned long long pd) {
   const Geo& G = a.G;
+  if (SRC == kSrcPbits) {  // accept bits straight from the bit planes (bit i = draw i)
+    const uint32_t key[2] = {key0, key1};
+    for (int ch = 0; ch < G.nch; ch++) {
+      uint32_t acc[2];
+      if (CB == 32) pbits_group<2>((pd >> 5) + ch, pl, a.pk, key, 2, acc);
+      else pbits_chunk<2>(pd + 32ull * ch, CB ? CB : chunk_bits(G, ch), pl, a.pk, key, 2, acc);
+      outk[ch * 16] = acc[0];
+      outk[pstride + ch * 16] = acc[1];
+    }
+    return;
+  }
   for (int ch = 0; ch < G.nch; ch++) {
     const int L = CB ? CB : chunk_bits(G, ch);  // CB: compile-time chunk width (32, 16) or 0
     uint32_t acc0 = 0, acc1 = 0;
@@ -106,7 +118,7 @@ __device__ __forceinline__ void win_segment_k(const WinArgs& a, XState& st, uint
         for (int i = 0; i < L; i += 4) {
           const unsigned long long c = (d0 + i) >> 2;
           uint32_t x0 = (uint32_t)c, x1 = (uint32_t)(c >> 32), x2 = st.a0, x3 = st.a1;
-          philox10(x0, x1, x2, x3, a.seed_lo, a.seed_hi);
+          philox10k(x0, x1, x2, x3, a.pk);
           const uint32_t xs[4] = {x0, x1, x2, x3};
 #pragma unroll
           for (int q = 0; q < 4; q++) {
@@ -119,7 +131,7 @@ __device__ __forceinline__ void win_segment_k(const WinArgs& a, XState& st, uint
         for (int i = 0; i < L; i++) {
           const unsigned long long d = d0 + i, c = d >> 2;
           uint32_t x0 = (uint32_t)c, x1 = (uint32_t)(c >> 32), x2 = st.a0, x3 = st.a1;
-          philox10(x0, x1, x2, x3, a.seed_lo, a.seed_hi);
+          philox10k(x0, x1, x2, x3, a.pk);
           const int e = (int)(d & 3);
           const uint32_t h9 = (e == 0 ? x0 : e == 1 ? x1 : e == 2 ? x2 : x3) << 9;
           acc_reject(acc0, h9, key0);
@@ -202,6 +214,7 @@ __device__ __forceinline__ void win_produce(const WinArgs& a, const uint4* __res
       const uint32_t key0 = a.thr9[w.s], key1 = a.thr9[G.n_sim + w.s];
       uint32_t* slot = a.planes + (size_t)w.j * a.slot_words;
       XState st;
+      PbitsLane pl = {0, 0, 0, 0};
       uint32_t jw[8] = {0, 0, 0, 0, 0, 0, 0, 0}, r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       int nib = 0, jacc = 0;
       if (XO) {
@@ -213,15 +226,31 @@ __device__ __forceinline__ void win_produce(const WinArgs& a, const uint4* __res
             ((unsigned long long)G.sim_offset + (unsigned long long)w.s) * cells + w.gamma - 1;
         st.a0 = (uint32_t)sid;
         st.a1 = (uint32_t)(sid >> 32);
+        if (SRC == kSrcPbits) pl = pbits_lane(st.a0, st.a1);
       }
       for (int sg = 0; sg < a.nseg; sg++) {
         const int seg = w.seg + sg, X = seg >> 2, q = seg & 3;
         const int lr = w.lr >= 0 ? w.lr : seg_row(G.m, w.gamma, X, q);
         uint32_t* out = slot + plane_off(G, 2, X, 0, w.s, lr);
         const unsigned long long pseg = (a.block0 + 2ull * w.j + X) * 2 * n + (unsigned long long)q * (n / 2);
+        if (SRC == kSrcPbits && CB == 16 && !(a.kr & 1)) {
+          // n = 512: one bit-plane group is the 16 draws of k (even) and of
+          // k + 1 -- resolve it once for both rows of plane words
+          const uint32_t key[2] = {key0, key1};
+          for (int kk = 0; kk < a.kr; kk += 2) {
+            const int k = w.k0 + kk;
+            uint32_t acc[2];
+            pbits_group<2>((pseg + (unsigned long long)k * 16) >> 5, pl, a.pk, key, 2, acc);
+            out[t_of_k(k)] = acc[0] & 0xFFFFu;
+            out[pstride + t_of_k(k)] = acc[1] & 0xFFFFu;
+            out[t_of_k(k + 1)] = acc[0] >> 16;
+            out[pstride + t_of_k(k + 1)] = acc[1] >> 16;
+          }
+          continue;
+        }
         for (int kk = 0; kk < a.kr; kk++) {
           const int k = w.k0 + kk;
-          win_segment_k<SRC, CB>(a, st, out + t_of_k(k), key0, key1, pstride,
+          win_segment_k<SRC, CB>(a, st, pl, out + t_of_k(k), key0, key1, pstride,
                                    pseg + (unsigned long long)k * G.words);
           if (XO) {  // the 8 jump words, spread evenly over the piece's kit k-iterations
             jacc += 8;
@@ -550,6 +579,7 @@ void fill_win_args(WinArgs& w, const msb_geom* g, const msb_sweep_params* p, int
   w.seed_lo = (uint32_t)p->seed;
   w.seed_hi = (uint32_t)(p->seed >> 32);
   w.block0 = p->block;
+  w.pk = philox_keys(p->seed);
 }
 
 }  // namespace
@@ -715,14 +745,14 @@ int msb_window_sweep(const msb_geom* g, const msb_sweep_params* p, int32_t S, in
     }
     if (env_pw > 0) pwarps = std::min(32, env_pw);
   }
-  const bool philox = p->rng == MSB_RNG_PHILOX;
+  const bool philox = p->rng == MSB_RNG_PHILOX, pbits = p->rng == MSB_RNG_PHILOX_BITS;
   // compile-time chunk width: every chunk 32 draws (n/32 % 32 == 0), a
   // single 16-draw chunk (n = 512), or generic
   const int cb = (wa.G.words % 32) == 0 ? 32 : (wa.G.words == 16 ? 16 : 0);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)sms);
   cfg.blockDim = dim3(kRngThreads);
-  cfg.dynamicSmemBytes = (philox || pwarps == 0) ? 0 : (size_t)kJumpWords * 4;
+  cfg.dynamicSmemBytes = (philox || pbits || pwarps == 0) ? 0 : (size_t)kJumpWords * 4;
   cfg.stream = as_stream(stream);
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
@@ -744,9 +774,11 @@ int msb_window_sweep(const msb_geom* g, const msb_sweep_params* p, int32_t S, in
   } while (0)
   if (ha.on) {
     if (philox) MSB_LAUNCH_WIN_CB(kSrcPhilox, true);
+    else if (pbits) MSB_LAUNCH_WIN_CB(kSrcPbits, true);
     else MSB_LAUNCH_WIN_CB(kSrcXoshiro, true);
   } else {
     if (philox) MSB_LAUNCH_WIN_CB(kSrcPhilox, false);
+    else if (pbits) MSB_LAUNCH_WIN_CB(kSrcPbits, false);
     else MSB_LAUNCH_WIN_CB(kSrcXoshiro, false);
   }
 #undef MSB_LAUNCH_WIN_CB

@@ -37,12 +37,12 @@ import numpy as np
 
 from . import _lib
 from ._lib import (call, geom, MsbError, SweepParams, WindowIO, MSB_FLIP_SLOTS, MSB_MAX_PLANES, MSB_MODE_GENERIC,
-                   MSB_RNG_PHILOX, MSB_RNG_XOSHIRO, MSB_SWEEP_AHEAD_IN, MSB_SWEEP_AHEAD_OUT, MSB_SWEEP_SERIAL)
+                   MSB_RNG_PHILOX, MSB_RNG_XOSHIRO, RNG_MODES, MSB_SWEEP_AHEAD_IN, MSB_SWEEP_AHEAD_OUT, MSB_SWEEP_SERIAL)
 from .layout import (
     ALL_CODES, ArrayCode, LatticeDims, PackedArrays, check_spins, halo_audit_index, unpack,
 )
 from .observables import Trajectory
-from .rng import DeviceStreams, PhiloxStreams
+from .rng import DeviceStreams, PhiloxBitStreams, PhiloxStreams
 
 __all__ = ["FLIP_RED", "FLIP_BLUE", "build_exp_table", "Engine", "run_simulations"]
 
@@ -158,7 +158,9 @@ class Engine:
     "xoshiro" (default) draws the reference's own xoshiro256++ streams;
     "philox" draws the counter-based ``rng.PhiloxStreams``, which
     the reference Engine reproduces bit-exactly when handed the same object
-    as its ``streams``.
+    as its ``streams``; "philox-bits" draws ``rng.PhiloxBitStreams``, the
+    bit-plane form whose comparisons the GPU resolves from the most
+    significant plane down, generating only the planes they need.
     """
 
     def __init__(self, dims: LatticeDims, temperatures, seed: int, init: str = "random",
@@ -176,8 +178,8 @@ class Engine:
         self._tables = np.stack([build_exp_table(t, coupling) for t in self.temperatures])
         if init not in ("random", "all-up"):
             raise ValueError(f"unknown init mode {init!r} (expected 'random' or 'all-up')")
-        if stream not in ("xoshiro", "philox"):
-            raise ValueError(f"unknown stream {stream!r} (expected 'xoshiro' or 'philox')")
+        if stream not in RNG_MODES:
+            raise ValueError(f"unknown stream {stream!r} (expected 'xoshiro', 'philox' or 'philox-bits')")
         self.stream = stream
 
         torch = _torch()
@@ -207,7 +209,7 @@ class Engine:
         self._params.jump = self._jump.data_ptr()
         self._params.thr9 = self._thr.data_ptr()
         self._params.work = self._work.data_ptr()
-        self._params.rng = MSB_RNG_PHILOX if stream == "philox" else MSB_RNG_XOSHIRO
+        self._params.rng = RNG_MODES[stream]
         self._params.seed = self.seed & _M64
         self._tab_key = None
         self.fault = 0  # test-only adder corruption (selftest seam, cli.py:467-480)
@@ -241,7 +243,8 @@ class Engine:
                  ctypes.c_uint64(0), -1, _p(self._pow), _p(self._states), self._cs)
             self.streams = DeviceStreams(self.seed, self.n_sim * dims.cells, self.sim_offset * dims.cells)
         else:
-            self.streams = PhiloxStreams(self.seed, self.n_sim * dims.cells, self.sim_offset * dims.cells)
+            cls = PhiloxStreams if stream == "philox" else PhiloxBitStreams
+            self.streams = cls(self.seed, self.n_sim * dims.cells, self.sim_offset * dims.cells)
         self._own_streams = self.streams
         self._blocks = 0        # stream blocks consumed (one per colour phase)
         self._pos = [0, 1]      # block each colour's pieces are positioned at

@@ -34,7 +34,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from ._lib import call, geom, SweepParams, MSB_FLIP_SLOTS, MSB_MAX_PLANES, MSB_RNG_PHILOX, MSB_RNG_XOSHIRO
+from ._lib import call, geom, SweepParams, MSB_FLIP_SLOTS, MSB_MAX_PLANES, MSB_RNG_PHILOX, MSB_RNG_XOSHIRO, RNG_MODES
 from .engine import _M64, _jump_table, _p, _pow_tables, _sweep_jump_table, _torch, build_exp_table
 from .layout import LatticeDims
 
@@ -103,10 +103,10 @@ class SlabLattice:
         p.mode, p.n_planes = mode.value, npl.value
         p.code_plane[:] = list(codes)
         p.thr9, p.kg, p.jump, p.work = self._thr.data_ptr(), self.kg, self._jump.data_ptr(), self._work.data_ptr()
-        if stream not in ("xoshiro", "philox"):
+        if stream not in RNG_MODES:
             raise ValueError(f"unknown stream {stream!r}")
         self.stream = stream
-        p.rng = MSB_RNG_PHILOX if stream == "philox" else MSB_RNG_XOSHIRO
+        p.rng = RNG_MODES[stream]
         p.seed = self.seed & _M64
         self._params = p
         if init == "random":

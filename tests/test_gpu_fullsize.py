@@ -101,13 +101,14 @@ def test_cfg5_full_size_slab_ring():
     _observables_match(*run.observables(), o, dims.sites)
 
 
-def test_cfg2_full_size_philox():
-    """The counter-based stream mode at cfg2's full size (a partial window)."""
+@pytest.mark.parametrize("stream", ["philox", "philox-bits"])
+def test_cfg2_full_size_philox(stream):
+    """The counter-based stream modes at cfg2's full size (a partial window)."""
     from oracle import oracle as orc
     from paper_2404_16990_b200 import Engine, LatticeDims
     temps = list(np.linspace(1.5, 3.5, 64))
-    e = Engine(LatticeDims(1024, 1024), temps, 2024, stream="philox")
-    o = orc.OracleEngine(1024, 1024, temps, 2024, stream="philox")
+    e = Engine(LatticeDims(1024, 1024), temps, 2024, stream=stream)
+    o = orc.OracleEngine(1024, 1024, temps, 2024, stream=stream)
     e._sweeps(2)
     o.sweep(2)
     assert e.flips == o.flips

@@ -172,27 +172,31 @@ def test_forced_tables():
 
 # ---- counter-based stream ------------------------------------------
 
-def test_philox_reference_runs_bit_exact(golden):
-    """Engine(stream="philox") == the reference Engine fed PhiloxStreams."""
+@pytest.mark.parametrize("stream,cases", [("philox", "_philox"), ("philox-bits", "_pbits")])
+def test_philox_reference_runs_bit_exact(golden, stream, cases):
+    """Engine(stream="philox") == the reference Engine fed PhiloxStreams;
+    Engine(stream="philox-bits") == the reference Engine fed PhiloxBitStreams."""
     from paper_2404_16990_b200 import Engine, LatticeDims
-    for c in golden["_philox"]:
+    for c in golden[cases]:
         name = c["name"]
         e = Engine(LatticeDims(c["m"], c["n"]), c["temperatures"], int(c["seed"]), init=c["init"],
-                   coupling=c["coupling"], sim_offset=c["sim_offset"], stream="philox")
+                   coupling=c["coupling"], sim_offset=c["sim_offset"], stream=stream)
         traj = e.run(c["n_sweeps"], c["measure_interval"])
         assert (e.lattices() == unpack_lattice(golden[f"{name}/final"], c["n"])).all(), name
         assert (traj.abs_m == golden[f"{name}/abs_m"]).all() and (traj.energy == golden[f"{name}/energy"]).all()
         assert e.flips == int(golden[f"{name}/flips"][0]), name
 
 
+@pytest.mark.parametrize("stream", ["philox", "philox-bits"])
 @pytest.mark.parametrize("m,n,n_sim,sweeps", [(64, 1024, 2, 3), (1024, 1024, 2, 2), (96, 14336, 1, 2),
-                                              (36, 96, 3, 5), (20, 160, 2, 4)])
-def test_philox_vs_oracle_shapes(m, n, n_sim, sweeps):
+                                              (36, 96, 3, 5), (20, 160, 2, 4), (32, 512, 3, 9),
+                                              (8, 2048, 1, 3)])
+def test_philox_vs_oracle_shapes(m, n, n_sim, sweeps, stream):
     from oracle import oracle as orc
     from paper_2404_16990_b200 import Engine, LatticeDims
     temps = list(np.linspace(1.8, 3.0, n_sim))
-    e = Engine(LatticeDims(m, n), temps, seed=77, sim_offset=2, stream="philox")
-    o = orc.OracleEngine(m, n, temps, 77, sim_offset=2, stream="philox")
+    e = Engine(LatticeDims(m, n), temps, seed=77, sim_offset=2, stream=stream)
+    o = orc.OracleEngine(m, n, temps, 77, sim_offset=2, stream=stream)
     e.run(sweeps, measure_interval=1)
     o.sweep(sweeps)
     assert (e.lattices() == o.spins).all()
@@ -200,16 +204,18 @@ def test_philox_vs_oracle_shapes(m, n, n_sim, sweeps):
     assert (e.energy_per_spin() == o.energy_per_spin()).all()
 
 
-def test_philox_phase_by_phase_and_external_streams():
-    """Manual phases, the recorder and an external PhiloxStreams object (host
-    draws through the duck-typed seam) all agree with the fused path."""
+@pytest.mark.parametrize("stream", ["philox", "philox-bits"])
+def test_philox_phase_by_phase_and_external_streams(stream):
+    """Manual phases, the recorder and an external PhiloxStreams /
+    PhiloxBitStreams object (host draws through the duck-typed seam) all
+    agree with the fused path."""
     from paper_2404_16990_b200 import Engine, LatticeDims
-    from paper_2404_16990_b200.rng import PhiloxStreams
+    from paper_2404_16990_b200.rng import PhiloxBitStreams, PhiloxStreams
     dims = LatticeDims(32, 128)
-    a = Engine(dims, [2.1, 2.6], seed=5, stream="philox")
-    b = Engine(dims, [2.1, 2.6], seed=5, stream="philox")
+    a = Engine(dims, [2.1, 2.6], seed=5, stream=stream)
+    b = Engine(dims, [2.1, 2.6], seed=5, stream=stream)
     c = Engine(dims, [2.1, 2.6], seed=5)             # xoshiro engine, streams swapped
-    c.streams = PhiloxStreams(5, 2 * dims.cells, 0)
+    c.streams = (PhiloxStreams if stream == "philox" else PhiloxBitStreams)(5, 2 * dims.cells, 0)
     a.run(6, measure_interval=3)
     for _ in range(6):
         b.flip_red()
@@ -236,3 +242,29 @@ def test_fault_injection_is_detected():
         o.sweep(5)
         assert (e.lattices() != o.spins).any(), f"fault not visible (generic={generic})"
         e.fault = 0
+
+
+@pytest.mark.parametrize("stream", ["philox", "philox-bits"])
+def test_counter_streams_generic_and_forced_tables(stream):
+    """Generic tables (more than two thresholds, incl. 0 and 1 entries) and a
+    J<0 engine on the counter-based streams: the per-sweep producer with up
+    to MSB_MAX_PLANES keys, against the oracle."""
+    from oracle import oracle as orc
+    from paper_2404_16990_b200 import Engine, LatticeDims
+    e = Engine(LatticeDims(20, 160), [2.0, 2.7], seed=99, stream=stream)
+    o = orc.OracleEngine(20, 160, [2.0, 2.7], 99, stream=stream)
+    e._tables[:, 1] = 0.3
+    o.tables[:, 1] = 0.3
+    e._tables[:, 3] = 0.0        # K = 0: never accepted
+    o.tables[:, 3] = 0.0
+    e._tables[0, 12] = 0.61
+    o.tables[0, 12] = 0.61
+    assert e.flip_mode == 2
+    e.run(7, measure_interval=7)
+    o.sweep(7)
+    assert (e.lattices() == o.spins).all() and e.flips == o.flips
+    a = Engine(LatticeDims(16, 1024), [1.7, 3.3], seed=4, coupling=-1.0, stream=stream)
+    b = orc.OracleEngine(16, 1024, [1.7, 3.3], 4, coupling=-1.0, stream=stream)
+    a.run(10, measure_interval=5)
+    b.sweep(10)
+    assert (a.lattices() == b.spins).all() and a.flips == b.flips

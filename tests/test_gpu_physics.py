@@ -39,10 +39,11 @@ def test_criterion5_tc_crossing_256():
     assert crossing is not None and 2.1 <= crossing <= 2.45, (crossing, TC_OVER_J)
 
 
-def test_criterion4_philox_stream():
-    """The counter-based stream samples the same physics."""
+@pytest.mark.parametrize("stream", ["philox", "philox-bits"])
+def test_criterion4_philox_stream(stream):
+    """The counter-based streams sample the same physics."""
     from paper_2404_16990_b200 import Engine, LatticeDims, onsager_magnetization
-    eng = Engine(LatticeDims(128, 128), (1.5, 2.0), seed=SEED, init="all-up", stream="philox")
+    eng = Engine(LatticeDims(128, 128), (1.5, 2.0), seed=SEED, init="all-up", stream=stream)
     traj = eng.run(20_000, measure_interval=100)
     means = traj.abs_m[traj.n_measurements // 5:].mean(axis=0)
     assert abs(means[0] - onsager_magnetization(1.5)) <= 0.01

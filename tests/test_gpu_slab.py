@@ -49,7 +49,8 @@ def test_slabs_large_rows_vs_oracle():
 # ---- fused slab windows (in-kernel halo exchange, msb_halo) ---------------------
 
 @pytest.mark.parametrize("m,n,n_sim,stream,window", [
-    (16, 128, 2, "xoshiro", None), (16, 128, 2, "philox", None), (64, 1024, 1, "xoshiro", 3),
+    (16, 128, 2, "xoshiro", None), (16, 128, 2, "philox", None), (16, 128, 2, "philox-bits", None),
+    (64, 1024, 1, "xoshiro", 3), (32, 14336, 1, "philox-bits", 3),
     (12, 96, 3, "xoshiro", 2), (32, 14336, 1, "xoshiro", None),
 ])
 def test_fused_slab_single_ring_vs_oracle(m, n, n_sim, stream, window):

@@ -26,7 +26,7 @@ def _same(e, o):
 
 
 @pytest.mark.parametrize("window", [1, 2, 3, 8])
-@pytest.mark.parametrize("stream", ["xoshiro", "philox"])
+@pytest.mark.parametrize("stream", ["xoshiro", "philox", "philox-bits"])
 def test_window_lengths(window, stream):
     """Partial windows (11 sweeps, measured every 3) for several S."""
     e, o = _pair(32, 160, [1.9, 2.4, 3.1], 41, window=window, stream=stream)
@@ -37,11 +37,13 @@ def test_window_lengths(window, stream):
     assert list(traj.sweeps) == [3, 6, 9, 11]
 
 
-@pytest.mark.parametrize("m,n,n_sim", [(64, 1024, 3), (8, 32768, 1), (36, 96, 2)])
-def test_window_shapes(m, n, n_sim):
-    """Full chunks (n/32 % 32 == 0), many chunks per k, and partial chunks."""
+@pytest.mark.parametrize("stream", ["xoshiro", "philox-bits"])
+@pytest.mark.parametrize("m,n,n_sim", [(64, 1024, 3), (8, 32768, 1), (36, 96, 2), (32, 512, 5)])
+def test_window_shapes(m, n, n_sim, stream):
+    """Full chunks (n/32 % 32 == 0), many chunks per k, partial chunks and
+    16-draw chunks (n = 512: a bit-plane group spans two k)."""
     temps = list(np.linspace(1.7, 3.2, n_sim))
-    e, o = _pair(m, n, temps, 5)
+    e, o = _pair(m, n, temps, 5, stream=stream)
     e._sweeps(2 * e.window + 1)
     o.sweep(2 * e.window + 1)
     _same(e, o)
@@ -77,7 +79,7 @@ def test_window_table_change_and_lone_phases():
     assert e.flips == o.flips
 
 
-@pytest.mark.parametrize("stream", ["xoshiro", "philox"])
+@pytest.mark.parametrize("stream", ["xoshiro", "philox", "philox-bits"])
 def test_per_sweep_fused_abi_path(stream):
     """msb_sweep's cooperative per-sweep kernel (flips of sweep k beside the
     planes of k+1), reached through the ABI directly."""
@@ -144,6 +146,8 @@ def test_packed_io_round_trip_and_hazards():
     (20, 128, 3, "xoshiro"),    # rows do not split into even bands: quad walker
     (16, 3072, 2, "xoshiro"),   # 12 quads per row: 3 segments of 4 (edge words loaded)
     (8, 14336, 1, "philox"),    # 56 quads per row: 7 segments of 8 (cfg4 rows)
+    (8, 14336, 1, "philox-bits"),
+    (16, 96, 2, "philox-bits"),
     (8, 16384, 1, "xoshiro"),   # 64 quads per row: 2 segments of 32
     (4, 32768, 1, "xoshiro"),   # 128 quads per row: 4 segments of 32 (cfg5 rows)
     (16, 2080, 1, "xoshiro"),   # 3 chunks, the last one partial (1 bit): 12 quads in segments of 4
