@@ -246,6 +246,22 @@ int msb_window_sweep(const msb_geom *g, const msb_sweep_params *p, int32_t S, in
                      int32_t count, uint32_t *next, uint64_t *flips, const msb_halo *halo,
                      const msb_window_io *io, void *stream);
 
+/* Direct sweeps (MSB_RNG_PHILOX_BITS, FERRO/ANTI tables): no accept planes.
+ * One cooperative launch flips n_sweeps sweeps (red, blue, ... separated by
+ * grid barriers) with every warp of every SM; each word's Metropolis tests
+ * are decided from its neighbour classes, and only the sites with
+ * Delta E > 0 compare their draw (bit planes generated on demand, most
+ * significant first) against the Delta E = 4|J| or 8|J| key.  p->block is the
+ * stream block of the first sweep's red phase (2 per sweep).  halo / io as in
+ * msb_window_sweep.  The draws are those of PhiloxBitStreams, so results
+ * equal the window path and the reference Engine fed that stream.
+ * msb_direct_ok: 1 if (g, p) can take this path (n/32 % 32 == 0 or n = 512,
+ * rows in bands of 2 x 32/quads-per-row), else 0.  Replaces: engine.py:353-360
+ * (Engine.sweep) for the counter-based stream. */
+int msb_direct_ok(const msb_geom *g, const msb_sweep_params *p);
+int msb_direct_sweep(const msb_geom *g, const msb_sweep_params *p, uint32_t *spins, int32_t n_sweeps,
+                     uint64_t *flips, const msb_halo *halo, const msb_window_io *io, void *stream);
+
 /* ---- observables (engine.py:372-386) ------------------------------------- */
 /* Adds, per replica, the number of +1 spins and the number of unsatisfied
  * bonds owned by the held rows (bonds of red sites) into ups[n_sim] and

@@ -201,6 +201,43 @@ __device__ __forceinline__ PbitsLane pbits_lane(uint32_t s0, uint32_t s1) {
   return L;
 }
 
+// The group-shared part of rounds 1-3 of a group's blocks.
+struct PbitsPrefix {
+  uint32_t base, r1c3, r2c1, q2h, q2l;
+};
+
+__device__ __forceinline__ PbitsPrefix pbits_prefix(unsigned long long g, const PbitsLane& L, const PhiloxKeys& K) {
+  PbitsPrefix f;
+  // round 1 (keys 0, 1): c0 = base ^ j, c1 = l1, c2 = r1c2, c3 = r1c3
+  const uint64_t q0 = (uint64_t)(uint32_t)g * kPhiloxM0;
+  f.base = L.h1 ^ K.k[0] ^ ((uint32_t)(g >> 32) << 3);
+  const uint32_t r1c2 = (uint32_t)(q0 >> 32) ^ K.k[1] ^ L.s1d;
+  f.r1c3 = (uint32_t)q0;
+  // round 2, shared half: c0' = hi(r1c2 M1) ^ l1 ^ k2, c1' = lo(r1c2 M1)
+  const uint64_t q1 = (uint64_t)r1c2 * kPhiloxM1;
+  const uint32_t r2c0 = (uint32_t)(q1 >> 32) ^ K.k[2] ^ L.l1;
+  f.r2c1 = (uint32_t)q1;
+  // round 3, shared product: r2c0 M0
+  const uint64_t q2 = (uint64_t)r2c0 * kPhiloxM0;
+  f.q2h = (uint32_t)(q2 >> 32);
+  f.q2l = (uint32_t)q2;
+  return f;
+}
+
+// Block j of a group: planes 4j .. 4j+3.
+__device__ __forceinline__ void pbits_block(const PbitsPrefix& f, int j, const PhiloxKeys& K, uint32_t (&xs)[4]) {
+  // round 2, block half
+  const uint64_t pj = (uint64_t)(f.base ^ (uint32_t)j) * kPhiloxM0;
+  const uint32_t r2c2 = (uint32_t)(pj >> 32) ^ K.k[3] ^ f.r1c3, r2c3 = (uint32_t)pj;
+  // round 3
+  const uint64_t p3 = (uint64_t)r2c2 * kPhiloxM1;
+  uint32_t x0 = (uint32_t)(p3 >> 32) ^ K.k[4] ^ f.r2c1, x1 = (uint32_t)p3;
+  uint32_t x2 = f.q2h ^ K.k[5] ^ r2c3, x3 = f.q2l;
+#pragma unroll
+  for (int r = 3; r < 10; r++) philox_round(x0, x1, x2, x3, K.k[2 * r], K.k[2 * r + 1]);
+  xs[0] = x0; xs[1] = x1; xs[2] = x2; xs[3] = x3;
+}
+
 template <int NPMAX>
 __device__ __forceinline__ void pbits_group(unsigned long long g, const PbitsLane& L, const PhiloxKeys& K,
                                             const uint32_t (&key)[NPMAX], int np, uint32_t (&acc)[NPMAX]) {
@@ -213,29 +250,12 @@ __device__ __forceinline__ void pbits_group(unsigned long long g, const PbitsLan
     any |= und[p];
   }
   if (!any) return;
-  // round 1 (keys 0, 1): c0 = base ^ j, c1 = l1, c2 = r1c2, c3 = r1c3
-  const uint64_t q0 = (uint64_t)(uint32_t)g * kPhiloxM0;
-  const uint32_t base = L.h1 ^ K.k[0] ^ ((uint32_t)(g >> 32) << 3);
-  const uint32_t r1c2 = (uint32_t)(q0 >> 32) ^ K.k[1] ^ L.s1d, r1c3 = (uint32_t)q0;
-  // round 2, shared half: c0' = hi(r1c2 M1) ^ l1 ^ k2, c1' = lo(r1c2 M1)
-  const uint64_t q1 = (uint64_t)r1c2 * kPhiloxM1;
-  const uint32_t r2c0 = (uint32_t)(q1 >> 32) ^ K.k[2] ^ L.l1, r2c1 = (uint32_t)q1;
-  // round 3, shared product: r2c0 M0
-  const uint64_t q2 = (uint64_t)r2c0 * kPhiloxM0;
-  const uint32_t q2h = (uint32_t)(q2 >> 32), q2l = (uint32_t)q2;
+  const PbitsPrefix f = pbits_prefix(g, L, K);
 #pragma unroll
   for (int j = 0; j < 6; j++) {
     if (j > 0 && !any) break;
-    // round 2, block half
-    const uint64_t pj = (uint64_t)(base ^ (uint32_t)j) * kPhiloxM0;
-    const uint32_t r2c2 = (uint32_t)(pj >> 32) ^ K.k[3] ^ r1c3, r2c3 = (uint32_t)pj;
-    // round 3
-    const uint64_t p3 = (uint64_t)r2c2 * kPhiloxM1;
-    uint32_t x0 = (uint32_t)(p3 >> 32) ^ K.k[4] ^ r2c1, x1 = (uint32_t)p3;
-    uint32_t x2 = q2h ^ K.k[5] ^ r2c3, x3 = q2l;
-#pragma unroll
-    for (int r = 3; r < 10; r++) philox_round(x0, x1, x2, x3, K.k[2 * r], K.k[2 * r + 1]);
-    const uint32_t xs[4] = {x0, x1, x2, x3};
+    uint32_t xs[4];
+    pbits_block(f, j, K, xs);
     any = 0;
 #pragma unroll
     for (int p = 0; p < NPMAX; p++) {
@@ -243,14 +263,49 @@ __device__ __forceinline__ void pbits_group(unsigned long long g, const PbitsLan
       for (int e = 0; e < 4; e++) {
         const int b = 4 * j + e;
         if (b < 23) {
-          const uint32_t km = key_mask(key[p], b);                       // bit 22-b of K, all lanes
-          acc[p] |= und[p] & ~xs[e] & km;                                // u bit 0, K bit 1: u < K
-          und[p] &= ~(xs[e] ^ km);                                       // still equal
+          const uint32_t km = key_mask(key[p], b);  // bit 22-b of K, all lanes
+          acc[p] |= und[p] & ~xs[e] & km;           // u bit 0, K bit 1: u < K
+          und[p] &= ~(xs[e] ^ km);                  // still equal
         }
       }
       any |= und[p];
     }
   }
+}
+
+// Flip-time form: only the sites in `und` need a draw; a site in c4 is
+// tested against key4 (Delta E = 4|J|), any other against key8 (8|J|).
+// Draws 32g + o + i for bit i (o = 0, or 16 for 16-draw rows).  Returns the
+// accepted sites among und.  The block loop stays rolled (one copy of the
+// ten rounds): it runs inside the flip walk, next to its neighbour words.
+__device__ __forceinline__ uint32_t pbits_accept_sel(unsigned long long g, int o, const PbitsLane& L,
+                                                     const PhiloxKeys& K, uint32_t und, uint32_t c4, uint32_t key4,
+                                                     uint32_t key8) {
+  uint32_t acc = 0;
+  if (key4 == kKeyAlways) { acc |= und & c4; und &= ~c4; }
+  else if (key4 == 0u) und &= ~c4;
+  if (key8 == kKeyAlways) { acc |= und & ~c4; und &= c4; }
+  else if (key8 == 0u) und &= c4;
+  if (!und) return acc;
+  const PbitsPrefix f = pbits_prefix(g, L, K);
+  // kk4 / kk8: the keys shifted so that the current plane's K bit is bit 31
+  uint32_t kk4 = key4, kk8 = key8;
+#pragma unroll 1
+  for (int j = 0; j < 6 && und; j++) {
+    uint32_t xs[4];
+    pbits_block(f, j, K, xs);
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      const uint32_t x = xs[e] >> o;
+      const uint32_t km = (c4 & (uint32_t)((int32_t)kk4 >> 31)) | (~c4 & (uint32_t)((int32_t)kk8 >> 31));
+      const uint32_t live = (j < 5 || e < 3) ? und : 0u;  // plane 23 does not exist
+      acc |= live & ~x & km;
+      und &= ~(live & (x ^ km));
+      kk4 <<= 1;
+      kk8 <<= 1;
+    }
+  }
+  return acc;
 }
 
 // Accept bits of draws [d0, d0 + L) (1 <= L <= 32) of one stream: bit i =

@@ -239,8 +239,22 @@ __device__ __forceinline__ unsigned flip_quad(const FlipArgs& a, unsigned i, int
 // band_nseg segments of band_sq quads (band_sq | 32): lanes = (band, quad of
 // the segment); when a row has several segments, the lanes at a segment's
 // edges read their outer neighbour word from the row instead (one load).
-template <bool COHERENT, bool PUSH = false, bool SEG = false>
-__device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0, unsigned g1, int X) {
+//
+// DIRECT (bit-plane Philox stream, PbitsDirect): no accept planes.  Each
+// word's Metropolis tests are decided right here from the neighbour classes:
+// sites with >= 2 disagreeing neighbours flip, the others compare their draw
+// against the Delta E = 4|J| or 8|J| key, and only those comparisons pull
+// bit planes (pbits_accept_sel).  DIRECT = 32: 32-draw rows (n/32 % 32 ==
+// 0); 16: n = 512, a word is the low or high half of a group.
+struct PbitsDirect {
+  const uint32_t* thr9;    // [2][n_sim] keys (FERRO/ANTI)
+  PhiloxKeys pk;
+  unsigned long long blk;  // stream block of this colour phase (2 per sweep)
+};
+
+template <bool COHERENT, bool PUSH = false, bool SEG = false, int DIRECT = 0>
+__device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0, unsigned g1, int X,
+                                                  const PbitsDirect* dp = nullptr) {
   const Geo& G = a.G;
   const int lane = threadIdx.x & 31;
   const int sq = a.band_sq, nseg = SEG ? a.band_nseg : 1;  // quads per segment, segments per row (SEG: > 1)
@@ -262,7 +276,22 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
   };
   auto ld1 = [](const uint32_t* p) { return COHERENT ? __ldcg(p) : __ldg(p); };
   unsigned cnt = 0;
+  // The accept planes were written a window earlier and live in HBM: one
+  // lane per band bulk-prefetches the band's plane rows (both planes, H
+  // contiguous rows) into L2 one group ahead, so the walk's plane loads hit
+  // L2 instead of serialising an HBM round trip per row.
+  auto prefetch_band = [&](unsigned g) {
+    const unsigned s = g / groups_per_sim;
+    const int lr0 = (int)(g - s * groups_per_sim) * gb * H + bi * H;
+    const uint32_t* pr =
+        a.planes + ((((unsigned)X * (unsigned)a.np) * (unsigned)G.n_sim + s) * (unsigned)G.rows + (unsigned)lr0) * Wp;
+    const unsigned bytes = (unsigned)H * Wp * 4u;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pr), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pr + pstride), "r"(bytes) : "memory");
+  };
+  if (!DIRECT && !SEG && q == 0 && g0 < g1) prefetch_band(g0);
   for (unsigned g = g0; g < g1; g++) {
+    if (!DIRECT && !SEG && q == 0 && g + 1 < g1) prefetch_band(g + 1);
     const unsigned gr = SEG ? g / (unsigned)nseg : g;
     const int seg = (int)(g - gr * (unsigned)nseg);
     const unsigned s = gr / groups_per_sim;
@@ -283,7 +312,13 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
     const uint32_t* yrow = ybase + (unsigned)br0 * Wp;
     uint32_t* orow = a.spins + (s * 2u + (unsigned)X) * colour_words + (unsigned)br0 * Wp + w0;
     const uint32_t* prow =
-        a.planes + ((((unsigned)X * (unsigned)a.np) * (unsigned)G.n_sim + s) * (unsigned)G.rows + (unsigned)lr0) * Wp + w0;
+        DIRECT ? nullptr
+               : a.planes + ((((unsigned)X * (unsigned)a.np) * (unsigned)G.n_sim + s) * (unsigned)G.rows + (unsigned)lr0) * Wp + w0;
+    uint32_t key4 = 0, key8 = 0;
+    if (DIRECT) {
+      key4 = dp->thr9[s];
+      key8 = dp->thr9[G.n_sim + s];
+    }
     // one row; the parity P of its red sites is a compile-time constant: bands
     // are even-aligned with even H, so rows alternate P, !P from the band's
     // first row and the loop below steps two rows at a time
@@ -293,8 +328,11 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
       const uint32_t* drow = br + 1 < G.R ? yrow + Wp : ybase;
       const uint4 D = ld4(drow);
       const uint4 O = *reinterpret_cast<const uint4*>(orow);
-      const uint4 P4 = __ldg(reinterpret_cast<const uint4*>(prow));
-      const uint4 P8 = __ldg(reinterpret_cast<const uint4*>(prow + pstride));
+      uint4 P4 = make_uint4(0, 0, 0, 0), P8 = P4;
+      if (!DIRECT) {
+        P4 = __ldg(reinterpret_cast<const uint4*>(prow));
+        P8 = __ldg(reinterpret_cast<const uint4*>(prow + pstride));
+      }
       uint32_t edge;
       if (P) {  // word t0+4, or the chunk wrap: (first word >> 1) | (next chunk's bit 0 << vb-1)
         uint32_t xa = __shfl_sync(0xFFFFFFFFu, Y.x, s_next);
@@ -315,12 +353,54 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
       const uint32_t a4[4] = {P4.x, P4.y, P4.z, P4.w};
       const uint32_t a8[4] = {P8.x, P8.y, P8.z, P8.w};
       uint32_t res[4];
+      if (DIRECT) {
+        // the row's stream and the first draw of this quad's chunk in the phase
+        const RowStream rs = row_stream(G.m, G.row0 + lr, X);
+        const unsigned long long sid =
+            ((unsigned long long)G.sim_offset + s) * (unsigned long long)(G.m / 4) + (unsigned long long)(rs.gamma - 1);
+        const PbitsLane L = pbits_lane((uint32_t)sid, (uint32_t)(sid >> 32));
+        const unsigned long long nn = (unsigned long long)G.n;
+        // word t0 + k of the chunk holds draw index k(t) = 4 k + t0 / 4 of the row's quarter
+        unsigned long long d = dp->blk * 2 * nn + (unsigned long long)rs.q * (nn / 2) + 32ull * ch +
+                               (unsigned long long)((w0 & 15) >> 2) * (unsigned)G.words;
+        const unsigned long long dstep = 4ull * (unsigned)G.words;
+        // neighbour classes of the 4 words (static indices), then the draws
+        // word by word in a rolled loop over rotating registers
+        uint32_t gw[4], cw[4];
 #pragma unroll
-      for (int k = 0; k < 4; k++) {
-        const uint32_t n4 = P ? (k < 3 ? y[k + 1] : edge) : (k > 0 ? y[k - 1] : edge);
-        const uint32_t f = flip_word(a, false, o[k], u4[k], d4[k], y[k], n4, nullptr, 0, a4[k], a8[k]) & vm;
-        res[k] = o[k] ^ f;
-        cnt += __popc(f);
+        for (int k = 0; k < 4; k++) {
+          const uint32_t n4 = P ? (k < 3 ? y[k + 1] : edge) : (k > 0 ? y[k - 1] : edge);
+          const uint32_t ow = o[k] ^ a.inv;
+          const uint32_t x1 = u4[k] ^ ow, x2 = d4[k] ^ ow, x3 = y[k] ^ ow;
+          const uint32_t x4 = a.fault ? 0u : (n4 ^ ow);
+          const uint32_t o12 = x1 | x2, a12 = x1 & x2, o34 = x3 | x4, a34 = x3 & x4;
+          gw[k] = a12 | a34 | (o12 & o34);  // >= 2 disagreeing neighbours: Delta E <= 0
+          cw[k] = (o12 | o34) & ~gw[k];    // exactly one: Delta E = 4|J|
+        }
+        uint32_t g0 = gw[0], g1 = gw[1], g2 = gw[2], g3 = gw[3], q0 = cw[0], q1 = cw[1], q2 = cw[2], q3 = cw[3];
+        uint32_t f0 = 0, f1 = 0, f2 = 0, f3 = 0;
+#pragma unroll 1
+        for (int k = 0; k < 4; k++) {
+          const uint32_t acc =
+              pbits_accept_sel(d >> 5, DIRECT == 16 ? (int)(d & 16) : 0, L, dp->pk, ~g0 & vm, q0, key4, key8);
+          const uint32_t f = (g0 & vm) | acc;
+          cnt += __popc(f);
+          g0 = g1; g1 = g2; g2 = g3; q0 = q1; q1 = q2; q2 = q3;
+          f0 = f1; f1 = f2; f2 = f3; f3 = f;
+          d += dstep;
+        }
+        res[0] = o[0] ^ f0;
+        res[1] = o[1] ^ f1;
+        res[2] = o[2] ^ f2;
+        res[3] = o[3] ^ f3;
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          const uint32_t n4 = P ? (k < 3 ? y[k + 1] : edge) : (k > 0 ? y[k - 1] : edge);
+          const uint32_t f = flip_word(a, false, o[k], u4[k], d4[k], y[k], n4, nullptr, 0, a4[k], a8[k]) & vm;
+          res[k] = o[k] ^ f;
+          cnt += __popc(f);
+        }
       }
       const uint4 out = make_uint4(res[0], res[1], res[2], res[3]);
       *reinterpret_cast<uint4*>(orow) = out;
@@ -334,7 +414,7 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
       Y = D;
       yrow = drow;
       orow += Wp;
-      prow += Wp;
+      if (!DIRECT) prow += Wp;
     };
     using P0 = std::integral_constant<int, 0>;
     using P1 = std::integral_constant<int, 1>;

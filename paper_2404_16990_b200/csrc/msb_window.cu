@@ -395,7 +395,7 @@ __device__ __forceinline__ void win_export(const Geo& G, const uint32_t* spins, 
 // last phase the flip warps export io.lin_out / the observables in their
 // slack behind the producers.  (The flip warps alone took ~190 us to
 // convert beside 28 producer warps per SM, and became the critical path.)
-template <int SRC, int CB, bool HALO>
+template <int SRC, int CB, bool HALO, int DIRECT = 0>
 __global__ void __launch_bounds__(kRngThreads, 1) k_win(const WinArgs wa, const FlipArgs fa0, const HaloArgs ha,
                                                         const WinIO io, const uint32_t* cur, int first, int count,
                                                         int pwarps) {
@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(kRngThreads, 1) k_win(const WinArgs wa, const 
     MSB_TRACE_PUT(5, gtimer());  // prologue done (this CTA)
 #endif
   }
-  if (warp < pwarps) {
+  if (!DIRECT && warp < pwarps) {
     win_produce<SRC, CB>(wa, jt, warp, pwarps);
   } else if (count > 0) {
     const int nwc = (kRngThreads >> 5) - pwarps;
@@ -469,18 +469,25 @@ __global__ void __launch_bounds__(kRngThreads, 1) k_win(const WinArgs wa, const 
     }
     for (int i = 0; i < 2 * count; i++) {
       const int X = i & 1;
-      fa.planes = cur + (size_t)(first + (i >> 1)) * wa.slot_words;
+      PbitsDirect dp;
+      if (DIRECT) {  // inline bit-plane draws: the phase's stream block instead of a plane slot
+        dp.thr9 = wa.thr9;
+        dp.pk = wa.pk;
+        dp.blk = wa.block0 + 2ull * (unsigned)(first + (i >> 1)) + (unsigned)X;
+      } else {
+        fa.planes = cur + (size_t)(first + (i >> 1)) * wa.slot_words;
+      }
       if (band) {
         if (fa.band_nseg > 1) {  // wide rows (cfg4, cfg5): segment-edge words from memory
-          if (HALO) cnt += flip_band_run<true, true, true>(fa, lo, hi, X);
-          else if (i == 0 && !pro) cnt += flip_band_run<false, false, true>(fa, lo, hi, X);
-          else cnt += flip_band_run<true, false, true>(fa, lo, hi, X);
+          if (HALO) cnt += flip_band_run<true, true, true, DIRECT>(fa, lo, hi, X, &dp);
+          else if (i == 0 && !pro) cnt += flip_band_run<false, false, true, DIRECT>(fa, lo, hi, X, &dp);
+          else cnt += flip_band_run<true, false, true, DIRECT>(fa, lo, hi, X, &dp);
         } else {
-          if (HALO) cnt += flip_band_run<true, true>(fa, lo, hi, X);
-          else if (i == 0 && !pro) cnt += flip_band_run<false>(fa, lo, hi, X);
-          else cnt += flip_band_run<true>(fa, lo, hi, X);
+          if (HALO) cnt += flip_band_run<true, true, false, DIRECT>(fa, lo, hi, X, &dp);
+          else if (i == 0 && !pro) cnt += flip_band_run<false, false, false, DIRECT>(fa, lo, hi, X, &dp);
+          else cnt += flip_band_run<true, false, false, DIRECT>(fa, lo, hi, X, &dp);
         }
-      } else {
+      } else if (!DIRECT) {
         if (HALO) cnt += flip_run<true, true>(fa, i0, hi, X);
         else if (i == 0 && !pro) cnt += flip_run<false>(fa, i0, hi, X);
         else cnt += flip_run<true>(fa, i0, hi, X);
@@ -534,6 +541,60 @@ __global__ void k_win_init(const WinArgs a, uint64_t seed, const uint4* __restri
   const uint64_t sid = ((uint64_t)G.sim_offset + (uint64_t)w.s) * cells + (uint64_t)(w.gamma - 1);
   const uint64_t D = (a.block0 + 2ull * w.j) * 2 * n + (uint64_t)w.seg * (n / 2) + (uint64_t)w.k0 * (n / 32);
   store_state(jump_by(stream_state(seed, sid), D, pow), a.states, a.npieces, gi);
+}
+
+int make_win_io(const msb_geom* g, const msb_window_io* io, int count, const msb_halo* halo, WinIO& wio) {
+  wio = WinIO{};
+  if (io && (io->lin_in || io->lin_out || io->ups || io->unsat)) {
+    if (count == 0 || halo || g->ghost) return fail(MSB_ERR_ARG, "msb_window_io needs a flip launch of a whole lattice");
+    if ((io->ups == nullptr) != (io->unsat == nullptr)) return fail(MSB_ERR_ARG, "ups and unsat go together");
+    const Geo G = make_geo(g);
+    const long long chunks = (long long)g->n_sim * g->rows * G.nch;
+    if (((long long)g->rows * G.nch) % kIoCpw) return fail(MSB_ERR_UNSUPPORTED, "msb_window_io needs rows * chunks % 4 == 0");
+    if (32LL * chunks >= (1LL << 31)) return fail(MSB_ERR_UNSUPPORTED, "too many chunks for msb_window_io");
+    wio.lin_in = reinterpret_cast<const uint32_t*>(io->lin_in);
+    wio.lin_out = reinterpret_cast<uint32_t*>(io->lin_out);
+    wio.ups = reinterpret_cast<long long*>(io->ups);
+    wio.unsat = reinterpret_cast<long long*>(io->unsat);
+    wio.ngroups = (unsigned)(chunks / kIoCpw);
+    wio.load16 = ((long long)g->rows * G.nch) % 16 == 0;
+  }
+  return MSB_OK;
+}
+
+int check_halo(const msb_geom* g, const msb_halo* halo, int count) {
+  if (count > 0 && g->ghost && !halo) return fail(MSB_ERR_ARG, "slab windows flip with an msb_halo (in-kernel exchange)");
+  if (halo && !g->ghost) return fail(MSB_ERR_ARG, "msb_halo needs a slab geometry (ghost = 1)");
+  if (halo && (!halo->up_spins || !halo->down_spins || !halo->up_flags || !halo->down_flags || !halo->my_flags ||
+               halo->up_R < 4 || halo->down_R < 4))
+    return fail(MSB_ERR_ARG, "incomplete msb_halo");
+  return MSB_OK;
+}
+
+void set_halo(const msb_halo* halo, int count, FlipArgs& fa, HaloArgs& ha) {
+  ha = HaloArgs{};
+  if (halo && count > 0) {
+    fa.up_spins = halo->up_spins;
+    fa.down_spins = halo->down_spins;
+    fa.up_R = halo->up_R;
+    fa.down_R = halo->down_R;
+    ha.up_flags = halo->up_flags;
+    ha.down_flags = halo->down_flags;
+    ha.my_flags = halo->my_flags;
+    ha.phase0 = halo->phase0;
+    ha.on = 1;
+  }
+}
+
+// Direct (bit-plane Philox) flips walk bands of 2 rows: all 32 warps of
+// every SM flip, so the phase needs as many lane groups as possible.
+bool direct_band(FlipArgs& fa, const msb_geom* g) {
+  if (fa.band_h <= 0) return false;
+  const int gb = fa.band_gb;
+  if (g->rows % (gb * 2)) return false;
+  fa.band_h = 2;
+  fa.band_groups = (unsigned)((long long)g->n_sim * g->rows / (gb * 2) * fa.band_nseg);
+  return true;
 }
 
 int check_window(const msb_geom* g, int S, int P, long long* npieces) {
@@ -669,28 +730,11 @@ int msb_window_sweep(const msb_geom* g, const msb_sweep_params* p, int32_t S, in
   if (p->mode == MSB_MODE_GENERIC) return fail(MSB_ERR_UNSUPPORTED, "lookahead windows need FERRO/ANTI tables");
   if (first < 0 || count < 0 || first + count > S) return fail(MSB_ERR_ARG, "slots [first, first+count) outside the window");
   if (count > 0 && (!spins || !cur || !flips)) return fail(MSB_ERR_ARG, "null buffer");
-  if (count > 0 && g->ghost && !halo) return fail(MSB_ERR_ARG, "slab windows flip with an msb_halo (in-kernel exchange)");
+  if (int r = check_halo(g, halo, count)) return r;
   if (count > 0)
     if (int r = check_flip_extent(g, 2)) return r;
-  if (halo && !g->ghost) return fail(MSB_ERR_ARG, "msb_halo needs a slab geometry (ghost = 1)");
-  if (halo && (!halo->up_spins || !halo->down_spins || !halo->up_flags || !halo->down_flags || !halo->my_flags ||
-               halo->up_R < 4 || halo->down_R < 4))
-    return fail(MSB_ERR_ARG, "incomplete msb_halo");
   WinIO wio = {};
-  if (io && (io->lin_in || io->lin_out || io->ups || io->unsat)) {
-    if (count == 0 || halo || g->ghost) return fail(MSB_ERR_ARG, "msb_window_io needs a flip launch of a whole lattice");
-    if ((io->ups == nullptr) != (io->unsat == nullptr)) return fail(MSB_ERR_ARG, "ups and unsat go together");
-    const Geo G = make_geo(g);
-    const long long chunks = (long long)g->n_sim * g->rows * G.nch;
-    if (((long long)g->rows * G.nch) % kIoCpw) return fail(MSB_ERR_UNSUPPORTED, "msb_window_io needs rows * chunks % 4 == 0");
-    if (32LL * chunks >= (1LL << 31)) return fail(MSB_ERR_UNSUPPORTED, "too many chunks for msb_window_io");
-    wio.lin_in = reinterpret_cast<const uint32_t*>(io->lin_in);
-    wio.lin_out = reinterpret_cast<uint32_t*>(io->lin_out);
-    wio.ups = reinterpret_cast<long long*>(io->ups);
-    wio.unsat = reinterpret_cast<long long*>(io->unsat);
-    wio.ngroups = (unsigned)(chunks / kIoCpw);
-    wio.load16 = ((long long)g->rows * G.nch) % 16 == 0;
-  }
+  if (int r = make_win_io(g, io, count, halo, wio)) return r;
   if (!next && count == 0) {
     if (halo) {
       k_halo_wait<<<1, 32, 0, as_stream(stream)>>>(halo->my_flags, (unsigned)halo->phase0);
@@ -704,18 +748,8 @@ int msb_window_sweep(const msb_geom* g, const msb_sweep_params* p, int32_t S, in
   fill_win_args(wa, g, p, S, P, np, states, next);
   FlipArgs fa;
   fill_flip_args(fa, g, p, 0, spins, cur, flips);
-  HaloArgs ha = {};
-  if (halo && count > 0) {
-    fa.up_spins = halo->up_spins;
-    fa.down_spins = halo->down_spins;
-    fa.up_R = halo->up_R;
-    fa.down_R = halo->down_R;
-    ha.up_flags = halo->up_flags;
-    ha.down_flags = halo->down_flags;
-    ha.my_flags = halo->my_flags;
-    ha.phase0 = halo->phase0;
-    ha.on = 1;
-  }
+  HaloArgs ha;
+  set_halo(halo, count, fa, ha);
   // Warp split of the 32-warp CTAs.  A unit (32 pieces) is a whole window's
   // share of a stream, so an extra producer round costs a full unit: when the
   // units fit one round, give producers exactly that round and the rest of
@@ -783,6 +817,77 @@ int msb_window_sweep(const msb_geom* g, const msb_sweep_params* p, int32_t S, in
   }
 #undef MSB_LAUNCH_WIN_CB
 #undef MSB_LAUNCH_WIN
+  return MSB_OK;
+}
+
+int msb_direct_ok(const msb_geom* g, const msb_sweep_params* p) {
+  if (check_geom(g) || check_params(p)) return 0;
+  if (p->rng != MSB_RNG_PHILOX_BITS || p->mode == MSB_MODE_GENERIC) return 0;
+  const Geo G = make_geo(g);
+  if (G.words % 32 != 0 && G.words != 16) return 0;
+  FlipArgs fa;
+  fill_flip_args(fa, g, p, 0, nullptr, nullptr, nullptr);
+  return direct_band(fa, g) ? 1 : 0;
+}
+
+int msb_direct_sweep(const msb_geom* g, const msb_sweep_params* p, uint32_t* spins, int32_t n_sweeps, uint64_t* flips,
+                     const msb_halo* halo, const msb_window_io* io, void* stream) {
+  if (int r = check_geom(g)) return r;
+  if (int r = check_params(p)) return r;
+  if (p->rng != MSB_RNG_PHILOX_BITS) return fail(MSB_ERR_ARG, "direct sweeps draw the bit-plane Philox stream");
+  if (p->mode == MSB_MODE_GENERIC) return fail(MSB_ERR_UNSUPPORTED, "direct sweeps need FERRO/ANTI tables");
+  if (n_sweeps < 0 || n_sweeps > (1 << 20)) return fail(MSB_ERR_ARG, "sweep count must be in [0, 2^20]");
+  if (n_sweeps == 0) return MSB_OK;
+  if (!spins || !flips) return fail(MSB_ERR_ARG, "null buffer");
+  if (int r = check_halo(g, halo, n_sweeps)) return r;
+  if (int r = check_flip_extent(g, 2)) return r;
+  WinIO wio;
+  if (int r = make_win_io(g, io, n_sweeps, halo, wio)) return r;
+  const Geo G = make_geo(g);
+  const int cb = (G.words % 32) == 0 ? 32 : (G.words == 16 ? 16 : 0);
+  FlipArgs fa;
+  fill_flip_args(fa, g, p, 0, spins, nullptr, flips);
+  if (!cb || !direct_band(fa, g)) return fail(MSB_ERR_UNSUPPORTED, "direct sweeps need n/32 % 32 == 0 or n = 512 and band rows");
+  HaloArgs ha;
+  set_halo(halo, n_sweeps, fa, ha);
+  WinArgs wa = {};
+  wa.G = G;
+  wa.thr9 = p->thr9;
+  wa.work = p->work;
+  wa.pk = philox_keys(p->seed);
+  wa.block0 = p->block;
+  wa.seed_lo = (uint32_t)p->seed;
+  wa.seed_hi = (uint32_t)(p->seed >> 32);
+  int dev = 0, sms = 148;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)sms);
+  cfg.blockDim = dim3(kRngThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = as_stream(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const uint32_t* cur = nullptr;
+  const int first = 0, pwarps = 0;
+#define MSB_LAUNCH_DIRECT(CB, HALO)                                                                  \
+  do {                                                                                               \
+    static std::once_flag o_;                                                                        \
+    static cudaError_t e_;                                                                           \
+    if (int r = set_smem_attr(k_win<kSrcPbits, CB, HALO, CB>, o_, e_)) return r;                    \
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, k_win<kSrcPbits, CB, HALO, CB>, wa, fa, ha, wio, cur, first, n_sweeps, pwarps)); \
+  } while (0)
+  if (ha.on) {
+    if (cb == 32) MSB_LAUNCH_DIRECT(32, true);
+    else MSB_LAUNCH_DIRECT(16, true);
+  } else {
+    if (cb == 32) MSB_LAUNCH_DIRECT(32, false);
+    else MSB_LAUNCH_DIRECT(16, false);
+  }
+#undef MSB_LAUNCH_DIRECT
   return MSB_OK;
 }
 

@@ -502,7 +502,10 @@ class Engine:
         self._sync_tables()
         self._params.fault = int(bool(self.fault))
         if self.overlap and self._params.mode != MSB_MODE_GENERIC:
-            self._win_sweeps(k, io)
+            if self._direct_ok():
+                self._direct_sweeps(k, io)
+            else:
+                self._win_sweeps(k, io)
         elif self._pos == [self._blocks, self._blocks + 1] or self._ahead:
             self._sweep_call(k)
         else:  # per-phase positioning pending (a lone flip_red/flip_blue)
@@ -512,6 +515,36 @@ class Engine:
         self.sweeps_done += k
         self.attempts += self.dims.sites * self.n_sim * k
         self._touch()
+
+    # -- direct sweeps (msb_direct_sweep, bit-plane Philox stream) --------------
+
+    def _direct_ok(self) -> bool:
+        """The bit-plane stream with FERRO/ANTI tables flips without accept
+        planes: every warp flips and draws only the bit planes its Metropolis
+        tests need (msb_direct_sweep)."""
+        return self.stream == "philox-bits" and bool(
+            _lib.lib().msb_direct_ok(ctypes.byref(self._g), ctypes.byref(self._params)))
+
+    def _direct_sweeps(self, k: int, io=None) -> None:
+        """k sweeps in launches of up to ``window`` sweeps; with ``io`` the
+        load goes with the first launch, the export with the last."""
+        self._wvalid = False       # windows and per-sweep lookahead planes are stale now
+        self._ahead = False
+        first = True
+        while k > 0:
+            r = min(k, self.window)
+            lio = None
+            if io is not None:
+                lio = WindowIO(io.lin_in if first else None, None, None, None)
+                if r == k:
+                    lio.lin_out, lio.ups, lio.unsat = io.lin_out, io.ups, io.unsat
+            first = False
+            self._params.block = self._blocks
+            call("msb_direct_sweep", ctypes.byref(self._g), ctypes.byref(self._params), _p(self._spins), r,
+                 _p(self._flips_dev), None, ctypes.byref(lio) if lio is not None else None, self._cs)
+            self._blocks += 2 * r
+            k -= r
+        self._pos = [self._blocks, self._blocks + 1]  # counter-based: the per-phase path needs no positioning
 
     # -- lookahead windows (msb_window_sweep) ------------------------------------
 
@@ -611,7 +644,10 @@ class Engine:
         self._params.fault = int(bool(self.fault))
         ev0.record(self._stream)
         if self.overlap and self._params.mode != MSB_MODE_GENERIC:
-            self._win_sweeps(k)
+            if self._direct_ok():
+                self._direct_sweeps(k)
+            else:
+                self._win_sweeps(k)
         else:
             self._sweep_call(k)
         ev1.record(self._stream)
@@ -799,6 +835,8 @@ class Engine:
         slack behind the producers for the export).  Multi-round shapes have
         no such slack: cfg3's fused launch measured 2092 vs 1988 us for the
         separate kernels; cfg2's 611 vs 615 us."""
+        if self._direct_ok():  # every warp flips; the conversions go with them
+            return self._io_groups_ok
         if not hasattr(self, "_io_fused"):
             torch = _torch()
             units = -(-int(_lib.lib().msb_window_pieces(ctypes.byref(self._g), self.window, self._wP)) // 32)
