@@ -259,8 +259,16 @@ int msb_window_sweep(const msb_geom *g, const msb_sweep_params *p, int32_t S, in
  * rows in bands of 2 x 32/quads-per-row), else 0.  Replaces: engine.py:353-360
  * (Engine.sweep) for the counter-based stream. */
 int msb_direct_ok(const msb_geom *g, const msb_sweep_params *p);
+/* group_flags (optional, whole lattices whose rows are one band segment):
+ * msb_direct_flag_words(g, p) uint32 words, zeroed once by the caller and
+ * owned by one engine; flag_phase0 = 2 x the sweeps of all earlier direct
+ * calls on it.  Phases are then ordered by neighbour band-group flags
+ * instead of grid barriers.  NULL: grid barriers.  Returns -1 when
+ * msb_direct_ok is 0, 0 when flags do not apply. */
+int64_t msb_direct_flag_words(const msb_geom *g, const msb_sweep_params *p);
 int msb_direct_sweep(const msb_geom *g, const msb_sweep_params *p, uint32_t *spins, int32_t n_sweeps,
-                     uint64_t *flips, const msb_halo *halo, const msb_window_io *io, void *stream);
+                     uint64_t *flips, uint32_t *group_flags, uint32_t flag_phase0, const msb_halo *halo,
+                     const msb_window_io *io, void *stream);
 
 /* ---- observables (engine.py:372-386) ------------------------------------- */
 /* Adds, per replica, the number of +1 spins and the number of unsatisfied

@@ -90,7 +90,7 @@ EXPORTS = (
     "msb_init_const", "msb_from_linear", "msb_to_linear", "msb_to_ref16", "msb_from_ref16",
     "msb_plane_words", "msb_rng_planes", "msb_flip", "msb_phase", "msb_sweep",
     "msb_default_window", "msb_window_parts", "msb_window_pieces", "msb_window_words", "msb_window_init", "msb_window_sweep",
-    "msb_direct_ok", "msb_direct_sweep",
+    "msb_direct_ok", "msb_direct_flag_words", "msb_direct_sweep",
     "msb_observe", "msb_export", "msb_draws", "msb_pack_edges", "msb_unpack_ghosts", "msb_bench_int_peak",
 )
 
@@ -149,7 +149,9 @@ def lib() -> ctypes.CDLL:
         "msb_window_sweep": ([G, P, i32, i32, vp, vp, vp, i32, i32, vp, vp, ctypes.POINTER(Halo),
                               ctypes.POINTER(WindowIO), vp], ctypes.c_int),
         "msb_direct_ok": ([G, P], i32),
-        "msb_direct_sweep": ([G, P, vp, i32, vp, ctypes.POINTER(Halo), ctypes.POINTER(WindowIO), vp], ctypes.c_int),
+        "msb_direct_flag_words": ([G, P], i64),
+        "msb_direct_sweep": ([G, P, vp, i32, vp, vp, ctypes.c_uint32, ctypes.POINTER(Halo), ctypes.POINTER(WindowIO), vp],
+                             ctypes.c_int),
         "msb_observe": ([G, vp, vp, vp, vp], ctypes.c_int),
         "msb_export": ([G, vp, vp, vp, vp, vp], ctypes.c_int),
         "msb_draws": ([G, P, i32, vp, vp, vp], ctypes.c_int),

@@ -278,9 +278,13 @@ __device__ __forceinline__ void pbits_group(unsigned long long g, const PbitsLan
 // Draws 32g + o + i for bit i (o = 0, or 16 for 16-draw rows).  Returns the
 // accepted sites among und.  The block loop stays rolled (one copy of the
 // ten rounds): it runs inside the flip walk, next to its neighbour words.
+// TABLE: the warp shares one pair of keys, and kt holds their bit masks per
+// plane, block j at kt[2j] (key4's four planes) and kt[2j+1] (key8's), read
+// as shared-memory broadcasts; otherwise every lane shifts its own keys.
+template <bool TABLE>
 __device__ __forceinline__ uint32_t pbits_accept_sel(unsigned long long g, int o, const PbitsLane& L,
                                                      const PhiloxKeys& K, uint32_t und, uint32_t c4, uint32_t key4,
-                                                     uint32_t key8) {
+                                                     uint32_t key8, const uint4* kt) {
   uint32_t acc = 0;
   if (key4 == kKeyAlways) { acc |= und & c4; und &= ~c4; }
   else if (key4 == 0u) und &= ~c4;
@@ -294,15 +298,26 @@ __device__ __forceinline__ uint32_t pbits_accept_sel(unsigned long long g, int o
   for (int j = 0; j < 6 && und; j++) {
     uint32_t xs[4];
     pbits_block(f, j, K, xs);
+    uint32_t m4[4], m8[4];
+    if (TABLE) {
+      const uint4 a = kt[2 * j], b = kt[2 * j + 1];
+      m4[0] = a.x; m4[1] = a.y; m4[2] = a.z; m4[3] = a.w;
+      m8[0] = b.x; m8[1] = b.y; m8[2] = b.z; m8[3] = b.w;
+    }
 #pragma unroll
     for (int e = 0; e < 4; e++) {
       const uint32_t x = xs[e] >> o;
-      const uint32_t km = (c4 & (uint32_t)((int32_t)kk4 >> 31)) | (~c4 & (uint32_t)((int32_t)kk8 >> 31));
+      uint32_t km;
+      if (TABLE) {
+        km = (c4 & m4[e]) | (~c4 & m8[e]);
+      } else {
+        km = (c4 & (uint32_t)((int32_t)kk4 >> 31)) | (~c4 & (uint32_t)((int32_t)kk8 >> 31));
+        kk4 <<= 1;
+        kk8 <<= 1;
+      }
       const uint32_t live = (j < 5 || e < 3) ? und : 0u;  // plane 23 does not exist
       acc |= live & ~x & km;
       und &= ~(live & (x ^ km));
-      kk4 <<= 1;
-      kk8 <<= 1;
     }
   }
   return acc;

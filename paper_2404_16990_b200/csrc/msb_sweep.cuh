@@ -315,9 +315,24 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
         DIRECT ? nullptr
                : a.planes + ((((unsigned)X * (unsigned)a.np) * (unsigned)G.n_sim + s) * (unsigned)G.rows + (unsigned)lr0) * Wp + w0;
     uint32_t key4 = 0, key8 = 0;
+    bool kuni = false;  // DIRECT: the warp's lanes share one pair of keys (bands of one replica)
+    uint4* kt = nullptr;
     if (DIRECT) {
+      __shared__ uint4 kmt[32][12];  // per warp: 6 blocks x (key4, key8) x 4 plane masks
       key4 = dp->thr9[s];
       key8 = dp->thr9[G.n_sim + s];
+      kuni = __all_sync(0xFFFFFFFFu, key4 == __shfl_sync(0xFFFFFFFFu, key4, 0) &&
+                                         key8 == __shfl_sync(0xFFFFFFFFu, key8, 0));
+      kt = kmt[threadIdx.x >> 5];
+      if (kuni) {
+        __syncwarp();  // the previous group's reads of the table are done
+        if (lane < 24) {
+          uint32_t* t = reinterpret_cast<uint32_t*>(kt);
+          t[(lane >> 2) * 8 + (lane & 3)] = key_mask(key4, lane);
+          t[(lane >> 2) * 8 + 4 + (lane & 3)] = key_mask(key8, lane);
+        }
+        __syncwarp();
+      }
     }
     // one row; the parity P of its red sites is a compile-time constant: bands
     // are even-aligned with even H, so rows alternate P, !P from the band's
@@ -381,8 +396,9 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
         uint32_t f0 = 0, f1 = 0, f2 = 0, f3 = 0;
 #pragma unroll 1
         for (int k = 0; k < 4; k++) {
-          const uint32_t acc =
-              pbits_accept_sel(d >> 5, DIRECT == 16 ? (int)(d & 16) : 0, L, dp->pk, ~g0 & vm, q0, key4, key8);
+          const int o16 = DIRECT == 16 ? (int)(d & 16) : 0;
+          const uint32_t acc = kuni ? pbits_accept_sel<true>(d >> 5, o16, L, dp->pk, ~g0 & vm, q0, key4, key8, kt)
+                                    : pbits_accept_sel<false>(d >> 5, o16, L, dp->pk, ~g0 & vm, q0, key4, key8, kt);
           const uint32_t f = (g0 & vm) | acc;
           cnt += __popc(f);
           g0 = g1; g1 = g2; g2 = g3; q0 = q1; q1 = q2; q2 = q3;

@@ -41,7 +41,32 @@ struct WinArgs {
   uint32_t seed_lo, seed_hi;    // Philox key
   unsigned long long block0;    // stream block of slot 0's first phase
   PhiloxKeys pk;                // Philox round keys
+  unsigned* gflags;             // direct sweeps: per band group, phases completed (monotonic), or null
+  unsigned gphase0;             // gflags value every group holds at launch start
 };
+
+// Direct sweeps with band-group flags instead of grid barriers: a group's
+// phase i reads the other colour's rows of its own group and of the groups
+// just above and below (same replica, periodic), and overwrites rows those
+// groups read in phase i-1.  So it waits for both neighbours to have
+// completed phase i-1, and publishes its own completion; slow groups delay
+// only their neighbours instead of the whole grid.
+__device__ __forceinline__ void group_wait(const unsigned* flags, unsigned g, unsigned gps, unsigned need) {
+  if ((threadIdx.x & 31) == 0) {
+    const unsigned s0 = g - g % gps, l = g - s0;
+    const unsigned up = s0 + (l == 0 ? gps - 1 : l - 1), dn = s0 + (l + 1 == gps ? 0 : l + 1);
+    while (ld_acquire(flags + up) < need || ld_acquire(flags + dn) < need) __nanosleep(32);
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void group_done(unsigned* flags, unsigned g, unsigned v) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) {
+    __threadfence();
+    atomicExch(flags + g, v);
+  }
+}
 
 // One 32-bit word of the jump: 8 nibble lookups (paired 3-input XORs) from the
 // piece's start state, consumed 4 bits at a time (jw0 is the current word).
@@ -467,6 +492,23 @@ __global__ void __launch_bounds__(kRngThreads, 1) k_win(const WinArgs wa, const 
       }
       asm volatile("bar.sync 1, %0;" ::"r"(nwc * 32) : "memory");
     }
+    if (DIRECT && !HALO && wa.gflags && band && fa.band_nseg == 1) {
+      // band groups in phase order, neighbour flags instead of grid barriers
+      const unsigned gps = (unsigned)fa0.G.rows / (unsigned)(fa0.band_gb * fa0.band_h);
+      for (int i = 0; i < 2 * count; i++) {
+        const int X = i & 1;
+        PbitsDirect dp;
+        dp.thr9 = wa.thr9;
+        dp.pk = wa.pk;
+        dp.blk = wa.block0 + 2ull * (unsigned)(first + (i >> 1)) + (unsigned)X;
+        for (unsigned g = lo; g < hi; g++) {
+          if (i > 0) group_wait(wa.gflags, g, gps, wa.gphase0 + (unsigned)i);
+          if (i == 0 && !pro) cnt += flip_band_run<false, false, false, DIRECT>(fa, g, g + 1, X, &dp);
+          else cnt += flip_band_run<true, false, false, DIRECT>(fa, g, g + 1, X, &dp);
+          group_done(wa.gflags, g, wa.gphase0 + (unsigned)i + 1u);
+        }
+      }
+    } else
     for (int i = 0; i < 2 * count; i++) {
       const int X = i & 1;
       PbitsDirect dp;
@@ -830,8 +872,17 @@ int msb_direct_ok(const msb_geom* g, const msb_sweep_params* p) {
   return direct_band(fa, g) ? 1 : 0;
 }
 
+int64_t msb_direct_flag_words(const msb_geom* g, const msb_sweep_params* p) {
+  if (!msb_direct_ok(g, p)) return -1;
+  FlipArgs fa;
+  fill_flip_args(fa, g, p, 0, nullptr, nullptr, nullptr);
+  direct_band(fa, g);
+  return fa.band_nseg == 1 ? (int64_t)fa.band_groups : 0;
+}
+
 int msb_direct_sweep(const msb_geom* g, const msb_sweep_params* p, uint32_t* spins, int32_t n_sweeps, uint64_t* flips,
-                     const msb_halo* halo, const msb_window_io* io, void* stream) {
+                     uint32_t* group_flags, uint32_t flag_phase0, const msb_halo* halo, const msb_window_io* io,
+                     void* stream) {
   if (int r = check_geom(g)) return r;
   if (int r = check_params(p)) return r;
   if (p->rng != MSB_RNG_PHILOX_BITS) return fail(MSB_ERR_ARG, "direct sweeps draw the bit-plane Philox stream");
@@ -858,6 +909,10 @@ int msb_direct_sweep(const msb_geom* g, const msb_sweep_params* p, uint32_t* spi
   wa.block0 = p->block;
   wa.seed_lo = (uint32_t)p->seed;
   wa.seed_hi = (uint32_t)(p->seed >> 32);
+  if (group_flags && !halo && fa.band_nseg == 1) {  // else grid barriers between phases
+    wa.gflags = group_flags;
+    wa.gphase0 = flag_phase0;
+  }
   int dev = 0, sms = 148;
   CUDA_TRY(cudaGetDevice(&dev));
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));

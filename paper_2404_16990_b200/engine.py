@@ -530,6 +530,13 @@ class Engine:
         load goes with the first launch, the export with the last."""
         self._wvalid = False       # windows and per-sweep lookahead planes are stale now
         self._ahead = False
+        if getattr(self, "_dflags", None) is None:  # band-group phase flags (monotonic)
+            torch = _torch()
+            words = int(_lib.lib().msb_direct_flag_words(ctypes.byref(self._g), ctypes.byref(self._params)))
+            with torch.cuda.device(self.device), torch.cuda.stream(self._stream):
+                self._dflags = torch.zeros(max(words, 1), dtype=torch.int32, device=self.device)
+            self._dflags_on = words > 0
+            self._dphase = 0
         first = True
         while k > 0:
             r = min(k, self.window)
@@ -540,8 +547,14 @@ class Engine:
                     lio.lin_out, lio.ups, lio.unsat = io.lin_out, io.ups, io.unsat
             first = False
             self._params.block = self._blocks
+            if self._dphase + 2 * r >= 1 << 31:  # keep the flags far from wrapping
+                with _torch().cuda.stream(self._stream):
+                    self._dflags.zero_()
+                self._dphase = 0
             call("msb_direct_sweep", ctypes.byref(self._g), ctypes.byref(self._params), _p(self._spins), r,
-                 _p(self._flips_dev), None, ctypes.byref(lio) if lio is not None else None, self._cs)
+                 _p(self._flips_dev), _p(self._dflags) if self._dflags_on else None, ctypes.c_uint32(self._dphase),
+                 None, ctypes.byref(lio) if lio is not None else None, self._cs)
+            self._dphase += 2 * r
             self._blocks += 2 * r
             k -= r
         self._pos = [self._blocks, self._blocks + 1]  # counter-based: the per-phase path needs no positioning

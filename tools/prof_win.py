@@ -1,6 +1,7 @@
 """Fixed workload for ncu captures of one window-kernel variant (development
 tool): python tools/prof_win.py <stream> <mode> [m n n_sim]
-mode: fused (flips + production), produce (production only), flips (flips only).
+mode: fused (flips + production), produce (production only), flips (flips only),
+direct (msb_direct_sweep, philox-bits).
 Runs 3 launches of the chosen variant after a warm-up window."""
 import sys
 import numpy as np
@@ -14,7 +15,9 @@ S = e.window
 e._sweeps(2 * S)
 e.synchronize()
 for _ in range(3):
-    if mode == "fused":
+    if mode == "direct":
+        e._direct_sweeps(S)
+    elif mode == "fused":
         e._win_launch(0, S, True)
     elif mode == "produce":
         e._win_launch(0, 0, True)
