@@ -392,6 +392,36 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
           gw[k] = a12 | a34 | (o12 & o34);  // >= 2 disagreeing neighbours: Delta E <= 0
           cw[k] = (o12 | o34) & ~gw[k];    // exactly one: Delta E = 4|J|
         }
+        if (DIRECT == 16) {
+          // n = 512: the 16 draws of word k (quad lane q, k = 4 kk + q) are
+          // one half of a 32-draw group whose other half is word kk of lane
+          // q ^ 1.  The lane pair resolves each group once: the even lane
+          // groups kk = 0, 1, the odd lane kk = 2, 3, over both halves.
+          const bool odd = q & 1;
+          uint32_t fo[4];
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const int own = odd ? 2 + h : h;  // static after unrolling both ways below
+            const uint32_t u_own = ~(odd ? gw[2 + h] : gw[h]) & vm, c_own = odd ? cw[2 + h] : cw[h];
+            const uint32_t u_snd = ~(odd ? gw[h] : gw[2 + h]) & vm, c_snd = odd ? cw[h] : cw[2 + h];
+            const uint32_t u_pa = __shfl_xor_sync(0xFFFFFFFFu, u_snd, 1), c_pa = __shfl_xor_sync(0xFFFFFFFFu, c_snd, 1);
+            const uint32_t und = odd ? (u_pa | (u_own << 16)) : (u_own | (u_pa << 16));
+            const uint32_t c4 = odd ? (c_pa | (c_own << 16)) : (c_own | (c_pa << 16));
+            const unsigned long long dg = d + (unsigned long long)own * dstep;
+            const uint32_t acc = kuni ? pbits_accept_sel<true>(dg >> 5, 0, L, dp->pk, und, c4, key4, key8, kt)
+                                      : pbits_accept_sel<false>(dg >> 5, 0, L, dp->pk, und, c4, key4, key8, kt);
+            const uint32_t a_own = odd ? acc >> 16 : acc & 0xFFFFu, a_snd = odd ? acc & 0xFFFFu : acc >> 16;
+            const uint32_t a_back = __shfl_xor_sync(0xFFFFFFFFu, a_snd, 1);  // the partner's result for our word
+            if (odd) { fo[2 + h] = a_own; fo[h] = a_back; }
+            else { fo[h] = a_own; fo[2 + h] = a_back; }
+          }
+#pragma unroll
+          for (int k = 0; k < 4; k++) {
+            const uint32_t f = (gw[k] & vm) | fo[k];
+            cnt += __popc(f);
+            res[k] = o[k] ^ f;
+          }
+        } else {
         uint32_t g0 = gw[0], g1 = gw[1], g2 = gw[2], g3 = gw[3], q0 = cw[0], q1 = cw[1], q2 = cw[2], q3 = cw[3];
         uint32_t f0 = 0, f1 = 0, f2 = 0, f3 = 0;
 #pragma unroll 1
@@ -409,6 +439,7 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
         res[1] = o[1] ^ f1;
         res[2] = o[2] ^ f2;
         res[3] = o[3] ^ f3;
+        }
       } else {
 #pragma unroll
         for (int k = 0; k < 4; k++) {
