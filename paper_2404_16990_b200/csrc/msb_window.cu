@@ -492,7 +492,8 @@ __global__ void __launch_bounds__(kRngThreads, 1) k_win(const WinArgs wa, const 
       }
       asm volatile("bar.sync 1, %0;" ::"r"(nwc * 32) : "memory");
     }
-    if (DIRECT && !HALO && wa.gflags && band && fa.band_nseg == 1) {
+    const bool gflag_path = DIRECT && !HALO && wa.gflags && band && fa.band_nseg == 1;
+    if (gflag_path) {
       // band groups in phase order, neighbour flags instead of grid barriers
       const unsigned gps = (unsigned)fa0.G.rows / (unsigned)(fa0.band_gb * fa0.band_h);
       for (int i = 0; i < 2 * count; i++) {
@@ -550,7 +551,8 @@ __global__ void __launch_bounds__(kRngThreads, 1) k_win(const WinArgs wa, const 
     MSB_TRACE_PUT(7, gtimer());  // flips done (before the epilogue)
 #endif
     if (epi) {  // every flip of the launch is done before any export read
-      consumer_barrier(wa.work + 1, base + gridDim.x * (unsigned)(2 * count), nwc * 32, leader);
+      // (the flag path has no per-phase grid barriers: this is its first)
+      consumer_barrier(wa.work + 1, base + gridDim.x * (gflag_path ? 1u : (unsigned)(2 * count)), nwc * 32, leader);
       if (io.lin_out && io.ups) win_export<true, true>(fa0.G, fa0.spins, io, cw, nc);
       else if (io.lin_out) win_export<true, false>(fa0.G, fa0.spins, io, cw, nc);
       else win_export<false, true>(fa0.G, fa0.spins, io, cw, nc);

@@ -328,16 +328,19 @@ class FusedSlabRun:
         else:
             self.S = int(window)
             self.P = int(L.msb_window_parts(g, self.S))
-        npieces = int(L.msb_window_pieces(g, self.S, self.P))
-        self._words = int(L.msb_window_words(g, self.S))
-        if npieces < 0 or self._words < 0:
-            raise _lib.MsbError(f"slab window S={self.S} P={self.P}: {L.msb_last_error().decode()}")
+        # bit-plane stream: direct sweeps (no accept planes), S sweeps per launch
+        self.direct = slab.stream == "philox-bits" and bool(L.msb_direct_ok(g, ctypes.byref(slab._params)))
         self.world = dist.get_world_size(group) if (dist.is_available() and dist.is_initialized()) else 1
         self.rank = dist.get_rank(group) if self.world > 1 else 0
-        with torch.cuda.device(slab.device), slab.stream_ctx():
-            self._wstates = torch.empty(8 * npieces, dtype=torch.int32, device=slab.device)
-            self._wplanes = torch.empty(2 * self._words, dtype=torch.int32, device=slab.device)
-        self._jump = _jump_table(slab.device, self.S * 4 * slab.dims.n)
+        if not self.direct:
+            npieces = int(L.msb_window_pieces(g, self.S, self.P))
+            self._words = int(L.msb_window_words(g, self.S))
+            if npieces < 0 or self._words < 0:
+                raise _lib.MsbError(f"slab window S={self.S} P={self.P}: {L.msb_last_error().decode()}")
+            with torch.cuda.device(slab.device), slab.stream_ctx():
+                self._wstates = torch.empty(8 * npieces, dtype=torch.int32, device=slab.device)
+                self._wplanes = torch.empty(2 * self._words, dtype=torch.int32, device=slab.device)
+            self._jump = _jump_table(slab.device, self.S * 4 * slab.dims.n)
         R = slab.rows + 2
         h = _lib.Halo()
         if self.world == 1:
@@ -394,6 +397,16 @@ class FusedSlabRun:
         s = self.slab
         k = int(n_sweeps)
         if k <= 0:
+            return
+        if self.direct:
+            while k > 0:
+                r = min(k, self.S)
+                s._params.block = 2 * s.sweeps_done
+                call("msb_direct_sweep", ctypes.byref(s._g), ctypes.byref(s._params), _p(s._spins), r, _p(s._flips),
+                     None, ctypes.c_uint32(0), ctypes.byref(self._halo), None, s._cs)
+                self._halo.phase0 += 2 * r
+                s.sweeps_done += r
+                k -= r
             return
         if not self._valid:
             self._wbase, self._wc, self._cur = 2 * s.sweeps_done, 0, 0

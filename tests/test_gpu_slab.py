@@ -50,7 +50,8 @@ def test_slabs_large_rows_vs_oracle():
 
 @pytest.mark.parametrize("m,n,n_sim,stream,window", [
     (16, 128, 2, "xoshiro", None), (16, 128, 2, "philox", None), (16, 128, 2, "philox-bits", None),
-    (64, 1024, 1, "xoshiro", 3), (32, 14336, 1, "philox-bits", 3),
+    (64, 1024, 1, "xoshiro", 3), (32, 14336, 1, "philox-bits", 3), (64, 1024, 2, "philox-bits", 3),
+    (32, 512, 3, "philox-bits", None),
     (12, 96, 3, "xoshiro", 2), (32, 14336, 1, "xoshiro", None),
 ])
 def test_fused_slab_single_ring_vs_oracle(m, n, n_sim, stream, window):

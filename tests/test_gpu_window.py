@@ -163,14 +163,17 @@ def test_band_walk_geometries(m, n, n_sim, stream):
 
 
 @pytest.mark.parametrize("window,k", [(8, 8), (4, 6), (3, 3)])
-def test_step_packed_equals_separate_calls(window, k):
+@pytest.mark.parametrize("stream", ["xoshiro", "philox-bits"])
+def test_step_packed_equals_separate_calls(window, k, stream):
     """Engine.step_packed (one host-I/O step through the copy streams) ==
-    load_packed + sweeps + store_packed + observe_async."""
+    load_packed + sweeps + store_packed + observe_async (philox-bits: the
+    direct kernel carries the conversions)."""
     import torch
     from paper_2404_16990_b200 import Engine, LatticeDims
     dims = LatticeDims(32, 1024)
     temps = [1.8, 2.3, 2.9]
-    fused, plain = Engine(dims, temps, 21, window=window), Engine(dims, temps, 21, window=window)
+    fused = Engine(dims, temps, 21, window=window, stream=stream)
+    plain = Engine(dims, temps, 21, window=window, stream=stream)
     nb = fused.packed_nbytes()
     pin = lambda: torch.empty(nb, dtype=torch.uint8, pin_memory=True)
     fb, pb = [pin() for _ in range(3)], [pin() for _ in range(3)]
@@ -230,7 +233,8 @@ def test_export_one_pass(m, n, n_sim):
     assert (host[n_sim:] == unsat).all()
 
 
-def test_step_packed_fused_edge_cases():
+@pytest.mark.parametrize("stream", ["xoshiro", "philox-bits"])
+def test_step_packed_fused_edge_cases(stream):
     """The fused path (msb_window_io) with device-side destinations, after a
     table change (window invalid: production-only launch first), and a sweep
     count spanning three launches; each step against the plain calls."""
@@ -238,7 +242,7 @@ def test_step_packed_fused_edge_cases():
     from paper_2404_16990_b200 import Engine, LatticeDims
     dims = LatticeDims(32, 2048)
     temps = [1.9, 2.6]
-    fused, plain = Engine(dims, temps, 5, window=4), Engine(dims, temps, 5, window=4)
+    fused, plain = Engine(dims, temps, 5, window=4, stream=stream), Engine(dims, temps, 5, window=4, stream=stream)
     nb = fused.packed_nbytes()
     src = torch.empty(nb, dtype=torch.uint8, pin_memory=True)
     plain.store_packed(src)
@@ -260,3 +264,35 @@ def test_step_packed_fused_edge_cases():
         p_ups, p_uns = plain._observe()
         assert ups.cpu().tolist() == p_ups.tolist() and uns.cpu().tolist() == p_uns.tolist(), k
         assert fused.flips == plain.flips
+
+
+@pytest.mark.parametrize("m,n,n_sim,J", [(64, 1024, 3, 1.0), (32, 512, 4, 1.0), (16, 2048, 2, -1.0),
+                                         (48, 1024, 1, 1.0)])
+def test_direct_matches_window_path(m, n, n_sim, J):
+    """philox-bits: the direct kernel (inline lazy draws, band-group flags)
+    == the window path (accept planes from the bit-plane producer), and both
+    == the oracle; includes a lone phase between runs, J < 0 and extreme
+    temperatures (K = 2^23 and tiny K)."""
+    from oracle import oracle as orc
+    from paper_2404_16990_b200 import Engine, LatticeDims
+    temps = list(np.linspace(0.3, 3.0, n_sim)) if n_sim > 1 else [1e9]
+    dims = LatticeDims(m, n)
+    d = Engine(dims, temps, 17, coupling=J, stream="philox-bits")
+    w = Engine(dims, temps, 17, coupling=J, stream="philox-bits")
+    w._direct_ok = lambda: False  # force the lookahead-window path
+    o = orc.OracleEngine(m, n, temps, 17, coupling=J, stream="philox-bits")
+    for e in (d, w):
+        e._sweeps(11)
+        e.flip_red()
+        e._sweeps(5)
+    assert d._direct_ok()
+    import ctypes
+    L = orc.lib()
+    p = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    tab = np.ascontiguousarray(o.tables)
+    phases = [(b, b % 2) for b in range(22)] + [(22, 0)] + [(23 + i, i % 2) for i in range(10)]
+    for b, ph in phases:  # blocks in consumption order: 11 sweeps, a lone red phase, 5 sweeps
+        L.orc_flip_phase_philox_bits(n_sim, m, n, ph, ctypes.c_uint64(17), ctypes.c_uint64(0), ctypes.c_uint64(b),
+                                     p(tab), p(o.spins), p(o._flips))
+    assert (d.lattices() == w.lattices()).all() and d.flips == w.flips
+    assert (d.lattices() == o.spins).all() and d.flips == o.flips
