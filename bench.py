@@ -42,7 +42,7 @@ METRIC = "spin flip attempts/sec (aggregate, device-timed)"
 UNIT = "attempts/s"
 A_INT_XOSHIRO = 27.5  # int32 ops per attempt, reference xoshiro256++ stream
 A_INT_PHILOX = 13.5   # counter-based Philox4x32-10 stream
-A_INT_PBITS = 6.0     # bit-plane Philox stream, lazily compared
+A_INT_PBITS = 3.7     # bit-plane Philox stream, direct sweeps: lazily drawn planes (tools/pbits_ops.py)
 A_INT = {"xoshiro": A_INT_XOSHIRO, "philox": A_INT_PHILOX, "philox-bits": A_INT_PBITS}
 STREAM_DESC = {
     "xoshiro": "reference xoshiro256++ (bit-exact with multispin.Engine)",

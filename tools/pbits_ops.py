@@ -1,0 +1,41 @@
+"""Algorithmic int32 ops per attempt of the direct bit-plane sweep (development
+tool).  Equilibrates cfg2-like replicas with the oracle
+(T = linspace(1.5, 3.5, R), 128 x 1024 lattices), then, for every colour-split
+32-site word, counts the sites whose Metropolis test needs a draw (Delta E >
+0) and the expected number of Philox blocks (4 planes each) until all of them
+are decided: P(site still undecided after b planes) = 2^-b, so
+E[blocks | k sites] = sum_{j>=0} 1 - (1 - 2^(-4j))^k.
+python tools/pbits_ops.py [replicas] [sweeps]"""
+import json
+import sys
+import numpy as np
+sys.path.insert(0, ".")
+from oracle import oracle as orc
+
+R = int(sys.argv[1]) if len(sys.argv) > 1 else 16
+SW = int(sys.argv[2]) if len(sys.argv) > 2 else 300
+m, n = 128, 1024
+temps = list(np.linspace(1.5, 3.5, R))
+o = orc.OracleEngine(m, n, temps, 7, stream="philox-bits")
+o.sweep(SW)
+s = o.spins.astype(np.int32)
+nb = np.roll(s, 1, 1) + np.roll(s, -1, 1) + np.roll(s, 1, 2) + np.roll(s, -1, 2)
+need = (s * nb) > 0                      # Delta E = 2 s sum > 0: a draw decides
+# colour-split words: 32 consecutive same-colour sites of a row
+blocks = []
+for X in (0, 1):
+    sel = need[:, :, X::2] if True else None
+    w = sel.reshape(R, m, -1, 32).sum(-1)   # sites per word needing a draw (approximately the colour split)
+    k = w.astype(np.float64)
+    eb = np.zeros_like(k)
+    for j in range(6):
+        eb += np.where(k > 0, 1.0 - (1.0 - 2.0 ** (-4 * j)) ** k, 0.0) if j > 0 else (k > 0)
+    blocks.append(eb)
+eb = np.concatenate([b.ravel() for b in blocks])
+frac = need.mean()
+B = eb.mean()
+# per 32-site word: neighbour classes 16, group prefix 10, per block 33 (Philox) + 4 planes x 4 (compare)
+ops_word = 16 + 10 * (eb > 0).mean() + B * (33 + 16)
+print(json.dumps({"replicas": R, "sweeps": SW, "frac_sites_needing_draw": round(float(frac), 4),
+                  "blocks_per_word": round(float(B), 4), "ops_per_word": round(float(ops_word), 2),
+                  "ops_per_attempt": round(float(ops_word) / 32, 3)}))
