@@ -420,8 +420,17 @@ __device__ __forceinline__ void win_export(const Geo& G, const uint32_t* spins, 
 // last phase the flip warps export io.lin_out / the observables in their
 // slack behind the producers.  (The flip warps alone took ~190 us to
 // convert beside 28 producer warps per SM, and became the critical path.)
+// Threads per direct launch (tuning define).  1024 measured best at cfg2
+// (1.99 T) against 768 (1.54 T) and 512 (1.68 T): with fewer warps the
+// band groups no longer spread one per warp, which costs more than the
+// 64-register cap's spills.
+#ifndef MSB_DIRECT_THREADS
+#define MSB_DIRECT_THREADS 1024
+#endif
+constexpr int kDirectThreads = MSB_DIRECT_THREADS;
+
 template <int SRC, int CB, bool HALO, int DIRECT = 0>
-__global__ void __launch_bounds__(kRngThreads, 1) k_win(const WinArgs wa, const FlipArgs fa0, const HaloArgs ha,
+__global__ void __launch_bounds__(DIRECT ? kDirectThreads : kRngThreads, 1) k_win(const WinArgs wa, const FlipArgs fa0, const HaloArgs ha,
                                                         const WinIO io, const uint32_t* cur, int first, int count,
                                                         int pwarps) {
   extern __shared__ uint4 jt[];
@@ -466,7 +475,7 @@ __global__ void __launch_bounds__(kRngThreads, 1) k_win(const WinArgs wa, const 
   if (!DIRECT && warp < pwarps) {
     win_produce<SRC, CB>(wa, jt, warp, pwarps);
   } else if (count > 0) {
-    const int nwc = (kRngThreads >> 5) - pwarps;
+    const int nwc = (int)(blockDim.x >> 5) - pwarps;
     const unsigned nc = gridDim.x * nwc;
     const unsigned cw = (warp - pwarps) * gridDim.x + blockIdx.x;
     // band walk: contiguous band groups per warp; else quads, lanes interleaved
@@ -920,7 +929,7 @@ int msb_direct_sweep(const msb_geom* g, const msb_sweep_params* p, uint32_t* spi
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)sms);
-  cfg.blockDim = dim3(kRngThreads);
+  cfg.blockDim = dim3(kDirectThreads);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = as_stream(stream);
   cudaLaunchAttribute attr[1];
