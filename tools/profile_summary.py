@@ -1,6 +1,7 @@
 """Summarise an ncu launch list + full capture into profiles/*.json.
 
 python tools/profile_summary.py <launches.csv> <capture.ncu-rep> <tag> [kernel-key] [attempts-per-launch]
+                                [output.json] [bench flags]
 """
 import collections
 import csv
@@ -12,6 +13,8 @@ import sys
 launches, rep, tag = sys.argv[1], sys.argv[2], sys.argv[3]
 key = sys.argv[4] if len(sys.argv) > 4 else "k_win"
 attempts = int(sys.argv[5]) if len(sys.argv) > 5 else 8 * 64 * 1024 * 1024
+out_path = sys.argv[6] if len(sys.argv) > 6 else "profiles/ncu_summary.json"
+bench_flags = sys.argv[7] if len(sys.argv) > 7 else ""
 rows = list(csv.reader(open(launches)))
 hdr = None
 tot = collections.defaultdict(lambda: [0, 0.0])
@@ -27,7 +30,8 @@ for r in rows:
         tot[name][0] += 1
         tot[name][1] += float(d["Metric Value"])
 allt = sum(v for c, v in tot.values())
-lsum = {"command": "ncu --metrics gpu__time_duration.sum --clock-control none python bench.py --steps 10 --warmup 3 --no-cpu",
+lsum = {"command": "ncu --metrics gpu__time_duration.sum --clock-control none python bench.py --steps 10 --warmup 3 --no-cpu "
+                   + bench_flags,
         "unit": "ns",
         "note": f"cold-cache serialised launches; each timed bench step is one {key} launch. k_int_peak = INT32 "
                 "peak microbenchmark, FillFunctor<uchar> = L2 flush between steps, linear/observe kernels = e2e leg",
@@ -58,8 +62,8 @@ cap = {
     "inst_executed_warp": insts, "inst_per_attempt": round(insts * 32 / attempts, 2),
 }
 summary = {"round": 1, "tag": tag,
-           "command": f"python bench.py --steps 10 --warmup 3 --no-cpu (cfg2 64 x 1024^2); ncu --set full "
+           "command": f"python bench.py --steps 10 --warmup 3 --no-cpu {bench_flags} (cfg2 64 x 1024^2); ncu --set full "
                       f"--clock-control none -k regex:{key} -s 5 -c 1",
            key: cap, "launch_list": f"profiles/launches_{tag}_summary.json"}
-json.dump(summary, open("profiles/ncu_summary.json", "w"), indent=1)
+json.dump(summary, open(out_path, "w"), indent=1)
 print(json.dumps(summary, indent=1))
