@@ -301,6 +301,41 @@ def run_ours(args, cfg):
         e2e_s = float(t.item())
     e2e = attempts_step * Ke * ws / e2e_s
 
+    # the counter-based bit-plane stream on the same workload (direct sweeps),
+    # device-timed like `value`; reported beside the headline, which stays on
+    # the reference's own xoshiro256++ streams
+    alt = None
+    if args.stream == "xoshiro" and not args.no_alt:
+        alt_eng = Engine(LatticeDims(cfg["m"], cfg["n"]), temps, cfg["seed"], init=cfg["init"],
+                         sim_offset=rank * n_sim, device=dev, stream="philox-bits")
+        alt_eng._sweeps(args.warmup * S)
+        alt_eng.synchronize()
+        Ka = min(K, 200)
+        aevs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(Ka)]
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for k in range(Ka):
+            with torch.cuda.stream(alt_eng._stream):
+                flush.zero_()
+            alt_eng._timed_sweeps(S, *aevs[k])
+        torch.cuda.synchronize()
+        a_ms = [a.elapsed_time(b) for a, b in aevs]
+        a_tot = float(sum(a_ms))
+        if ws > 1:
+            t = torch.tensor([a_tot], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            a_tot = float(t.item())
+        a_val = attempts_step * Ka * ws / (a_tot * 1e-3)
+        a_ach = A_INT_PBITS * attempts_step / (statistics.mean(a_ms) * 1e-3) / 1e12
+        alt = {"philox-bits": {
+            "value": a_val, "unit": UNIT, "steps": Ka, "ms_per_step": a_tot / Ka,
+            "stream": STREAM_DESC["philox-bits"],
+            "path": "Engine(stream='philox-bits'): msb_direct_sweep, one launch per step of S sweeps, no accept planes",
+            "roofline": {"bound": "int32", "achieved": a_ach, "peak": peak, "unit": "Tops/s", "frac": a_ach / peak,
+                         "per_launch": f"{attempts_step} attempts x {A_INT_PBITS} int32 ops (tools/pbits_ops.py)"},
+            "vs_xoshiro": a_val / value}}
+
     if rank == 0:
         kern_avg_s = statistics.mean(step_ms) * 1e-3
         a_int = A_INT[args.stream]
@@ -341,6 +376,8 @@ def run_ours(args, cfg):
             "wall_s_timed_region": t_wall,
             "flips_per_ns": value / 1e9,
         }
+        if alt is not None:
+            line["other_streams"] = alt
         if ws == 1 and not args.no_cpu:
             line["cpu_baseline"] = cpu_baseline(cfg)
         print(json.dumps(line), flush=True)
@@ -445,6 +482,7 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2")
     ap.add_argument("--kg", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-alt", action="store_true", help="skip the philox-bits comparison leg (other_streams)")
     ap.add_argument("--stream", choices=sorted(A_INT), default="xoshiro",
                     help="xoshiro: the reference's own streams (default); philox, philox-bits: counter-based "
                          "(SURVEY F1)")
