@@ -194,3 +194,46 @@ def test_window_io_argument_errors():
     for gg, first, count, io, halo, text in cases:
         assert sweep(gg, first, count, io, halo) == -1, text
         assert text in L.msb_last_error().decode()
+
+
+def test_direct_sweep_host_checks():
+    """msb_direct_ok / msb_direct_flag_words / msb_direct_sweep argument
+    handling (host logic only; no GPU needed): which shapes and tables take
+    the direct path, and the errors raised before any device work."""
+    from paper_2404_16990_b200._lib import (Halo, SweepParams, MSB_MODE_FERRO, MSB_MODE_GENERIC,
+                                             MSB_RNG_PHILOX, MSB_RNG_PHILOX_BITS)
+    L = _lib.lib()
+    dummy = np.zeros(64, np.uint32)
+    ptr = dummy.ctypes.data
+    p = SweepParams(mode=MSB_MODE_FERRO, n_planes=2, thr9=ptr, kg=1, jump=ptr, work=ptr, rng=MSB_RNG_PHILOX_BITS)
+    ok = lambda g, pp=p: L.msb_direct_ok(ctypes.byref(g), ctypes.byref(pp))
+    # 32-draw rows (n/32 % 32 == 0) and n = 512 take it; other widths do not
+    assert ok(geom(64, 1024, 1024)) == 1 and ok(geom(3, 512, 512)) == 1 and ok(geom(1, 64, 14336)) == 1
+    assert ok(geom(2, 64, 96)) == 0 and ok(geom(2, 64, 160)) == 0
+    # rows must split into bands of 2 rows x (32 / quads per row) lanes
+    assert ok(geom(1, 12, 1024)) == 0
+    # other streams and generic tables do not
+    assert ok(geom(2, 64, 1024), SweepParams(mode=MSB_MODE_FERRO, n_planes=2, rng=MSB_RNG_PHILOX, work=ptr)) == 0
+    assert ok(geom(2, 64, 1024), SweepParams(mode=MSB_MODE_GENERIC, n_planes=3, rng=MSB_RNG_PHILOX_BITS,
+                                             work=ptr)) == 0
+    # band-group flags: one per group of 16 rows at n = 1024 (8 bands of 2 rows); none for multi-segment rows
+    g = geom(64, 1024, 1024)
+    assert L.msb_direct_flag_words(ctypes.byref(g), ctypes.byref(p)) == 64 * 1024 // 16
+    assert L.msb_direct_flag_words(ctypes.byref(geom(1, 64, 14336)), ctypes.byref(p)) == 0
+    assert L.msb_direct_flag_words(ctypes.byref(geom(2, 64, 96)), ctypes.byref(p)) == -1
+
+    def sweep(gg, pp, n, spins=ptr, halo=None):
+        return L.msb_direct_sweep(ctypes.byref(gg), ctypes.byref(pp), spins, n, ptr, None, 0,
+                                  ctypes.byref(halo) if halo is not None else None, None, None)
+
+    assert sweep(g, p, 0) == 0                      # nothing to do
+    px = SweepParams(mode=MSB_MODE_FERRO, n_planes=2, thr9=ptr, kg=1, work=ptr, rng=MSB_RNG_PHILOX)
+    for gg, pp, n, spins, halo, text in [
+        (g, px, 2, ptr, None, "bit-plane Philox stream"),
+        (g, p, -1, ptr, None, "sweep count"),
+        (g, p, 2, None, None, "null buffer"),
+        (g, p, 2, ptr, Halo(), "msb_halo needs a slab geometry"),
+        (geom(2, 64, 96), p, 2, ptr, None, "direct sweeps need"),
+    ]:
+        assert sweep(gg, pp, n, spins, halo) < 0, text
+        assert text in L.msb_last_error().decode(), (text, L.msb_last_error())
