@@ -502,6 +502,15 @@ __global__ void __launch_bounds__(DIRECT ? kDirectThreads : kRngThreads, 1) k_wi
       asm volatile("bar.sync 1, %0;" ::"r"(nwc * 32) : "memory");
     }
     const bool gflag_path = DIRECT && !HALO && wa.gflags && band && fa.band_nseg == 1;
+    bool push_warp = true;  // HALO: this warp's bands include a slab's first or last row
+    if (HALO && band) {
+      const unsigned gps = (unsigned)fa0.G.rows / (unsigned)(fa0.band_gb * fa0.band_h), nseg = (unsigned)fa0.band_nseg;
+      push_warp = false;
+      for (unsigned g = lo; g < hi; g++) {
+        const unsigned l = (g / nseg) % gps;
+        push_warp |= l == 0 || l + 1 == gps;
+      }
+    }
     if (gflag_path) {
       // band groups in phase order, neighbour flags instead of grid barriers
       const unsigned gps = (unsigned)fa0.G.rows / (unsigned)(fa0.band_gb * fa0.band_h);
@@ -546,7 +555,9 @@ __global__ void __launch_bounds__(DIRECT ? kDirectThreads : kRngThreads, 1) k_wi
       }
       const bool more = i + 1 < 2 * count;
       if (HALO) {
-        __threadfence_system();  // this thread's halo pushes (if any) before the neighbours are told
+        // the halo pushes (peer stores) before the neighbours are told; only
+        // warps holding a slab's first or last row push
+        if (push_warp) __threadfence_system();
         halo_gate(ha, wa.work, i, more, nwc * 32, leader, gpu_leader);
       } else if (more) {
 #ifdef MSB_TRACE
