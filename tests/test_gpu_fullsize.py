@@ -6,7 +6,8 @@ against the CPU oracle (multithreaded, so every case finishes in seconds):
 * cfg3: 754 replicas x 512^2 (many producer unit rounds per window);
 * cfg4: one 14336^2 lattice, through the whole-lattice engine and through the
   fused slab ring (the bench's slab path, in-kernel halo exchange);
-* cfg5: one 32768^2 lattice (1.07e9 sites) through the fused slab ring.
+* cfg5: one 32768^2 lattice (1.07e9 sites) through the fused slab ring;
+* the bit-plane counter stream (direct sweeps) at cfg3 and cfg4 full size.
 
 Lattices, flip counts and the integer observables are compared; the large
 lattices in row blocks to bound host memory."""
@@ -113,3 +114,39 @@ def test_cfg2_full_size_philox(stream):
     o.sweep(2)
     assert e.flips == o.flips
     _same_rows(e.lattices, o.spins)
+
+
+def test_philox_bits_full_size_cfg3_cfg4():
+    """The bit-plane counter stream through the direct kernel at full size:
+    cfg3 (754 x 512^2: lane-pair groups of 16-draw words, band-group flags,
+    a launch spanning a full and a partial window) and cfg4 (14336^2 through
+    the whole-lattice engine and the fused slab ring: multi-segment rows,
+    halo gate), against the oracle."""
+    from oracle import oracle as orc
+    from paper_2404_16990_b200 import Engine, LatticeDims
+    from paper_2404_16990_b200.slab import FusedSlabRun, SlabLattice
+    temps = list(np.random.default_rng(2024).uniform(2.0, 2.6, 754))
+    e = Engine(LatticeDims(512, 512), temps, 2024, init="all-up", stream="philox-bits")
+    o = orc.OracleEngine(512, 512, temps, 2024, init="all-up", stream="philox-bits")
+    e._sweeps(e.window + 2)
+    o.sweep(e.window + 2)
+    assert e._direct_ok()
+    assert e.flips == o.flips
+    _same_rows(e.lattices, o.spins)
+    _observables_match(*e._observe(), o, 512 * 512)
+    del e, o
+    dims = LatticeDims(14336, 14336)
+    o = orc.OracleEngine(14336, 14336, [2.269], 2024, stream="philox-bits")
+    o.sweep(3)
+    e = Engine(dims, [2.269], 2024, stream="philox-bits")
+    e._sweeps(3)
+    assert e.flips == o.flips
+    _same_rows(lambda: e.lattice(0), o.spins[0])
+    del e
+    slab = SlabLattice(dims, [2.269], 2024, 0, 14336, stream="philox-bits")
+    run = FusedSlabRun(slab, window=2)
+    assert run.direct
+    run.sweep(3)
+    assert slab.flips == o.flips
+    _same_rows(lambda: slab.lattice_rows()[0], o.spins[0])
+    _observables_match(*run.observables(), o, dims.sites)
