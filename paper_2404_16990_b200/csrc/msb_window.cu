@@ -429,8 +429,8 @@ __device__ __forceinline__ void win_export(const Geo& G, const uint32_t* spins, 
 #endif
 constexpr int kDirectThreads = MSB_DIRECT_THREADS;
 
-template <int SRC, int CB, bool HALO, int DIRECT = 0>
-__global__ void __launch_bounds__(DIRECT ? kDirectThreads : kRngThreads, 1) k_win(const WinArgs wa, const FlipArgs fa0, const HaloArgs ha,
+template <int SRC, int CB, bool HALO, int DIRECT = 0, int NT = 0>
+__global__ void __launch_bounds__(NT ? NT : (DIRECT ? kDirectThreads : kRngThreads), 1) k_win(const WinArgs wa, const FlipArgs fa0, const HaloArgs ha,
                                                         const WinIO io, const uint32_t* cur, int first, int count,
                                                         int pwarps) {
   extern __shared__ uint4 jt[];
@@ -957,6 +957,20 @@ int msb_direct_sweep(const msb_geom* g, const msb_sweep_params* p, uint32_t* spi
     if (int r = set_smem_attr(k_win<kSrcPbits, CB, HALO, CB>, o_, e_)) return r;                    \
     CUDA_TRY(cudaLaunchKernelEx(&cfg, k_win<kSrcPbits, CB, HALO, CB>, wa, fa, ha, wio, cur, first, n_sweeps, pwarps)); \
   } while (0)
+  // Band groups that fit one per warp in 28 warps per SM (cfg2: 4096 groups,
+  // 148 x 28 = 4144 warps) run 896-thread CTAs: no warp idles, and ptxas gets
+  // 72 registers instead of 64.
+  const long long g28 = 28LL * sms, g24 = 24LL * sms;
+  static const int env_nt = [] { const char* e = getenv("MSB_DIRECT_NT"); return e ? atoi(e) : -1; }();
+  if (!ha.on && cb == 32 && env_nt != 0 && (long long)fa.band_groups <= g28 && (long long)fa.band_groups > g24) {
+    cfg.blockDim = dim3(896);
+    static std::once_flag o_;
+    static cudaError_t e_;
+    if (int r = set_smem_attr(k_win<kSrcPbits, 32, false, 32, 896>, o_, e_)) return r;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, k_win<kSrcPbits, 32, false, 32, 896>, wa, fa, ha, wio, cur, first, n_sweeps,
+                                pwarps));
+    return MSB_OK;
+  }
   if (ha.on) {
     if (cb == 32) MSB_LAUNCH_DIRECT(32, true);
     else MSB_LAUNCH_DIRECT(16, true);
