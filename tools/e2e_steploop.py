@@ -1,11 +1,12 @@
 """Wall time per Engine.step_packed step at cfg2 (bench.py's e2e loop), plus
 GPU-side event gaps around the engine's stream (development tool)."""
-import json, time
+import json, sys, time
 import numpy as np
 import torch
 from paper_2404_16990_b200 import Engine, LatticeDims
 
-e = Engine(LatticeDims(1024, 1024), list(np.linspace(1.5, 3.5, 64)), 2024)
+e = Engine(LatticeDims(1024, 1024), list(np.linspace(1.5, 3.5, 64)), 2024,
+           stream=sys.argv[1] if len(sys.argv) > 1 else "xoshiro")
 S = e.window
 nb = e.packed_nbytes()
 bufs = [torch.empty(nb, dtype=torch.uint8, pin_memory=True) for _ in range(3)]

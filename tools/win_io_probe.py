@@ -10,8 +10,9 @@ import argparse
 ap = argparse.ArgumentParser()
 ap.add_argument("--m", type=int, default=1024); ap.add_argument("--n", type=int, default=1024)
 ap.add_argument("--n-sim", type=int, default=64)
+ap.add_argument("--stream", default="xoshiro")
 args = ap.parse_args()
-e = Engine(LatticeDims(args.m, args.n), list(np.linspace(1.5, 3.5, args.n_sim)), 2024)
+e = Engine(LatticeDims(args.m, args.n), list(np.linspace(1.5, 3.5, args.n_sim)), 2024, stream=args.stream)
 S = e.window
 words = e.packed_nbytes() // 8
 lin_in = torch.empty(words, dtype=torch.int64, device=e._spins.device)
