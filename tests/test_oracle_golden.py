@@ -118,3 +118,27 @@ def test_philox_bits_host_stream_matches_oracle():
     for j in range(4):
         for r in range(70):
             assert blk[r, j] == orc.lib().orc_pbits_draw(seed, 10 + j, 29 + r)
+
+
+def test_philox_bits_stream_chunking_and_offsets():
+    """PhiloxBitStreams as the reference consumes it: blocks read in pieces of
+    any size equal one long read (group boundaries inside a piece), stream
+    offsets select the same columns, and every draw is the u23 of its 23
+    bit planes (bit 22-b of the draw = bit i of plane b)."""
+    from paper_2404_16990_b200.rng import PBITS_PLANES, PhiloxBitStreams
+    seed = 0x1234_5678_9ABC_DEF0
+    whole = PhiloxBitStreams(seed, 6, 3).raw_block(200)
+    parts = PhiloxBitStreams(seed, 6, 3)
+    got = np.concatenate([parts.raw_block(c) for c in (1, 31, 33, 64, 7, 64)], axis=0)
+    assert (got == whole).all() and parts.position == 200
+    sub = PhiloxBitStreams(seed, 2, 5).raw_block(200)          # streams 5, 6 = columns 2, 3
+    assert (sub == whole[:, 2:4]).all()
+    pl = PhiloxBitStreams(seed, 6, 3).planes(2, 1)[0]          # group 2: draws 64..95
+    for i in (0, 17, 31):
+        u = 0
+        for b in range(PBITS_PLANES):
+            u |= ((int(pl[4, b]) >> i) & 1) << (PBITS_PLANES - 1 - b)
+        assert u == int(whole[64 + i, 4])
+    assert whole.max() < 1 << 23
+    unit = PhiloxBitStreams(seed, 6, 3).unit_block(10)
+    assert (unit == whole[:10] * 2.0 ** -23).all()
