@@ -1,24 +1,33 @@
 #!/usr/bin/env python3
 """Benchmark of the B200 multispin hot path.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2|cfg3|cfg4|cfg5]
 
-One step = one full checkerboard sweep (red + blue phase) of every replica
-held by a GPU: one accept-plane kernel (the reference xoshiro256++ streams,
-both colours) plus two flip kernels.  Workload (BASELINE.json configs[1],
-"cfg2"): 64 independent replicas of a 1024x1024 periodic lattice per GPU,
-J=1, h=0, T = linspace(1.5, 3.5, 64), random initial spins from seed.  With
-N GPUs each rank runs its own 64 replicas (global replica index offset
-rank*64, distinct streams): weak scaling, no data-path collective.
+One step = one lookahead window: S = 8 full checkerboard sweeps of every
+replica a GPU holds, executed as ONE cooperative k_win launch (the flips of
+these S sweeps + the accept planes of the next S, the reference's
+xoshiro256++ streams).  Default workload (BASELINE.json configs[1], "cfg2"):
+64 independent replicas of a 1024x1024 periodic lattice per GPU, J=1, h=0,
+T = linspace(1.5, 3.5, 64), random initial spins from seed.  With N GPUs
+each rank runs its own 64 replicas (global replica offset rank*64, distinct
+streams): weak scaling, no data-path collective.  cfg3 splits its 754
+replicas over the ranks with the reference's np.linspace slices (strong
+scaling); cfg4 / cfg5 are row slabs of one lattice (slab.FusedSlabRun).
+
+``--gpus N`` without a torchrun environment re-launches itself under
+``torch.distributed.run`` with N ranks (one per GPU); it refuses to run when
+fewer than N GPUs are visible.
 
 Prints one JSON line (rank 0).  ``value`` is device-timed (CUDA events on
-the launching stream, L2 flushed between timed steps, max over ranks);
-``e2e`` is the same metric through the public Engine API with the lattice
-copied host->device and back from pinned memory every step; ``roofline``
-reports the dominant kernel against the measured INT32 issue peak;
-``cpu_baseline`` times the CPU oracle (a C restatement of the reference
-path, oracle/) on this host's cores.  ``--impl reference`` times only that
-CPU implementation on the same workload and metric.
+the launching stream, L2 flushed by a read pass between timed steps, max
+over ranks); ``e2e`` is the same metric through the public Engine API with
+the lattice copied host->device and back from pinned memory every step;
+``roofline`` reports the dominant kernel against the measured INT32 issue
+peak; ``cpu_baseline`` times the CPU oracle (a C restatement of the
+reference path, oracle/) on this host's cores, with the unmodified Python
+reference (baseline/_ref, when installed) timed beside it.  ``--impl
+reference`` times only the CPU implementation on the same workload and
+metric.
 """
 
 from __future__ import annotations
@@ -53,14 +62,27 @@ STREAM_DESC = {
 A_BYTES = 0.375   # algorithmic HBM bytes per attempt
 L2_FLUSH_BYTES = 256 << 20
 
+
+def _hbm_gbs() -> float:
+    """Measured HBM copy bandwidth of this pool's B200s (MEASURED_PEAKS.json,
+    driver-written), else the survey's measured 6532.9 GB/s."""
+    try:
+        return float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+    except Exception:
+        return 6532.9
+
+
+HBM_GBS = _hbm_gbs()
+
 CONFIGS = {
     "cfg2": dict(m=1024, n=1024, n_sim=64, init="random", seed=2024,
                  temps=lambda n: np.linspace(1.5, 3.5, n),
                  desc="cfg2: 64 replicas x 1024x1024 per GPU, periodic, J=1, h=0, "
                       "T=linspace(1.5,3.5,64), random init from seed, reference xoshiro256++ streams"),
-    "cfg3": dict(m=512, n=512, n_sim=754, init="all-up", seed=2024,
+    "cfg3": dict(m=512, n=512, n_sim=754, init="all-up", seed=2024, split=True,
                  temps=lambda n: np.random.default_rng(2024).uniform(2.0, 2.6, n),
-                 desc="cfg3: 754 replicas x 512x512, periodic, J=1, T~U[2.0,2.6] from seed, all-up init"),
+                 desc="cfg3: 754 replicas x 512x512, periodic, J=1, T~U[2.0,2.6] from seed, all-up init; "
+                      "np.linspace replica slices over the GPUs (strong scaling)"),
     "cfg4": dict(m=14336, n=14336, n_sim=1, init="random", seed=2024, slab="strong",
                  temps=lambda n: np.full(n, 2.269),
                  desc="cfg4: one 14336x14336 lattice, periodic, J=1, T=2.269, random init; row slabs over the "
@@ -161,6 +183,51 @@ def cpu_baseline(cfg, budget_s: float = 8.0):
                       f"({cfg['m']}x{cfg['n']}) on {threads} threads, {dt:.1f} s (oracle/msb_oracle.c)"}
 
 
+def python_reference(cfg, budget_s: float = 6.0):
+    """The unmodified reference Engine (pure Python/numpy, baseline/_ref from
+    tools/install_reference.sh) on this host: one Engine on one thread, and
+    one Engine per core on contiguous sim_offset slices in a thread pool --
+    run_simulations' own mechanism (engine.py:443-492).  Each leg times whole
+    Engine.sweep() calls after construction, sized to about budget_s."""
+    try:
+        from paper_2404_16990_b200.backend import import_reference
+        import_reference()
+        import multispin
+        from multispin.engine import Engine as RefEngine
+    except Exception as exc:  # not installed on this box: say so, never substitute
+        return {"unavailable": f"reference package not importable ({exc.__class__.__name__})"}
+    if RefEngine.__module__ != "multispin.engine":
+        return {"unavailable": "multispin.engine.Engine is re-bound (backend installed)"}
+    from concurrent.futures import ThreadPoolExecutor
+    dims = multispin.LatticeDims(cfg["m"], cfg["n"])
+    temps = [float(t) for t in cfg["temps"](cfg["n_sim"])]
+    cores = os.cpu_count() or 1
+
+    def timed(engines, k):
+        with ThreadPoolExecutor(max_workers=len(engines)) as pool:
+            t0 = time.perf_counter()
+            list(pool.map(lambda e: [e.sweep() for _ in range(k)], engines))
+            return time.perf_counter() - t0
+
+    out = {"kind": "reference", "impl": f"multispin {getattr(multispin, '__version__', '?')} (unmodified, "
+                                        "pure Python/numpy)", "unit": UNIT}
+    one = RefEngine(dims, temps[:1], cfg["seed"], init=cfg["init"])
+    dt = timed([one], 1)
+    k1 = int(max(1, min(20, budget_s / 2 / dt)))
+    dt = timed([one], k1)
+    out["one_thread"] = {"value": dims.m * dims.n * k1 / dt, "cores": 1,
+                         "sample": f"{k1} sweep(s) of 1 replica ({dims.m}x{dims.n}), one Engine, {dt:.2f} s"}
+    n_eng = min(cores, cfg["n_sim"])
+    engines = [RefEngine(dims, temps[i:i + 1], cfg["seed"], init=cfg["init"], sim_offset=i) for i in range(n_eng)]
+    kc = int(max(1, min(20, budget_s / 2 / max(dt / k1, 1e-3))))
+    dtc = timed(engines, kc)
+    out["all_cores"] = {"value": n_eng * dims.m * dims.n * kc / dtc, "cores": cores,
+                        "sample": f"{kc} sweep(s) of {n_eng} replicas, one Engine per replica on {n_eng} threads "
+                                  f"(sim_offset slices, as run_simulations), {dtc:.2f} s"}
+    out["value"] = out["all_cores"]["value"]
+    return out
+
+
 def run_reference(args, cfg):
     ws, rank, _ = dist_info()
     if rank != 0:
@@ -182,7 +249,7 @@ def run_reference(args, cfg):
     value = attempts / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": value,
-        "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u64 (xoshiro) / i8 spins / f64 compare", "data": "synthetic",
         "config": {"workload": cfg["desc"], "m": cfg["m"], "n": cfg["n"], "replicas_per_gpu": cfg["n_sim"],
@@ -190,9 +257,11 @@ def run_reference(args, cfg):
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"each step = 1 sweep of {replicas} of the {cfg['n_sim']} replicas on "
                                    f"{threads} threads (oracle/msb_oracle.c, the C restatement of the "
-                                   "reference path; the reference itself is Python and is not on this box)"},
+                                   "reference path, pinned to the reference's own outputs)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not args.no_cpu:
+        line["python_reference"] = python_reference(cfg)
     print(json.dumps(line), flush=True)
     return 0
 
@@ -212,73 +281,75 @@ def int_peak_tops(stream) -> float:
     return best
 
 
-def load_traffic():
+def load_traffic(kernel: str = "k_win"):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full
+    capture (profiles/ncu_summary.json; the capture names its template)."""
     p = ROOT / "profiles" / "ncu_summary.json"
     try:
         d = json.loads(p.read_text())
-        return d.get("k_win", {}).get("dram_bytes_per_launch")
+        e = d.get(kernel, {})
+        return {"bytes_per_launch": e.get("dram_bytes_per_launch"), "kernel": e.get("kernel"),
+                "capture": e.get("capture")} if e else None
     except Exception:
         return None
 
 
-def run_ours(args, cfg):
-    import torch
-    import torch.distributed as dist
-    from paper_2404_16990_b200 import Engine, LatticeDims
-    from paper_2404_16990_b200._lib import call
+class L2Flush:
+    """Evicts L2 between timed steps with a READ pass over a buffer larger
+    than L2 (a write pass would leave dirty lines that drain inside the next
+    timed kernel and show up as its DRAM writes)."""
 
-    ws, rank, local = dist_info()
-    if ws > 1:
-        dist.init_process_group("nccl")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    n_sim = cfg["n_sim"]
-    temps = list(cfg["temps"](n_sim))
-    eng = Engine(LatticeDims(cfg["m"], cfg["n"]), temps, cfg["seed"], init=cfg["init"],
-                 sim_offset=rank * n_sim, device=dev, kg=args.kg, stream=args.stream)
-    st = eng._stream
-    S = eng.window                      # one step = one lookahead window of S sweeps = one launch
-    attempts_step = n_sim * cfg["m"] * cfg["n"] * S
-    peak = int_peak_tops(st)
+    def __init__(self, torch, dev, nbytes=L2_FLUSH_BYTES):
+        self.buf = torch.ones(nbytes // 8, dtype=torch.int64, device=dev)
+        self.sink = torch.empty((), dtype=torch.int64, device=dev)
+        self.torch = torch
 
-    # warm-up (public path), whole windows
-    eng._sweeps(args.warmup * S)
-    eng.synchronize()
+    def __call__(self, stream):
+        with self.torch.cuda.stream(stream):
+            self.torch.sum(self.buf, out=self.sink)
 
-    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
-    K = args.steps
+
+def device_rate(torch, dist, ws, eng, S, K, attempts_step, flush):
+    """Device-timed steps of one window each (CUDA events on the engine's
+    stream around each launch, L2 flushed in between, outside the events):
+    (total ms max over ranks, per-step ms of this rank)."""
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    sampler = ClockSampler(local)
-    sampler.start()
-    time.sleep(0.02)
-    t_wall = time.perf_counter()
     for k in range(K):
-        with torch.cuda.stream(st):
-            flush.zero_()          # L2 flush between timed steps (outside the events)
+        flush(eng._stream)
         eng._timed_sweeps(S, *evs[k])
     torch.cuda.synchronize()
-    t_wall = time.perf_counter() - t_wall
-    sampler.stop()
     step_ms = [a.elapsed_time(b) for a, b in evs]
-    total_ms = float(sum(step_ms))
-    if ws > 1:
-        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-        dist.barrier()
-    value = attempts_step * K * ws / (total_ms * 1e-3)
+    return max_over_ranks(torch, dist, ws, float(sum(step_ms))), step_ms
 
-    # end to end through the public API, host buffers both ways every step:
-    # Engine.step_packed = lattices from pinned memory -> one window of sweeps
-    # -> lattices into pinned memory + observables (the layout conversions and
-    # the observables run inside the window launch, msb_window_io).  The engine copies in and out
-    # on its own copy streams (double-buffered staging), so with three host
-    # buffers (step k reads buffer k%3, writes (k+2)%3: two interleaved
-    # chains) the copies of one step overlap the sweeps of the previous one.
-    Ke = min(K, 200)
+
+def max_over_ranks(torch, dist, ws, x: float) -> float:
+    if ws > 1:
+        t = torch.tensor([x], device=torch.device("cuda", torch.cuda.current_device()), dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+    return x
+
+
+def sum_over_ranks(torch, dist, ws, x: int) -> int:
+    if ws > 1:
+        t = torch.tensor([x], device=torch.device("cuda", torch.cuda.current_device()), dtype=torch.int64)
+        dist.all_reduce(t)
+        return int(t.item())
+    return x
+
+
+def e2e_rate(torch, dist, ws, eng, S, Ke, n_sim):
+    """End to end through the public API, host buffers both ways every step:
+    Engine.step_packed = lattices from pinned memory -> one window of sweeps
+    -> lattices into pinned memory + observables (on the window path the
+    layout conversions and the observables run inside the window launch,
+    msb_window_io).  The engine copies on its own copy streams (double-
+    buffered staging); with three host buffers (step k reads buffer k%3,
+    writes (k+2)%3) one step's copies overlap the previous step's sweeps.
+    Returns (wall seconds max over ranks, h2d bytes, d2h bytes per step)."""
     nbytes = eng.packed_nbytes()
     bufs = [torch.empty(nbytes, dtype=torch.uint8, pin_memory=True) for _ in range(3)]
     ups = torch.empty(n_sim, dtype=torch.int64, pin_memory=True)
@@ -294,12 +365,59 @@ def run_ours(args, cfg):
     for k in range(Ke):
         eng.step_packed(bufs[k % 3], S, bufs[(k + 2) % 3], ups, uns)
     eng.synchronize()
-    e2e_s = time.perf_counter() - t0
+    return max_over_ranks(torch, dist, ws, time.perf_counter() - t0), nbytes, nbytes + 16 * n_sim
+
+
+def replica_share(cfg, ws, rank):
+    """(n_sim, sim_offset) of this rank.  cfg2 (a per-GPU batch): 64 replicas
+    per rank at offset rank*64 (weak scaling).  cfg3 (754 replicas over the
+    GPUs): the reference's np.linspace slice (engine.py:470), strong scaling."""
+    if cfg.get("split"):
+        from paper_2404_16990_b200.distributed import replica_slices
+        sl = replica_slices(cfg["n_sim"], ws)
+        lo, hi = sl[rank] if rank < len(sl) else (cfg["n_sim"], cfg["n_sim"])
+        return hi - lo, lo
+    return cfg["n_sim"], rank * cfg["n_sim"]
+
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+    from paper_2404_16990_b200 import Engine, LatticeDims
+
+    ws, rank, local = dist_info()
     if ws > 1:
-        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e = attempts_step * Ke * ws / e2e_s
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    n_sim, sim_offset = replica_share(cfg, ws, rank)
+    if n_sim <= 0:
+        raise SystemExit(f"rank {rank}: no replicas of {cfg['n_sim']} left for {ws} ranks")
+    all_temps = list(cfg["temps"](cfg["n_sim"]))
+    temps = all_temps[sim_offset:sim_offset + n_sim] if cfg.get("split") else all_temps
+    eng = Engine(LatticeDims(cfg["m"], cfg["n"]), temps, cfg["seed"], init=cfg["init"],
+                 sim_offset=sim_offset, device=dev, kg=args.kg, stream=args.stream)
+    S = eng.window                      # one step = one lookahead window of S sweeps = one launch
+    my_step = n_sim * cfg["m"] * cfg["n"] * S
+    attempts_step = sum_over_ranks(torch, dist, ws, my_step)   # whole job, all ranks
+    peak = int_peak_tops(eng._stream)
+    flush = L2Flush(torch, dev)
+
+    eng._sweeps(args.warmup * S)        # warm-up (public path), whole windows
+    eng.synchronize()
+    K = args.steps
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.02)
+    t_wall = time.perf_counter()
+    total_ms, step_ms = device_rate(torch, dist, ws, eng, S, K, attempts_step, flush)
+    t_wall = time.perf_counter() - t_wall
+    sampler.stop()
+    value = attempts_step * K / (total_ms * 1e-3)
+
+    Ke = min(K, 200)
+    e2e_s, h2d, d2h = e2e_rate(torch, dist, ws, eng, S, Ke, n_sim)
+    e2e = attempts_step * Ke / e2e_s
 
     # the counter-based bit-plane stream on the same workload (direct sweeps),
     # device-timed like `value`; reported beside the headline, which stays on
@@ -307,69 +425,67 @@ def run_ours(args, cfg):
     alt = None
     if args.stream == "xoshiro" and not args.no_alt:
         alt_eng = Engine(LatticeDims(cfg["m"], cfg["n"]), temps, cfg["seed"], init=cfg["init"],
-                         sim_offset=rank * n_sim, device=dev, stream="philox-bits")
+                         sim_offset=sim_offset, device=dev, stream="philox-bits")
         alt_eng._sweeps(args.warmup * S)
         alt_eng.synchronize()
         Ka = min(K, 200)
-        aevs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(Ka)]
-        if ws > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        for k in range(Ka):
-            with torch.cuda.stream(alt_eng._stream):
-                flush.zero_()
-            alt_eng._timed_sweeps(S, *aevs[k])
-        torch.cuda.synchronize()
-        a_ms = [a.elapsed_time(b) for a, b in aevs]
-        a_tot = float(sum(a_ms))
-        if ws > 1:
-            t = torch.tensor([a_tot], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            a_tot = float(t.item())
-        a_val = attempts_step * Ka * ws / (a_tot * 1e-3)
-        a_ach = A_INT_PBITS * attempts_step / (statistics.mean(a_ms) * 1e-3) / 1e12
-        # end to end through Engine.step_packed, as the headline's e2e
-        alt_eng.store_packed(bufs[0])
-        alt_eng.store_packed(bufs[1])
-        for k in range(2):
-            alt_eng.step_packed(bufs[k % 3], S, bufs[(k + 2) % 3], ups, uns)
-        alt_eng.synchronize()
-        if ws > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        for k in range(Ke):
-            alt_eng.step_packed(bufs[k % 3], S, bufs[(k + 2) % 3], ups, uns)
-        alt_eng.synchronize()
-        a_e2e_s = time.perf_counter() - t0
-        if ws > 1:
-            t = torch.tensor([a_e2e_s], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            a_e2e_s = float(t.item())
+        a_tot, a_ms = device_rate(torch, dist, ws, alt_eng, S, Ka, attempts_step, flush)
+        a_val = attempts_step * Ka / (a_tot * 1e-3)
+        a_ach = A_INT_PBITS * my_step / (statistics.mean(a_ms) * 1e-3) / 1e12
+        a_e2e_s, _, _ = e2e_rate(torch, dist, ws, alt_eng, S, Ke, n_sim)
         alt = {"philox-bits": {
             "value": a_val, "unit": UNIT, "steps": Ka, "ms_per_step": a_tot / Ka,
             "stream": STREAM_DESC["philox-bits"],
             "path": "Engine(stream='philox-bits'): msb_direct_sweep, one launch per step of S sweeps, no accept planes",
             "roofline": {"bound": "int32", "achieved": a_ach, "peak": peak, "unit": "Tops/s", "frac": a_ach / peak,
-                         "per_launch": f"{attempts_step} attempts x {A_INT_PBITS} int32 ops (tools/pbits_ops.py)"},
-            "e2e": {"value": attempts_step * Ke * ws / a_e2e_s, "unit": UNIT, "h2d_bytes_per_step": nbytes,
-                    "d2h_bytes_per_step": nbytes + 16 * n_sim, "steps": Ke,
+                         "per_launch": f"{my_step} attempts x {A_INT_PBITS} int32 ops (tools/pbits_ops.py)"},
+            "e2e": {"value": attempts_step * Ke / a_e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "steps": Ke,
                     "path": "Engine.step_packed (as the headline e2e); conversions inside the direct launch"},
             "vs_xoshiro": a_val / value}}
+        del alt_eng
+
+    # cfg3 (the paper's 754-replica configuration) beside the cfg2 headline:
+    # same stream, same timing rules, its own device value and e2e
+    extra = None
+    if args.config == "cfg2" and not args.no_alt:
+        c3 = CONFIGS["cfg3"]
+        n3, off3 = replica_share(c3, ws, rank)
+        e3 = Engine(LatticeDims(c3["m"], c3["n"]), list(c3["temps"](c3["n_sim"]))[off3:off3 + n3], c3["seed"],
+                    init=c3["init"], sim_offset=off3, device=dev, stream=args.stream)
+        S3 = e3.window
+        my3 = n3 * c3["m"] * c3["n"] * S3
+        att3 = sum_over_ranks(torch, dist, ws, my3)
+        e3._sweeps(args.warmup * S3)
+        e3.synchronize()
+        K3 = min(K, 100)
+        t3, ms3 = device_rate(torch, dist, ws, e3, S3, K3, att3, flush)
+        e2e3_s, h3, d3 = e2e_rate(torch, dist, ws, e3, S3, min(K3, 50), n3)
+        ach3 = A_INT[args.stream] * my3 / (statistics.mean(ms3) * 1e-3) / 1e12
+        extra = {"cfg3": {
+            "value": att3 * K3 / (t3 * 1e-3), "unit": UNIT, "steps": K3, "ms_per_step": t3 / K3,
+            "workload": c3["desc"], "scaling": "strong", "replicas_this_rank": n3,
+            "roofline": {"bound": "int32", "achieved": ach3, "peak": peak, "unit": "Tops/s", "frac": ach3 / peak},
+            "e2e": {"value": att3 * min(K3, 50) / e2e3_s, "unit": UNIT, "h2d_bytes_per_step": h3,
+                    "d2h_bytes_per_step": d3, "steps": min(K3, 50)}}}
+        del e3
 
     if rank == 0:
         kern_avg_s = statistics.mean(step_ms) * 1e-3
         a_int = A_INT[args.stream]
-        achieved = a_int * attempts_step / kern_avg_s / 1e12
+        achieved = a_int * my_step / kern_avg_s / 1e12
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": args.warmup,
-            "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "strong" if cfg.get("split") else "weak",
+            "vs_baseline": None,
             "dtype": "u32", "data": "synthetic (random +/-1 initial spins from the reference init stream)",
             "config": {
                 "workload": cfg["desc"].replace("reference xoshiro256++", f"{args.stream}")
-                if args.stream != "xoshiro" else cfg["desc"], "m": cfg["m"], "n": cfg["n"], "replicas_per_gpu": n_sim,
-                "global_replicas": n_sim * ws, "attempts_per_step": attempts_step * ws,
+                if args.stream != "xoshiro" else cfg["desc"], "m": cfg["m"], "n": cfg["n"],
+                "replicas_rank0": n_sim,
+                "attempts_per_step": attempts_step,
                 "parallelism": f"replicas sharded over {ws} GPU(s), no data-path collective",
-                "l2": f"flushed between timed steps ({L2_FLUSH_BYTES >> 20} MiB write, outside the events)",
+                "l2": f"flushed between timed steps (read pass over {L2_FLUSH_BYTES >> 20} MiB, outside the events)",
                 "stream": STREAM_DESC[args.stream],
                 "step": f"one lookahead window: {S} sweeps in one launch (flips of these {S} sweeps + "
                         f"accept planes of the next {S})",
@@ -378,28 +494,34 @@ def run_ours(args, cfg):
             "roofline": {
                 "bound": "int32", "achieved": achieved, "peak": peak, "unit": "Tops/s",
                 "frac": achieved / peak, "traffic": load_traffic(),
-                "kernel": "k_win", "per_launch": f"{attempts_step} attempts x {a_int} int32 ops",
+                "kernel": "k_win", "per_launch": f"{my_step} attempts x {a_int} int32 ops",
                 "peak_source": "msb_bench_int_peak: issue-bound LOP3+IMAD mix, measured in this run",
             },
             "roofline_attempts": {
-                "int_term": peak * 1e12 / a_int, "hbm_term": 6532.9e9 / A_BYTES,
-                "frac_of_min": value / ws / min(peak * 1e12 / a_int, 6532.9e9 / A_BYTES),
+                "int_term": peak * 1e12 / a_int, "hbm_term": HBM_GBS * 1e9 / A_BYTES,
+                "frac_of_min": value / ws / min(peak * 1e12 / a_int, HBM_GBS * 1e9 / A_BYTES),
             },
             "kernel_ms": {"k_win_mean": statistics.mean(step_ms), "k_win_median": statistics.median(step_ms)},
-            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": nbytes,
-                    "d2h_bytes_per_step": nbytes + 16 * n_sim, "steps": Ke,
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "steps": Ke,
                     "path": "per step: Engine.step_packed(pinned host lattices in, one window of sweeps, pinned host "
-                            "lattices + observables out); one k_win launch per step: every warp converts the loaded lattice "
-                            "first, the flip warps export lattice + observables after the last phase (msb_window_io), copies on the engine's copy streams overlap the previous step (3 host buffers)"},
+                            "lattices + observables out); one k_win launch per step: every warp converts the loaded "
+                            "lattice first, the flip warps export lattice + observables after the last phase "
+                            "(msb_window_io); copies on the engine's copy streams overlap the previous step "
+                            "(3 host buffers)"},
             "gpu_launches": K,
             "clocks": sampler.summary(),
             "wall_s_timed_region": t_wall,
             "flips_per_ns": value / 1e9,
         }
+        line["config"]["global_replicas"] = cfg["n_sim"] if cfg.get("split") else cfg["n_sim"] * ws
         if alt is not None:
             line["other_streams"] = alt
+        if extra is not None:
+            line["other_configs"] = extra
         if ws == 1 and not args.no_cpu:
             line["cpu_baseline"] = cpu_baseline(cfg)
+            line["cpu_baseline"]["python_reference"] = python_reference(cfg)
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
@@ -493,6 +615,25 @@ def run_slab(args, cfg):
     return 0
 
 
+def spawn_ranks(n: int) -> int:
+    """``--gpus N`` outside torchrun: re-launch this command under
+    torch.distributed.run with N ranks on this node (rank r on GPU r).
+    Refuses when fewer than N GPUs are visible."""
+    import socket
+    import subprocess
+    import torch
+    have = torch.cuda.device_count()
+    if have < n:
+        print(f"bench.py: --gpus {n} but only {have} GPU(s) visible; not running", file=sys.stderr)
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
@@ -513,6 +654,13 @@ def main():
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)
+    ws_env = os.environ.get("WORLD_SIZE")
+    if ws_env is None and args.gpus > 1:
+        return spawn_ranks(args.gpus)
+    if int(ws_env or 1) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws_env}: refusing to report n_gpus != N",
+              file=sys.stderr)
+        return 2
     if cfg.get("slab"):
         return run_slab(args, cfg)
     return run_ours(args, cfg)

@@ -90,7 +90,22 @@ typedef struct msb_sweep_params {
   uint64_t seed;                 /* Philox key (the engine's master seed), both Philox streams */
   uint64_t block;                /* Philox: stream block (2 per sweep; red = even) of the first
                                     phase whose draws the call generates */
+  uint32_t *flags;               /* device: msb_flag_words() uint32, zeroed once by the caller and
+                                    owned by one engine / slab (nullable for whole lattices).
+                                    Band-group phase flags of the window and direct launches:
+                                    flags[0] counts the colour phases completed by earlier flag
+                                    launches and is advanced by each launch itself, so callers
+                                    never pass a phase count.  Null: grid-wide barriers. */
 } msb_sweep_params;
+
+/* Words of a msb_sweep_params.flags buffer for geometry g:
+ *   [0]                 phases completed (advanced by every window / direct flip launch)
+ *   [1, 1+S)            "from above": per (replica, row segment), phases the slab above has
+ *                       completed on its last row (written by that slab, peer memory)
+ *   [1+S, 1+2S)         "from below": the same for the slab below's first row
+ *   [1+2S, ...)         one flag per band group of the flip walk (phases completed)
+ * S = n_sim * row segments.  Whole lattices use [0] and the group flags; slabs all of it. */
+int64_t msb_flag_words(const msb_geom *g);
 
 /* ---- status -------------------------------------------------------------- */
 const char *msb_status_string(int status);
@@ -206,20 +221,24 @@ int msb_sweep(const msb_geom *g, const msb_sweep_params *p, uint32_t *spins, uin
  * halos IN the kernel.  Each flip of the first / last owned row is also
  * stored into the ghost row of the slab above / below (up_spins /
  * down_spins: their spin buffers, e.g. NVLink peer mappings from symmetric
- * memory; a single slab ring passes its own buffer).  Between phases the
- * slabs handshake through monotonic flag counters (system-scope atomics):
- * after its g-th phase a slab adds 1 to up_flags[1] and down_flags[0];
- * before its g-th phase it waits until my_flags[0] and my_flags[1] reach g.
- * phase0 = phases this slab completed in earlier calls; the flags start at
- * 0 with ghost rows already valid.  A call with count == 0, next == NULL and
- * a halo waits (on the stream) until both neighbours completed phase0
- * phases, i.e. the ghost rows are current (before observables). */
+ * memory; a single slab ring passes its own buffer).  Phases are ordered per
+ * band group (p->flags required): an interior group of rows waits only for
+ * its neighbour groups on the same GPU; a group holding the slab's first /
+ * last row also waits for the matching row segment of the slab above /
+ * below to finish the previous phase (its "from above" / "from below" slot,
+ * written by that slab), and after its own phase publishes completion into
+ * the neighbour's slot (system-scope release in peer memory: up_flags /
+ * down_flags are the neighbours' flag buffers).  Interior rows therefore
+ * never wait on another GPU, and a slab's edge rows overlap its interior.
+ * When the rows admit no band walk, every phase ends in a GPU-wide gate
+ * instead (the same slots, one per neighbour).  All slabs of a ring start
+ * from zeroed flags with valid ghost rows.  A call with count == 0, next ==
+ * NULL and a halo waits (on the stream) until both neighbours completed the
+ * phases in flags[0], i.e. the ghost rows are current (before observables). */
 typedef struct msb_halo {
   uint32_t *up_spins, *down_spins; /* spin buffers of the slabs above / below */
   int32_t up_R, down_R;            /* their rows per colour (rows + 2) */
-  uint32_t *up_flags, *down_flags; /* their flag pairs */
-  uint32_t *my_flags;              /* ours: [0] from the slab above, [1] from below */
-  uint64_t phase0;
+  uint32_t *up_flags, *down_flags; /* their msb_sweep_params.flags buffers */
 } msb_halo;
 /* Host I/O fused into a flip launch (whole lattices: no halo, count > 0).
  * lin_in: every warp of the launch first converts this linear lattice into
@@ -247,28 +266,50 @@ int msb_window_sweep(const msb_geom *g, const msb_sweep_params *p, int32_t S, in
                      const msb_window_io *io, void *stream);
 
 /* Direct sweeps (MSB_RNG_PHILOX_BITS, FERRO/ANTI tables): no accept planes.
- * One cooperative launch flips n_sweeps sweeps (red, blue, ... separated by
- * grid barriers) with every warp of every SM; each word's Metropolis tests
- * are decided from its neighbour classes, and only the sites with
- * Delta E > 0 compare their draw (bit planes generated on demand, most
- * significant first) against the Delta E = 4|J| or 8|J| key.  p->block is the
- * stream block of the first sweep's red phase (2 per sweep).  halo / io as in
- * msb_window_sweep.  The draws are those of PhiloxBitStreams, so results
- * equal the window path and the reference Engine fed that stream.
- * msb_direct_ok: 1 if (g, p) can take this path (n/32 % 32 == 0 or n = 512,
- * rows in bands of 2 x 32/quads-per-row), else 0.  Replaces: engine.py:353-360
- * (Engine.sweep) for the counter-based stream. */
+ * One cooperative launch flips n_sweeps sweeps with every warp of every SM;
+ * each word's Metropolis tests are decided from its neighbour classes, and
+ * only the sites with Delta E > 0 compare their draw (bit planes generated
+ * on demand, most significant first) against the Delta E = 4|J| or 8|J|
+ * key.  p->block is the stream block of the first sweep's red phase (2 per
+ * sweep).  Phases are ordered by p->flags band-group flags when given
+ * (grid barriers otherwise); halo / io as in msb_window_sweep.  The draws
+ * are those of PhiloxBitStreams, so results equal the window path and the
+ * reference Engine fed that stream.  msb_direct_ok: 1 if (g, p) can take
+ * this path (n/32 % 32 == 0 or n = 512, rows in bands of 2 x
+ * 32/quads-per-row), else 0.  Replaces: engine.py:353-360 (Engine.sweep)
+ * for the counter-based stream. */
 int msb_direct_ok(const msb_geom *g, const msb_sweep_params *p);
-/* group_flags (optional, whole lattices whose rows are one band segment):
- * msb_direct_flag_words(g, p) uint32 words, zeroed once by the caller and
- * owned by one engine; flag_phase0 = 2 x the sweeps of all earlier direct
- * calls on it.  Phases are then ordered by neighbour band-group flags
- * instead of grid barriers.  NULL: grid barriers.  Returns -1 when
- * msb_direct_ok is 0, 0 when flags do not apply. */
-int64_t msb_direct_flag_words(const msb_geom *g, const msb_sweep_params *p);
 int msb_direct_sweep(const msb_geom *g, const msb_sweep_params *p, uint32_t *spins, int32_t n_sweeps,
-                     uint64_t *flips, uint32_t *group_flags, uint32_t flag_phase0, const msb_halo *halo,
-                     const msb_window_io *io, void *stream);
+                     uint64_t *flips, const msb_halo *halo, const msb_window_io *io, void *stream);
+
+/* ---- a ring of row slabs in ONE launch (several slabs per GPU) ---------- */
+/* The slabs of a lattice held by one process on one device (the periodic
+ * ring of one lattice in row slabs, or a part of a larger ring): one
+ * cooperative launch runs them all, the CTAs split evenly between the
+ * slabs, each slab with its own buffers, work counters, flags and msb_halo
+ * (neighbour pointers may name slabs of this ring or peer memory).  Same
+ * per-slab semantics as msb_window_sweep / msb_direct_sweep with a halo;
+ * every slab shares S, P, the table mode and the stream kind.  ctx:
+ * device scratch of msb_ring_ctx_bytes(nslabs) bytes (per-slab kernel
+ * arguments, copied on the stream).  This is also how the multi-GPU halo
+ * protocol is exercised on one GPU: a GPU cannot run several cooperative
+ * launches that wait on one another, but one launch over several slabs can. */
+typedef struct msb_ring_slab {
+  const msb_geom *g;
+  const msb_sweep_params *p;
+  uint32_t *spins;
+  uint32_t *states;      /* window path: piece states (xoshiro); direct: unused */
+  const uint32_t *cur;   /* window path: window being flipped; direct: unused */
+  uint32_t *next;        /* window path: window being produced (nullable); direct: unused */
+  uint64_t *flips;
+  const msb_halo *halo;
+} msb_ring_slab;
+#define MSB_RING_MAX 16
+int64_t msb_ring_ctx_bytes(int32_t nslabs);
+int msb_window_sweep_ring(int32_t nslabs, const msb_ring_slab *slabs, int32_t S, int32_t P, int32_t first,
+                          int32_t count, void *ctx, void *stream);
+int msb_direct_sweep_ring(int32_t nslabs, const msb_ring_slab *slabs, int32_t n_sweeps, void *ctx,
+                          void *stream);
 
 /* ---- observables (engine.py:372-386) ------------------------------------- */
 /* Adds, per replica, the number of +1 spins and the number of unsatisfied

@@ -62,16 +62,27 @@ class SweepParams(ctypes.Structure):
         ("rng", ctypes.c_int32),
         ("seed", ctypes.c_uint64),
         ("block", ctypes.c_uint64),
+        ("flags", ctypes.c_void_p),
     ]
 
 
 class Halo(ctypes.Structure):
-    """msb_halo: in-kernel halo exchange of a slab window (include/msb200.h)."""
+    """msb_halo: in-kernel halo exchange of a slab (include/msb200.h): the
+    neighbours' spin buffers and row counts, and their flag buffers."""
     _fields_ = [
         ("up_spins", ctypes.c_void_p), ("down_spins", ctypes.c_void_p),
         ("up_R", ctypes.c_int32), ("down_R", ctypes.c_int32),
-        ("up_flags", ctypes.c_void_p), ("down_flags", ctypes.c_void_p), ("my_flags", ctypes.c_void_p),
-        ("phase0", ctypes.c_uint64),
+        ("up_flags", ctypes.c_void_p), ("down_flags", ctypes.c_void_p),
+    ]
+
+
+class RingSlab(ctypes.Structure):
+    """msb_ring_slab: one slab of a ring launch (msb_window_sweep_ring /
+    msb_direct_sweep_ring)."""
+    _fields_ = [
+        ("g", ctypes.POINTER(Geom)), ("p", ctypes.POINTER(SweepParams)),
+        ("spins", ctypes.c_void_p), ("states", ctypes.c_void_p), ("cur", ctypes.c_void_p),
+        ("next", ctypes.c_void_p), ("flips", ctypes.c_void_p), ("halo", ctypes.POINTER(Halo)),
     ]
 
 
@@ -90,7 +101,8 @@ EXPORTS = (
     "msb_init_const", "msb_from_linear", "msb_to_linear", "msb_to_ref16", "msb_from_ref16",
     "msb_plane_words", "msb_rng_planes", "msb_flip", "msb_phase", "msb_sweep",
     "msb_default_window", "msb_window_parts", "msb_window_pieces", "msb_window_words", "msb_window_init", "msb_window_sweep",
-    "msb_direct_ok", "msb_direct_flag_words", "msb_direct_sweep",
+    "msb_direct_ok", "msb_direct_sweep", "msb_flag_words",
+    "msb_ring_ctx_bytes", "msb_window_sweep_ring", "msb_direct_sweep_ring",
     "msb_observe", "msb_export", "msb_draws", "msb_pack_edges", "msb_unpack_ghosts", "msb_bench_int_peak",
 )
 
@@ -149,9 +161,11 @@ def lib() -> ctypes.CDLL:
         "msb_window_sweep": ([G, P, i32, i32, vp, vp, vp, i32, i32, vp, vp, ctypes.POINTER(Halo),
                               ctypes.POINTER(WindowIO), vp], ctypes.c_int),
         "msb_direct_ok": ([G, P], i32),
-        "msb_direct_flag_words": ([G, P], i64),
-        "msb_direct_sweep": ([G, P, vp, i32, vp, vp, ctypes.c_uint32, ctypes.POINTER(Halo), ctypes.POINTER(WindowIO), vp],
-                             ctypes.c_int),
+        "msb_flag_words": ([G], i64),
+        "msb_direct_sweep": ([G, P, vp, i32, vp, ctypes.POINTER(Halo), ctypes.POINTER(WindowIO), vp], ctypes.c_int),
+        "msb_ring_ctx_bytes": ([i32], i64),
+        "msb_window_sweep_ring": ([i32, ctypes.POINTER(RingSlab), i32, i32, i32, i32, vp, vp], ctypes.c_int),
+        "msb_direct_sweep_ring": ([i32, ctypes.POINTER(RingSlab), i32, vp, vp], ctypes.c_int),
         "msb_observe": ([G, vp, vp, vp, vp], ctypes.c_int),
         "msb_export": ([G, vp, vp, vp, vp, vp], ctypes.c_int),
         "msb_draws": ([G, P, i32, vp, vp, vp], ctypes.c_int),

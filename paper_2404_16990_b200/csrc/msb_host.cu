@@ -85,7 +85,7 @@ const char* msb_status_string(int status) {
 
 const char* msb_last_error(void) { return g_last_error.c_str(); }
 
-int msb_abi_version(void) { return 1; }
+int msb_abi_version(void) { return 2; }
 
 int msb_check_geom(const msb_geom* g) { return check_geom(g); }
 

@@ -252,7 +252,36 @@ struct PbitsDirect {
   unsigned long long blk;  // stream block of this colour phase (2 per sweep)
 };
 
-template <bool COHERENT, bool PUSH = false, bool SEG = false, int DIRECT = 0>
+// L2 prefetch of the accept-plane rows (both planes) of band group g,
+// colour X, issued by one lane per band (single-segment rows): the plane
+// rows were written a window earlier and live in HBM.
+__device__ __forceinline__ void band_prefetch(const FlipArgs& a, unsigned g, int X) {
+  const Geo& G = a.G;
+  const int lane = threadIdx.x & 31, sq = a.band_sq, bi = lane / sq, q = lane - bi * sq;
+  if (q != 0) return;
+  const int H = a.band_h, gb = a.band_gb;
+  const unsigned Wp = (unsigned)G.Wp, pstride = (unsigned)G.n_sim * (unsigned)G.rows * Wp;
+  const unsigned groups_per_sim = (unsigned)G.rows / (unsigned)(gb * H);
+  const unsigned s = g / groups_per_sim;
+  const int lr0 = (int)(g - s * groups_per_sim) * gb * H + bi * H;
+  const uint32_t* pr =
+      a.planes + ((((unsigned)X * (unsigned)a.np) * (unsigned)G.n_sim + s) * (unsigned)G.rows + (unsigned)lr0) * Wp;
+  const unsigned bytes = (unsigned)H * Wp * 4u;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pr), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pr + pstride), "r"(bytes) : "memory");
+}
+
+// The warps' key-mask tables of the direct walk (pbits_accept_sel<true>):
+// ONE static shared array per kernel however many walk instantiations it
+// inlines (a __shared__ inside the template would be one per instantiation).
+__device__ __forceinline__ uint4 (*direct_key_tables())[12] {
+  __shared__ uint4 kmt[32][12];
+  return kmt;
+}
+
+// PF: prefetch the plane rows of the run's groups one group ahead (callers
+// that walk one group at a time prefetch themselves, band_prefetch).
+template <bool COHERENT, bool PUSH = false, bool SEG = false, int DIRECT = 0, bool PF = true>
 __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0, unsigned g1, int X,
                                                   const PbitsDirect* dp = nullptr) {
   const Geo& G = a.G;
@@ -289,9 +318,9 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pr), "r"(bytes) : "memory");
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pr + pstride), "r"(bytes) : "memory");
   };
-  if (!DIRECT && !SEG && q == 0 && g0 < g1) prefetch_band(g0);
+  if (PF && !DIRECT && !SEG && q == 0 && g0 < g1) prefetch_band(g0);
   for (unsigned g = g0; g < g1; g++) {
-    if (!DIRECT && !SEG && q == 0 && g + 1 < g1) prefetch_band(g + 1);
+    if (PF && !DIRECT && !SEG && q == 0 && g + 1 < g1) prefetch_band(g + 1);
     const unsigned gr = SEG ? g / (unsigned)nseg : g;
     const int seg = (int)(g - gr * (unsigned)nseg);
     const unsigned s = gr / groups_per_sim;
@@ -318,7 +347,7 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
     bool kuni = false;  // DIRECT: the warp's lanes share one pair of keys (bands of one replica)
     uint4* kt = nullptr;
     if (DIRECT) {
-      __shared__ uint4 kmt[32][12];  // per warp: 6 blocks x (key4, key8) x 4 plane masks
+      uint4(*kmt)[12] = direct_key_tables();  // per warp: 6 blocks x (key4, key8) x 4 plane masks
       key4 = dp->thr9[s];
       key8 = dp->thr9[G.n_sim + s];
       kuni = __all_sync(0xFFFFFFFFu, key4 == __shfl_sync(0xFFFFFFFFu, key4, 0) &&

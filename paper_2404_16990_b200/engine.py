@@ -2,12 +2,16 @@
 
 Same constructor, methods, attributes, counters and error behaviour as the
 reference engine (pkg/src/multispin/engine.py:216-492), but the spins live
-on the GPU in a colour-split bit layout and every sweep runs as two fused
-sm_100a kernels (libmsb200, include/msb200.h): per colour phase, each piece
-of a reference xoshiro256++ stream generates its draws, compares them with
-integer Boltzmann thresholds and flips its row's spins with bit-sliced
-neighbour logic.  Results are bit-identical to the reference on identical
-seeds, dimensions, temperatures and couplings.
+on the GPU in a colour-split bit layout and the sweeps run as sm_100a
+kernels (libmsb200, include/msb200.h).  Steady state (``run`` / ``_sweeps``
+with FERRO/ANTI tables): lookahead windows, ONE cooperative launch per S = 8
+sweeps in which producer warps turn the next window's reference xoshiro256++
+draws into accept bit planes while the other warps flip this window's
+sweeps with bit-sliced neighbour logic (msb_window_sweep); the bit-plane
+counter stream flips without planes (msb_direct_sweep).  ``flip_red`` /
+``flip_blue`` alone, forced generic tables, host-supplied ``streams`` and the
+recorder take the per-phase kernels (msb_phase).  Results are bit-identical
+to the reference on identical seeds, dimensions, temperatures and couplings.
 
 Reference surfaces kept (file:line in pkg/src/multispin/engine.py):
   ``Engine(dims, temperatures, seed, init, coupling, sim_offset)`` 238-272
@@ -202,6 +206,11 @@ class Engine:
             self._planes_t = None
             self._work = torch.zeros(4, dtype=torch.int32, device=self.device)
             self._obs = torch.zeros(2 * self.n_sim, dtype=torch.int64, device=self.device)
+            # band-group phase flags of the window / direct launches (header word
+            # advanced by the launches themselves, include/msb200.h)
+            self._flags = torch.zeros(int(_lib.lib().msb_flag_words(ctypes.byref(self._g))), dtype=torch.int32,
+                                      device=self.device)
+        self._fphases = 0  # phases launched on _flags (re-zeroed long before the uint32 counters wrap)
         self._pow = _pow_tables(self.device)
         self._jump = _sweep_jump_table(self.device, dims.n)
         self._params = SweepParams()
@@ -211,6 +220,7 @@ class Engine:
         self._params.work = self._work.data_ptr()
         self._params.rng = RNG_MODES[stream]
         self._params.seed = self.seed & _M64
+        self._params.flags = self._flags.data_ptr()
         self._tab_key = None
         self.fault = 0  # test-only adder corruption (selftest seam, cli.py:467-480)
         self.overlap = True  # run the next sweep's RNG concurrently with this sweep's flips
@@ -245,7 +255,7 @@ class Engine:
         else:
             cls = PhiloxStreams if stream == "philox" else PhiloxBitStreams
             self.streams = cls(self.seed, self.n_sim * dims.cells, self.sim_offset * dims.cells)
-        self._own_streams = self.streams
+        self._own_streams = self._streams
         self._blocks = 0        # stream blocks consumed (one per colour phase)
         self._pos = [0, 1]      # block each colour's pieces are positioned at
         self._ahead = False     # next sweep's accept planes already generated (states one sweep on)
@@ -264,6 +274,21 @@ class Engine:
         self.recorder = None
         self.update_red_bc()
         self.update_blue_bc()
+
+    @property
+    def streams(self):
+        """The flip streams (reference seam, engine.py:259-261, 336).  The
+        engine's own counter-based stream object is returned positioned at
+        the draws the device has consumed (64 * words per stream and colour
+        phase), so it can continue this run on the reference Engine."""
+        s = self._streams
+        if s is getattr(self, "_own_streams", None) and hasattr(s, "position"):
+            s.position = self._blocks * 64 * self.dims.words
+        return s
+
+    @streams.setter
+    def streams(self, value) -> None:
+        self._streams = value
 
     @property
     def _planes(self):
@@ -394,7 +419,7 @@ class Engine:
         engine.py:336): u23 integers in the reference block order."""
         torch = _torch()
         d = self.dims
-        block = np.asarray(self.streams.unit_block(4 * 16 * d.words), dtype=np.float64)
+        block = np.asarray(self._streams.unit_block(4 * 16 * d.words), dtype=np.float64)
         expect = (4 * 16 * d.words, self.n_sim * d.cells)
         if block.shape != expect:
             raise ValueError(f"streams.unit_block returned {block.shape}, expected {expect}")
@@ -442,7 +467,7 @@ class Engine:
         h = self._blocks
         ext = None
         self._params.block = h
-        if self.streams is not self._own_streams:
+        if self._streams is not self._own_streams:
             ext = self._host_draws(phase)
             self._pos[phase] = None
         else:
@@ -483,7 +508,7 @@ class Engine:
         for name in ("sweep", "flip_red", "flip_blue", "update_red_bc", "update_blue_bc"):
             if name in self.__dict__ or getattr(cls, name) is not getattr(Engine, name):
                 return False
-        return self.recorder is None and self.streams is self._own_streams
+        return self.recorder is None and self._streams is self._own_streams
 
     def _sweeps(self, k: int, io=None) -> None:
         """k sweeps through the library, no host sync: lookahead windows
@@ -527,16 +552,10 @@ class Engine:
 
     def _direct_sweeps(self, k: int, io=None) -> None:
         """k sweeps in launches of up to ``window`` sweeps; with ``io`` the
-        load goes with the first launch, the export with the last."""
+        load goes with the first launch, the export with the last.  Phases
+        are ordered by band-group flags (``_flags``)."""
         self._wvalid = False       # windows and per-sweep lookahead planes are stale now
         self._ahead = False
-        if getattr(self, "_dflags", None) is None:  # band-group phase flags (monotonic)
-            torch = _torch()
-            words = int(_lib.lib().msb_direct_flag_words(ctypes.byref(self._g), ctypes.byref(self._params)))
-            with torch.cuda.device(self.device), torch.cuda.stream(self._stream):
-                self._dflags = torch.zeros(max(words, 1), dtype=torch.int32, device=self.device)
-            self._dflags_on = words > 0
-            self._dphase = 0
         first = True
         while k > 0:
             r = min(k, self.window)
@@ -547,17 +566,21 @@ class Engine:
                     lio.lin_out, lio.ups, lio.unsat = io.lin_out, io.ups, io.unsat
             first = False
             self._params.block = self._blocks
-            if self._dphase + 2 * r >= 1 << 31:  # keep the flags far from wrapping
-                with _torch().cuda.stream(self._stream):
-                    self._dflags.zero_()
-                self._dphase = 0
+            self._flag_phases(2 * r)
             call("msb_direct_sweep", ctypes.byref(self._g), ctypes.byref(self._params), _p(self._spins), r,
-                 _p(self._flips_dev), _p(self._dflags) if self._dflags_on else None, ctypes.c_uint32(self._dphase),
-                 None, ctypes.byref(lio) if lio is not None else None, self._cs)
-            self._dphase += 2 * r
+                 _p(self._flips_dev), None, ctypes.byref(lio) if lio is not None else None, self._cs)
             self._blocks += 2 * r
             k -= r
         self._pos = [self._blocks, self._blocks + 1]  # counter-based: the per-phase path needs no positioning
+
+    def _flag_phases(self, phases: int) -> None:
+        """Account for a flag launch of `phases` colour phases; the uint32
+        counters are re-zeroed (stream-ordered) long before they could wrap."""
+        if self._fphases + phases >= 1 << 31:
+            with _torch().cuda.stream(self._stream):
+                self._flags.zero_()
+            self._fphases = 0
+        self._fphases += phases
 
     # -- lookahead windows (msb_window_sweep) ------------------------------------
 
@@ -578,8 +601,10 @@ class Engine:
 
     @property
     def _io_groups_ok(self) -> bool:
-        """msb_window_io works in groups of 4 chunks of 1024 sites."""
-        return (self.dims.m * -(-self.dims.n // 1024)) % 4 == 0
+        """msb_window_io works in groups of 4 chunks of 1024 sites, with
+        fewer than 2^31 / 32 chunks (make_win_io, msb_window.cuh)."""
+        chunks = self.n_sim * self.dims.m * -(-self.dims.n // 1024)
+        return (self.dims.m * -(-self.dims.n // 1024)) % 4 == 0 and 32 * chunks < (1 << 31)
 
     def _win_launch(self, first: int, count: int, produce: bool, io=None) -> None:
         states, planes, words, jump = self._wbuf
@@ -590,6 +615,7 @@ class Engine:
         self._params.jump = jump.data_ptr()
         # Philox: block of the produced window's slot 0
         self._params.block = self._wbase if count == 0 else self._wbase + 2 * self.window
+        self._flag_phases(2 * count)
         call("msb_window_sweep", ctypes.byref(self._g), ctypes.byref(self._params), self.window, self._wP,
              _p(self._spins), _p(states), _p(cur) if cur is not None else None, first, count,
              _p(nxt) if produce else None, _p(self._flips_dev), None,

@@ -18,12 +18,15 @@ Transports:
   DistExchange   one slab per torch.distributed rank: batched send/recv of
                  the edge rows (NCCL over NVLink on GPUs, gloo on CPU).
 
-FusedSlabRun drops the host from the loop: one slab per process, lookahead
-windows (msb_window_sweep) whose flip warps store the slab's first/last rows
+FusedSlabRun drops the host from the loop: lookahead windows
+(msb_window_sweep) whose flip warps store each slab's first/last rows
 straight into the neighbours' ghost rows -- peer memory over NVLink from
-symmetric memory -- and handshake every phase through flag counters in peer
-memory.  One process with one slab is the periodic ring of a single slab
-(its own neighbour), which runs the same kernel path.
+symmetric memory with one slab per process, or plain device memory for the
+slabs of one process -- and order the phases per band group through flags
+the slabs write into each other's memory, so only the edge bands ever wait
+on a neighbour.  Several slabs of one process run in one cooperative launch
+(msb_window_sweep_ring); one slab alone is the periodic ring of a single
+slab (its own neighbour), on the same kernel path.
 """
 
 from __future__ import annotations
@@ -95,6 +98,12 @@ class SlabLattice:
             self._work = torch.zeros(4, dtype=torch.int32, device=self.device)
             self._flips = torch.zeros(MSB_FLIP_SLOTS, dtype=torch.int64, device=self.device)
             self._obs = torch.zeros(2 * self.n_sim, dtype=torch.int64, device=self.device)
+            # phase flags (header, halo slots from the neighbour slabs, band groups):
+            # written by the neighbours too, so in the same memory kind as the spins
+            nflags = int(L.msb_flag_words(ctypes.byref(self._g)))
+            self._flags = (alloc(nflags, self.device) if alloc is not None
+                           else torch.empty(nflags, dtype=torch.int32, device=self.device))
+            self._flags.zero_()
             self._edge = torch.empty(self.n_sim * 2 * self.Wp, dtype=torch.int32, device=self.device)
             self._ghost = torch.empty(self.n_sim * 2 * self.Wp, dtype=torch.int32, device=self.device)
         self._pow = _pow_tables(self.device)
@@ -103,6 +112,7 @@ class SlabLattice:
         p.mode, p.n_planes = mode.value, npl.value
         p.code_plane[:] = list(codes)
         p.thr9, p.kg, p.jump, p.work = self._thr.data_ptr(), self.kg, self._jump.data_ptr(), self._work.data_ptr()
+        p.flags = self._flags.data_ptr()
         if stream not in RNG_MODES:
             raise ValueError(f"unknown stream {stream!r}")
         self.stream = stream
@@ -191,12 +201,22 @@ def ring_plan(m: int, world: int, rank: int) -> dict:
 
 def symmetric_alloc(group=None):
     """Allocator for SlabLattice(alloc=...): int32 buffers in torch symmetric
-    memory, so every rank of `group` can map them (FusedSlabRun)."""
+    memory, so every rank of `group` can map them (FusedSlabRun).  Symmetric
+    buffers must have one size on every rank, and slabs of an uneven split
+    differ by a row or two: each allocation is the group's largest request
+    (one MAX all-reduce per buffer; every rank allocates the same buffers in
+    the same order), returned as a view of the requested length."""
+    import torch.distributed as dist
     import torch.distributed._symmetric_memory as symm_mem
     torch = _torch()
 
     def alloc(nwords: int, device):
-        return symm_mem.empty(nwords, dtype=torch.int32, device=device)
+        top = int(nwords)
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+            t = torch.tensor([top], dtype=torch.int64, device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+            top = int(t.item())
+        return symm_mem.empty(top, dtype=torch.int32, device=device)[:nwords]
     return alloc
 
 
@@ -296,31 +316,42 @@ class SlabRun:
 
 
 class FusedSlabRun:
-    """One slab per process, halos exchanged inside the window kernel.
+    """Slabs whose halos are exchanged inside the flip kernels.
 
-    Per call of ``sweep(k)`` the slab runs lookahead windows of S sweeps
-    (``msb_window_sweep`` with an ``msb_halo``): producer warps generate the
-    next window's accept planes for the slab's own rows while the flip warps
-    flip the current window phase by phase; every flip of the first / last
-    owned row is also stored into the neighbour's ghost row (peer memory), and
-    the slabs handshake each phase through monotonic flag counters (system-
-    scope atomics on peer memory), so no host synchronisation or separate
-    exchange step remains.
+    Per call of ``sweep(k)`` every slab runs lookahead windows of S sweeps
+    (``msb_window_sweep`` with an ``msb_halo``; the bit-plane stream: direct
+    sweeps): producer warps generate the next window's accept planes for the
+    slab's own rows while the flip warps flip the current window; every flip
+    of a slab's first / last row is also stored into the neighbour's ghost
+    row, and phases are ordered per band group -- interior bands wait only
+    for their neighbours on the same GPU, the edge bands also for the
+    neighbour slab's edge band (flags written into each other's memory) --
+    so no host synchronisation or separate exchange step remains and the
+    halo traffic overlaps the interior flips.
 
-    world 1 (no process group): the slab is its own upper and lower
-    neighbour -- the periodic single-slab ring, same kernel path.  world > 1:
-    build the slab with ``alloc=symmetric_alloc(group)`` and rows from
-    ``ring_plan``; spins and flags are mapped from every peer.
+    ``slabs``: one SlabLattice, or a list of them forming the whole ring on
+    this process's device (consecutive ring_plan / slab_bounds slabs of one
+    lattice).  With one process, the slabs are each other's neighbours (a
+    single slab is its own: the periodic ring of one slab); several slabs run
+    in ONE cooperative launch per window (msb_window_sweep_ring), the CTAs
+    split between them.  With a process group of world > 1: exactly one slab
+    per rank, built with ``alloc=symmetric_alloc(group)`` and rows from
+    ``ring_plan``; spins and flags of the ring neighbours are mapped from
+    symmetric memory (NVLink peer memory).
     """
 
-    def __init__(self, slab: SlabLattice, group=None, window: int | None = None):
+    def __init__(self, slabs, group=None, window: int | None = None):
         import torch.distributed as dist
         torch = _torch()
-        self.slab = slab
+        self.slabs = list(slabs) if isinstance(slabs, (list, tuple)) else [slabs]
+        s0 = self.slab = self.slabs[0]
         L = _lib.lib()
-        g = ctypes.byref(slab._g)
-        if slab._params.mode == 2:
-            raise ValueError("fused slab windows need FERRO/ANTI tables")
+        g = ctypes.byref(s0._g)
+        for s in self.slabs:
+            if s._params.mode == 2:
+                raise ValueError("fused slab windows need FERRO/ANTI tables")
+            if s.stream != s0.stream or s.device != s0.device or s.dims != s0.dims or s.n_sim != s0.n_sim:
+                raise ValueError("the slabs of a ring share the lattice, stream kind and device")
         if window is None:
             S, P = ctypes.c_int32(), ctypes.c_int32()
             call("msb_default_window", g, ctypes.byref(S), ctypes.byref(P))
@@ -329,98 +360,149 @@ class FusedSlabRun:
             self.S = int(window)
             self.P = int(L.msb_window_parts(g, self.S))
         # bit-plane stream: direct sweeps (no accept planes), S sweeps per launch
-        self.direct = slab.stream == "philox-bits" and bool(L.msb_direct_ok(g, ctypes.byref(slab._params)))
-        self.world = dist.get_world_size(group) if (dist.is_available() and dist.is_initialized()) else 1
+        self.direct = s0.stream == "philox-bits" and all(
+            bool(L.msb_direct_ok(ctypes.byref(s._g), ctypes.byref(s._params))) for s in self.slabs)
+        dist_on = dist.is_available() and dist.is_initialized()
+        if dist_on and group is None:
+            group = dist.group.WORLD
+        self.group = group
+        self.world = dist.get_world_size(group) if dist_on else 1
         self.rank = dist.get_rank(group) if self.world > 1 else 0
+        if self.world > 1 and len(self.slabs) != 1:
+            raise ValueError("one slab per rank when the ring spans processes")
+        self._wb = []
         if not self.direct:
-            npieces = int(L.msb_window_pieces(g, self.S, self.P))
-            self._words = int(L.msb_window_words(g, self.S))
-            if npieces < 0 or self._words < 0:
-                raise _lib.MsbError(f"slab window S={self.S} P={self.P}: {L.msb_last_error().decode()}")
-            with torch.cuda.device(slab.device), slab.stream_ctx():
-                self._wstates = torch.empty(8 * npieces, dtype=torch.int32, device=slab.device)
-                self._wplanes = torch.empty(2 * self._words, dtype=torch.int32, device=slab.device)
-            self._jump = _jump_table(slab.device, self.S * 4 * slab.dims.n)
-        R = slab.rows + 2
-        h = _lib.Halo()
+            for s in self.slabs:
+                sg = ctypes.byref(s._g)
+                npieces = int(L.msb_window_pieces(sg, self.S, self.P))
+                words = int(L.msb_window_words(sg, self.S))
+                if npieces < 0 or words < 0:
+                    raise _lib.MsbError(f"slab window S={self.S} P={self.P}: {L.msb_last_error().decode()}")
+                with torch.cuda.device(s.device), s.stream_ctx():
+                    self._wb.append((torch.empty(8 * npieces, dtype=torch.int32, device=s.device),
+                                     torch.empty(2 * words, dtype=torch.int32, device=s.device), words))
+            self._jump = _jump_table(s0.device, self.S * 4 * s0.dims.n)
+        self._halos = []
         if self.world == 1:
-            with slab.stream_ctx():
-                self._flags = torch.zeros(2, dtype=torch.int32, device=slab.device)
-            sp, fl = slab._spins.data_ptr(), self._flags.data_ptr()
-            h.up_spins = h.down_spins = sp
-            h.up_flags = h.down_flags = h.my_flags = fl
-            h.up_R = h.down_R = R
-            LocalExchange().exchange([slab], 0)
-            LocalExchange().exchange([slab], 1)
+            V = len(self.slabs)
+            for v, s in enumerate(self.slabs):
+                up, dn = self.slabs[(v - 1) % V], self.slabs[(v + 1) % V]
+                if (up.row0 + up.rows) % s.dims.m != s.row0 or (s.row0 + s.rows) % s.dims.m != dn.row0:
+                    raise ValueError("the slabs must be consecutive row ranges covering the lattice")
+                h = _lib.Halo()
+                h.up_spins, h.down_spins = up._spins.data_ptr(), dn._spins.data_ptr()
+                h.up_flags, h.down_flags = up._flags.data_ptr(), dn._flags.data_ptr()
+                h.up_R, h.down_R = up.rows + 2, dn.rows + 2
+                self._halos.append(h)
+            for X in (0, 1):
+                LocalExchange().exchange(self.slabs, X)
         else:
             import torch.distributed._symmetric_memory as symm_mem
-            plan = ring_plan(slab.dims.m, self.world, self.rank)
-            if (plan["row0"], plan["rows"]) != (slab.row0, slab.rows):
+            plan = ring_plan(s0.dims.m, self.world, self.rank)
+            if (plan["row0"], plan["rows"]) != (s0.row0, s0.rows):
                 raise ValueError("slab rows must follow ring_plan(m, world, rank)")
-            self._flags = symm_mem.empty(2, dtype=torch.int32, device=slab.device)
-            self._flags.zero_()
-            hs = symm_mem.rendezvous(slab._spins, group)
-            hf = symm_mem.rendezvous(self._flags, group)
+
+            def base(t):
+                return t._base if t._base is not None else t
+            hs = symm_mem.rendezvous(base(s0._spins), self.group)
+            hf = symm_mem.rendezvous(base(s0._flags), self.group)
 
             def peer(hdl, t, r):  # peer r's mapping of the same buffer
                 return int(hdl.buffer_ptrs[r]) + (t.data_ptr() - int(hdl.buffer_ptrs[self.rank]))
-            h.up_spins, h.down_spins = peer(hs, slab._spins, plan["up"]), peer(hs, slab._spins, plan["down"])
-            h.up_flags, h.down_flags = peer(hf, self._flags, plan["up"]), peer(hf, self._flags, plan["down"])
-            h.my_flags = self._flags.data_ptr()
+            h = _lib.Halo()
+            h.up_spins, h.down_spins = peer(hs, s0._spins, plan["up"]), peer(hs, s0._spins, plan["down"])
+            h.up_flags, h.down_flags = peer(hf, s0._flags, plan["up"]), peer(hf, s0._flags, plan["down"])
             h.up_R, h.down_R = plan["up_R"], plan["down_R"]
-            DistExchange(group).exchange([slab], 0)
-            DistExchange(group).exchange([slab], 1)
-            torch.cuda.synchronize(slab.device)
-            dist.barrier(group)
-        h.phase0 = 0
-        self._halo = h
+            self._halos.append(h)
+            self._handles = (hs, hf)
+            DistExchange(self.group).exchange([s0], 0)
+            DistExchange(self.group).exchange([s0], 1)
+            torch.cuda.synchronize(s0.device)
+            dist.barrier(self.group)
+        if len(self.slabs) > 1:
+            with torch.cuda.device(s0.device), s0.stream_ctx():
+                self._ctx = torch.empty(int(L.msb_ring_ctx_bytes(len(self.slabs))), dtype=torch.uint8,
+                                        device=s0.device)
+            # one launch runs every slab: the slabs share the first slab's stream
+            # from here on (their construction work, on their own streams, first)
+            for s in self.slabs[1:]:
+                s.synchronize()
+                s._stream, s._cs = s0._stream, s0._cs
         self._valid = False
         self._cur = 0
         self._wc = 0
         self._wbase = 0
 
+    def _ring(self, first: int, count: int, produce: bool):
+        arr = (_lib.RingSlab * len(self.slabs))()
+        for v, s in enumerate(self.slabs):
+            r = arr[v]
+            r.g, r.p = ctypes.pointer(s._g), ctypes.pointer(s._params)
+            r.spins, r.flips, r.halo = s._spins.data_ptr(), s._flips.data_ptr(), ctypes.pointer(self._halos[v])
+            if not self.direct:
+                states, planes, w = self._wb[v]
+                cur = planes[self._cur * w:(self._cur + 1) * w]
+                nxt = planes[(1 - self._cur) * w:(2 - self._cur) * w]
+                if count == 0:
+                    nxt, cur = cur, None
+                r.states = states.data_ptr()
+                r.cur = cur.data_ptr() if cur is not None else None
+                r.next = nxt.data_ptr() if produce else None
+        return arr
+
     def _launch(self, first: int, count: int, produce: bool) -> None:
-        s = self.slab
-        w = self._words
-        cur = self._wplanes[self._cur * w:(self._cur + 1) * w]
-        nxt = self._wplanes[(1 - self._cur) * w:(2 - self._cur) * w]
-        if count == 0:
-            nxt, cur = cur, None
-        s._params.jump = self._jump.data_ptr()
-        s._params.block = self._wbase if count == 0 else self._wbase + 2 * self.S
-        call("msb_window_sweep", ctypes.byref(s._g), ctypes.byref(s._params), self.S, self.P, _p(s._spins),
-             _p(self._wstates), _p(cur) if cur is not None else None, first, count,
-             _p(nxt) if produce else None, _p(s._flips), ctypes.byref(self._halo), None, s._cs)
-        s._params.jump = s._jump.data_ptr()
+        s0 = self.slab
+        for s in self.slabs:
+            s._params.jump = self._jump.data_ptr()
+            s._params.block = self._wbase if count == 0 else self._wbase + 2 * self.S
+        if len(self.slabs) == 1:
+            states, planes, w = self._wb[0]
+            cur = planes[self._cur * w:(self._cur + 1) * w]
+            nxt = planes[(1 - self._cur) * w:(2 - self._cur) * w]
+            if count == 0:
+                nxt, cur = cur, None
+            call("msb_window_sweep", ctypes.byref(s0._g), ctypes.byref(s0._params), self.S, self.P, _p(s0._spins),
+                 _p(states), _p(cur) if cur is not None else None, first, count, _p(nxt) if produce else None,
+                 _p(s0._flips), ctypes.byref(self._halos[0]), None, s0._cs)
+        else:
+            arr = self._ring(first, count, produce)
+            call("msb_window_sweep_ring", len(self.slabs), arr, self.S, self.P, first, count, _p(self._ctx), s0._cs)
+        for s in self.slabs:
+            s._params.jump = s._jump.data_ptr()
 
     def sweep(self, n_sweeps: int = 1) -> None:
-        s = self.slab
+        s0 = self.slab
         k = int(n_sweeps)
         if k <= 0:
             return
         if self.direct:
             while k > 0:
                 r = min(k, self.S)
-                s._params.block = 2 * s.sweeps_done
-                call("msb_direct_sweep", ctypes.byref(s._g), ctypes.byref(s._params), _p(s._spins), r, _p(s._flips),
-                     None, ctypes.c_uint32(0), ctypes.byref(self._halo), None, s._cs)
-                self._halo.phase0 += 2 * r
-                s.sweeps_done += r
+                for s in self.slabs:
+                    s._params.block = 2 * s.sweeps_done
+                if len(self.slabs) == 1:
+                    call("msb_direct_sweep", ctypes.byref(s0._g), ctypes.byref(s0._params), _p(s0._spins), r,
+                         _p(s0._flips), ctypes.byref(self._halos[0]), None, s0._cs)
+                else:
+                    call("msb_direct_sweep_ring", len(self.slabs), self._ring(0, r, False), r, _p(self._ctx), s0._cs)
+                for s in self.slabs:
+                    s.sweeps_done += r
                 k -= r
             return
         if not self._valid:
-            self._wbase, self._wc, self._cur = 2 * s.sweeps_done, 0, 0
-            if s.stream == "xoshiro":
-                call("msb_window_init", ctypes.byref(s._g), ctypes.c_uint64(s.seed & _M64), self.S, self.P,
-                     ctypes.c_uint64(self._wbase), _p(s._pow), _p(self._wstates), s._cs)
+            self._wbase, self._wc, self._cur = 2 * s0.sweeps_done, 0, 0
+            if s0.stream == "xoshiro":
+                for s, (states, _, _) in zip(self.slabs, self._wb):
+                    call("msb_window_init", ctypes.byref(s._g), ctypes.c_uint64(s.seed & _M64), self.S, self.P,
+                         ctypes.c_uint64(self._wbase), _p(s._pow), _p(states), s0._cs)
             self._launch(0, 0, True)
             self._valid = True
         while k > 0:
             r = min(k, self.S - self._wc)
             finish = self._wc + r == self.S
             self._launch(self._wc, r, finish)
-            self._halo.phase0 += 2 * r
-            s.sweeps_done += r
+            for s in self.slabs:
+                s.sweeps_done += r
             k -= r
             if finish:
                 self._cur, self._wc, self._wbase = 1 - self._cur, 0, self._wbase + 2 * self.S
@@ -428,19 +510,28 @@ class FusedSlabRun:
                 self._wc += r
 
     def observe_async(self):
-        """Device int64 [2*n_sim] (ups, unsat) of this slab, stream-ordered: a
-        device-side wait until both neighbours finished the phases so far (our
-        ghost rows are current), then msb_observe.  No host synchronisation;
-        callers with world > 1 all-reduce the result."""
-        s = self.slab
-        call("msb_window_sweep", ctypes.byref(s._g), ctypes.byref(s._params), self.S, self.P, None, None, None,
-             0, 0, None, None, ctypes.byref(self._halo), None, s._cs)
-        return s.observe()
+        """Device int64 [2*n_sim] (ups, unsat) of this process's slabs,
+        stream-ordered: a device-side wait until the neighbours finished the
+        phases so far (our ghost rows are current), then msb_observe.  No
+        host synchronisation; callers with world > 1 all-reduce the result."""
+        s0 = self.slab
+        total = None
+        for v, s in enumerate(self.slabs):
+            call("msb_window_sweep", ctypes.byref(s._g), ctypes.byref(s._params), self.S, self.P, None, None, None,
+                 0, 0, None, None, ctypes.byref(self._halos[v]), None, s0._cs)
+            with s0.stream_ctx():
+                s._obs.zero_()
+            call("msb_observe", ctypes.byref(s._g), _p(s._spins), _p(s._obs[: s.n_sim]), _p(s._obs[s.n_sim:]), s0._cs)
+            total = s._obs if total is None else total + s._obs
+        return total
 
     def observables(self):
-        """(ups, unsat) int64 per replica of this slab (host copies)."""
+        """(ups, unsat) int64 per replica of this process's slabs (host copies)."""
         o = self.observe_async()
         self.slab.synchronize()
         h = o.cpu().numpy()
         n = self.slab.n_sim
         return h[:n].copy(), h[n:].copy()
+
+    def synchronize(self) -> None:
+        self.slab.synchronize()

@@ -21,6 +21,16 @@ def cuda_available() -> bool:
         return False
 
 
+def reference_available() -> bool:
+    """The unmodified reference package (baseline/_ref, tools/install_reference.sh, or installed)."""
+    try:
+        from paper_2404_16990_b200.backend import import_reference
+        import_reference()
+        return True
+    except Exception:
+        return False
+
+
 @pytest.fixture(scope="session")
 def golden():
     import json

@@ -26,7 +26,7 @@ def test_exports_every_declared_symbol():
     missing = [name for name in sorted(declared) if not hasattr(L, name)]
     assert not missing, missing
     assert set(_lib.EXPORTS) <= declared
-    assert L.msb_abi_version() == 1
+    assert L.msb_abi_version() == 2
 
 
 def test_geometry_validation_messages():
@@ -188,8 +188,8 @@ def test_window_io_argument_errors():
         (g, 0, 9, WindowIO(ptr, None, None, None), None, "outside the window"),
         (g, 0, 8, None, Halo(), "msb_halo needs a slab geometry"),
         (geom(1, 64, 1024, row0=0, rows=16, ghost=1), 0, 8, WindowIO(ptr, None, None, None),
-         Halo(up_spins=ptr, down_spins=ptr, up_R=18, down_R=18, up_flags=ptr, down_flags=ptr, my_flags=ptr),
-         "needs a flip launch of a whole lattice"),
+         Halo(up_spins=ptr, down_spins=ptr, up_R=18, down_R=18, up_flags=ptr, down_flags=ptr),
+         "slab launches need msb_sweep_params.flags"),
     ]
     for gg, first, count, io, halo, text in cases:
         assert sweep(gg, first, count, io, halo) == -1, text
@@ -197,7 +197,7 @@ def test_window_io_argument_errors():
 
 
 def test_direct_sweep_host_checks():
-    """msb_direct_ok / msb_direct_flag_words / msb_direct_sweep argument
+    """msb_direct_ok / msb_flag_words / msb_direct_sweep argument
     handling (host logic only; no GPU needed): which shapes and tables take
     the direct path, and the errors raised before any device work."""
     from paper_2404_16990_b200._lib import (Halo, SweepParams, MSB_MODE_FERRO, MSB_MODE_GENERIC,
@@ -216,14 +216,20 @@ def test_direct_sweep_host_checks():
     assert ok(geom(2, 64, 1024), SweepParams(mode=MSB_MODE_FERRO, n_planes=2, rng=MSB_RNG_PHILOX, work=ptr)) == 0
     assert ok(geom(2, 64, 1024), SweepParams(mode=MSB_MODE_GENERIC, n_planes=3, rng=MSB_RNG_PHILOX_BITS,
                                              work=ptr)) == 0
-    # band-group flags: one per group of 16 rows at n = 1024 (8 bands of 2 rows); none for multi-segment rows
+    # flag buffer: header + 2 halo slots per (replica, row segment) + one flag per
+    # band group of the direct walk (2-row bands x 32/quads-per-row lanes)
     g = geom(64, 1024, 1024)
-    assert L.msb_direct_flag_words(ctypes.byref(g), ctypes.byref(p)) == 64 * 1024 // 16
-    assert L.msb_direct_flag_words(ctypes.byref(geom(1, 64, 14336)), ctypes.byref(p)) == 0
-    assert L.msb_direct_flag_words(ctypes.byref(geom(2, 64, 96)), ctypes.byref(p)) == -1
+    assert L.msb_flag_words(ctypes.byref(g)) == 1 + 2 * 64 + 64 * 1024 // 16
+    # n = 14336: 56 quads per row -> 7 segments of 8 quads, bands of 2 rows x 4 lanes
+    assert L.msb_flag_words(ctypes.byref(geom(1, 64, 14336))) == 1 + 2 * 7 + 64 // 8 * 7
+    # slab geometry: the held rows only
+    assert L.msb_flag_words(ctypes.byref(geom(2, 64, 1024, row0=16, rows=32, ghost=1))) == 1 + 2 * 2 + 2 * 32 // 16
+    # no band walk (12 rows do not split into 16-row groups): header + slots only
+    assert L.msb_flag_words(ctypes.byref(geom(2, 12, 1024))) == 1 + 2 * 2
+    assert L.msb_flag_words(ctypes.byref(geom(2, 10, 96))) == -1
 
     def sweep(gg, pp, n, spins=ptr, halo=None):
-        return L.msb_direct_sweep(ctypes.byref(gg), ctypes.byref(pp), spins, n, ptr, None, 0,
+        return L.msb_direct_sweep(ctypes.byref(gg), ctypes.byref(pp), spins, n, ptr,
                                   ctypes.byref(halo) if halo is not None else None, None, None)
 
     assert sweep(g, p, 0) == 0                      # nothing to do
@@ -233,7 +239,41 @@ def test_direct_sweep_host_checks():
         (g, p, -1, ptr, None, "sweep count"),
         (g, p, 2, None, None, "null buffer"),
         (g, p, 2, ptr, Halo(), "msb_halo needs a slab geometry"),
+        (geom(1, 64, 1024, row0=0, rows=32, ghost=1), p, 2, ptr,
+         Halo(up_spins=ptr, down_spins=ptr, up_R=34, down_R=34, up_flags=ptr, down_flags=ptr),
+         "need msb_sweep_params.flags"),
         (geom(2, 64, 96), p, 2, ptr, None, "direct sweeps need"),
     ]:
         assert sweep(gg, pp, n, spins, halo) < 0, text
         assert text in L.msb_last_error().decode(), (text, L.msb_last_error())
+
+
+def test_ring_host_checks():
+    """msb_window_sweep_ring / msb_direct_sweep_ring / msb_ring_ctx_bytes
+    argument handling on the host (no GPU)."""
+    from paper_2404_16990_b200._lib import (Halo, RingSlab, SweepParams, MSB_MODE_FERRO, MSB_RNG_PHILOX_BITS,
+                                             MSB_RNG_XOSHIRO)
+    L = _lib.lib()
+    assert L.msb_ring_ctx_bytes(0) == -1 and L.msb_ring_ctx_bytes(17) == -1
+    one = L.msb_ring_ctx_bytes(1)
+    assert one > 0 and L.msb_ring_ctx_bytes(8) == 8 * one
+    dummy = np.zeros(64, np.uint32)
+    ptr = dummy.ctypes.data
+    arr = (RingSlab * 2)()
+    assert L.msb_window_sweep_ring(0, arr, 8, 8, 0, 8, ptr, None) == -1
+    assert "ring of 1..MSB_RING_MAX" in L.msb_last_error().decode()
+    px = SweepParams(mode=MSB_MODE_FERRO, n_planes=2, thr9=ptr, kg=1, jump=ptr, work=ptr, rng=MSB_RNG_XOSHIRO,
+                     flags=ptr)
+    pb = SweepParams(mode=MSB_MODE_FERRO, n_planes=2, thr9=ptr, kg=1, jump=ptr, work=ptr, rng=MSB_RNG_PHILOX_BITS,
+                     flags=ptr)
+    g0, g1 = geom(1, 64, 1024, row0=0, rows=32, ghost=1), geom(1, 64, 1024, row0=32, rows=32, ghost=1)
+    h = Halo(up_spins=ptr, down_spins=ptr, up_R=34, down_R=34, up_flags=ptr, down_flags=ptr)
+    for v, (g, p) in enumerate(((g0, px), (g1, pb))):
+        arr[v].g, arr[v].p, arr[v].spins, arr[v].flips = ctypes.pointer(g), ctypes.pointer(p), ptr, ptr
+        arr[v].halo = ctypes.pointer(h)
+    assert L.msb_window_sweep_ring(2, arr, 8, 8, 0, 8, ptr, None) == -1
+    assert "share the stream kind" in L.msb_last_error().decode()
+    arr[1].p = ctypes.pointer(px)
+    assert L.msb_window_sweep_ring(2, arr, 8, 8, 0, 8, None, None) == -1
+    assert "null ring context" in L.msb_last_error().decode()
+    assert L.msb_direct_sweep_ring(2, arr, 2, None, None) == -1

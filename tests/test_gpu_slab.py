@@ -90,3 +90,66 @@ def test_fused_slab_matches_host_exchange_path():
         host.sweep(1)
         assert (a.lattice_rows() == b.lattice_rows()).all()
     assert a.flips == b.flips
+
+
+# ---- rings of slabs in ONE launch (msb_window_sweep_ring / msb_direct_sweep_ring) --
+
+@pytest.mark.parametrize("m,n,n_sim,V,stream,window", [
+    (64, 1024, 2, 2, "xoshiro", None),       # one band group per slab: both edges in one group
+    (64, 1024, 2, 2, "philox", 3),
+    (64, 1024, 2, 2, "philox-bits", None),   # direct: 2-row bands, 2 groups per replica
+    (64, 1024, 1, 4, "xoshiro", 3),
+    (256, 14336, 1, 2, "xoshiro", None),     # 7 row segments, 2 band groups per slab
+    (128, 14336, 1, 4, "philox-bits", 3),
+    (128, 32768, 1, 2, "xoshiro", 3),        # 4 segments x 4 band groups per slab
+    (128, 32768, 1, 2, "philox-bits", None),
+    (96, 512, 3, 3, "philox-bits", None),    # n = 512: 16-draw words
+    (96, 512, 3, 3, "xoshiro", None),
+    (60, 1024, 2, 3, "xoshiro", 2),          # 20-row slabs: no band walk, the GPU-wide gate
+    (132, 1024, 1, 4, "xoshiro", None),      # 32/34/32/34 rows: band-group slabs next to gate slabs
+    (132, 1024, 1, 4, "philox-bits", 3),     # (not all direct-capable: window path for every slab)
+])
+def test_fused_ring_vs_oracle(m, n, n_sim, V, stream, window):
+    """V slabs of one lattice on one GPU in one cooperative launch: each slab
+    pushes its edge rows into its neighbours' ghost rows and orders its
+    phases through the flags the neighbours write into its memory (the
+    multi-GPU halo protocol with distinct buffers), bit-exact against the
+    oracle through full and partial windows, and its observables."""
+    from oracle import oracle as orc
+    from paper_2404_16990_b200 import LatticeDims
+    from paper_2404_16990_b200.slab import FusedSlabRun, SlabLattice, slab_bounds
+    dims = LatticeDims(m, n)
+    temps = list(np.linspace(1.9, 2.8, n_sim))
+    slabs = [SlabLattice(dims, temps, 77, a, b - a, sim_offset=1, stream=stream) for a, b in slab_bounds(m, V)]
+    run = FusedSlabRun(slabs, window=window)
+    o = orc.OracleEngine(m, n, temps, 77, sim_offset=1, stream=stream)
+    for k in (1, run.S, 2, run.S + 1):
+        run.sweep(k)
+        o.sweep(k)
+        got = np.concatenate([s.lattice_rows() for s in slabs], axis=1)
+        assert (got == o.spins).all(), f"after {k} more sweeps"
+    assert sum(s.flips for s in slabs) == o.flips
+    ups, unsat = run.observables()
+    o_ups, o_bonds = o.observe()
+    assert ups.tolist() == o_ups.tolist()
+    assert (2 * m * n - 2 * unsat).tolist() == o_bonds.tolist()
+
+
+def test_fused_ring_equals_single_slab_and_engine():
+    """The same lattice as 1 slab, as a ring of 4 and as the whole-lattice
+    Engine: identical lattices and flip counts, sweep by sweep."""
+    from paper_2404_16990_b200 import Engine, LatticeDims
+    from paper_2404_16990_b200.slab import FusedSlabRun, SlabLattice, slab_bounds
+    dims = LatticeDims(128, 2048)
+    one = SlabLattice(dims, [2.3], 5, 0, 128)
+    ring = [SlabLattice(dims, [2.3], 5, a, b - a) for a, b in slab_bounds(128, 4)]
+    r1, r4 = FusedSlabRun(one, window=4), FusedSlabRun(ring, window=4)
+    eng = Engine(dims, [2.3], 5)
+    for k in (3, 4, 5):
+        r1.sweep(k)
+        r4.sweep(k)
+        eng._sweeps(k)
+        lat = eng.lattice(0)
+        assert (one.lattice_rows()[0] == lat).all()
+        assert (np.concatenate([s.lattice_rows()[0] for s in ring], axis=0) == lat).all()
+    assert one.flips == sum(s.flips for s in ring) == eng.flips
