@@ -306,7 +306,7 @@ class L2Flush:
 
     def __call__(self, stream):
         with self.torch.cuda.stream(stream):
-            self.torch.sum(self.buf, out=self.sink)
+            self.torch.sum(self.buf, dim=0, out=self.sink)
 
 
 def device_rate(torch, dist, ws, eng, S, K, attempts_step, flush):

@@ -32,6 +32,7 @@ from .engine import Engine, run_simulations
 __all__ = ["import_reference", "BackendEngine", "install", "gpu_backend"]
 
 _LOCAL_REF = Path(__file__).resolve().parents[1] / "baseline" / "_ref"
+_PRISTINE_ADD4 = [None]  # the reference's own multispin.engine.bitwise_add4, captured at install()
 
 
 def import_reference():
@@ -56,13 +57,11 @@ class BackendEngine(Engine):
     its own adder corruption (``Engine.fault``, the kernels' ``fault`` flag).
     """
 
-    _pristine_add4 = None
-
     @property
     def fault(self):
         mod = sys.modules.get("multispin.engine")
-        seam = mod is not None and self._pristine_add4 is not None and \
-            getattr(mod, "bitwise_add4", None) is not self._pristine_add4
+        pristine = _PRISTINE_ADD4[0]
+        seam = mod is not None and pristine is not None and getattr(mod, "bitwise_add4", None) is not pristine
         return int(bool(self._fault) or seam)
 
     @fault.setter
@@ -87,7 +86,7 @@ def install():
     originals = {"Engine": ref_engine.Engine, "run_simulations": ref_engine.run_simulations}
     if getattr(ref_engine.Engine, "__module__", "").startswith(__package__):
         return lambda: None  # already installed
-    BackendEngine._pristine_add4 = getattr(ref_engine, "bitwise_add4", None)
+    _PRISTINE_ADD4[0] = getattr(ref_engine, "bitwise_add4", None)
     swaps = {"Engine": BackendEngine, "run_simulations": run_simulations}
     done = []
     for mod in _multispin_modules():
