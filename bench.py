@@ -171,16 +171,18 @@ def cpu_rate(cfg, replicas: int, sweeps: int, threads: int):
     return replicas * cfg["m"] * cfg["n"] * sweeps / dt, dt
 
 
-def cpu_baseline(cfg, budget_s: float = 8.0):
+def cpu_baseline(cfg, budget_s: float = 12.0):
+    """The oracle (C restatement of the reference path, oracle/) on all host
+    threads over the config's replicas, sized to about budget_s of CPU work."""
     threads = os.cpu_count() or 1
-    r1, dt1 = cpu_rate(cfg, 1, 1, threads)  # calibration
-    per_sweep_replica = cfg["m"] * cfg["n"] / r1
-    replicas = int(max(1, min(cfg["n_sim"], budget_s / 2 / per_sweep_replica)))
-    sweeps = int(max(1, min(20, budget_s / (replicas * per_sweep_replica))))
-    rate, dt = cpu_rate(cfg, replicas, sweeps, threads)
+    reps = min(cfg["n_sim"], threads)
+    r0, _ = cpu_rate(cfg, reps, 1, threads)  # calibration: one sweep, every thread busy
+    full_sweep_s = cfg["n_sim"] * cfg["m"] * cfg["n"] / r0
+    sweeps = int(max(1, min(2000, budget_s / full_sweep_s)))
+    rate, dt = cpu_rate(cfg, cfg["n_sim"], sweeps, threads)
     return {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{sweeps} sweep(s) of {replicas} of the {cfg['n_sim']} replicas "
-                      f"({cfg['m']}x{cfg['n']}) on {threads} threads, {dt:.1f} s (oracle/msb_oracle.c)"}
+            "sample": f"{sweeps} sweep(s) of all {cfg['n_sim']} replicas ({cfg['m']}x{cfg['n']}) on {threads} "
+                      f"threads, {dt:.1f} s (oracle/msb_oracle.c, pinned to the reference's own outputs)"}
 
 
 def python_reference(cfg, budget_s: float = 6.0):
@@ -303,10 +305,14 @@ class L2Flush:
         self.buf = torch.ones(nbytes // 8, dtype=torch.int64, device=dev)
         self.sink = torch.empty((), dtype=torch.int64, device=dev)
         self.torch = torch
+        self.write = os.environ.get("MSB_BENCH_FLUSH") == "write"  # round-1 style, for comparison only
 
     def __call__(self, stream):
         with self.torch.cuda.stream(stream):
-            self.torch.sum(self.buf, dim=0, out=self.sink)
+            if self.write:
+                self.buf.zero_()
+            else:
+                self.torch.sum(self.buf, dim=0, out=self.sink)
 
 
 def device_rate(torch, dist, ws, eng, S, K, attempts_step, flush):
@@ -530,33 +536,40 @@ def run_ours(args, cfg):
 
 def run_slab(args, cfg):
     """cfg4 / cfg5: one lattice in row slabs, one per rank, halos exchanged
-    inside the window kernel (FusedSlabRun: NVLink peer stores + flag
-    handshake; symmetric memory maps the neighbours' buffers).  One step =
-    one window (cfg5: 10 sweeps, then |M| and E all-reduced)."""
+    inside the flip kernels (FusedSlabRun: the edge bands push their rows
+    into the neighbours' ghost rows -- NVLink peer stores, symmetric memory
+    -- and only they wait on the neighbour slab's flags; interior bands run
+    on).  ``--ring V`` (one GPU): the GPU's rows as a ring of V slabs in one
+    cooperative launch, the multi-GPU halo protocol with V distinct buffers.
+    One step = one window (cfg5: 10 sweeps, then |M| and E all-reduced)."""
     import torch
     import torch.distributed as dist
     from paper_2404_16990_b200 import LatticeDims
-    from paper_2404_16990_b200.slab import FusedSlabRun, SlabLattice, ring_plan, symmetric_alloc
+    from paper_2404_16990_b200.slab import FusedSlabRun, SlabLattice, ring_plan, slab_bounds, symmetric_alloc
 
     ws, rank, local = dist_info()
     if ws > 1:
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     m = cfg["m"] * (ws if cfg["slab"] == "weak" else 1)
     n = cfg["n"]
     plan = ring_plan(m, ws, rank)
     a, b = plan["row0"], plan["row0"] + plan["rows"]
-    slab = SlabLattice(LatticeDims(m, n), list(cfg["temps"](1)), cfg["seed"], a, b - a, init=cfg["init"],
-                       device=dev, kg=args.kg, stream=args.stream,
-                       alloc=symmetric_alloc() if ws > 1 else None)
+    dims = LatticeDims(m, n)
+    V = max(1, args.ring) if ws == 1 else 1
+    bounds = slab_bounds(m, V) if V > 1 else [(a, b)]
+    slabs = [SlabLattice(dims, list(cfg["temps"](1)), cfg["seed"], lo, hi - lo, init=cfg["init"], device=dev,
+                         kg=args.kg, stream=args.stream, alloc=symmetric_alloc() if ws > 1 else None)
+             for lo, hi in bounds]
     every = cfg.get("measure", 0)
-    run = FusedSlabRun(slab, window=every or None)
+    run = FusedSlabRun(slabs if V > 1 else slabs[0], window=every or None)
+    slab = slabs[0]
     S = run.S
     peak = int_peak_tops(slab._stream)
     run.sweep(args.warmup * S)
     torch.cuda.synchronize()
-    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    flush = L2Flush(torch, dev)
     K = args.steps
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
     obs = torch.zeros(2, dtype=torch.int64, device=dev)
@@ -566,8 +579,7 @@ def run_slab(args, cfg):
     sampler.start()
     time.sleep(0.02)
     for k in range(K):
-        with slab.stream_ctx():
-            flush.zero_()
+        flush(slab._stream)
         evs[k][0].record(slab._stream)
         run.sweep(S)
         if every:  # |M| and E of the whole lattice every `every` sweeps (device all-reduce)
@@ -580,33 +592,57 @@ def run_slab(args, cfg):
     torch.cuda.synchronize()
     sampler.stop()
     step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
-    total_ms = float(sum(step_ms))
-    if ws > 1:
-        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = max_over_ranks(torch, dist, ws, float(sum(step_ms)))
     attempts_step = m * n * S
     value = attempts_step * K / (total_ms * 1e-3)
+
+    # end to end through the public API: every step FusedSlabRun.sweep(S),
+    # then |M| and E of the whole lattice reduced on the device (all ranks)
+    # and read into pinned host memory (the step's result; the lattice itself
+    # is generated on the device from the seed and stays resident)
+    Ke = min(K, 100)
+    host = torch.empty(2, dtype=torch.int64, pin_memory=True)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for k in range(Ke):
+        run.sweep(S)
+        o = run.observe_async()
+        with slab.stream_ctx():
+            obs.copy_(o[:2])
+            if ws > 1:
+                dist.all_reduce(obs)
+            host.copy_(obs, non_blocking=True)
+        slab.synchronize()
+    e2e_s = max_over_ranks(torch, dist, ws, time.perf_counter() - t0)
     if rank == 0:
         a_int = A_INT[args.stream]
-        achieved = a_int * (b - a) * n * S / (statistics.mean(step_ms) * 1e-3) / 1e12
+        rows_here = sum(hi - lo for lo, hi in bounds)
+        achieved = a_int * rows_here * n * S / (statistics.mean(step_ms) * 1e-3) / 1e12
+        ring_desc = (f"; this GPU's rows as a ring of {V} slabs in one cooperative launch (msb_window_sweep_ring): "
+                     "the multi-GPU halo protocol with distinct buffers" if V > 1 else "")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": args.warmup,
             "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": cfg["slab"], "vs_baseline": None,
             "dtype": "u32", "data": "synthetic (random +/-1 initial spins from the reference init stream)",
-            "config": {"workload": cfg["desc"], "m": m, "n": n, "rows_per_gpu": b - a,
-                       "parallelism": f"row slabs over {ws} GPU(s); halo rows pushed into the neighbours' ghost rows "
-                                      "inside the window kernel (peer memory), flag handshake per phase",
-                       "l2": f"flushed between timed steps ({L2_FLUSH_BYTES >> 20} MiB write, outside the events)",
+            "config": {"workload": cfg["desc"], "m": m, "n": n, "rows_per_gpu": b - a, "slabs_per_gpu": V,
+                       "parallelism": f"row slabs over {ws} GPU(s); edge rows pushed into the neighbours' ghost rows "
+                                      "inside the flip kernel (peer memory); only the edge band groups wait on the "
+                                      "neighbour slab's flags, interior bands overlap" + ring_desc,
+                       "l2": f"flushed between timed steps (read pass over {L2_FLUSH_BYTES >> 20} MiB, outside the "
+                             "events)",
                        "stream": args.stream, "sweeps_per_step": S, "window_parts": run.P,
                        "step": f"one lookahead window of {S} sweeps" + (" + device all-reduce of |M|, E" if every
                                                                        else "")},
             "roofline": {"bound": "int32", "achieved": achieved, "peak": peak, "unit": "Tops/s",
                          "frac": achieved / peak, "traffic": None, "kernel": "k_win (slab, in-kernel halo exchange)"},
-            "e2e": None,
-            "e2e_note": "none for the slab configurations: the lattice is generated on the device from the seed "
-                        "(init='random') and stays resident; a step's only host traffic is the observables. The "
-                        "end-to-end leg (host lattices in and out every step) is the cfg2 line's.",
+            "e2e": {"value": attempts_step * Ke / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 16, "steps": Ke,
+                    "path": "FusedSlabRun.sweep(S) + observe_async (|M|, E reduced on the device"
+                            + (", NCCL all-reduce" if ws > 1 else "") + ") + copy into pinned host memory + host "
+                            "sync, every step; the lattice is generated on the device from the seed and stays "
+                            "resident, so a step has no host->device input"},
             "gpu_launches": K * (1 + (1 if every else 0)), "clocks": sampler.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -642,6 +678,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2")
     ap.add_argument("--kg", type=int, default=None)
+    ap.add_argument("--ring", type=int, default=1,
+                    help="cfg4/cfg5 on one GPU: split the rows into a ring of this many slabs, one launch")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-alt", action="store_true", help="skip the philox-bits comparison leg (other_streams)")
     ap.add_argument("--stream", choices=sorted(A_INT), default="xoshiro",

@@ -279,11 +279,18 @@ __device__ __forceinline__ uint4 (*direct_key_tables())[12] {
   return kmt;
 }
 
+// Per-group hooks of a band run: pre(g) before group g's flips, post(g)
+// after them (phase ordering by band-group flags; NoHooks: none).
+struct NoHooks {
+  __device__ __forceinline__ void pre(unsigned) const {}
+  __device__ __forceinline__ void post(unsigned) const {}
+};
+
 // PF: prefetch the plane rows of the run's groups one group ahead (callers
 // that walk one group at a time prefetch themselves, band_prefetch).
-template <bool COHERENT, bool PUSH = false, bool SEG = false, int DIRECT = 0, bool PF = true>
+template <bool COHERENT, bool PUSH = false, bool SEG = false, int DIRECT = 0, bool PF = true, class HK = NoHooks>
 __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0, unsigned g1, int X,
-                                                  const PbitsDirect* dp = nullptr) {
+                                                  const PbitsDirect* dp = nullptr, const HK& hk = HK{}) {
   const Geo& G = a.G;
   const int lane = threadIdx.x & 31;
   const int sq = a.band_sq, nseg = SEG ? a.band_nseg : 1;  // quads per segment, segments per row (SEG: > 1)
@@ -321,6 +328,7 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
   if (PF && !DIRECT && !SEG && q == 0 && g0 < g1) prefetch_band(g0);
   for (unsigned g = g0; g < g1; g++) {
     if (PF && !DIRECT && !SEG && q == 0 && g + 1 < g1) prefetch_band(g + 1);
+    hk.pre(g);
     const unsigned gr = SEG ? g / (unsigned)nseg : g;
     const int seg = (int)(g - gr * (unsigned)nseg);
     const unsigned s = gr / groups_per_sim;
@@ -505,6 +513,7 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
         step(P1(), h + 1);
       }
     }
+    hk.post(g);
   }
   return cnt;
 }

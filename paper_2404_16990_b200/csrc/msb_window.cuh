@@ -109,46 +109,152 @@ struct GroupOrder {
   unsigned gps, nseg;
 };
 
-// local = false (the first phase of a launch): the neighbours on this GPU
-// finished the previous launch (stream order), only the slots count.
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_relaxed_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(unsigned* p, unsigned v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys(unsigned* p, unsigned v) {
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Neighbours of band group g in the group order, and which of them another
+// warp (or another slab: sys) owns.  [lo, hi) is the calling warp's range:
+// a neighbour inside it was handled by this warp earlier in program order,
+// so it needs neither a wait nor a published flag.
+struct GroupNb {
+  const unsigned *pu, *pd, *pl, *pr;
+  bool ext_u, ext_d, ext_h, sys_u, sys_d;
+  unsigned slot, l;
+};
+
 template <bool HALO>
-__device__ __forceinline__ void gf_wait(const GroupOrder& f, unsigned g, unsigned need, bool local) {
+__device__ __forceinline__ GroupNb group_nb(const GroupOrder& f, unsigned g, unsigned lo, unsigned hi) {
+  GroupNb n;
+  const unsigned gr = g / f.nseg, seg = g - gr * f.nseg, s = gr / f.gps, l = gr - s * f.gps;
+  n.l = l;
+  n.slot = s * f.nseg + seg;
+  n.sys_u = HALO && l == 0;
+  n.sys_d = HALO && l + 1 == f.gps;
+  const unsigned gu = l == 0 ? g + (f.gps - 1) * f.nseg : g - f.nseg;
+  const unsigned gd = l + 1 == f.gps ? g - (f.gps - 1) * f.nseg : g + f.nseg;
+  const unsigned gl = seg == 0 ? g + f.nseg - 1 : g - 1;
+  const unsigned gr2 = seg + 1 == f.nseg ? g + 1 - f.nseg : g + 1;
+  n.pu = n.sys_u ? f.above + n.slot : f.grp + gu;
+  n.pd = n.sys_d ? f.below + n.slot : f.grp + gd;
+  n.pl = f.grp + gl;
+  n.pr = f.grp + gr2;
+  auto out = [&](unsigned x) { return x < lo || x >= hi; };
+  n.ext_u = n.sys_u || out(gu);
+  n.ext_d = n.sys_d || out(gd);
+  n.ext_h = f.nseg > 1 && (out(gl) || out(gr2));
+  return n;
+}
+
+// Wait until group g's neighbours owned elsewhere completed phase need-1
+// (acquire polls: one L2 round trip when the neighbour is already done, the
+// common case; a relaxed poll followed by acquires measured two).  local =
+// false (the first phase of a launch): the neighbours on this GPU finished
+// the previous launch (stream order), only the slots written by the
+// neighbour slabs count.
+template <bool HALO>
+__device__ __forceinline__ void gf_wait(const GroupOrder& f, unsigned g, unsigned need, bool local, unsigned lo,
+                                        unsigned hi) {
   if ((threadIdx.x & 31) == 0) {
-    const unsigned gr = g / f.nseg, seg = g - gr * f.nseg, s = gr / f.gps, l = gr - s * f.gps;
-    const unsigned slot = s * f.nseg + seg;
-    const bool sys_u = HALO && l == 0, sys_d = HALO && l + 1 == f.gps;
-    const unsigned* pu = sys_u ? f.above + slot : f.grp + (l == 0 ? g + (f.gps - 1) * f.nseg : g - f.nseg);
-    const unsigned* pd = sys_d ? f.below + slot : f.grp + (l + 1 == f.gps ? g - (f.gps - 1) * f.nseg : g + f.nseg);
-    const unsigned* pl = f.grp + (seg == 0 ? g + f.nseg - 1 : g - 1);
-    const unsigned* pr = f.grp + (seg + 1 == f.nseg ? g + 1 - f.nseg : g + 1);
-    bool ok_u = !sys_u && !local, ok_d = !sys_d && !local, ok_h = f.nseg == 1 || !local;
+    const GroupNb n = group_nb<HALO>(f, g, lo, hi);
+    bool ok_u = !(n.ext_u && (local || n.sys_u)), ok_d = !(n.ext_d && (local || n.sys_d)), ok_h = !(n.ext_h && local);
     while (!(ok_u && ok_d && ok_h)) {
-      if (!ok_u) ok_u = (sys_u ? ld_acquire_sys(pu) : ld_acquire(pu)) >= need;
-      if (!ok_d) ok_d = (sys_d ? ld_acquire_sys(pd) : ld_acquire(pd)) >= need;
-      if (!ok_h) ok_h = ld_acquire(pl) >= need && ld_acquire(pr) >= need;
+      if (!ok_u) ok_u = (n.sys_u ? ld_acquire_sys(n.pu) : ld_acquire(n.pu)) >= need;
+      if (!ok_d) ok_d = (n.sys_d ? ld_acquire_sys(n.pd) : ld_acquire(n.pd)) >= need;
+      if (!ok_h) ok_h = ld_acquire(n.pl) >= need && ld_acquire(n.pr) >= need;
       if (!(ok_u && ok_d && ok_h)) __nanosleep(32);
     }
   }
   __syncwarp();
 }
 
+// Publish group g's completion of a phase (value v) to whoever waits on it:
+// neighbours owned by other warps (a release: one acq_rel fence, then a
+// relaxed store), and for a slab's edge bands the neighbour slab (system
+// scope: our halo pushes into its ghost rows are ordered before).  A group
+// whose neighbours are all in this warp's range publishes nothing.
 template <bool HALO>
-__device__ __forceinline__ void gf_done(const GroupOrder& f, unsigned g, unsigned v) {
+__device__ __forceinline__ void gf_done(const GroupOrder& f, unsigned g, unsigned v, unsigned lo, unsigned hi) {
   __syncwarp();
   if ((threadIdx.x & 31) == 0) {
-    bool edge = false;
-    if (HALO) {
-      const unsigned gr = g / f.nseg, seg = g - gr * f.nseg, s = gr / f.gps, l = gr - s * f.gps;
-      const unsigned slot = s * f.nseg + seg;
-      edge = l == 0 || l + 1 == f.gps;
-      if (edge) {
-        __threadfence_system();  // our halo pushes (peer stores) before the neighbour hears of them
-        if (l == 0) atomicExch_system(f.up_below + slot, v);
-        if (l + 1 == f.gps) atomicExch_system(f.down_above + slot, v);
+    const GroupNb n = group_nb<HALO>(f, g, lo, hi);
+    const bool edge = n.sys_u || n.sys_d;
+    if (edge) {
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      if (n.sys_u) st_relaxed_sys(f.up_below + n.slot, v);
+      if (n.sys_d) st_relaxed_sys(f.down_above + n.slot, v);
+      st_relaxed(f.grp + g, v);
+    } else if (n.ext_u || n.ext_d || n.ext_h) {
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      st_relaxed(f.grp + g, v);
+    }
+  }
+}
+
+// flip_band_run hook of the group order: wait before a group (when `wait`:
+// later phases, or the first phase of a slab's edge bands).  Completion is
+// published per CTA after the phase (gf_publish_cta).
+// PER_GROUP: publish each group right after it (gf_done) -- the direct
+// walk, whose 32 warps per SM diverge too much to meet at a CTA barrier every
+// phase (1.73 -> 1.27 T at cfg4 with gf_publish_cta); the window consumers
+// publish per CTA instead.
+template <bool HALO, bool PER_GROUP>
+struct GfHooks {
+  const GroupOrder* f;
+  unsigned need, lo, hi;
+  bool local, wait;
+  __device__ __forceinline__ void pre(unsigned g) const {
+    if (wait) gf_wait<HALO>(*f, g, need, local, lo, hi);
+  }
+  __device__ __forceinline__ void post(unsigned g) const {
+    if (PER_GROUP) gf_done<HALO>(*f, g, need + 1u, lo, hi);
+  }
+};
+
+// End of a phase of the group order, per CTA: the flip warps meet at a named
+// barrier, then the CTA's leader issues ONE fence (system scope if one of the
+// CTA's groups holds a slab edge row: its pushes into the neighbour's ghost
+// rows) and publishes value v for every group of the CTA's warps that a
+// warp elsewhere or a neighbour slab waits on.  A fence per group cost
+// ~3% at cfg4 (the fence drains the warp's outstanding stores each time).
+template <bool HALO>
+__device__ __forceinline__ void gf_publish_cta(const GroupOrder& f, unsigned v, unsigned per, unsigned total, int nwc,
+                                               unsigned vgrid, unsigned vb, bool leader) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nwc * 32) : "memory");
+  if (!leader) return;
+  bool sys = false;
+  if (HALO) {
+    for (int j = 0; j < nwc && !sys; j++) {
+      const unsigned lo = min(total, ((unsigned)j * vgrid + vb) * per), hi = min(total, lo + per);
+      for (unsigned g = lo; g < hi && !sys; g++) {
+        const unsigned l = (g / f.nseg) % f.gps;
+        sys = l == 0 || l + 1 == f.gps;
       }
     }
-    if (!edge) __threadfence();
-    atomicExch(f.grp + g, v);
+  }
+  if (sys) asm volatile("fence.acq_rel.sys;" ::: "memory");
+  else asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  for (int j = 0; j < nwc; j++) {
+    const unsigned lo = min(total, ((unsigned)j * vgrid + vb) * per), hi = min(total, lo + per);
+    for (unsigned g = lo; g < hi; g++) {
+      const GroupNb n = group_nb<HALO>(f, g, lo, hi);
+      if (n.sys_u) st_relaxed_sys(f.up_below + n.slot, v);
+      if (n.sys_d) st_relaxed_sys(f.down_above + n.slot, v);
+      if (n.ext_u || n.ext_d || n.ext_h) st_relaxed(f.grp + g, v);
+    }
   }
 }
 
@@ -668,14 +774,11 @@ __device__ __forceinline__ void win_body(const WinArgs& wa, const FlipArgs& fa0,
           dp.blk = wa.block0 + 2ull * (unsigned)(first + (i >> 1)) + (unsigned)X;
         } else {
           fa.planes = cur + (size_t)(first + (i >> 1)) * wa.slot_words;
-          if (!GSEG && lo < hi) band_prefetch(fa, lo, X);
         }
-        for (unsigned g = lo; g < hi; g++) {
-          if (!DIRECT && !GSEG && g + 1 < hi) band_prefetch(fa, g + 1, X);  // the next group's plane rows
-          if (HALO || i > 0) gf_wait<HALO>(go, g, fbase + (unsigned)i, i > 0);
-          cnt += flip_band_run<true, HALO, GSEG, DIRECT, false>(fa, g, g + 1, X, &dp);
-          gf_done<HALO>(go, g, fbase + (unsigned)i + 1u);
-        }
+        constexpr bool PG = DIRECT != 0;
+        const GfHooks<HALO, PG> hk{&go, fbase + (unsigned)i, lo, hi, i > 0, HALO || i > 0};
+        cnt += flip_band_run<true, HALO, GSEG, DIRECT, true, GfHooks<HALO, PG>>(fa, lo, hi, X, &dp, hk);
+        if (!PG) gf_publish_cta<HALO>(go, fbase + (unsigned)i + 1u, per, total, nwc, vgrid, vb, leader);
       }
     } else
     for (int i = 0; i < 2 * count; i++) {
@@ -973,6 +1076,23 @@ int producer_warps(long long units, int ctas, int Wp, int P, bool produce, int c
   return pwarps;
 }
 
+// Band height of a slab's window flips: the default (tallest) band, or
+// MSB_BAND_H (tuning).  Measured at cfg4 (one slab, and a ring of 8 slabs of
+// 1792 rows on 18 SMs each, where 16-row bands leave a third of the flip
+// warps without a group): 16 rows 0.941 / 0.850 T, 8: 0.938 / 0.845, 4:
+// 0.918 / 0.833, 2: 0.853 / 0.786 -- a band's setup and its group waits
+// cost more than the idle flip warps.  The flag buffer is sized for 2-row
+// bands (msb_flag_words).
+void fit_band_h(FlipArgs& fa, const msb_geom* g) {
+  if (fa.band_h <= 0) return;
+  const int gb = fa.band_gb;
+  static const int env_h = [] { const char* e = getenv("MSB_BAND_H"); return e ? atoi(e) : 0; }();
+  if (env_h >= 2 && env_h <= fa.band_h && !(env_h & (env_h - 1)) && g->rows % (gb * env_h) == 0) {
+    fa.band_h = env_h;
+    fa.band_groups = (unsigned)((long long)g->n_sim * g->rows / (gb * env_h) * fa.band_nseg);
+  }
+}
+
 // compile-time chunk width: every chunk 32 draws (n/32 % 32 == 0), a single
 // 16-draw chunk (n = 512), or generic
 int chunk_width(const Geo& G) { return (G.words % 32) == 0 ? 32 : (G.words == 16 ? 16 : 0); }
@@ -1052,6 +1172,7 @@ int window_run(int nslabs, const msb_ring_slab* slabs, bool ring, int S, int P, 
       return e;
     if (int e = sm_count(&sms)) return e;
     const int pwarps = producer_warps((np + 31) / 32, sms, fa.G.Wp, P, r.next != nullptr, count);
+    if (ha.on) fit_band_h(fa, r.g);
     const int cb = chunk_width(wa.G);
     const bool pj = SRC == kSrcXoshiro && pwarps > 0;
     cudaLaunchAttribute attr[1];
@@ -1087,6 +1208,7 @@ int window_run(int nslabs, const msb_ring_slab* slabs, bool ring, int S, int P, 
   const int vg = sms / nslabs;
   if (vg < 1) return fail(MSB_ERR_UNSUPPORTED, "more slabs than SMs");
   const int pwarps = producer_warps(units, vg, host[0].fa.G.Wp, P, next_all, count);
+  for (int v = 0; v < nslabs; v++) fit_band_h(host[v].fa, slabs[v].g);
   CUDA_TRY(cudaMemcpyAsync(ctx, host, sizeof(SlabCtx) * nslabs, cudaMemcpyHostToDevice, as_stream(stream)));
   const bool pj = SRC == kSrcXoshiro && pwarps > 0;
   cudaLaunchAttribute attr[1];
