@@ -136,10 +136,11 @@ struct GroupNb {
   unsigned slot, l;
 };
 
+// (s, l, seg) = replica, band, segment of group g (g = (s gps + l) nseg + seg).
 template <bool HALO>
-__device__ __forceinline__ GroupNb group_nb(const GroupOrder& f, unsigned g, unsigned lo, unsigned hi) {
+__device__ __forceinline__ GroupNb group_nb_at(const GroupOrder& f, unsigned g, unsigned s, unsigned l, unsigned seg,
+                                               unsigned lo, unsigned hi) {
   GroupNb n;
-  const unsigned gr = g / f.nseg, seg = g - gr * f.nseg, s = gr / f.gps, l = gr - s * f.gps;
   n.l = l;
   n.slot = s * f.nseg + seg;
   n.sys_u = HALO && l == 0;
@@ -159,23 +160,31 @@ __device__ __forceinline__ GroupNb group_nb(const GroupOrder& f, unsigned g, uns
   return n;
 }
 
-// Wait until group g's neighbours owned elsewhere completed phase need-1
-// (acquire polls: one L2 round trip when the neighbour is already done, the
-// common case; a relaxed poll followed by acquires measured two).  local =
-// false (the first phase of a launch): the neighbours on this GPU finished
-// the previous launch (stream order), only the slots written by the
-// neighbour slabs count.
 template <bool HALO>
-__device__ __forceinline__ void gf_wait(const GroupOrder& f, unsigned g, unsigned need, bool local, unsigned lo,
-                                        unsigned hi) {
+__device__ __forceinline__ GroupNb group_nb(const GroupOrder& f, unsigned g, unsigned lo, unsigned hi) {
+  const unsigned gr = g / f.nseg, seg = g - gr * f.nseg, s = gr / f.gps, l = gr - s * f.gps;
+  return group_nb_at<HALO>(f, g, s, l, seg, lo, hi);
+}
+
+// Wait until the neighbours of a group that are owned elsewhere completed
+// phase need-1 (acquire polls: one L2 round trip when the neighbour is
+// already done, the common case; a relaxed poll followed by acquires
+// measured two; backing off so spinning warps leave the issue slots to the
+// working ones).  local = false (the first phase of a launch): the
+// neighbours on this GPU finished the previous launch (stream order), only
+// the slots written by the neighbour slabs count.
+__device__ __forceinline__ void gf_wait_nb(const GroupNb& n, unsigned need, bool local) {
   if ((threadIdx.x & 31) == 0) {
-    const GroupNb n = group_nb<HALO>(f, g, lo, hi);
     bool ok_u = !(n.ext_u && (local || n.sys_u)), ok_d = !(n.ext_d && (local || n.sys_d)), ok_h = !(n.ext_h && local);
+    unsigned ns = 32;
     while (!(ok_u && ok_d && ok_h)) {
       if (!ok_u) ok_u = (n.sys_u ? ld_acquire_sys(n.pu) : ld_acquire(n.pu)) >= need;
       if (!ok_d) ok_d = (n.sys_d ? ld_acquire_sys(n.pd) : ld_acquire(n.pd)) >= need;
       if (!ok_h) ok_h = ld_acquire(n.pl) >= need && ld_acquire(n.pr) >= need;
-      if (!(ok_u && ok_d && ok_h)) __nanosleep(32);
+      if (!(ok_u && ok_d && ok_h)) {
+        __nanosleep(ns);
+        ns = min(ns * 2, 512u);
+      }
     }
   }
   __syncwarp();
@@ -186,13 +195,10 @@ __device__ __forceinline__ void gf_wait(const GroupOrder& f, unsigned g, unsigne
 // relaxed store), and for a slab's edge bands the neighbour slab (system
 // scope: our halo pushes into its ghost rows are ordered before).  A group
 // whose neighbours are all in this warp's range publishes nothing.
-template <bool HALO>
-__device__ __forceinline__ void gf_done(const GroupOrder& f, unsigned g, unsigned v, unsigned lo, unsigned hi) {
+__device__ __forceinline__ void gf_done_nb(const GroupOrder& f, const GroupNb& n, unsigned g, unsigned v) {
   __syncwarp();
   if ((threadIdx.x & 31) == 0) {
-    const GroupNb n = group_nb<HALO>(f, g, lo, hi);
-    const bool edge = n.sys_u || n.sys_d;
-    if (edge) {
+    if (n.sys_u || n.sys_d) {
       asm volatile("fence.acq_rel.sys;" ::: "memory");
       if (n.sys_u) st_relaxed_sys(f.up_below + n.slot, v);
       if (n.sys_d) st_relaxed_sys(f.down_above + n.slot, v);
@@ -216,11 +222,29 @@ struct GfHooks {
   const GroupOrder* f;
   unsigned need, lo, hi;
   bool local, wait;
+  // cursor of the walk (groups come in order lo, lo+1, ...): no divisions per group
+  mutable unsigned g_next = ~0u, cs = 0, cl = 0, cseg = 0;
+  mutable GroupNb nb;
   __device__ __forceinline__ void pre(unsigned g) const {
-    if (wait) gf_wait<HALO>(*f, g, need, local, lo, hi);
+    if (g != g_next) {
+      const unsigned gr = g / f->nseg;
+      cseg = g - gr * f->nseg;
+      cs = gr / f->gps;
+      cl = gr - cs * f->gps;
+    }
+    nb = group_nb_at<HALO>(*f, g, cs, cl, cseg, lo, hi);
+    if (wait) gf_wait_nb(nb, need, local);
   }
   __device__ __forceinline__ void post(unsigned g) const {
-    if (PER_GROUP) gf_done<HALO>(*f, g, need + 1u, lo, hi);
+    if (PER_GROUP) gf_done_nb(*f, nb, g, need + 1u);
+    g_next = g + 1;
+    if (++cseg == f->nseg) {
+      cseg = 0;
+      if (++cl == f->gps) {
+        cl = 0;
+        cs++;
+      }
+    }
   }
 };
 

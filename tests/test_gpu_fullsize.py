@@ -54,14 +54,37 @@ def test_cfg2_full_size():
     _observables_match(*win._observe(), o, dims.sites)
 
 
+def test_cfg2_1000_sweeps_trajectory():
+    """cfg2 exactly as BASELINE states it: 64 x 1024^2, 1000 sweeps through
+    the public Engine.run(1000, measure_interval=100) -- 125 full windows in
+    steady state, including every inter-window jump -- against the oracle
+    (16-thread C): final lattices, flips, and |M| and E/N of every replica at
+    every measurement, as float64 bit patterns."""
+    from oracle import oracle as orc
+    from paper_2404_16990_b200 import Engine, LatticeDims
+    temps = list(np.linspace(1.5, 3.5, 64))
+    e = Engine(LatticeDims(1024, 1024), temps, 2024)
+    traj = e.run(1000, measure_interval=100)
+    o = orc.OracleEngine(1024, 1024, temps, 2024)
+    sw, am, en = o.run(1000, 100)
+    assert traj.sweeps.tolist() == list(sw) == list(range(100, 1001, 100))
+    assert np.array_equal(traj.abs_m.view(np.uint64), np.asarray(am).view(np.uint64))
+    assert np.array_equal(traj.energy.view(np.uint64), np.asarray(en).view(np.uint64))
+    assert e.flips == o.flips
+    assert e.attempts == 64 * 1024 * 1024 * 1000
+    _same_rows(e.lattices, o.spins)
+
+
 def test_cfg3_full_size():
+    """754 x 512^2 through S + 1 sweeps: a full window, the jump of every
+    stream piece to the next window, and the first sweep of that window."""
     from oracle import oracle as orc
     from paper_2404_16990_b200 import Engine, LatticeDims
     temps = list(np.random.default_rng(2024).uniform(2.0, 2.6, 754))
     e = Engine(LatticeDims(512, 512), temps, 2024, init="all-up")
     o = orc.OracleEngine(512, 512, temps, 2024, init="all-up")
-    e._sweeps(2)
-    o.sweep(2)
+    e._sweeps(e.window + 1)
+    o.sweep(e.window + 1)
     assert e.flips == o.flips
     _same_rows(e.lattices, o.spins)
     _observables_match(*e._observe(), o, 512 * 512)
@@ -72,16 +95,17 @@ def test_cfg4_full_size_engine_and_slab_ring():
     from paper_2404_16990_b200 import Engine, LatticeDims
     from paper_2404_16990_b200.slab import FusedSlabRun, SlabLattice
     dims = LatticeDims(14336, 14336)
-    o = orc.OracleEngine(14336, 14336, [2.269], 2024)
-    o.sweep(2)
     e = Engine(dims, [2.269], 2024)
-    e._sweeps(2)
+    S = e.window
+    o = orc.OracleEngine(14336, 14336, [2.269], 2024)
+    o.sweep(S + 1)
+    e._sweeps(S + 1)
     assert e.flips == o.flips
     _same_rows(lambda: e.lattice(0), o.spins[0])
     del e
     slab = SlabLattice(dims, [2.269], 2024, 0, 14336)
     run = FusedSlabRun(slab)
-    run.sweep(2)
+    run.sweep(S + 1)
     assert slab.flips == o.flips
     _same_rows(lambda: slab.lattice_rows()[0], o.spins[0])
     _observables_match(*run.observables(), o, dims.sites)
@@ -94,9 +118,9 @@ def test_cfg5_full_size_slab_ring():
     dims = LatticeDims(32768, 32768)
     slab = SlabLattice(dims, [2.0], 2024, 0, 32768)
     run = FusedSlabRun(slab)
-    run.sweep(1)
+    run.sweep(run.S + 1)
     o = orc.OracleEngine(32768, 32768, [2.0], 2024)
-    o.sweep(1)
+    o.sweep(run.S + 1)
     assert slab.flips == o.flips
     _same_rows(lambda: slab.lattice_rows()[0], o.spins[0])
     _observables_match(*run.observables(), o, dims.sites)
@@ -149,4 +173,28 @@ def test_philox_bits_full_size_cfg3_cfg4():
     run.sweep(3)
     assert slab.flips == o.flips
     _same_rows(lambda: slab.lattice_rows()[0], o.spins[0])
+    _observables_match(*run.observables(), o, dims.sites)
+
+
+@pytest.mark.parametrize("stream", ["xoshiro", "philox-bits"])
+def test_cfg4_full_size_as_8_slabs(stream):
+    """cfg4 in exactly the 8-GPU partition (8 slabs of 1792 rows), all eight
+    in one cooperative launch on this GPU (msb_window_sweep_ring): each slab
+    pushes its edge rows into its neighbours' ghost rows and its edge bands
+    wait on the neighbour slab's flags, the protocol the 8 GPUs run over
+    NVLink.  S + 1 sweeps against the oracle, lattice, flips, observables."""
+    from oracle import oracle as orc
+    from paper_2404_16990_b200 import LatticeDims
+    from paper_2404_16990_b200.slab import FusedSlabRun, SlabLattice, ring_plan
+    dims = LatticeDims(14336, 14336)
+    slabs = []
+    for r in range(8):
+        p = ring_plan(14336, 8, r)
+        slabs.append(SlabLattice(dims, [2.269], 2024, p["row0"], p["rows"], stream=stream))
+    run = FusedSlabRun(slabs)
+    run.sweep(run.S + 1)
+    o = orc.OracleEngine(14336, 14336, [2.269], 2024, stream=stream)
+    o.sweep(run.S + 1)
+    assert sum(s.flips for s in slabs) == o.flips
+    _same_rows(lambda: np.concatenate([s.lattice_rows()[0] for s in slabs], axis=0), o.spins[0])
     _observables_match(*run.observables(), o, dims.sites)
