@@ -8,6 +8,8 @@ int window_run_xoshiro(int nslabs, const msb_ring_slab* slabs, bool ring, int S,
 }
 }  // namespace msbk
 
+using namespace msbk;
+
 extern "C" {
 #ifdef MSB_TRACE
 int msb_debug_trace_win(uint64_t* host_out, int32_t n) {

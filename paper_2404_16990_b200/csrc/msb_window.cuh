@@ -432,6 +432,13 @@ __device__ __forceinline__ WinPiece win_piece(const WinArgs& a, unsigned gi) {
   return w;
 }
 
+// Where a window piece jumps its stream to the next window: after its draws
+// (1) or spread through the draw loop (0, 8 nibble-table words at a time).
+#ifndef MSB_JUMP_END
+#define MSB_JUMP_END 0
+#endif
+constexpr bool kJumpEnd = MSB_JUMP_END;
+
 // One producer warp's share of a window (pieces numbered as win_piece).
 template <int SRC, int CB>
 __device__ __forceinline__ void win_produce(const WinArgs& a, const uint4* __restrict__ jt, int role_warp,
@@ -458,8 +465,10 @@ __device__ __forceinline__ void win_produce(const WinArgs& a, const uint4* __res
       int nib = 0, jacc = 0;
       if (XO) {
         load_state(st, a.states, a.npieces, gi);
-        jw[0] = st.a0; jw[1] = st.a1; jw[2] = st.b0; jw[3] = st.b1;
-        jw[4] = st.c0; jw[5] = st.c1; jw[6] = st.d0; jw[7] = st.d1;
+        if (!kJumpEnd) {
+          jw[0] = st.a0; jw[1] = st.a1; jw[2] = st.b0; jw[3] = st.b1;
+          jw[4] = st.c0; jw[5] = st.c1; jw[6] = st.d0; jw[7] = st.d1;
+        }
       } else {  // Philox: the stream id rides in st.a0 / st.a1
         const unsigned long long sid =
             ((unsigned long long)G.sim_offset + (unsigned long long)w.s) * cells + w.gamma - 1;
@@ -472,6 +481,36 @@ __device__ __forceinline__ void win_produce(const WinArgs& a, const uint4* __res
         const int lr = w.lr >= 0 ? w.lr : seg_row(G.m, w.gamma, X, q);
         uint32_t* out = slot + plane_off(G, 2, X, 0, w.s, lr);
         const unsigned long long pseg = (a.block0 + 2ull * w.j + X) * 2 * n + (unsigned long long)q * (n / 2);
+        if (XO && CB == 16 && !(a.kr & 1)) {
+          // n = 512: the 16 draws of k (even) and the 16 of k + 1 are one
+          // run of 32 consecutive draws of the stream: one 32-draw loop (as
+          // for 32-draw rows) fills both plane words, halving the per-k
+          // stores, addressing and jump bookkeeping
+          for (int kk = 0; kk < a.kr; kk += 2) {
+            const int k = w.k0 + kk;
+            uint32_t acc0 = 0, acc1 = 0;
+#pragma unroll kChunkUnroll
+            for (int i = 0; i < 32; i++) {
+              const uint32_t h9 = xstep(st) << 9;
+              acc_reject(acc0, h9, key0);
+              acc_reject(acc1, h9, key1);
+            }
+            // REJECT bits, newest draw in bit 0: reversed, bit i = draw i
+            const uint32_t a0 = ~__brev(acc0), a1 = ~__brev(acc1);
+            out[t_of_k(k)] = a0 & 0xFFFFu;
+            out[pstride + t_of_k(k)] = a1 & 0xFFFFu;
+            out[t_of_k(k + 1)] = a0 >> 16;
+            out[pstride + t_of_k(k + 1)] = a1 >> 16;
+            if (!kJumpEnd) {
+              jacc += 16;
+              while (jacc >= a.kit) {
+                jacc -= a.kit;
+                jump_word(jt, nib, jw, r);
+              }
+            }
+          }
+          continue;
+        }
         if (SRC == kSrcPbits && CB == 16 && !(a.kr & 1)) {
           // n = 512: one bit-plane group is the 16 draws of k (even) and of
           // k + 1 -- resolve it once for both rows of plane words
@@ -491,7 +530,7 @@ __device__ __forceinline__ void win_produce(const WinArgs& a, const uint4* __res
           const int k = w.k0 + kk;
           win_segment_k<SRC, CB>(a, st, pl, out + t_of_k(k), key0, key1, pstride,
                                    pseg + (unsigned long long)k * G.words);
-          if (XO) {  // the 8 jump words, spread evenly over the piece's kit k-iterations
+          if (XO && !kJumpEnd) {  // the 8 jump words, spread evenly over the piece's kit k-iterations
             jacc += 8;
             while (jacc >= a.kit) {
               jacc -= a.kit;
@@ -500,7 +539,13 @@ __device__ __forceinline__ void win_produce(const WinArgs& a, const uint4* __res
           }
         }
       }
-      if (XO) {
+      if (XO && kJumpEnd) {
+        // the jump after the draws: the piece's start state is still in
+        // memory, and the draw loop keeps no 16 jump registers live
+        XState s0;
+        load_state(s0, a.states, a.npieces, gi);
+        store_state(jump_apply(s0, jt), a.states, a.npieces, gi);  // same piece, next window
+      } else if (XO) {
         XState nx;
         nx.a0 = r[0]; nx.a1 = r[1]; nx.b0 = r[2]; nx.b1 = r[3];
         nx.c0 = r[4]; nx.c1 = r[5]; nx.d0 = r[6]; nx.d1 = r[7];

@@ -61,7 +61,7 @@ cap = {
     "registers": get("launch__registers_per_thread"), "grid": get("launch__grid_size"), "block": get("launch__block_size"),
     "inst_executed_warp": insts, "inst_per_attempt": round(insts * 32 / attempts, 2),
 }
-summary = {"round": 1, "tag": tag,
+summary = {"round": 2, "tag": tag, "capture": rep,
            "command": f"python bench.py --steps 10 --warmup 3 --no-cpu {bench_flags} (cfg2 64 x 1024^2); ncu --set full "
                       f"--clock-control none -k regex:{key} -s 5 -c 1",
            key: cap, "launch_list": f"profiles/launches_{tag}_summary.json"}
