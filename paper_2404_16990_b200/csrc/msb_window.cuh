@@ -71,11 +71,23 @@ __device__ __forceinline__ unsigned flags_base(const WinArgs& a) {
 // completed phase i-1, and publishes its own completion; slow groups delay
 // only their neighbours instead of the whole grid.  (Whole lattices whose
 // rows are one band segment; the general form is gf_wait / gf_done.)
+#ifndef MSB_WAIT_MAX_NS
+#define MSB_WAIT_MAX_NS 512
+#endif
+constexpr unsigned kWaitMaxNs = MSB_WAIT_MAX_NS;
+
 __device__ __forceinline__ void group_wait(const unsigned* flags, unsigned g, unsigned gps, unsigned need) {
   if ((threadIdx.x & 31) == 0) {
     const unsigned s0 = g - g % gps, l = g - s0;
     const unsigned up = s0 + (l == 0 ? gps - 1 : l - 1), dn = s0 + (l + 1 == gps ? 0 : l + 1);
-    while (ld_acquire(flags + up) < need || ld_acquire(flags + dn) < need) __nanosleep(32);
+    // backing off: spinning lanes issue instructions the working warps of
+    // the SM need (the polls were 7% of the cfg2 direct kernel's
+    // instructions at a fixed 32 ns)
+    unsigned ns = 32;
+    while (ld_acquire(flags + up) < need || ld_acquire(flags + dn) < need) {
+      __nanosleep(ns);
+      ns = min(ns * 2, kWaitMaxNs);
+    }
   }
   __syncwarp();
 }
@@ -183,7 +195,7 @@ __device__ __forceinline__ void gf_wait_nb(const GroupNb& n, unsigned need, bool
       if (!ok_h) ok_h = ld_acquire(n.pl) >= need && ld_acquire(n.pr) >= need;
       if (!(ok_u && ok_d && ok_h)) {
         __nanosleep(ns);
-        ns = min(ns * 2, 512u);
+        ns = min(ns * 2, kWaitMaxNs);
       }
     }
   }
