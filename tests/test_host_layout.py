@@ -89,3 +89,32 @@ def test_ring_plan_neighbours():
             if r + 1 < world:
                 assert plans[r + 1]["row0"] == p["row0"] + p["rows"]
             assert p["rows"] % 2 == 0 and p["row0"] % 2 == 0
+
+
+def test_boundary_contract_equals_reference():
+    """The boundary rules derived from the fold geometry, the halo sources,
+    the neighbour indices and the Onsager curve equal the reference's
+    (lattice.py:276-355) on every boundary word of several shapes."""
+    from tests.conftest import reference_available
+    if not reference_available():
+        pytest.skip("reference not installed")
+    import multispin.lattice as R
+    from paper_2404_16990_b200 import layout as L
+    for c in R.ALL_CODES:
+        rp, lp = R.BOUNDARY_RULES[c], L.BOUNDARY_RULES[L.ArrayCode(c.value)]
+        assert (rp[0].value, rp[1], rp[2]) == (lp[0].value, lp[1], lp[2])
+    for m, n in [(4, 32), (12, 96), (16, 64), (8, 128)]:
+        rd, ld = R.LatticeDims(m, n), L.LatticeDims(m, n)
+        for c in R.ALL_CODES:
+            for g in range(rd.cols):
+                for e in range(rd.vec_len):
+                    if 1 <= g <= rd.cells and 1 <= e <= rd.words:
+                        continue
+                    a = R.canonical_halo_source(c, g, e, rd)
+                    b = L.canonical_halo_source(L.ArrayCode(c.value), g, e, ld)
+                    assert (a is None) == (b is None)
+                    if a is not None:
+                        assert (a.code.value, a.cell, a.word) == (b.code.value, b.cell, b.word)
+        assert all(R.neighbor_indices(i, rd) == L.neighbor_indices(i, ld) for i in range(rd.sites))
+    for T in (0.5, 1.0, 2.0, 2.269, 2.27, 3.0):
+        assert R.onsager_magnetization(T) == L.onsager_magnetization(T)
