@@ -42,7 +42,7 @@ from .engine import _M64, _jump_table, _p, _pow_tables, _sweep_jump_table, _torc
 from .layout import LatticeDims
 
 __all__ = ["slab_bounds", "ring_plan", "SlabLattice", "LocalExchange", "DistExchange", "SlabRun", "FusedSlabRun",
-           "symmetric_alloc"]
+           "symmetric_alloc", "resolve_group", "peer_halo"]
 
 
 def slab_bounds(m: int, parts: int) -> list[tuple[int, int]]:
@@ -197,6 +197,34 @@ def ring_plan(m: int, world: int, rank: int) -> dict:
     (a, b) = bounds[rank]
     return {"row0": a, "rows": b - a, "up": up, "down": down,
             "up_R": bounds[up][1] - bounds[up][0] + 2, "down_R": bounds[down][1] - bounds[down][0] + 2}
+
+
+def resolve_group(group=None):
+    """(group, world, rank) of a ring spanning processes: ``group`` or, when
+    torch.distributed is initialised, the default group (symmetric memory
+    needs a real group object: ``rendezvous(t, None)`` raises); world 1 and
+    rank 0 without torch.distributed."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return None, 1, 0
+    if group is None:
+        group = dist.group.WORLD
+    world = dist.get_world_size(group)
+    return group, world, (dist.get_rank(group) if world > 1 else 0)
+
+
+def peer_halo(plan: dict, rank: int, spins_handle, flags_handle, spins_ptr: int, flags_ptr: int):
+    """msb_halo of ring member `rank` from the symmetric-memory handles of
+    its spin and flag buffers: the neighbours' mappings of the same buffers
+    (buffer_ptrs[r] is rank r's allocation as mapped here; our buffers may
+    be views at an offset into the allocation)."""
+    def peer(hdl, ptr, r):
+        return int(hdl.buffer_ptrs[r]) + (ptr - int(hdl.buffer_ptrs[rank]))
+    h = _lib.Halo()
+    h.up_spins, h.down_spins = peer(spins_handle, spins_ptr, plan["up"]), peer(spins_handle, spins_ptr, plan["down"])
+    h.up_flags, h.down_flags = peer(flags_handle, flags_ptr, plan["up"]), peer(flags_handle, flags_ptr, plan["down"])
+    h.up_R, h.down_R = plan["up_R"], plan["down_R"]
+    return h
 
 
 def symmetric_alloc(group=None):
@@ -362,12 +390,7 @@ class FusedSlabRun:
         # bit-plane stream: direct sweeps (no accept planes), S sweeps per launch
         self.direct = s0.stream == "philox-bits" and all(
             bool(L.msb_direct_ok(ctypes.byref(s._g), ctypes.byref(s._params))) for s in self.slabs)
-        dist_on = dist.is_available() and dist.is_initialized()
-        if dist_on and group is None:
-            group = dist.group.WORLD
-        self.group = group
-        self.world = dist.get_world_size(group) if dist_on else 1
-        self.rank = dist.get_rank(group) if self.world > 1 else 0
+        self.group, self.world, self.rank = resolve_group(group)
         if self.world > 1 and len(self.slabs) != 1:
             raise ValueError("one slab per rank when the ring spans processes")
         self._wb = []
@@ -406,14 +429,7 @@ class FusedSlabRun:
                 return t._base if t._base is not None else t
             hs = symm_mem.rendezvous(base(s0._spins), self.group)
             hf = symm_mem.rendezvous(base(s0._flags), self.group)
-
-            def peer(hdl, t, r):  # peer r's mapping of the same buffer
-                return int(hdl.buffer_ptrs[r]) + (t.data_ptr() - int(hdl.buffer_ptrs[self.rank]))
-            h = _lib.Halo()
-            h.up_spins, h.down_spins = peer(hs, s0._spins, plan["up"]), peer(hs, s0._spins, plan["down"])
-            h.up_flags, h.down_flags = peer(hf, s0._flags, plan["up"]), peer(hf, s0._flags, plan["down"])
-            h.up_R, h.down_R = plan["up_R"], plan["down_R"]
-            self._halos.append(h)
+            self._halos.append(peer_halo(plan, self.rank, hs, hf, s0._spins.data_ptr(), s0._flags.data_ptr()))
             self._handles = (hs, hf)
             DistExchange(self.group).exchange([s0], 0)
             DistExchange(self.group).exchange([s0], 1)

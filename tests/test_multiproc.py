@@ -114,3 +114,45 @@ def test_replica_slices_match_reference_split():
     assert replica_slices(754, 8) == [(0, 94), (94, 188), (188, 282), (282, 377), (377, 471), (471, 565),
                                       (565, 659), (659, 754)]
     assert replica_slices(4, 3) == [(0, 1), (1, 2), (2, 4)]
+
+
+def _group_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2404_16990_b200.slab import resolve_group
+    g, w, r = resolve_group(None)
+    out[rank] = (g is dist.group.WORLD, w, r)
+    dist.destroy_process_group()
+
+
+def test_fused_ring_resolves_the_default_group():
+    """FusedSlabRun(group=None) under torch.distributed uses the default
+    group (round 1 passed None to symm_mem.rendezvous, which raises)."""
+    from paper_2404_16990_b200.slab import resolve_group
+    assert resolve_group(None) == (None, 1, 0)
+    out = mp.Manager().dict()
+    mp.spawn(_group_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    assert out[0] == (True, 2, 0) and out[1] == (True, 2, 1)
+
+
+class _Handle:
+    def __init__(self, bases):
+        self.buffer_ptrs = bases
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_peer_halo_pointers(world):
+    """The halo a rank builds from symmetric-memory handles points at the
+    ring neighbours' mappings of the same buffers, offsets included."""
+    from paper_2404_16990_b200.slab import peer_halo, ring_plan
+    m = 14336
+    spin_bases = [0x7000_0000_0000 + 0x1_0000_0000 * r for r in range(world)]
+    flag_bases = [0x9000_0000_0000 + 0x10_0000 * r for r in range(world)]
+    for rank in range(world):
+        plan = ring_plan(m, world, rank)
+        h = peer_halo(plan, rank, _Handle(spin_bases), _Handle(flag_bases), spin_bases[rank] + 4096,
+                      flag_bases[rank])
+        up, down = (rank - 1) % world, (rank + 1) % world
+        assert (h.up_spins, h.down_spins) == (spin_bases[up] + 4096, spin_bases[down] + 4096)
+        assert (h.up_flags, h.down_flags) == (flag_bases[up], flag_bases[down])
+        assert h.up_R == ring_plan(m, world, up)["rows"] + 2 and h.down_R == ring_plan(m, world, down)["rows"] + 2
