@@ -283,17 +283,21 @@ def int_peak_tops(stream) -> float:
     return best
 
 
-def load_traffic(kernel: str = "k_win"):
-    """DRAM bytes per launch of `kernel` from the committed ncu --set full
-    capture (profiles/ncu_summary.json; the capture names its template)."""
-    p = ROOT / "profiles" / "ncu_summary.json"
+def load_traffic(stream: str = "xoshiro", config: str = "cfg2"):
+    """DRAM bytes (read + write) per launch of the stream's dominant kernel
+    from the committed ncu --set full capture (profiles/ncu_summary.json for
+    the xoshiro window kernel, ncu_summary_pbits.json for the direct
+    philox-bits kernel); returns (bytes, source) or (None, None)."""
+    name = {"xoshiro": "ncu_summary.json", "philox-bits": "ncu_summary_pbits.json"}.get(stream)
+    if name is None or config != "cfg2":  # the committed captures are of the cfg2 launch
+        return None, None
     try:
-        d = json.loads(p.read_text())
-        e = d.get(kernel, {})
-        return {"bytes_per_launch": e.get("dram_bytes_per_launch"), "kernel": e.get("kernel"),
-                "capture": e.get("capture")} if e else None
+        d = json.loads((ROOT / "profiles" / name).read_text())
+        e = d["k_win"]
+        return e["dram_bytes_per_launch"], {"summary": f"profiles/{name}", "kernel": e.get("kernel"),
+                                            "capture": d.get("capture"), "command": d.get("command")}
     except Exception:
-        return None
+        return None, None
 
 
 class L2Flush:
@@ -480,6 +484,7 @@ def run_ours(args, cfg):
         kern_avg_s = statistics.mean(step_ms) * 1e-3
         a_int = A_INT[args.stream]
         achieved = a_int * my_step / kern_avg_s / 1e12
+        traffic, traffic_src = load_traffic(args.stream, args.config)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": args.warmup,
             "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "strong" if cfg.get("split") else "weak",
@@ -499,7 +504,7 @@ def run_ours(args, cfg):
             },
             "roofline": {
                 "bound": "int32", "achieved": achieved, "peak": peak, "unit": "Tops/s",
-                "frac": achieved / peak, "traffic": load_traffic(),
+                "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                 "kernel": "k_win", "per_launch": f"{my_step} attempts x {a_int} int32 ops",
                 "peak_source": "msb_bench_int_peak: issue-bound LOP3+IMAD mix, measured in this run",
             },

@@ -34,10 +34,14 @@ def test_cli_runs_on_gpu_engine():
     from paper_2404_16990_b200 import backend
     from paper_2404_16990_b200.cli import main
     import multispin.engine
-    assert main(["simulate", "--m", "8", "--n", "64", "--temperature", "2.0", "--sweeps", "2"]) == 0
-    assert multispin.engine.Engine is backend.BackendEngine
-    eng = multispin.engine.Engine(multispin.LatticeDims(8, 64), [2.0], seed=1)
-    assert eng._spins.is_cuda
+    pristine = multispin.engine.Engine
+    with backend.gpu_backend():
+        assert main(["simulate", "--m", "8", "--n", "64", "--temperature", "2.0", "--sweeps", "2"]) == 0
+        assert multispin.engine.Engine is backend.BackendEngine
+        eng = multispin.engine.Engine(multispin.LatticeDims(8, 64), [2.0], seed=1)
+        assert eng._spins.is_cuda
+    assert main(["simulate", "--m", "8", "--n", "64", "--temperature", "2.0", "--sweeps", "1"]) == 0
+    assert multispin.engine.Engine is pristine  # main() restores the reference's names on return
 
 
 def test_selftest_with_fault_injection(capsys):
