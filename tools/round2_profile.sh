@@ -1,12 +1,11 @@
 #!/usr/bin/env bash
 # GPU-box session: bench lines per config and stream, the ncu launch list and
-# one --set full capture of the headline k_win and of the direct kernel, and
-# compute-sanitizer memcheck / synccheck / initcheck over tools/sanitize_cases.py.
+# one --set full capture of the headline k_win and of the direct kernel.
 # Usage (on the box): bash tools/round2_profile.sh [out_dir] [parts...]
-#   parts: bench ncu sanitize (default: all)
+#   parts: bench ncu (default: both)
 OUT=${1:-gpurun_out/r02}
 shift || true
-PARTS=${*:-bench ncu sanitize}
+PARTS=${*:-bench ncu}
 mkdir -p "$OUT"
 has() { [[ " $PARTS " == *" $1 "* ]]; }
 if has bench; then
@@ -33,12 +32,5 @@ if has ncu; then
     python bench.py --steps 10 --warmup 3 --no-cpu --no-alt --stream philox-bits > "$OUT/ncu_launches_pbits.log" 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_win -s 5 -c 1 -o "$OUT/k_win_pbits" -f \
     python bench.py --steps 10 --warmup 3 --no-cpu --no-alt --stream philox-bits > "$OUT/ncu_kwin_pbits.log" 2>&1
-fi
-if has sanitize; then
-  for tool in memcheck synccheck initcheck; do
-    timeout 900 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_cases.py \
-      > "$OUT/sanitizer_$tool.log" 2>&1
-    echo "$tool rc=$?" >> "$OUT/sanitizer_rc.txt"
-  done
 fi
 ls -la "$OUT"
