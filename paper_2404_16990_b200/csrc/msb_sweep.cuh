@@ -100,6 +100,10 @@ struct FlipArgs {
   int band_h, band_gb;
   int band_sq, band_nseg;  // quads per row segment (divides 32), segments per row
   unsigned band_groups;    // groups per colour phase (all replicas)
+  // n = 512 window planes (pk16): the plane word of t in {0..3, 8..11} also
+  // holds plane t + 4 in its high half (the 32 draws of k and k + 1 are one
+  // producer run), so a quad of t0 = 4, 12 reads the words of t0 - 4, >> 16
+  int pk16;
 };
 
 constexpr int kFlipSlots = 256;
@@ -166,8 +170,14 @@ __device__ __forceinline__ unsigned flip_quad_at(const FlipArgs& a, int s, int l
                   (unsigned)lr) * Wp + (unsigned)w0;
   uint4 P4 = make_uint4(0, 0, 0, 0), P8 = make_uint4(0, 0, 0, 0);
   if (!GENERIC) {
-    P4 = __ldg(reinterpret_cast<const uint4*>(pl));
-    P8 = __ldg(reinterpret_cast<const uint4*>(pl + pstride));
+    const int sh = a.pk16 ? (t0 & 4) * 4 : 0;
+    const uint32_t* pq = pl - (a.pk16 ? (t0 & 4) : 0);
+    P4 = __ldg(reinterpret_cast<const uint4*>(pq));
+    P8 = __ldg(reinterpret_cast<const uint4*>(pq + pstride));
+    if (sh) {
+      P4.x >>= 16; P4.y >>= 16; P4.z >>= 16; P4.w >>= 16;
+      P8.x >>= 16; P8.y >>= 16; P8.z >>= 16; P8.w >>= 16;
+    }
   }
   const int p = (c + X) & 1;
   const uint32_t y[4] = {Y.x, Y.y, Y.z, Y.w};
@@ -288,7 +298,8 @@ struct NoHooks {
 
 // PF: prefetch the plane rows of the run's groups one group ahead (callers
 // that walk one group at a time prefetch themselves, band_prefetch).
-template <bool COHERENT, bool PUSH = false, bool SEG = false, int DIRECT = 0, bool PF = true, class HK = NoHooks>
+template <bool COHERENT, bool PUSH = false, bool SEG = false, int DIRECT = 0, bool PF = true, class HK = NoHooks,
+          bool PK16 = false>
 __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0, unsigned g1, int X,
                                                   const PbitsDirect* dp = nullptr, const HK& hk = HK{}) {
   const Geo& G = a.G;
@@ -348,9 +359,12 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
     // the plane rows; the row below wraps only past a whole lattice's last row
     const uint32_t* yrow = ybase + (unsigned)br0 * Wp;
     uint32_t* orow = a.spins + (s * 2u + (unsigned)X) * colour_words + (unsigned)br0 * Wp + w0;
+    // PK16 (n = 512 window planes, a.pk16): quads of t0 = 4, 12 take the high halves of the words of t0 - 4
+    const bool phi = PK16 && a.pk16 && (w0 & 4);
     const uint32_t* prow =
         DIRECT ? nullptr
-               : a.planes + ((((unsigned)X * (unsigned)a.np) * (unsigned)G.n_sim + s) * (unsigned)G.rows + (unsigned)lr0) * Wp + w0;
+               : a.planes + ((((unsigned)X * (unsigned)a.np) * (unsigned)G.n_sim + s) * (unsigned)G.rows + (unsigned)lr0) * Wp +
+                     (PK16 && a.pk16 ? (w0 & ~4) : w0);
     uint32_t key4 = 0, key8 = 0;
     bool kuni = false;  // DIRECT: the warp's lanes share one pair of keys (bands of one replica)
     uint4* kt = nullptr;
@@ -384,6 +398,10 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
       if (!DIRECT) {
         P4 = __ldg(reinterpret_cast<const uint4*>(prow));
         P8 = __ldg(reinterpret_cast<const uint4*>(prow + pstride));
+        if (PK16 && phi) {
+          P4.x >>= 16; P4.y >>= 16; P4.z >>= 16; P4.w >>= 16;
+          P8.x >>= 16; P8.y >>= 16; P8.z >>= 16; P8.w >>= 16;
+        }
       }
       uint32_t edge;
       if (P) {  // word t0+4, or the chunk wrap: (first word >> 1) | (next chunk's bit 0 << vb-1)
@@ -588,6 +606,7 @@ inline void fill_flip_args(FlipArgs& a, const msb_geom* g, const msb_sweep_param
   a.band_h = a.band_gb = 0;
   a.band_sq = a.band_nseg = 0;
   a.band_groups = 0;
+  a.pk16 = 0;
   const int qpr = a.G.Wp / 4;  // 4 * chunks: a multiple of 4
   if (p->mode != MSB_MODE_GENERIC) {
     int sq = 32;

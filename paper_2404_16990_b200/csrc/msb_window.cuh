@@ -508,11 +508,9 @@ __device__ __forceinline__ void win_produce(const WinArgs& a, const uint4* __res
               acc_reject(acc1, h9, key1);
             }
             // REJECT bits, newest draw in bit 0: reversed, bit i = draw i
-            const uint32_t a0 = ~__brev(acc0), a1 = ~__brev(acc1);
-            out[t_of_k(k)] = a0 & 0xFFFFu;
-            out[pstride + t_of_k(k)] = a1 & 0xFFFFu;
-            out[t_of_k(k + 1)] = a0 >> 16;
-            out[pstride + t_of_k(k + 1)] = a1 >> 16;
+            // packed planes (FlipArgs::pk16): t(k + 1) = t(k) + 4 rides in the high half
+            out[t_of_k(k)] = ~__brev(acc0);
+            out[pstride + t_of_k(k)] = ~__brev(acc1);
             if (!kJumpEnd) {
               jacc += 16;
               while (jacc >= a.kit) {
@@ -531,10 +529,8 @@ __device__ __forceinline__ void win_produce(const WinArgs& a, const uint4* __res
             const int k = w.k0 + kk;
             uint32_t acc[2];
             pbits_group<2>((pseg + (unsigned long long)k * 16) >> 5, pl, a.pk, key, 2, acc);
-            out[t_of_k(k)] = acc[0] & 0xFFFFu;
-            out[pstride + t_of_k(k)] = acc[1] & 0xFFFFu;
-            out[t_of_k(k + 1)] = acc[0] >> 16;
-            out[pstride + t_of_k(k + 1)] = acc[1] >> 16;
+            out[t_of_k(k)] = acc[0];  // packed planes, as above
+            out[pstride + t_of_k(k)] = acc[1];
           }
           continue;
         }
@@ -858,7 +854,7 @@ __device__ __forceinline__ void win_body(const WinArgs& wa, const FlipArgs& fa0,
         }
         constexpr bool PG = DIRECT != 0;
         const GfHooks<HALO, PG> hk{&go, fbase + (unsigned)i, lo, hi, i > 0, HALO || i > 0};
-        cnt += flip_band_run<true, HALO, GSEG, DIRECT, true, GfHooks<HALO, PG>>(fa, lo, hi, X, &dp, hk);
+        cnt += flip_band_run<true, HALO, GSEG, DIRECT, true, GfHooks<HALO, PG>, CB == 16 && !DIRECT>(fa, lo, hi, X, &dp, hk);
         if (!PG) gf_publish_cta<HALO>(go, fbase + (unsigned)i + 1u, per, total, nwc, vgrid, vb, leader);
       }
     } else
@@ -874,14 +870,15 @@ __device__ __forceinline__ void win_body(const WinArgs& wa, const FlipArgs& fa0,
       }
       if constexpr (!GFX) {  // (GFX kernels get flags from the host: a band walk is always gf)
         if (band) {
+          constexpr bool PK = CB == 16 && !DIRECT;
           if (fa.band_nseg > 1) {  // wide rows (cfg4, cfg5): segment-edge words from memory
             if (HALO) cnt += flip_band_run<true, true, true, DIRECT>(fa, lo, hi, X, &dp);
             else if (i == 0 && !pro) cnt += flip_band_run<false, false, true, DIRECT>(fa, lo, hi, X, &dp);
             else cnt += flip_band_run<true, false, true, DIRECT>(fa, lo, hi, X, &dp);
           } else {
-            if (HALO) cnt += flip_band_run<true, true, false, DIRECT>(fa, lo, hi, X, &dp);
-            else if (i == 0 && !pro) cnt += flip_band_run<false, false, false, DIRECT>(fa, lo, hi, X, &dp);
-            else cnt += flip_band_run<true, false, false, DIRECT>(fa, lo, hi, X, &dp);
+            if (HALO) cnt += flip_band_run<true, true, false, DIRECT, true, NoHooks, PK>(fa, lo, hi, X, &dp);
+            else if (i == 0 && !pro) cnt += flip_band_run<false, false, false, DIRECT, true, NoHooks, PK>(fa, lo, hi, X, &dp);
+            else cnt += flip_band_run<true, false, false, DIRECT, true, NoHooks, PK>(fa, lo, hi, X, &dp);
           }
         }
       }
@@ -1194,6 +1191,8 @@ int plan_window(const msb_geom* g, const msb_sweep_params* p, int S, int P, uint
   if (next && p->rng == MSB_RNG_XOSHIRO && (!states || !p->jump)) return fail(MSB_ERR_ARG, "null RNG state or jump table");
   fill_win_args(wa, g, p, S, P, np, states, next);
   fill_flip_args(fa, g, p, 0, spins, cur, flips);
+  // the producer's packed n = 512 planes (one 32-draw run fills t(k) and t(k + 1) = t(k) + 4)
+  fa.pk16 = chunk_width(wa.G) == 16 && wa.kr % 2 == 0 && p->rng != MSB_RNG_PHILOX;
   wa.nslot = (unsigned)g_nslot(fa);
   set_halo(halo, count, fa, ha);
   return MSB_OK;
