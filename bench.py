@@ -94,11 +94,23 @@ CONFIGS = {
 }
 
 
+# Test mode (tests/test_gpu_bench_ranks.py): every rank on cuda:0 with gloo
+# collectives, to exercise the multi-rank plumbing (spawn, rendezvous,
+# barriers, max / sum over ranks, one line from rank 0) on a one-GPU box.
+# Replica ranks never wait on each other, so sharing a device is only slower;
+# the line is marked and is not a measurement.
+SHARE_DEVICE = os.environ.get("MSB_BENCH_SHARE_DEVICE") == "1"
+
+
 def dist_info():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if SHARE_DEVICE else int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
+
+
+def _coll_device(torch):
+    return torch.device("cpu") if SHARE_DEVICE else torch.device("cuda", torch.cuda.current_device())
 
 
 # ---------------------------------------------------------------------------
@@ -337,7 +349,7 @@ def device_rate(torch, dist, ws, eng, S, K, attempts_step, flush):
 
 def max_over_ranks(torch, dist, ws, x: float) -> float:
     if ws > 1:
-        t = torch.tensor([x], device=torch.device("cuda", torch.cuda.current_device()), dtype=torch.float64)
+        t = torch.tensor([x], device=_coll_device(torch), dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
     return x
@@ -345,7 +357,7 @@ def max_over_ranks(torch, dist, ws, x: float) -> float:
 
 def sum_over_ranks(torch, dist, ws, x: int) -> int:
     if ws > 1:
-        t = torch.tensor([x], device=torch.device("cuda", torch.cuda.current_device()), dtype=torch.int64)
+        t = torch.tensor([x], device=_coll_device(torch), dtype=torch.int64)
         dist.all_reduce(t)
         return int(t.item())
     return x
@@ -397,7 +409,10 @@ def run_ours(args, cfg):
 
     ws, rank, local = dist_info()
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if SHARE_DEVICE:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     n_sim, sim_offset = replica_share(cfg, ws, rank)
@@ -526,6 +541,8 @@ def run_ours(args, cfg):
             "flips_per_ns": value / 1e9,
         }
         line["config"]["global_replicas"] = cfg["n_sim"] if cfg.get("split") else cfg["n_sim"] * ws
+        if SHARE_DEVICE and ws > 1:
+            line["test_mode"] = f"MSB_BENCH_SHARE_DEVICE: {ws} ranks on one GPU (plumbing test, not a measurement)"
         if alt is not None:
             line["other_streams"] = alt
         if extra is not None:
@@ -664,7 +681,7 @@ def spawn_ranks(n: int) -> int:
     import subprocess
     import torch
     have = torch.cuda.device_count()
-    if have < n:
+    if have < n and not SHARE_DEVICE:
         print(f"bench.py: --gpus {n} but only {have} GPU(s) visible; not running", file=sys.stderr)
         return 2
     with socket.socket() as sk:
@@ -705,6 +722,9 @@ def main():
               file=sys.stderr)
         return 2
     if cfg.get("slab"):
+        if SHARE_DEVICE and args.gpus > 1:
+            print("bench.py: MSB_BENCH_SHARE_DEVICE covers the replica configurations only", file=sys.stderr)
+            return 2
         return run_slab(args, cfg)
     return run_ours(args, cfg)
 
