@@ -104,6 +104,12 @@ struct FlipArgs {
   // holds plane t + 4 in its high half (the 32 draws of k and k + 1 are one
   // producer run), so a quad of t0 = 4, 12 reads the words of t0 - 4, >> 16
   int pk16;
+  // n = 512 packed spin rows inside a window launch (pks, flip_band_run
+  // PKS): word j of a row holds the sites of t = tl(j) (low half) and
+  // tl(j) + 4 (high half), tl(j) = j (j < 4) or j + 4, of w = bit -- the
+  // pairing of the pk16 plane words, so plane word tl(j) gates word j
+  // without shifts.  The row keeps its 16-word pitch; words 0..7 are used.
+  int pks;
 };
 
 constexpr int kFlipSlots = 256;
@@ -299,7 +305,7 @@ struct NoHooks {
 // PF: prefetch the plane rows of the run's groups one group ahead (callers
 // that walk one group at a time prefetch themselves, band_prefetch).
 template <bool COHERENT, bool PUSH = false, bool SEG = false, int DIRECT = 0, bool PF = true, class HK = NoHooks,
-          bool PK16 = false>
+          bool PK16 = false, bool PKS = false>
 __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0, unsigned g1, int X,
                                                   const PbitsDirect* dp = nullptr, const HK& hk = HK{}) {
   const Geo& G = a.G;
@@ -347,7 +353,7 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
     const int qg = seg * sq + q;  // quad of the row
     const int ch = qg >> 2, w0 = qg * 4;
     const int vb = chunk_bits(G, ch);
-    const uint32_t vm = chunk_mask(G, ch);
+    const uint32_t vm = PKS ? 0xFFFFFFFFu : chunk_mask(G, ch);
     // a segment-edge lane's outer neighbour word, relative to its quad
     const int off_next = (w0 + 4 == (int)Wp ? 0 : w0 + 4) - w0, off_prev = (w0 == 0 ? (int)Wp - 1 : w0 - 1) - w0;
     const uint32_t* ybase = a.spins + (s * 2u + (unsigned)(1 - X)) * colour_words + w0;
@@ -360,11 +366,11 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
     const uint32_t* yrow = ybase + (unsigned)br0 * Wp;
     uint32_t* orow = a.spins + (s * 2u + (unsigned)X) * colour_words + (unsigned)br0 * Wp + w0;
     // PK16 (n = 512 window planes, a.pk16): quads of t0 = 4, 12 take the high halves of the words of t0 - 4
-    const bool phi = PK16 && a.pk16 && (w0 & 4);
+    const bool phi = !PKS && PK16 && a.pk16 && (w0 & 4);
     const uint32_t* prow =
         DIRECT ? nullptr
                : a.planes + ((((unsigned)X * (unsigned)a.np) * (unsigned)G.n_sim + s) * (unsigned)G.rows + (unsigned)lr0) * Wp +
-                     (PK16 && a.pk16 ? (w0 & ~4) : w0);
+                     (PKS ? 2 * w0 : PK16 && a.pk16 ? (w0 & ~4) : w0);
     uint32_t key4 = 0, key8 = 0;
     bool kuni = false;  // DIRECT: the warp's lanes share one pair of keys (bands of one replica)
     uint4* kt = nullptr;
@@ -404,7 +410,22 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
         }
       }
       uint32_t edge;
-      if (P) {  // word t0+4, or the chunk wrap: (first word >> 1) | (next chunk's bit 0 << vb-1)
+      if (PKS) {
+        // packed rows (two lanes, words 0-3 and 4-7).  t + 1: word 3 ->
+        // (t 4 = word 0 high, t 8 = word 4 low); word 7 -> (t 12 = word 4
+        // high, t 16 = t 0 of w + 1: word 0 low rotated by one bit).  t - 1:
+        // word 0 -> (t -1 = t 15 of w - 1: word 7 high rotated, t 3 = word 3
+        // low); word 4 -> (t 7 = word 3 high, t 11 = word 7 low)
+        if (P) {
+          const uint32_t xa = __shfl_sync(0xFFFFFFFFu, Y.x, s_next);
+          const uint32_t other = q == 0 ? xa : (((xa & 0xFFFFu) >> 1) | ((xa & 1u) << 15));
+          edge = (Y.x >> 16) | (other << 16);
+        } else {
+          const uint32_t h = __shfl_sync(0xFFFFFFFFu, Y.w, s_prev) >> 16;
+          const uint32_t other = q == 0 ? (((h << 1) | (h >> 15)) & 0xFFFFu) : h;
+          edge = other | (Y.w << 16);
+        }
+      } else if (P) {  // word t0+4, or the chunk wrap: (first word >> 1) | (next chunk's bit 0 << vb-1)
         uint32_t xa = __shfl_sync(0xFFFFFFFFu, Y.x, s_next);
         const uint32_t xb = __shfl_sync(0xFFFFFFFFu, Y.x, s_first);
         if (SEG && seg_last) xa = ld1(yrow + off_next);
@@ -607,6 +628,7 @@ inline void fill_flip_args(FlipArgs& a, const msb_geom* g, const msb_sweep_param
   a.band_sq = a.band_nseg = 0;
   a.band_groups = 0;
   a.pk16 = 0;
+  a.pks = 0;
   const int qpr = a.G.Wp / 4;  // 4 * chunks: a multiple of 4
   if (p->mode != MSB_MODE_GENERIC) {
     int sq = 32;

@@ -636,6 +636,27 @@ struct WinIO {
   int load16;        // rows * nch % 16 == 0: the prologue loads 16 chunks per batch
 };
 
+// n = 512 rows <-> packed rows in place (FlipArgs::pks), one row per thread
+// (16 words in, 8 out, or back), rows [t, rows) step nt.
+template <bool UNPACK>
+__device__ __forceinline__ void pack_rows(uint32_t* spins, unsigned nrows, unsigned t, unsigned nt) {
+  for (unsigned r = t; r < nrows; r += nt) {
+    uint4* row = reinterpret_cast<uint4*>(spins + (size_t)r * 16);
+    if (!UNPACK) {
+      const uint4 a = __ldcg(row), b = __ldcg(row + 1), c = __ldcg(row + 2), d = __ldcg(row + 3);
+      // word j: (t, t + 4), t = j (j < 4) or j + 4
+      __stcg(row, make_uint4(a.x | (b.x << 16), a.y | (b.y << 16), a.z | (b.z << 16), a.w | (b.w << 16)));
+      __stcg(row + 1, make_uint4(c.x | (d.x << 16), c.y | (d.y << 16), c.z | (d.z << 16), c.w | (d.w << 16)));
+    } else {
+      const uint4 lo = __ldcg(row), hi = __ldcg(row + 1);
+      __stcg(row, make_uint4(lo.x & 0xFFFFu, lo.y & 0xFFFFu, lo.z & 0xFFFFu, lo.w & 0xFFFFu));
+      __stcg(row + 1, make_uint4(lo.x >> 16, lo.y >> 16, lo.z >> 16, lo.w >> 16));
+      __stcg(row + 2, make_uint4(hi.x & 0xFFFFu, hi.y & 0xFFFFu, hi.z & 0xFFFFu, hi.w & 0xFFFFu));
+      __stcg(row + 3, make_uint4(hi.x >> 16, hi.y >> 16, hi.z >> 16, hi.w >> 16));
+    }
+  }
+}
+
 // Prologue share of warp w of nw (every warp of the grid): groups of CPW
 // chunks.  With CPW = 16 a cfg2 lattice is fewer groups than warps, so each
 // warp has at most one group, i.e. 16 loads in flight, and the conversion
@@ -801,6 +822,7 @@ __device__ __forceinline__ void win_body(const WinArgs& wa, const FlipArgs& fa0,
       asm volatile("bar.sync 1, %0;" ::"r"(nwc * 32) : "memory");
     }
     const bool gflag_path = DIRECT && !GFX && !HALO && wa.flags && band && fa.band_nseg == 1;
+    unsigned epi_bar = 0;  // the epilogue barrier's index on the grid-barrier path
     bool push_warp = true;  // HALO: this warp's bands include a slab's first or last row
     if (HALO && band && !gf) {
       const unsigned gps = (unsigned)fa0.G.rows / (unsigned)(fa0.band_gb * fa0.band_h), nseg = (unsigned)fa0.band_nseg;
@@ -857,7 +879,18 @@ __device__ __forceinline__ void win_body(const WinArgs& wa, const FlipArgs& fa0,
         cnt += flip_band_run<true, HALO, GSEG, DIRECT, true, GfHooks<HALO, PG>, CB == 16 && !DIRECT>(fa, lo, hi, X, &dp, hk);
         if (!PG) gf_publish_cta<HALO>(go, fbase + (unsigned)i + 1u, per, total, nwc, vgrid, vb, leader);
       }
-    } else
+    } else {
+    // n = 512 window flips on packed rows (FlipArgs::pks): packed in place
+    // by the consumer warps after the prologue, unpacked after the last phase
+    constexpr bool kPks = CB == 16 && !DIRECT && !HALO && !GFX;
+    const bool pks = kPks && band && fa0.pks;
+    const unsigned ct = cw * 32u + (threadIdx.x & 31), nct = nc * 32u;
+    const unsigned nrows = (unsigned)fa0.G.n_sim * 2u * (unsigned)fa0.G.R;
+    unsigned nbar = 0;  // consumer barriers of this launch after the prologue's
+    if (pks) {
+      pack_rows<false>(fa0.spins, nrows, ct, nct);
+      consumer_barrier(wa.work + 1, base + vgrid * ++nbar, nwc * 32, leader);
+    }
     for (int i = 0; i < 2 * count; i++) {
       const int X = i & 1;
       PbitsDirect dp;
@@ -875,6 +908,8 @@ __device__ __forceinline__ void win_body(const WinArgs& wa, const FlipArgs& fa0,
             if (HALO) cnt += flip_band_run<true, true, true, DIRECT>(fa, lo, hi, X, &dp);
             else if (i == 0 && !pro) cnt += flip_band_run<false, false, true, DIRECT>(fa, lo, hi, X, &dp);
             else cnt += flip_band_run<true, false, true, DIRECT>(fa, lo, hi, X, &dp);
+          } else if (kPks && pks) {
+            cnt += flip_band_run<true, false, false, DIRECT, true, NoHooks, PK, kPks>(fa, lo, hi, X, &dp);
           } else {
             if (HALO) cnt += flip_band_run<true, true, false, DIRECT, true, NoHooks, PK>(fa, lo, hi, X, &dp);
             else if (i == 0 && !pro) cnt += flip_band_run<false, false, false, DIRECT, true, NoHooks, PK>(fa, lo, hi, X, &dp);
@@ -897,8 +932,15 @@ __device__ __forceinline__ void win_body(const WinArgs& wa, const FlipArgs& fa0,
 #ifdef MSB_TRACE
         if (i == 0) MSB_TRACE_PUT(6, gtimer());  // first phase done (before its barrier)
 #endif
-        consumer_barrier(wa.work + 1, base + vgrid * (unsigned)(i + 1), nwc * 32, leader);
+        consumer_barrier(wa.work + 1, base + vgrid * ++nbar, nwc * 32, leader);
       }
+    }
+    if (pks) {
+      consumer_barrier(wa.work + 1, base + vgrid * ++nbar, nwc * 32, leader);
+      pack_rows<true>(fa0.spins, nrows, ct, nct);
+    }
+    if (epi) nbar++;  // the epilogue's barrier below
+    epi_bar = nbar;
     }
     add_flips(fa.flips, cnt);
 #ifdef MSB_TRACE
@@ -906,7 +948,7 @@ __device__ __forceinline__ void win_body(const WinArgs& wa, const FlipArgs& fa0,
 #endif
     if (epi) {  // every flip of the launch is done before any export read
       // (the flag paths have no per-phase grid barriers: this is their first)
-      consumer_barrier(wa.work + 1, base + vgrid * (gflag_path || gf ? 1u : (unsigned)(2 * count)), nwc * 32, leader);
+      consumer_barrier(wa.work + 1, base + vgrid * (gflag_path || gf ? 1u : epi_bar), nwc * 32, leader);
       if (io.lin_out && io.ups) win_export<true, true>(fa0.G, fa0.spins, io, cw, nc);
       else if (io.lin_out) win_export<true, false>(fa0.G, fa0.spins, io, cw, nc);
       else win_export<false, true>(fa0.G, fa0.spins, io, cw, nc);
@@ -1195,6 +1237,22 @@ int plan_window(const msb_geom* g, const msb_sweep_params* p, int S, int P, uint
   fa.pk16 = chunk_width(wa.G) == 16 && wa.kr % 2 == 0 && p->rng != MSB_RNG_PHILOX;
   wa.nslot = (unsigned)g_nslot(fa);
   set_halo(halo, count, fa, ha);
+  // n = 512 whole lattices: the window's flips run on packed rows (two
+  // 16-site words per uint32, FlipArgs::pks), lanes = 2 quads per row.
+  // MSB_PACK16=0: the 16-bit words as they are (tuning / comparison).
+  static const int env_pk = [] { const char* e = getenv("MSB_PACK16"); return e ? atoi(e) : 1; }();
+  if (env_pk && fa.pk16 && !ha.on && count > 0 && fa.band_h > 0 && wa.G.words == 16 && wa.G.nch == 1) {
+    for (int h = 16; h >= 2; h >>= 1)
+      if (g->rows % (16 * h) == 0) {
+        fa.pks = 1;
+        fa.band_sq = 2;
+        fa.band_gb = 16;
+        fa.band_nseg = 1;
+        fa.band_h = h;
+        fa.band_groups = (unsigned)((long long)g->n_sim * g->rows / (16 * h));
+        break;
+      }
+  }
   return MSB_OK;
 }
 
