@@ -453,7 +453,7 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
         const unsigned long long nn = (unsigned long long)G.n;
         // word t0 + k of the chunk holds draw index k(t) = 4 k + t0 / 4 of the row's quarter
         unsigned long long d = dp->blk * 2 * nn + (unsigned long long)rs.q * (nn / 2) + 32ull * ch +
-                               (unsigned long long)((w0 & 15) >> 2) * (unsigned)G.words;
+                               (unsigned long long)(PKS ? w0 >> 1 : (w0 & 15) >> 2) * (unsigned)G.words;
         const unsigned long long dstep = 4ull * (unsigned)G.words;
         // neighbour classes of the 4 words (static indices), then the draws
         // word by word in a rolled loop over rotating registers

@@ -822,7 +822,11 @@ __device__ __forceinline__ void win_body(const WinArgs& wa, const FlipArgs& fa0,
       asm volatile("bar.sync 1, %0;" ::"r"(nwc * 32) : "memory");
     }
     const bool gflag_path = DIRECT && !GFX && !HALO && wa.flags && band && fa.band_nseg == 1;
-    unsigned epi_bar = 0;  // the epilogue barrier's index on the grid-barrier path
+    unsigned epi_bar = 1;  // the epilogue barrier's index among this launch's consumer barriers
+    // n = 512 rows packed in place for the flips (FlipArgs::pks): thread
+    // share of the rows
+    const unsigned ct = cw * 32u + (threadIdx.x & 31), nct = nc * 32u;
+    const unsigned nrows = (unsigned)fa0.G.n_sim * 2u * (unsigned)fa0.G.R;
     bool push_warp = true;  // HALO: this warp's bands include a slab's first or last row
     if (HALO && band && !gf) {
       const unsigned gps = (unsigned)fa0.G.rows / (unsigned)(fa0.band_gb * fa0.band_h), nseg = (unsigned)fa0.band_nseg;
@@ -836,6 +840,15 @@ __device__ __forceinline__ void win_body(const WinArgs& wa, const FlipArgs& fa0,
       // band groups in phase order, neighbour flags instead of grid barriers
       unsigned* gflags = flags_groups(wa);
       const unsigned gps = (unsigned)fa0.G.rows / (unsigned)(fa0.band_gb * fa0.band_h);
+      // n = 512 on packed rows: a packed word (t, t + 4) is one whole 32-draw
+      // group, so the 32-draw walk applies (DIRECT = 32 over CB = 16 rows)
+      constexpr bool kPksD = CB == 16 && DIRECT == 32;
+      const bool pksd = kPksD && fa0.pks;
+      unsigned nb = 0;
+      if (pksd) {
+        pack_rows<false>(fa0.spins, nrows, ct, nct);
+        consumer_barrier(wa.work + 1, base + vgrid * ++nb, nwc * 32, leader);
+      }
       for (int i = 0; i < 2 * count; i++) {
         const int X = i & 1;
         PbitsDirect dp;
@@ -844,11 +857,17 @@ __device__ __forceinline__ void win_body(const WinArgs& wa, const FlipArgs& fa0,
         dp.blk = wa.block0 + 2ull * (unsigned)(first + (i >> 1)) + (unsigned)X;
         for (unsigned g = lo; g < hi; g++) {
           if (i > 0) group_wait(gflags, g, gps, fbase + (unsigned)i);
-          if (i == 0 && !pro) cnt += flip_band_run<false, false, false, DIRECT>(fa, g, g + 1, X, &dp);
+          if (kPksD && pksd) cnt += flip_band_run<true, false, false, DIRECT, true, NoHooks, false, kPksD>(fa, g, g + 1, X, &dp);
+          else if (i == 0 && !pro) cnt += flip_band_run<false, false, false, DIRECT>(fa, g, g + 1, X, &dp);
           else cnt += flip_band_run<true, false, false, DIRECT>(fa, g, g + 1, X, &dp);
           group_done(gflags, g, fbase + (unsigned)i + 1u);
         }
       }
+      if (pksd) {
+        consumer_barrier(wa.work + 1, base + vgrid * ++nb, nwc * 32, leader);
+        pack_rows<true>(fa0.spins, nrows, ct, nct);
+      }
+      epi_bar = nb + 1;
     } else if (GFX && gf) {
       // general band-group order: whole lattices with rows in several
       // segments, and slabs, whose edge bands alone wait on the neighbours.
@@ -884,8 +903,6 @@ __device__ __forceinline__ void win_body(const WinArgs& wa, const FlipArgs& fa0,
     // by the consumer warps after the prologue, unpacked after the last phase
     constexpr bool kPks = CB == 16 && !DIRECT && !HALO && !GFX;
     const bool pks = kPks && band && fa0.pks;
-    const unsigned ct = cw * 32u + (threadIdx.x & 31), nct = nc * 32u;
-    const unsigned nrows = (unsigned)fa0.G.n_sim * 2u * (unsigned)fa0.G.R;
     unsigned nbar = 0;  // consumer barriers of this launch after the prologue's
     if (pks) {
       pack_rows<false>(fa0.spins, nrows, ct, nct);
@@ -948,7 +965,7 @@ __device__ __forceinline__ void win_body(const WinArgs& wa, const FlipArgs& fa0,
 #endif
     if (epi) {  // every flip of the launch is done before any export read
       // (the flag paths have no per-phase grid barriers: this is their first)
-      consumer_barrier(wa.work + 1, base + vgrid * (gflag_path || gf ? 1u : epi_bar), nwc * 32, leader);
+      consumer_barrier(wa.work + 1, base + vgrid * (gf ? 1u : epi_bar), nwc * 32, leader);
       if (io.lin_out && io.ups) win_export<true, true>(fa0.G, fa0.spins, io, cw, nc);
       else if (io.lin_out) win_export<true, false>(fa0.G, fa0.spins, io, cw, nc);
       else win_export<false, true>(fa0.G, fa0.spins, io, cw, nc);
@@ -1150,6 +1167,14 @@ int launch_direct(int cb, const cudaLaunchConfig_t& cfg, const WinArgs& wa, cons
     if constexpr (NT != 896) return launch_k_win<kSrcPbits, 16, HALO, 16, NT, GFX, RING>(cfg, wa, fa, ha, wio, nullptr, 0, count, 0, ring, nv);
   }
   return fail(MSB_ERR_ARG, "direct launch shape");
+}
+
+// n = 512 direct sweeps on packed rows (FlipArgs::pks): the 32-draw walk
+// over 16-site rows packed in place.
+template <int NT>
+int launch_direct_pks(const cudaLaunchConfig_t& cfg, const WinArgs& wa, const FlipArgs& fa, const HaloArgs& ha,
+                      const WinIO& wio, int count) {
+  return launch_k_win<kSrcPbits, 16, false, 32, NT, 0, false>(cfg, wa, fa, ha, wio, nullptr, 0, count, 0, nullptr, 0);
 }
 
 cudaLaunchConfig_t coop_config(unsigned grid, unsigned threads, size_t smem, void* stream, cudaLaunchAttribute* attr,
@@ -1386,6 +1411,26 @@ int direct_run_impl(int nslabs, const msb_ring_slab* slabs, bool ring, int n_swe
     // and the extra groups per warp cost little (measured 1.49 vs 1.45 T).
     static const int env_nt = [] { const char* e = getenv("MSB_DIRECT_NT"); return e ? atoi(e) : -1; }();
     const long long g28 = 28LL * sms, g24 = 24LL * sms;
+    // n = 512 with group flags: rows packed in place, two 16-draw words per
+    // uint32, i.e. one whole 32-draw group per word (MSB_PACK16=0: off)
+    static const int env_pk = [] { const char* e = getenv("MSB_PACK16"); return e ? atoi(e) : 1; }();
+    if (cb == 16 && env_pk && wa.flags && fa.G.nch == 1 && r.g->rows % 32 == 0) {
+      fa.pks = 1;
+      fa.band_sq = 2;
+      fa.band_gb = 16;
+      fa.band_nseg = 1;
+      fa.band_h = 2;
+      fa.band_groups = (unsigned)((long long)r.g->n_sim * r.g->rows / 32);
+      if (env_nt == 768) {
+        cfg.blockDim = dim3(768);
+        return launch_direct_pks<768>(cfg, wa, fa, ha, wio, n_sweeps);
+      }
+      if (env_nt != 0 && (long long)fa.band_groups <= g28 && (long long)fa.band_groups > g24) {
+        cfg.blockDim = dim3(896);
+        return launch_direct_pks<896>(cfg, wa, fa, ha, wio, n_sweeps);
+      }
+      return launch_direct_pks<0>(cfg, wa, fa, ha, wio, n_sweeps);
+    }
     if (cb == 32 && env_nt != 0 && (long long)fa.band_groups <= g28 && (long long)fa.band_groups > g24) {
       cfg.blockDim = dim3(896);
       return launch_direct<false, 0, false, 896>(cb, cfg, wa, fa, ha, wio, n_sweeps, nullptr, 0);
