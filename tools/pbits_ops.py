@@ -36,6 +36,37 @@ frac = need.mean()
 B = eb.mean()
 # per 32-site word: neighbour classes 16, group prefix 10, per block 33 (Philox) + 4 planes x 4 (compare)
 ops_word = 16 + 10 * (eb > 0).mean() + B * (33 + 16)
+
+# Executed work of the direct walk (flip_band_run, DIRECT = 32): lane (band
+# bi, quad q) of a warp walks rows g*16 + 2 bi + h (h = 0, 1) and, per row,
+# words t = 4 q + k (k = 0..3) one after another; a warp runs a word's block
+# loop until its slowest lane is done, so word slot (h, k) costs the warp the
+# MAX over its 32 words of the blocks needed.  Per site: planes needed =
+# position of the first bit where u and K differ, P(> b planes) = 2^-b
+# (capped at 23); blocks = ceil(planes / 4).  Colour-split word t of row
+# (c, X): sites i = 16 b + t, b = 0..31, at column r = 2 i + ((c + X) & 1).
+rng = np.random.default_rng(1)
+lane_blocks, warp_blocks = [], []
+for X in (0, 1):
+    for c0 in range(0, m, 16):
+        for h in (0, 1):
+            for k in range(4):
+                words = []
+                for bi in range(8):
+                    c = c0 + 2 * bi + h
+                    for q in range(4):
+                        t = 4 * q + k
+                        cols = 2 * (16 * np.arange(32) + t) + ((c + X) & 1)
+                        words.append(need[:, c, cols])          # [R, 32 sites]
+                wd = np.stack(words, 1)                        # [R, 32 lanes, 32 sites]
+                planes = np.minimum(rng.geometric(0.5, size=wd.shape), 23)
+                blk = np.where(wd, (planes + 3) // 4, 0).max(-1)   # [R, 32 lanes]
+                lane_blocks.append(blk.mean())
+                warp_blocks.append(blk.max(-1).mean())
+lb, wb = float(np.mean(lane_blocks)), float(np.mean(warp_blocks))
 print(json.dumps({"replicas": R, "sweeps": SW, "frac_sites_needing_draw": round(float(frac), 4),
                   "blocks_per_word": round(float(B), 4), "ops_per_word": round(float(ops_word), 2),
-                  "ops_per_attempt": round(float(ops_word) / 32, 3)}))
+                  "ops_per_attempt": round(float(ops_word) / 32, 3),
+                  "executed": {"lane_mean_blocks_per_word": round(lb, 3), "warp_blocks_per_word_slot": round(wb, 3),
+                               "divergence_factor": round(wb / lb, 3),
+                               "block_loop_instr_per_word_slot (58 per block, SASS)": round(58 * wb, 1)}}))
