@@ -991,15 +991,44 @@ class Engine:
         sweeps_at, abs_m, energy = [], [], []
         start_attempts = self.attempts
         t0 = time.perf_counter()
+        points = []
         k = 0
         while k < n_sweeps:
-            nxt = min((k // measure_interval + 1) * measure_interval, n_sweeps)
-            self._sweeps(nxt - k)
-            k = nxt
-            sweeps_at.append(self.sweeps_done)
-            abs_m.append(self.abs_magnetization())
-            energy.append(self.energy_per_spin())
-        self._stream.synchronize()
+            k = min((k // measure_interval + 1) * measure_interval, n_sweeps)
+            points.append(k)
+        cls = type(self)
+        if points and cls.abs_magnetization is Engine.abs_magnetization and \
+                cls.energy_per_spin is Engine.energy_per_spin:
+            # Measurements stay on the device: each one is an msb_observe into
+            # its own row of a device buffer, enqueued behind its sweeps, and
+            # the host reads them all once at the end.  The sweeps never wait
+            # for the host (a synchronising measurement every 8 sweeps cost
+            # cfg2 11%, every sweep 57%).  The float64 expressions are those of
+            # abs_magnetization / energy_per_spin (engine.py:372-386).
+            torch = _torch()
+            with torch.cuda.device(self.device), torch.cuda.stream(self._stream):
+                obs = torch.zeros((len(points), 2, self.n_sim), dtype=torch.int64, device=self.device)
+            k = 0
+            for i, nxt in enumerate(points):
+                self._sweeps(nxt - k)
+                k = nxt
+                sweeps_at.append(self.sweeps_done)
+                self._push_host_edits()
+                call("msb_observe", ctypes.byref(self._g), _p(self._spins), _p(obs[i, 0]), _p(obs[i, 1]), self._cs)
+            self._stream.synchronize()
+            host = obs.cpu().numpy()
+            ups, unsat = host[:, 0, :], host[:, 1, :]
+            abs_m = np.abs(2.0 * ups / self.dims.sites - 1.0)
+            energy = -self.coupling * (2 * self.dims.sites - 2 * unsat) / self.dims.sites
+        else:  # overridden observables (reference test wrappers): called per measurement, as the reference
+            k = 0
+            for nxt in points:
+                self._sweeps(nxt - k)
+                k = nxt
+                sweeps_at.append(self.sweeps_done)
+                abs_m.append(self.abs_magnetization())
+                energy.append(self.energy_per_spin())
+            self._stream.synchronize()
         elapsed = time.perf_counter() - t0
         return Trajectory(
             sweeps=np.array(sweeps_at, dtype=np.int64),

@@ -4,7 +4,8 @@ import numpy as np
 import torch
 from paper_2404_16990_b200 import Engine, LatticeDims
 
-for interval in (100, 96, 1000):
+import sys
+for interval in [int(x) for x in (sys.argv[1:] or ["100", "96", "1000"])]:
     e = Engine(LatticeDims(1024, 1024), list(np.linspace(1.5, 3.5, 64)), 2024)
     e.run(16, measure_interval=8)          # warm: window init, lazy buffers
     torch.cuda.synchronize()
