@@ -6,11 +6,17 @@ import numpy as np
 import torch
 from paper_2404_16990_b200 import Engine, LatticeDims
 
-e = Engine(LatticeDims(1024, 1024), list(np.linspace(1.5, 3.5, 64)), 2024)
+import sys
+if "cfg3" in sys.argv:
+    TEMPS = list(np.random.default_rng(2024).uniform(2.0, 2.6, 754))
+    e = Engine(LatticeDims(512, 512), TEMPS, 2024, init="all-up")
+else:
+    TEMPS = list(np.linspace(1.5, 3.5, 64))
+    e = Engine(LatticeDims(1024, 1024), TEMPS, 2024)
 S = e.window
 nb = e.packed_nbytes()
 hb = [torch.empty(nb, dtype=torch.uint8, pin_memory=True) for _ in range(3)]
-ups = torch.empty(64, dtype=torch.int64, pin_memory=True); uns = torch.empty(64, dtype=torch.int64, pin_memory=True)
+ups = torch.empty(len(TEMPS), dtype=torch.int64, pin_memory=True); uns = torch.empty(len(TEMPS), dtype=torch.int64, pin_memory=True)
 e.store_packed(hb[0]); e.store_packed(hb[1])
 for k in range(4):
     e.step_packed(hb[k % 3], S, hb[(k + 2) % 3], ups, uns)
