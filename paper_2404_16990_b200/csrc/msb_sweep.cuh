@@ -20,6 +20,18 @@ constexpr int kSrcPbits = 3;    // counter-based Philox4x32-10, bit-plane form (
 // mapping is its own inverse, engine.py:326-330)
 __device__ __forceinline__ int t_of_k(int k) { return 4 * (k & 3) + (k >> 2); }
 
+// n = 512 window planes (FlipArgs::pk16): the planes of k (even) and k + 1,
+// t and t + 4 (t = t_of_k(k) in {0..3, 8..11}), share one plane word, and the
+// four pairs of each t-half are words 0..3 and 4..7 of the plane row: one
+// whole 32-byte sector per plane row, written in full by its piece (a sector
+// left half written, words {0..3, 8..11}, was evicted dirty with a byte mask
+// and read back by the ECC read-modify-write: 3 GB of DRAM reads per cfg3
+// launch).
+__device__ __forceinline__ int pk16_word(int k) {
+  const int t = t_of_k(k);
+  return t - ((t & 8) >> 1);
+}
+
 __device__ __forceinline__ size_t plane_off(const Geo& G, int np, int X, int p, int s, int lr) {
   return ((((size_t)X * np + p) * G.n_sim + s) * G.rows + lr) * G.Wp;
 }
@@ -100,15 +112,16 @@ struct FlipArgs {
   int band_h, band_gb;
   int band_sq, band_nseg;  // quads per row segment (divides 32), segments per row
   unsigned band_groups;    // groups per colour phase (all replicas)
-  // n = 512 window planes (pk16): the plane word of t in {0..3, 8..11} also
-  // holds plane t + 4 in its high half (the 32 draws of k and k + 1 are one
-  // producer run), so a quad of t0 = 4, 12 reads the words of t0 - 4, >> 16
+  // n = 512 window planes (pk16, pk16_word): plane word t - (t & 8) / 2 of t
+  // in {0..3, 8..11} also holds plane t + 4 in its high half (the 32 draws of
+  // k and k + 1 are one producer run), so a quad of t0 reads plane words
+  // (t0 & 8) / 2 .. + 3, the high halves for t0 = 4, 12
   int pk16;
   // n = 512 packed spin rows inside a window launch (pks, flip_band_run
   // PKS): word j of a row holds the sites of t = tl(j) (low half) and
   // tl(j) + 4 (high half), tl(j) = j (j < 4) or j + 4, of w = bit -- the
-  // pairing of the pk16 plane words, so plane word tl(j) gates word j
-  // without shifts.  The row keeps its 16-word pitch; words 0..7 are used.
+  // pairing of the pk16 plane words, so plane word j gates word j without
+  // shifts.  The row keeps its 16-word pitch; words 0..7 are used.
   int pks;
 };
 
@@ -177,7 +190,7 @@ __device__ __forceinline__ unsigned flip_quad_at(const FlipArgs& a, int s, int l
   uint4 P4 = make_uint4(0, 0, 0, 0), P8 = make_uint4(0, 0, 0, 0);
   if (!GENERIC) {
     const int sh = a.pk16 ? (t0 & 4) * 4 : 0;
-    const uint32_t* pq = pl - (a.pk16 ? (t0 & 4) : 0);
+    const uint32_t* pq = pl - (a.pk16 ? t0 - ((t0 & 8) >> 1) : 0);
     P4 = __ldg(reinterpret_cast<const uint4*>(pq));
     P8 = __ldg(reinterpret_cast<const uint4*>(pq + pstride));
     if (sh) {
@@ -365,12 +378,12 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
     // the plane rows; the row below wraps only past a whole lattice's last row
     const uint32_t* yrow = ybase + (unsigned)br0 * Wp;
     uint32_t* orow = a.spins + (s * 2u + (unsigned)X) * colour_words + (unsigned)br0 * Wp + w0;
-    // PK16 (n = 512 window planes, a.pk16): quads of t0 = 4, 12 take the high halves of the words of t0 - 4
+    // PK16 (n = 512 window planes, a.pk16): a quad of t0 reads plane words (t0 & 8) / 2 .., the high halves for t0 = 4, 12
     const bool phi = !PKS && PK16 && a.pk16 && (w0 & 4);
     const uint32_t* prow =
         DIRECT ? nullptr
                : a.planes + ((((unsigned)X * (unsigned)a.np) * (unsigned)G.n_sim + s) * (unsigned)G.rows + (unsigned)lr0) * Wp +
-                     (PKS ? 2 * w0 : PK16 && a.pk16 ? (w0 & ~4) : w0);
+                     (PKS ? w0 : PK16 && a.pk16 ? (w0 & 8) >> 1 : w0);
     uint32_t key4 = 0, key8 = 0;
     bool kuni = false;  // DIRECT: the warp's lanes share one pair of keys (bands of one replica)
     uint4* kt = nullptr;

@@ -509,8 +509,8 @@ __device__ __forceinline__ void win_produce(const WinArgs& a, const uint4* __res
             }
             // REJECT bits, newest draw in bit 0: reversed, bit i = draw i
             // packed planes (FlipArgs::pk16): t(k + 1) = t(k) + 4 rides in the high half
-            out[t_of_k(k)] = ~__brev(acc0);
-            out[pstride + t_of_k(k)] = ~__brev(acc1);
+            out[pk16_word(k)] = ~__brev(acc0);
+            out[pstride + pk16_word(k)] = ~__brev(acc1);
             if (!kJumpEnd) {
               jacc += 16;
               while (jacc >= a.kit) {
@@ -529,8 +529,8 @@ __device__ __forceinline__ void win_produce(const WinArgs& a, const uint4* __res
             const int k = w.k0 + kk;
             uint32_t acc[2];
             pbits_group<2>((pseg + (unsigned long long)k * 16) >> 5, pl, a.pk, key, 2, acc);
-            out[t_of_k(k)] = acc[0];  // packed planes, as above
-            out[pstride + t_of_k(k)] = acc[1];
+            out[pk16_word(k)] = acc[0];  // packed planes, as above
+            out[pstride + pk16_word(k)] = acc[1];
           }
           continue;
         }
