@@ -43,10 +43,13 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_outpu
 r = list(csv.reader(io.StringIO(out)))
 h, u, v = r[0], r[1], r[2]
 get = lambda k: float(v[h.index(k)])
-dur_us = get("gpu__time_duration.sum")
+dur_us = get("gpu__time_duration.sum") * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}[
+    u[h.index("gpu__time_duration.sum")]]
 rd, wr = get("dram__bytes_read.sum"), get("dram__bytes_write.sum")
-unit_rd = u[h.index("dram__bytes_read.sum")]
-scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit_rd]
+_sc = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+rd *= _sc[u[h.index("dram__bytes_read.sum")]]
+wr *= _sc[u[h.index("dram__bytes_write.sum")]]
+scale = 1
 insts = get("smsp__inst_executed.sum")
 cap = {
     "kernel": v[h.index("Kernel Name")], "duration_us_cold": dur_us,
