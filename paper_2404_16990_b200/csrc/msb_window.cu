@@ -54,9 +54,13 @@ int msb_default_window(const msb_geom* g, int32_t* S, int32_t* P) {
   if (!S || !P) return fail(MSB_ERR_ARG, "null output");
   long long np = 0;
   if (int r = check_window(g, 1, g && g->ghost ? 8 : 1, &np)) return r;
-  // S = 8 sweeps unless two window buffers would exceed 8 GiB of planes
+  // Whole lattices: S = 64 sweeps per window launch (fewer launches, jumps,
+  // start-up and tail costs per sweep: cfg2 0.934 -> 0.965 T, cfg3 0.936 ->
+  // 0.963 T at S = 32; end to end, one host round trip per 64 sweeps), slabs
+  // S = 8; halved while the two window buffers would exceed 8 GiB of planes
+  // (cfg3: S = 32, 6.3 GB).
   const long long slot_bytes = 4LL * (long long)slot_words(g);
-  int s = 8;
+  int s = g->ghost ? 8 : 64;
   while (s > 1 && 2LL * s * slot_bytes > (8LL << 30)) s >>= 1;
   *S = s;
   *P = msb_window_parts(g, s);

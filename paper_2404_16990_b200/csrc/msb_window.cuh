@@ -1199,7 +1199,8 @@ cudaLaunchConfig_t coop_config(unsigned grid, unsigned threads, size_t smem, voi
 // insensitive).  Producers are capped so the plane rows being written stay
 // L2-resident (see msb_window_parts).  MSB_FLIP_WARPS / MSB_PRODUCER_WARPS
 // override (tuning).
-int producer_warps(long long units, int ctas, int Wp, int P, bool produce, int count) {
+int producer_warps(long long units, int ctas, int Wp, int P, bool produce, int count, bool whole = false,
+                   int S = 8) {
   static const int env_pw = [] { const char* e = getenv("MSB_PRODUCER_WARPS"); return e ? atoi(e) : 0; }();
   static const int env_cw = [] { const char* e = getenv("MSB_FLIP_WARPS"); return e ? atoi(e) : 0; }();
   // bytes of plane rows a producer warp has open: 2 rows (planes) per row
@@ -1213,6 +1214,23 @@ int producer_warps(long long units, int ctas, int Wp, int P, bool produce, int c
     } else {
       const long long one_round = (units + ctas - 1) / ctas;  // producer warps per CTA for a single round
       int cw = one_round <= 30 ? (int)(32 - one_round) : 8;
+      if (one_round > 30 && whole) {
+        // Several rounds (whole lattices): the producers are ALU-bound, so a
+        // round of pw units per SM lasts ~pw unit-times and the window
+        // ~pw * ceil(units / (ctas pw)); take the pw in [24, 28] that
+        // minimises it.  Ties: 28 for long windows (the flip warps' per-launch
+        // work, the n = 512 row packing, is amortised; cfg3 at S = 32: 4 flip
+        // warps 0.963 T, 8: 0.951), 24 for short ones (S = 8: 8 flip warps
+        // 0.936, 4: 0.904).
+        long long best = -1;
+        for (int pw = 24; pw <= 28; pw++) {
+          const long long cost = (long long)pw * ((units + (long long)ctas * pw - 1) / ((long long)ctas * pw));
+          if (best < 0 || cost < best || (cost == best && S >= 16)) {
+            best = cost;
+            cw = 32 - pw;
+          }
+        }
+      }
       if (env_cw > 0) cw = std::min(28, env_cw);
       pwarps = std::min(cap, 32 - cw);
     }
@@ -1334,7 +1352,7 @@ int window_run(int nslabs, const msb_ring_slab* slabs, bool ring, int S, int P, 
                             fa, ha, wio, np))
       return e;
     if (int e = sm_count(&sms)) return e;
-    const int pwarps = producer_warps((np + 31) / 32, sms, fa.G.Wp, P, r.next != nullptr, count);
+    const int pwarps = producer_warps((np + 31) / 32, sms, fa.G.Wp, P, r.next != nullptr, count, !ha.on, S);
     if (ha.on) fit_band_h(fa, r.g);
     const int cb = chunk_width(wa.G);
     const bool pj = SRC == kSrcXoshiro && pwarps > 0;

@@ -227,6 +227,8 @@ class Engine:
         S, P = ctypes.c_int32(), ctypes.c_int32()
         call("msb_default_window", ctypes.byref(self._g), ctypes.byref(S), ctypes.byref(P))
         self.window, self._wP = int(S.value), int(P.value)
+        self._window_user = window is not None
+        self._window_default = self.window
         if window is not None:
             self.window = int(window)
             if not 1 <= self.window <= 64:
@@ -605,6 +607,34 @@ class Engine:
         fewer than 2^31 / 32 chunks (make_win_io, msb_window.cuh)."""
         chunks = self.n_sim * self.dims.m * -(-self.dims.n // 1024)
         return (self.dims.m * -(-self.dims.n // 1024)) % 4 == 0 and 32 * chunks < (1 << 31)
+
+    def _fit_window(self, interval: int, n_sweeps: int) -> None:
+        """Window length for measurements every `interval` sweeps (unless the
+        caller chose the window).  A measurement that falls inside a window
+        splits it, and the launch flipping the remainder runs without
+        production, outside the producers' shadow.  So take the longest power
+        of two in [8, default] whose remainder is at most 1/16 of the
+        interval (cfg2: interval 8 at S = 64 0.75 T, at S = 8 0.92; 100 at S
+        = 64 0.87-0.91, at S = 32 0.92), and start the run on a window
+        boundary when measurements would otherwise fall inside windows all
+        along it.  Powers of two keep the producer units in whole rounds on
+        148 SMs; the sweeps do not depend on the window."""
+        if self._window_user or not self._window_route() or self._direct_ok():
+            return
+        S = self._window_default
+        if S >= 8:
+            while S > 8 and interval % S > interval / 16:
+                S //= 2
+        if S != self.window:
+            P = int(_lib.lib().msb_window_parts(ctypes.byref(self._g), S))
+            if P <= 0:
+                return
+            self.window, self._wP = S, P
+            self._wbuf = None
+            self._wvalid = False
+            self.__dict__.pop("_io_fused", None)  # its producer-round rule depends on the window
+        elif self._wvalid and self._wc and interval % S == 0 and n_sweeps >= 2 * S:
+            self._wvalid = False  # realign: the window restarts at the next sweep
 
     def _win_launch(self, first: int, count: int, produce: bool, io=None) -> None:
         states, planes, words, jump = self._wbuf
@@ -996,6 +1026,7 @@ class Engine:
         while k < n_sweeps:
             k = min((k // measure_interval + 1) * measure_interval, n_sweeps)
             points.append(k)
+        self._fit_window(measure_interval, n_sweeps)
         cls = type(self)
         if points and cls.abs_magnetization is Engine.abs_magnetization and \
                 cls.energy_per_spin is Engine.energy_per_spin:

@@ -30,7 +30,8 @@ def test_two_ranks_cfg2_weak():
     d = _bench("--gpus", "2", "--steps", "3", "--warmup", "3", "--no-cpu", "--no-alt")
     assert d["n_gpus"] == 2 and d["steps"] == 3 and "test_mode" in d
     assert d["config"]["global_replicas"] == 128 and d["config"]["replicas_rank0"] == 64
-    assert d["config"]["attempts_per_step"] == 2 * 64 * 1024 * 1024 * 8  # summed over ranks
+    S = d["config"]["sweeps_per_step"]
+    assert d["config"]["attempts_per_step"] == 2 * 64 * 1024 * 1024 * S  # summed over ranks
     assert d["value"] > 0 and d["e2e"]["value"] > 0 and "cpu_baseline" not in d
 
 
@@ -38,4 +39,4 @@ def test_two_ranks_cfg3_split():
     d = _bench("--gpus", "2", "--config", "cfg3", "--steps", "2", "--warmup", "3", "--no-cpu", "--no-alt")
     assert d["n_gpus"] == 2 and d["scaling"] == "strong"
     assert d["config"]["global_replicas"] == 754 and d["config"]["replicas_rank0"] == 377
-    assert d["config"]["attempts_per_step"] == 754 * 512 * 512 * 8
+    assert d["config"]["attempts_per_step"] == 754 * 512 * 512 * d["config"]["sweeps_per_step"]

@@ -78,8 +78,9 @@ def test_engine_paths_stay_in_bounds(guard, m, n, n_sim, stream):
     temps = list(np.linspace(1.7, 3.1, n_sim))
     e = Engine(LatticeDims(m, n), temps, 9, sim_offset=4, stream=stream)
     o = orc.OracleEngine(m, n, temps, 9, sim_offset=4, stream=stream)
-    e.run(e.window + 3, measure_interval=2)            # windows / direct launches, partial and full
-    o.sweep(e.window + 3)
+    k = e.window + 3
+    e.run(k, measure_interval=2)                       # windows / direct launches, partial and full
+    o.sweep(k)
     e.flip_red()                                       # per-phase kernels
     e.flip_blue()
     o.sweep(1)

@@ -56,10 +56,12 @@ def test_cfg2_full_size():
 
 def test_cfg2_1000_sweeps_trajectory():
     """cfg2 exactly as BASELINE states it: 64 x 1024^2, 1000 sweeps through
-    the public Engine.run(1000, measure_interval=100) -- 125 full windows in
-    steady state, including every inter-window jump -- against the oracle
-    (16-thread C): final lattices, flips, and |M| and E/N of every replica at
-    every measurement, as float64 bit patterns."""
+    the public Engine.run(1000, measure_interval=100) -- windows of 32 (the
+    run's choice for that interval), full and split at the measurements, with
+    every inter-window jump -- and again through 1000 sweeps measured every
+    1000 (windows of 64), against the oracle (16-thread C): final lattices,
+    flips, and |M| and E/N of every replica at every measurement, as float64
+    bit patterns."""
     from oracle import oracle as orc
     from paper_2404_16990_b200 import Engine, LatticeDims
     temps = list(np.linspace(1.5, 3.5, 64))
@@ -72,6 +74,14 @@ def test_cfg2_1000_sweeps_trajectory():
     assert np.array_equal(traj.energy.view(np.uint64), np.asarray(en).view(np.uint64))
     assert e.flips == o.flips
     assert e.attempts == 64 * 1024 * 1024 * 1000
+    _same_rows(e.lattices, o.spins)
+    assert e.window == 32
+    traj = e.run(1000, measure_interval=1000)  # windows of 64 from a realigned start
+    sw, am, en = o.run(1000, 1000)
+    assert e.window == 64 and traj.sweeps.tolist() == list(sw) == [2000]
+    assert np.array_equal(traj.abs_m.view(np.uint64), np.asarray(am).view(np.uint64))
+    assert np.array_equal(traj.energy.view(np.uint64), np.asarray(en).view(np.uint64))
+    assert e.flips == o.flips
     _same_rows(e.lattices, o.spins)
 
 
