@@ -3,9 +3,10 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2|cfg3|cfg4|cfg5]
 
-One step = one lookahead window: S = 8 full checkerboard sweeps of every
-replica a GPU holds, executed as ONE cooperative k_win launch (the flips of
-these S sweeps + the accept planes of the next S, the reference's
+One step = one lookahead window: S full checkerboard sweeps of every
+replica a GPU holds (the engine's default window: 64 for cfg2, 32 for cfg3
+under its plane-memory cap), executed as ONE cooperative k_win launch (the
+flips of these S sweeps + the accept planes of the next S, the reference's
 xoshiro256++ streams).  Default workload (BASELINE.json configs[1], "cfg2"):
 64 independent replicas of a 1024x1024 periodic lattice per GPU, J=1, h=0,
 T = linspace(1.5, 3.5, 64), random initial spins from seed.  With N GPUs

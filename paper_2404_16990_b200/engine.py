@@ -4,8 +4,9 @@ Same constructor, methods, attributes, counters and error behaviour as the
 reference engine (pkg/src/multispin/engine.py:216-492), but the spins live
 on the GPU in a colour-split bit layout and the sweeps run as sm_100a
 kernels (libmsb200, include/msb200.h).  Steady state (``run`` / ``_sweeps``
-with FERRO/ANTI tables): lookahead windows, ONE cooperative launch per S = 8
-sweeps in which producer warps turn the next window's reference xoshiro256++
+with FERRO/ANTI tables): lookahead windows, ONE cooperative launch per
+window of S sweeps (64 by default for whole lattices; ``run`` fits it to its
+measurement interval) in which producer warps turn the next window's reference xoshiro256++
 draws into accept bit planes while the other warps flip this window's
 sweeps with bit-sliced neighbour logic (msb_window_sweep); the bit-plane
 counter stream flips without planes (msb_direct_sweep).  ``flip_red`` /
