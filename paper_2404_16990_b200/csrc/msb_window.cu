@@ -57,10 +57,10 @@ int msb_default_window(const msb_geom* g, int32_t* S, int32_t* P) {
   // Whole lattices: S = 64 sweeps per window launch (fewer launches, jumps,
   // start-up and tail costs per sweep: cfg2 0.934 -> 0.965 T, cfg3 0.936 ->
   // 0.963 T at S = 32; end to end, one host round trip per 64 sweeps), slabs
-  // S = 8; halved while the two window buffers would exceed 8 GiB of planes
+  // S = 32; halved while the two window buffers would exceed 8 GiB of planes
   // (cfg3: S = 32, 6.3 GB).
   const long long slot_bytes = 4LL * (long long)slot_words(g);
-  int s = g->ghost ? 8 : 64;
+  int s = g->ghost ? 32 : 64;  // slabs: cfg4 S = 8 0.940, 16 0.955, 32 0.958 T (ring of 8: 0.853, 0.872, 0.877)
   while (s > 1 && 2LL * s * slot_bytes > (8LL << 30)) s >>= 1;
   *S = s;
   *P = msb_window_parts(g, s);
