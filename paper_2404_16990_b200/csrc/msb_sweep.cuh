@@ -68,6 +68,12 @@ constexpr int kRngThreads = 1024;
 #define MSB_CHUNK_UNROLL 4  // measured: 4 beats 8, 16 (-1.4%), 2 and 32 (spills)
 #endif
 constexpr int kChunkUnroll = MSB_CHUNK_UNROLL;
+// The window producer's 32-draw chunks (n/32 % 32 == 0): unrolled 8 since
+// the jump moved after the draws (cfg2 0.966 -> 0.970 T; 16: 0.967)
+#ifndef MSB_CHUNK_UNROLL32
+#define MSB_CHUNK_UNROLL32 8
+#endif
+constexpr int kChunkUnroll32 = MSB_CHUNK_UNROLL32;
 
 // Work counters (caller-owned, zeroed once, left zeroed by every kernel):
 //   work[0] next dynamic producer unit    work[1] consumer barrier arrivals

@@ -342,7 +342,7 @@ __device__ __forceinline__ void win_segment_k(const WinArgs& a, XState& st, cons
     uint32_t acc0 = 0, acc1 = 0;
     if (SRC == kSrcXoshiro) {
       if (L == 32) {
-#pragma unroll kChunkUnroll
+#pragma unroll kChunkUnroll32
         for (int i = 0; i < 32; i++) {
           const uint32_t h9 = xstep(st) << 9;
           acc_reject(acc0, h9, key0);
