@@ -875,6 +875,8 @@ class Engine:
         if (ups_out is None) != (unsat_out is None):
             raise ValueError("ups_out and unsat_out go together")
         n_sweeps = int(n_sweeps)
+        if n_sweeps > 0:
+            self._fit_window(n_sweeps, 0)  # windows that end where the steps end
         self._push_host_edits()
         src = self._packed_src(src)
         if dst is not None and dst.numel() * dst.element_size() != self.packed_nbytes():
