@@ -576,6 +576,216 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
   return cnt;
 }
 
+// Direct sweeps, split form (whole lattices, single-segment rows, bands of 2
+// rows, 32-draw words; PKS: n = 512 packed rows).  flip_band_run<DIRECT>
+// resolves each word's tests inside its walk: the block loop of a word runs
+// as long as the slowest lane of the warp needs planes (3.1 blocks per word
+// slot against a lane mean of 1.9), next to the walk's live neighbour words.
+// Here one band group's colour phase is three passes over a per-warp stash in
+// shared memory (kSplitWords words per warp):
+//   1. classify: each lane's 8 words (2 rows x 4) -> (>= 2 disagreeing
+//      neighbours, exactly one) masks into the stash; no draws;
+//   2. resolve: per word slot, Philox blocks 0 and 1 for every lane (8
+//      planes: warp-uniform, nothing but the stash live); the ~9% of words
+//      with tests still open are queued as (lane, slot);
+//   3. tail: the queued words one per lane (blocks 2..5, rarely more than
+//      one), accepted bits ORed into the owner's stash slot;
+// then each lane XORs its 8 flip words into its rows.
+constexpr int kSplitWords = 3 * 256 + 64;  // A (sure flips -> flips), B (Delta E = 4|J| sites), C (open tests), queue
+
+template <bool PKS>
+__device__ __forceinline__ unsigned direct_group_split(const FlipArgs& a, unsigned g, int X, const PbitsDirect& dp,
+                                                       uint32_t* st, int& kt_s) {
+  const Geo& G = a.G;
+  const int lane = threadIdx.x & 31;
+  const int sq = a.band_sq, gb = a.band_gb;
+  const int lsq = __ffs(sq) - 1;
+  const int bi = lane >> lsq, q = lane & (sq - 1), base = lane - q;
+  const unsigned Wp = (unsigned)G.Wp, colour_words = (unsigned)G.R * Wp;
+  const unsigned gps = (unsigned)G.rows / (unsigned)(gb * 2);
+  const unsigned s = g / gps;
+  const int lrg = (int)(g - s * gps) * gb * 2;  // the group's first row
+  const int lr0 = lrg + bi * 2;
+  const int ch = q >> 2, w0 = q * 4;
+  const int vb = chunk_bits(G, ch), lastbits = chunk_bits(G, G.nch - 1);
+  const uint32_t vm = PKS ? 0xFFFFFFFFu : chunk_mask(G, ch);
+  uint32_t* A = st;
+  uint32_t* B = st + 256;
+  uint32_t* C = st + 512;
+  unsigned char* Q = reinterpret_cast<unsigned char*>(st + 768);
+  // key masks of the group's replica (per warp, rebuilt when the replica changes)
+  uint4(*kmt)[12] = direct_key_tables();
+  const uint4* kt = kmt[threadIdx.x >> 5];
+  const uint32_t key4 = dp.thr9[s], key8 = dp.thr9[G.n_sim + s];
+  if (kt_s != (int)s) {
+    __syncwarp();
+    if (lane < 24) {
+      uint32_t* t = reinterpret_cast<uint32_t*>(kmt[threadIdx.x >> 5]);
+      t[(lane >> 2) * 8 + (lane & 3)] = key_mask(key4, lane);
+      t[(lane >> 2) * 8 + 4 + (lane & 3)] = key_mask(key8, lane);
+    }
+    kt_s = (int)s;
+  }
+  // --- 1. classify ---
+  const int s_next = base + ((q + 1) & (sq - 1)), s_first = base + (q & ~3), s_last = base + (q | 3),
+            s_prev = base + ((q + sq - 1) & (sq - 1));
+  const bool chunk_last = (q & 3) == 3, chunk_first = (q & 3) == 0;
+  const uint32_t* ybase = a.spins + (s * 2u + (unsigned)(1 - X)) * colour_words + w0;
+  uint32_t* orow = a.spins + (s * 2u + (unsigned)X) * colour_words + (unsigned)(lr0 + G.ghost) * Wp + w0;
+  {
+    const int br0 = lr0 + G.ghost;
+    int bu, bd;
+    vert_rows(G, br0, bu, bd);
+    auto ld4 = [](const uint32_t* p) { return __ldcg(reinterpret_cast<const uint4*>(p)); };
+    const uint4 U = ld4(ybase + (unsigned)bu * Wp), Y0 = ld4(ybase + (unsigned)br0 * Wp),
+                Y1 = ld4(ybase + (unsigned)(br0 + 1) * Wp),
+                D1 = ld4(br0 + 2 < G.R ? ybase + (unsigned)(br0 + 2) * Wp : ybase);
+    const uint4 O0 = *reinterpret_cast<const uint4*>(orow), O1 = *reinterpret_cast<const uint4*>(orow + Wp);
+    auto classify = [&](auto PC, const uint4& Uq, const uint4& Yq, const uint4& Dq, const uint4& Oq, int slot0) {
+      constexpr int P = decltype(PC)::value;
+      uint32_t edge;
+      if (PKS) {
+        if (P) {
+          const uint32_t xa = __shfl_sync(0xFFFFFFFFu, Yq.x, s_next);
+          const uint32_t other = q == 0 ? xa : (((xa & 0xFFFFu) >> 1) | ((xa & 1u) << 15));
+          edge = (Yq.x >> 16) | (other << 16);
+        } else {
+          const uint32_t h = __shfl_sync(0xFFFFFFFFu, Yq.w, s_prev) >> 16;
+          const uint32_t other = q == 0 ? (((h << 1) | (h >> 15)) & 0xFFFFu) : h;
+          edge = other | (Yq.w << 16);
+        }
+      } else if (P) {
+        const uint32_t xa = __shfl_sync(0xFFFFFFFFu, Yq.x, s_next);
+        const uint32_t xb = __shfl_sync(0xFFFFFFFFu, Yq.x, s_first);
+        edge = chunk_last ? ((xb >> 1) | ((xa & 1u) << (vb - 1))) : xa;
+      } else {
+        const uint32_t wa = __shfl_sync(0xFFFFFFFFu, Yq.w, s_prev);
+        const uint32_t wb = __shfl_sync(0xFFFFFFFFu, Yq.w, s_last);
+        const uint32_t carry = ch > 0 ? (wa >> 31) : ((wa >> (lastbits - 1)) & 1u);
+        edge = chunk_first ? (((wb << 1) | carry) & vm) : wa;
+      }
+      const uint32_t y[4] = {Yq.x, Yq.y, Yq.z, Yq.w}, o[4] = {Oq.x, Oq.y, Oq.z, Oq.w};
+      const uint32_t u4[4] = {Uq.x, Uq.y, Uq.z, Uq.w}, d4[4] = {Dq.x, Dq.y, Dq.z, Dq.w};
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const uint32_t n4 = P ? (k < 3 ? y[k + 1] : edge) : (k > 0 ? y[k - 1] : edge);
+        const uint32_t ow = o[k] ^ a.inv;
+        const uint32_t x1 = u4[k] ^ ow, x2 = d4[k] ^ ow, x3 = y[k] ^ ow;
+        const uint32_t x4 = a.fault ? 0u : (n4 ^ ow);
+        const uint32_t o12 = x1 | x2, a12 = x1 & x2, o34 = x3 | x4, a34 = x3 & x4;
+        const uint32_t ge2 = a12 | a34 | (o12 & o34);
+        A[(slot0 + k) * 32 + lane] = ge2 & vm;
+        B[(slot0 + k) * 32 + lane] = (o12 | o34) & ~ge2;
+      }
+    };
+    using P0 = std::integral_constant<int, 0>;
+    using P1 = std::integral_constant<int, 1>;
+    if ((G.row0 + lr0 + X) & 1) {  // warp-uniform
+      classify(P1(), U, Y0, Y1, O0, 0);
+      classify(P0(), Y0, Y1, D1, O1, 4);
+    } else {
+      classify(P0(), U, Y0, Y1, O0, 0);
+      classify(P1(), Y0, Y1, D1, O1, 4);
+    }
+  }
+  __syncwarp();  // the key table, and (same lane) the stash
+  // --- 2. resolve: blocks 0 and 1 of every word slot ---
+  const unsigned long long nn = (unsigned long long)G.n;
+  const unsigned long long dphase = dp.blk * 2 * nn;
+  const unsigned dstep = 4u * (unsigned)G.words;
+  const unsigned long long simbase = ((unsigned long long)G.sim_offset + s) * (unsigned long long)(G.m / 4);
+  const uint32_t ltmask = (1u << lane) - 1u;
+  unsigned qn = 0;
+#pragma unroll 1
+  for (int h = 0; h < 2; h++) {
+    const RowStream rs = row_stream(G.m, G.row0 + lr0 + h, X);
+    const unsigned long long sid = simbase + (unsigned long long)(rs.gamma - 1);
+    const PbitsLane L = pbits_lane((uint32_t)sid, (uint32_t)(sid >> 32));
+    unsigned long long d = dphase + (unsigned long long)((unsigned)rs.q * (unsigned)(G.n / 2) + 32u * (unsigned)ch +
+                                                         (unsigned)(PKS ? w0 >> 1 : (w0 & 15) >> 2) * (unsigned)G.words);
+#pragma unroll 1
+    for (int kk = 0; kk < 4; kk++, d += dstep) {
+      const int k = h * 4 + kk;
+      const uint32_t sure = A[k * 32 + lane], c4 = B[k * 32 + lane];
+      uint32_t und = ~sure & vm, acc = 0;
+      if (key4 == kKeyAlways) { acc |= und & c4; und &= ~c4; }
+      else if (key4 == 0u) und &= ~c4;
+      if (key8 == kKeyAlways) { acc |= und & ~c4; und &= c4; }
+      else if (key8 == 0u) und &= c4;
+      if (__any_sync(0xFFFFFFFFu, und != 0u)) {
+        const PbitsPrefix f = pbits_prefix(d >> 5, L, dp.pk);
+#pragma unroll 1
+        for (int j = 0; j < 2; j++) {
+          uint32_t xs[4];
+          pbits_block(f, j, dp.pk, xs);
+          const uint4 ma = kt[2 * j], mb = kt[2 * j + 1];
+          const uint32_t m4[4] = {ma.x, ma.y, ma.z, ma.w}, m8[4] = {mb.x, mb.y, mb.z, mb.w};
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            const uint32_t km = (c4 & m4[e]) | (~c4 & m8[e]);
+            acc |= und & ~xs[e] & km;
+            und &= ~(xs[e] ^ km);
+          }
+        }
+        const uint32_t open = __ballot_sync(0xFFFFFFFFu, und != 0u);
+        if (und) {
+          C[k * 32 + lane] = und;
+          Q[qn + __popc(open & ltmask)] = (unsigned char)(lane | (k << 5));
+        }
+        qn += __popc(open);
+      }
+      A[k * 32 + lane] = sure | acc;
+    }
+  }
+  // --- 3. tail: the words with tests still open after 8 planes, one per lane ---
+  if (qn) {
+    __syncwarp();
+    for (unsigned i = lane; i < qn; i += 32) {
+      const unsigned e = Q[i], sl = e & 31u, k = e >> 5;
+      uint32_t und = C[k * 32 + sl];
+      const uint32_t c4 = B[k * 32 + sl];
+      const int q2 = (int)(sl & (unsigned)(sq - 1)), w02 = q2 * 4;
+      const int row = lrg + (int)(sl >> lsq) * 2 + (int)(k >> 2);
+      const RowStream rs = row_stream(G.m, G.row0 + row, X);
+      const unsigned long long sid = simbase + (unsigned long long)(rs.gamma - 1);
+      const PbitsLane L = pbits_lane((uint32_t)sid, (uint32_t)(sid >> 32));
+      const unsigned long long d =
+          dphase + (unsigned long long)((unsigned)rs.q * (unsigned)(G.n / 2) + 32u * (unsigned)(q2 >> 2) +
+                                        (unsigned)(PKS ? w02 >> 1 : (w02 & 15) >> 2) * (unsigned)G.words +
+                                        (k & 3u) * dstep);
+      const PbitsPrefix f = pbits_prefix(d >> 5, L, dp.pk);
+      uint32_t acc = 0;
+#pragma unroll 1
+      for (int j = 2; j < 6 && und; j++) {
+        uint32_t xs[4];
+        pbits_block(f, j, dp.pk, xs);
+        const uint4 ma = kt[2 * j], mb = kt[2 * j + 1];
+        const uint32_t m4[4] = {ma.x, ma.y, ma.z, ma.w}, m8[4] = {mb.x, mb.y, mb.z, mb.w};
+#pragma unroll
+        for (int e2 = 0; e2 < 4; e2++) {
+          const uint32_t km = (c4 & m4[e2]) | (~c4 & m8[e2]);
+          const uint32_t live = (j < 5 || e2 < 3) ? und : 0u;  // plane 23 does not exist
+          acc |= live & ~xs[e2] & km;
+          und &= ~(live & (xs[e2] ^ km));
+        }
+      }
+      if (acc) A[k * 32 + sl] |= acc;
+    }
+    __syncwarp();
+  }
+  // --- flips into the rows ---
+  unsigned cnt = 0;
+#pragma unroll
+  for (int h = 0; h < 2; h++) {
+    const uint4 O = *reinterpret_cast<const uint4*>(orow + h * Wp);
+    const uint32_t f0 = A[(h * 4 + 0) * 32 + lane], f1 = A[(h * 4 + 1) * 32 + lane], f2 = A[(h * 4 + 2) * 32 + lane],
+                   f3 = A[(h * 4 + 3) * 32 + lane];
+    cnt += __popc(f0) + __popc(f1) + __popc(f2) + __popc(f3);
+    *reinterpret_cast<uint4*>(orow + h * Wp) = make_uint4(O.x ^ f0, O.y ^ f1, O.z ^ f2, O.w ^ f3);
+  }
+  return cnt;
+}
+
 template <bool COHERENT, bool PUSH = false>
 __device__ __forceinline__ unsigned flip_run(const FlipArgs& a, unsigned i0, unsigned i1, int X) {
   const Geo& G = a.G;

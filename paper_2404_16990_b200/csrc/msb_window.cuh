@@ -719,6 +719,13 @@ __device__ __forceinline__ void win_export(const Geo& G, const uint32_t* spins, 
 // (1.99 T) against 768 (1.54 T) and 512 (1.68 T): with fewer warps the
 // band groups no longer spread one per warp, which costs more than the
 // 64-register cap's spills.
+// Direct sweeps of single-segment whole lattices in the split form
+// (direct_group_split, msb_sweep.cuh).
+#ifndef MSB_DIRECT_SPLIT
+#define MSB_DIRECT_SPLIT 1
+#endif
+constexpr bool kDirectSplit = MSB_DIRECT_SPLIT != 0;
+
 #ifndef MSB_DIRECT_THREADS
 #define MSB_DIRECT_THREADS 1024
 #endif
@@ -847,6 +854,7 @@ __device__ __forceinline__ void win_body(const WinArgs& wa, const FlipArgs& fa0,
       constexpr bool kPksD = CB == 16 && DIRECT == 32;
       const bool pksd = kPksD && fa0.pks;
       unsigned nb = 0;
+      int kt_s = -1;  // replica whose key masks the warp's table holds (direct_group_split)
       if (pksd) {
         pack_rows<false>(fa0.spins, nrows, ct, nct);
         consumer_barrier(wa.work + 1, base + vgrid * ++nb, nwc * 32, leader);
@@ -859,6 +867,11 @@ __device__ __forceinline__ void win_body(const WinArgs& wa, const FlipArgs& fa0,
         dp.blk = wa.block0 + 2ull * (unsigned)(first + (i >> 1)) + (unsigned)X;
         for (unsigned g = lo; g < hi; g++) {
           if (i > 0) group_wait(gflags, g, gps, fbase + (unsigned)i);
+          if constexpr (kDirectSplit && DIRECT == 32) {
+            uint32_t* st = reinterpret_cast<uint32_t*>(jt) + (size_t)warp * kSplitWords;
+            if (kPksD && pksd) cnt += direct_group_split<kPksD>(fa, g, X, dp, st, kt_s);
+            else cnt += direct_group_split<false>(fa, g, X, dp, st, kt_s);
+          } else
           if (kPksD && pksd) cnt += flip_band_run<true, false, false, DIRECT, true, NoHooks, false, kPksD>(fa, g, g + 1, X, &dp);
           else if (i == 0 && !pro) cnt += flip_band_run<false, false, false, DIRECT>(fa, g, g + 1, X, &dp);
           else cnt += flip_band_run<true, false, false, DIRECT>(fa, g, g + 1, X, &dp);
@@ -1418,6 +1431,7 @@ int direct_run_impl(int nslabs, const msb_ring_slab* slabs, bool ring, int n_swe
     if (int e = sm_count(&sms)) return e;
     cudaLaunchAttribute attr[1];
     cudaLaunchConfig_t cfg = coop_config((unsigned)sms, kDirectThreads, 0, stream, attr, true);
+    if (kDirectSplit) cfg.dynamicSmemBytes = (size_t)(kDirectThreads / 32) * kSplitWords * 4;  // the warps' stashes
     if (ha.on) return launch_direct<true, 2, false, 0>(cb, cfg, wa, fa, ha, wio, n_sweeps, nullptr, 0);
     // rows in several segments: the general group order (flags) or grid barriers
     if (fa.band_nseg > 1) {
