@@ -594,24 +594,22 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
 constexpr int kSplitWords = 3 * 256 + 64;  // A (sure flips -> flips), B (Delta E = 4|J| sites), C (open tests), queue
 
 template <bool PKS>
-__device__ __forceinline__ unsigned direct_group_split(const FlipArgs& a, unsigned g, int X, const PbitsDirect& dp,
-                                                       uint32_t* st, int& kt_s) {
+__device__ __forceinline__ unsigned direct_group_split(const FlipArgs& a, unsigned g, unsigned s, unsigned l, int X,
+                                                       const PbitsDirect& dp, uint32_t* st, int& kt_s) {
   const Geo& G = a.G;
   const int lane = threadIdx.x & 31;
   const int sq = a.band_sq, gb = a.band_gb;
   const int lsq = __ffs(sq) - 1;
   const int bi = lane >> lsq, q = lane & (sq - 1), base = lane - q;
   const unsigned Wp = (unsigned)G.Wp, colour_words = (unsigned)G.R * Wp;
-  const unsigned gps = (unsigned)G.rows / (unsigned)(gb * 2);
-  const unsigned s = g / gps;
-  const int lrg = (int)(g - s * gps) * gb * 2;  // the group's first row
+  const int lrg = (int)l * gb * 2;  // the group's first row (band l of replica s)
   const int lr0 = lrg + bi * 2;
   const int ch = q >> 2, w0 = q * 4;
   const int vb = chunk_bits(G, ch), lastbits = chunk_bits(G, G.nch - 1);
   const uint32_t vm = PKS ? 0xFFFFFFFFu : chunk_mask(G, ch);
-  uint32_t* A = st;
-  uint32_t* B = st + 256;
-  uint32_t* C = st + 512;
+  uint32_t* A = st + lane;        // [slot][lane]: sure flips -> flips
+  uint32_t* B = st + 256 + lane;  // Delta E = 4|J| sites
+  uint32_t* C = st + 512 + lane;  // open tests
   unsigned char* Q = reinterpret_cast<unsigned char*>(st + 768);
   // key masks of the group's replica (per warp, rebuilt when the replica changes)
   uint4(*kmt)[12] = direct_key_tables();
@@ -626,12 +624,17 @@ __device__ __forceinline__ unsigned direct_group_split(const FlipArgs& a, unsign
     }
     kt_s = (int)s;
   }
+  // keys that need no draw (K = 2^23: always, K = 0: never), as masks
+  const bool special = key4 == kKeyAlways || key4 == 0u || key8 == kKeyAlways || key8 == 0u;
+  const uint32_t al4 = key4 == kKeyAlways ? ~0u : 0u, al8 = key8 == kKeyAlways ? ~0u : 0u;
+  const uint32_t dc4 = (key4 == kKeyAlways || key4 == 0u) ? ~0u : 0u, dc8 = (key8 == kKeyAlways || key8 == 0u) ? ~0u : 0u;
   // --- 1. classify ---
   const int s_next = base + ((q + 1) & (sq - 1)), s_first = base + (q & ~3), s_last = base + (q | 3),
             s_prev = base + ((q + sq - 1) & (sq - 1));
   const bool chunk_last = (q & 3) == 3, chunk_first = (q & 3) == 0;
   const uint32_t* ybase = a.spins + (s * 2u + (unsigned)(1 - X)) * colour_words + w0;
   uint32_t* orow = a.spins + (s * 2u + (unsigned)X) * colour_words + (unsigned)(lr0 + G.ghost) * Wp + w0;
+  uint32_t anyund = 0;
   {
     const int br0 = lr0 + G.ghost;
     int bu, bd;
@@ -674,8 +677,16 @@ __device__ __forceinline__ unsigned direct_group_split(const FlipArgs& a, unsign
         const uint32_t x4 = a.fault ? 0u : (n4 ^ ow);
         const uint32_t o12 = x1 | x2, a12 = x1 & x2, o34 = x3 | x4, a34 = x3 & x4;
         const uint32_t ge2 = a12 | a34 | (o12 & o34);
-        A[(slot0 + k) * 32 + lane] = ge2 & vm;
-        B[(slot0 + k) * 32 + lane] = (o12 | o34) & ~ge2;
+        const uint32_t c4 = (o12 | o34) & ~ge2;
+        uint32_t sure = ge2 & vm, und = ~ge2 & vm;
+        if (special) {  // warp-uniform
+          sure |= und & ((c4 & al4) | (~c4 & al8));
+          und &= ~((c4 & dc4) | (~c4 & dc8));
+        }
+        A[(slot0 + k) * 32] = sure;
+        B[(slot0 + k) * 32] = c4;
+        C[(slot0 + k) * 32] = und;
+        anyund |= und;
       }
     };
     using P0 = std::integral_constant<int, 0>;
@@ -688,33 +699,32 @@ __device__ __forceinline__ unsigned direct_group_split(const FlipArgs& a, unsign
       classify(P1(), Y0, Y1, D1, O1, 4);
     }
   }
-  __syncwarp();  // the key table, and (same lane) the stash
-  // --- 2. resolve: blocks 0 and 1 of every word slot ---
+  __syncwarp();  // the key table
   const unsigned long long nn = (unsigned long long)G.n;
   const unsigned long long dphase = dp.blk * 2 * nn;
   const unsigned dstep = 4u * (unsigned)G.words;
   const unsigned long long simbase = ((unsigned long long)G.sim_offset + s) * (unsigned long long)(G.m / 4);
-  const uint32_t ltmask = (1u << lane) - 1u;
-  unsigned qn = 0;
+  if (__any_sync(0xFFFFFFFFu, anyund != 0u)) {
+    // --- 2. resolve: blocks 0 and 1 of every word slot (no control flow
+    // inside a row, so the slots' Philox chains interleave) ---
+    uint32_t om = 0;  // this lane's slots with tests still open
 #pragma unroll 1
-  for (int h = 0; h < 2; h++) {
-    const RowStream rs = row_stream(G.m, G.row0 + lr0 + h, X);
-    const unsigned long long sid = simbase + (unsigned long long)(rs.gamma - 1);
-    const PbitsLane L = pbits_lane((uint32_t)sid, (uint32_t)(sid >> 32));
-    unsigned long long d = dphase + (unsigned long long)((unsigned)rs.q * (unsigned)(G.n / 2) + 32u * (unsigned)ch +
-                                                         (unsigned)(PKS ? w0 >> 1 : (w0 & 15) >> 2) * (unsigned)G.words);
-#pragma unroll 1
-    for (int kk = 0; kk < 4; kk++, d += dstep) {
-      const int k = h * 4 + kk;
-      const uint32_t sure = A[k * 32 + lane], c4 = B[k * 32 + lane];
-      uint32_t und = ~sure & vm, acc = 0;
-      if (key4 == kKeyAlways) { acc |= und & c4; und &= ~c4; }
-      else if (key4 == 0u) und &= ~c4;
-      if (key8 == kKeyAlways) { acc |= und & ~c4; und &= c4; }
-      else if (key8 == 0u) und &= c4;
-      if (__any_sync(0xFFFFFFFFu, und != 0u)) {
-        const PbitsPrefix f = pbits_prefix(d >> 5, L, dp.pk);
-#pragma unroll 1
+    for (int h = 0; h < 2; h++) {
+      const RowStream rs = row_stream(G.m, G.row0 + lr0 + h, X);
+      const unsigned long long sid = simbase + (unsigned long long)(rs.gamma - 1);
+      const PbitsLane L = pbits_lane((uint32_t)sid, (uint32_t)(sid >> 32));
+      const unsigned long long d0 =
+          dphase + (unsigned long long)((unsigned)rs.q * (unsigned)(G.n / 2) + 32u * (unsigned)ch +
+                                        (unsigned)(PKS ? w0 >> 1 : (w0 & 15) >> 2) * (unsigned)G.words);
+      uint32_t* Ah = A + h * 128;
+      uint32_t* Bh = B + h * 128;
+      uint32_t* Ch = C + h * 128;
+#pragma unroll
+      for (int kk = 0; kk < 4; kk++) {
+        const uint32_t c4 = Bh[kk * 32];
+        uint32_t und = Ch[kk * 32], acc = 0;
+        const PbitsPrefix f = pbits_prefix((d0 + (unsigned long long)kk * dstep) >> 5, L, dp.pk);
+#pragma unroll
         for (int j = 0; j < 2; j++) {
           uint32_t xs[4];
           pbits_block(f, j, dp.pk, xs);
@@ -727,59 +737,68 @@ __device__ __forceinline__ unsigned direct_group_split(const FlipArgs& a, unsign
             und &= ~(xs[e] ^ km);
           }
         }
-        const uint32_t open = __ballot_sync(0xFFFFFFFFu, und != 0u);
+        Ah[kk * 32] |= acc;
         if (und) {
-          C[k * 32 + lane] = und;
-          Q[qn + __popc(open & ltmask)] = (unsigned char)(lane | (k << 5));
+          Ch[kk * 32] = und;
+          om |= 1u << (h * 4 + kk);
         }
-        qn += __popc(open);
       }
-      A[k * 32 + lane] = sure | acc;
     }
-  }
-  // --- 3. tail: the words with tests still open after 8 planes, one per lane ---
-  if (qn) {
-    __syncwarp();
-    for (unsigned i = lane; i < qn; i += 32) {
-      const unsigned e = Q[i], sl = e & 31u, k = e >> 5;
-      uint32_t und = C[k * 32 + sl];
-      const uint32_t c4 = B[k * 32 + sl];
-      const int q2 = (int)(sl & (unsigned)(sq - 1)), w02 = q2 * 4;
-      const int row = lrg + (int)(sl >> lsq) * 2 + (int)(k >> 2);
-      const RowStream rs = row_stream(G.m, G.row0 + row, X);
-      const unsigned long long sid = simbase + (unsigned long long)(rs.gamma - 1);
-      const PbitsLane L = pbits_lane((uint32_t)sid, (uint32_t)(sid >> 32));
-      const unsigned long long d =
-          dphase + (unsigned long long)((unsigned)rs.q * (unsigned)(G.n / 2) + 32u * (unsigned)(q2 >> 2) +
-                                        (unsigned)(PKS ? w02 >> 1 : (w02 & 15) >> 2) * (unsigned)G.words +
-                                        (k & 3u) * dstep);
-      const PbitsPrefix f = pbits_prefix(d >> 5, L, dp.pk);
-      uint32_t acc = 0;
-#pragma unroll 1
-      for (int j = 2; j < 6 && und; j++) {
-        uint32_t xs[4];
-        pbits_block(f, j, dp.pk, xs);
-        const uint4 ma = kt[2 * j], mb = kt[2 * j + 1];
-        const uint32_t m4[4] = {ma.x, ma.y, ma.z, ma.w}, m8[4] = {mb.x, mb.y, mb.z, mb.w};
+    // --- 3. tail: the words with tests still open after 8 planes, queued
+    // as (lane, slot) and finished one per lane ---
+    const unsigned nopen = __popc(om);
+    unsigned off = nopen;  // inclusive scan over the lanes
 #pragma unroll
-        for (int e2 = 0; e2 < 4; e2++) {
-          const uint32_t km = (c4 & m4[e2]) | (~c4 & m8[e2]);
-          const uint32_t live = (j < 5 || e2 < 3) ? und : 0u;  // plane 23 does not exist
-          acc |= live & ~xs[e2] & km;
-          und &= ~(live & (xs[e2] ^ km));
-        }
-      }
-      if (acc) A[k * 32 + sl] |= acc;
+    for (int dlt = 1; dlt < 32; dlt <<= 1) {
+      const unsigned t = __shfl_up_sync(0xFFFFFFFFu, off, dlt);
+      if (lane >= dlt) off += t;
     }
-    __syncwarp();
+    const unsigned qn = __shfl_sync(0xFFFFFFFFu, off, 31);
+    if (qn) {
+      off -= nopen;
+      for (uint32_t m = om; m; m &= m - 1) Q[off++] = (unsigned char)(lane | ((__ffs(m) - 1) << 5));
+      __syncwarp();
+      for (unsigned i = lane; i < qn; i += 32) {
+        const unsigned e = Q[i], sl = e & 31u, k = e >> 5;
+        uint32_t und = st[512 + k * 32 + sl];
+        const uint32_t c4 = st[256 + k * 32 + sl];
+        const int q2 = (int)(sl & (unsigned)(sq - 1)), w02 = q2 * 4;
+        const int row = lrg + (int)(sl >> lsq) * 2 + (int)(k >> 2);
+        const RowStream rs = row_stream(G.m, G.row0 + row, X);
+        const unsigned long long sid = simbase + (unsigned long long)(rs.gamma - 1);
+        const PbitsLane L = pbits_lane((uint32_t)sid, (uint32_t)(sid >> 32));
+        const unsigned long long d =
+            dphase + (unsigned long long)((unsigned)rs.q * (unsigned)(G.n / 2) + 32u * (unsigned)(q2 >> 2) +
+                                          (unsigned)(PKS ? w02 >> 1 : (w02 & 15) >> 2) * (unsigned)G.words +
+                                          (k & 3u) * dstep);
+        const PbitsPrefix f = pbits_prefix(d >> 5, L, dp.pk);
+        uint32_t acc = 0;
+#pragma unroll 1
+        for (int j = 2; j < 6 && und; j++) {
+          uint32_t xs[4];
+          pbits_block(f, j, dp.pk, xs);
+          const uint4 ma = kt[2 * j], mb = kt[2 * j + 1];
+          const uint32_t m4[4] = {ma.x, ma.y, ma.z, ma.w}, m8[4] = {mb.x, mb.y, mb.z, mb.w};
+#pragma unroll
+          for (int e2 = 0; e2 < 4; e2++) {
+            const uint32_t km = (c4 & m4[e2]) | (~c4 & m8[e2]);
+            const uint32_t live = (j < 5 || e2 < 3) ? und : 0u;  // plane 23 does not exist
+            acc |= live & ~xs[e2] & km;
+            und &= ~(live & (xs[e2] ^ km));
+          }
+        }
+        if (acc) st[k * 32 + sl] |= acc;
+      }
+      __syncwarp();
+    }
   }
   // --- flips into the rows ---
   unsigned cnt = 0;
 #pragma unroll
   for (int h = 0; h < 2; h++) {
     const uint4 O = *reinterpret_cast<const uint4*>(orow + h * Wp);
-    const uint32_t f0 = A[(h * 4 + 0) * 32 + lane], f1 = A[(h * 4 + 1) * 32 + lane], f2 = A[(h * 4 + 2) * 32 + lane],
-                   f3 = A[(h * 4 + 3) * 32 + lane];
+    const uint32_t f0 = A[(h * 4 + 0) * 32], f1 = A[(h * 4 + 1) * 32], f2 = A[(h * 4 + 2) * 32],
+                   f3 = A[(h * 4 + 3) * 32];
     cnt += __popc(f0) + __popc(f1) + __popc(f2) + __popc(f3);
     *reinterpret_cast<uint4*>(orow + h * Wp) = make_uint4(O.x ^ f0, O.y ^ f1, O.z ^ f2, O.w ^ f3);
   }

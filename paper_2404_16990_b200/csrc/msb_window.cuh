@@ -92,6 +92,19 @@ __device__ __forceinline__ void group_wait(const unsigned* flags, unsigned g, un
   __syncwarp();
 }
 
+// group_wait for band l of its replica (no division).
+__device__ __forceinline__ void group_wait_at(const unsigned* flags, unsigned g, unsigned l, unsigned gps, unsigned need) {
+  if ((threadIdx.x & 31) == 0) {
+    const unsigned up = l == 0 ? g + gps - 1 : g - 1, dn = l + 1 == gps ? g + 1 - gps : g + 1;
+    unsigned ns = 32;
+    while (ld_acquire(flags + up) < need || ld_acquire(flags + dn) < need) {
+      __nanosleep(ns);
+      ns = min(ns * 2, kWaitMaxNs);
+    }
+  }
+  __syncwarp();
+}
+
 __device__ __forceinline__ void group_done(unsigned* flags, unsigned g, unsigned v) {
   __syncwarp();
   if ((threadIdx.x & 31) == 0) {
@@ -855,6 +868,7 @@ __device__ __forceinline__ void win_body(const WinArgs& wa, const FlipArgs& fa0,
       const bool pksd = kPksD && fa0.pks;
       unsigned nb = 0;
       int kt_s = -1;  // replica whose key masks the warp's table holds (direct_group_split)
+      unsigned gs = 0, gl = 0;  // replica and band of the current group (direct_group_split)
       if (pksd) {
         pack_rows<false>(fa0.spins, nrows, ct, nct);
         consumer_barrier(wa.work + 1, base + vgrid * ++nb, nwc * 32, leader);
@@ -866,16 +880,28 @@ __device__ __forceinline__ void win_body(const WinArgs& wa, const FlipArgs& fa0,
         dp.pk = wa.pk;
         dp.blk = wa.block0 + 2ull * (unsigned)(first + (i >> 1)) + (unsigned)X;
         for (unsigned g = lo; g < hi; g++) {
-          if (i > 0) group_wait(gflags, g, gps, fbase + (unsigned)i);
           if constexpr (kDirectSplit && DIRECT == 32) {
+            // (replica, band) of the group, stepped from the warp's first group
+            if (g == lo) {
+              gs = lo / gps;
+              gl = lo - gs * gps;
+            }
+            if (i > 0) group_wait_at(gflags, g, gl, gps, fbase + (unsigned)i);
             uint32_t* st = reinterpret_cast<uint32_t*>(jt) + (size_t)warp * kSplitWords;
-            if (kPksD && pksd) cnt += direct_group_split<kPksD>(fa, g, X, dp, st, kt_s);
-            else cnt += direct_group_split<false>(fa, g, X, dp, st, kt_s);
-          } else
-          if (kPksD && pksd) cnt += flip_band_run<true, false, false, DIRECT, true, NoHooks, false, kPksD>(fa, g, g + 1, X, &dp);
-          else if (i == 0 && !pro) cnt += flip_band_run<false, false, false, DIRECT>(fa, g, g + 1, X, &dp);
-          else cnt += flip_band_run<true, false, false, DIRECT>(fa, g, g + 1, X, &dp);
-          group_done(gflags, g, fbase + (unsigned)i + 1u);
+            if (kPksD && pksd) cnt += direct_group_split<kPksD>(fa, g, gs, gl, X, dp, st, kt_s);
+            else cnt += direct_group_split<false>(fa, g, gs, gl, X, dp, st, kt_s);
+            group_done(gflags, g, fbase + (unsigned)i + 1u);
+            if (++gl == gps) {
+              gl = 0;
+              gs++;
+            }
+          } else {
+            if (i > 0) group_wait(gflags, g, gps, fbase + (unsigned)i);
+            if (kPksD && pksd) cnt += flip_band_run<true, false, false, DIRECT, true, NoHooks, false, kPksD>(fa, g, g + 1, X, &dp);
+            else if (i == 0 && !pro) cnt += flip_band_run<false, false, false, DIRECT>(fa, g, g + 1, X, &dp);
+            else cnt += flip_band_run<true, false, false, DIRECT>(fa, g, g + 1, X, &dp);
+            group_done(gflags, g, fbase + (unsigned)i + 1u);
+          }
         }
       }
       if (pksd) {
