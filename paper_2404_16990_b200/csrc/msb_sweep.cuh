@@ -593,8 +593,13 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
 // then each lane XORs its 8 flip words into its rows.
 constexpr int kSplitWords = 3 * 256 + 64;  // A (sure flips -> flips), B (Delta E = 4|J| sites), C (open tests), queue
 
-template <bool PKS>
-__device__ __forceinline__ unsigned direct_group_split(const FlipArgs& a, unsigned g, unsigned s, unsigned l, int X,
+//
+// SEG: rows in several segments of band_sq quads (cfg4, cfg5): the group is
+// (replica s, band l, segment seg), and the lanes at a segment's edges read
+// their outer neighbour word from the row.  PUSH: slabs, whose first / last
+// row also goes into the neighbour slabs' ghost rows.
+template <bool PKS, bool SEG = false, bool PUSH = false>
+__device__ __forceinline__ unsigned direct_group_split(const FlipArgs& a, unsigned s, unsigned l, unsigned seg, int X,
                                                        const PbitsDirect& dp, uint32_t* st, int& kt_s) {
   const Geo& G = a.G;
   const int lane = threadIdx.x & 31;
@@ -604,7 +609,8 @@ __device__ __forceinline__ unsigned direct_group_split(const FlipArgs& a, unsign
   const unsigned Wp = (unsigned)G.Wp, colour_words = (unsigned)G.R * Wp;
   const int lrg = (int)l * gb * 2;  // the group's first row (band l of replica s)
   const int lr0 = lrg + bi * 2;
-  const int ch = q >> 2, w0 = q * 4;
+  const int qg = SEG ? (int)seg * sq + q : q;  // quad of the row
+  const int ch = qg >> 2, w0 = qg * 4;
   const int vb = chunk_bits(G, ch), lastbits = chunk_bits(G, G.nch - 1);
   const uint32_t vm = PKS ? 0xFFFFFFFFu : chunk_mask(G, ch);
   uint32_t* A = st + lane;        // [slot][lane]: sure flips -> flips
@@ -644,7 +650,19 @@ __device__ __forceinline__ unsigned direct_group_split(const FlipArgs& a, unsign
                 Y1 = ld4(ybase + (unsigned)(br0 + 1) * Wp),
                 D1 = ld4(br0 + 2 < G.R ? ybase + (unsigned)(br0 + 2) * Wp : ybase);
     const uint4 O0 = *reinterpret_cast<const uint4*>(orow), O1 = *reinterpret_cast<const uint4*>(orow + Wp);
-    auto classify = [&](auto PC, const uint4& Uq, const uint4& Yq, const uint4& Dq, const uint4& Oq, int slot0) {
+    // SEG: a segment-edge lane's outer neighbour word of each row (the word
+    // after the segment for a row of parity 1, the word before it for 0)
+    const bool p0 = ((G.row0 + lr0 + X) & 1) != 0;
+    const bool seg_last = SEG && q == sq - 1, seg_first = SEG && q == 0;
+    uint32_t e0 = 0, e1 = 0;
+    if (SEG) {
+      const int off_next = (w0 + 4 == (int)Wp ? 0 : w0 + 4) - w0, off_prev = (w0 == 0 ? (int)Wp - 1 : w0 - 1) - w0;
+      const uint32_t* y0 = ybase + (unsigned)br0 * Wp;
+      if (p0 ? seg_last : seg_first) e0 = __ldcg(y0 + (p0 ? off_next : off_prev));
+      if (p0 ? seg_first : seg_last) e1 = __ldcg(y0 + Wp + (p0 ? off_prev : off_next));
+    }
+    auto classify = [&](auto PC, const uint4& Uq, const uint4& Yq, const uint4& Dq, const uint4& Oq, int slot0,
+                        uint32_t eo) {
       constexpr int P = decltype(PC)::value;
       uint32_t edge;
       if (PKS) {
@@ -658,12 +676,14 @@ __device__ __forceinline__ unsigned direct_group_split(const FlipArgs& a, unsign
           edge = other | (Yq.w << 16);
         }
       } else if (P) {
-        const uint32_t xa = __shfl_sync(0xFFFFFFFFu, Yq.x, s_next);
+        uint32_t xa = __shfl_sync(0xFFFFFFFFu, Yq.x, s_next);
         const uint32_t xb = __shfl_sync(0xFFFFFFFFu, Yq.x, s_first);
+        if (SEG && seg_last) xa = eo;
         edge = chunk_last ? ((xb >> 1) | ((xa & 1u) << (vb - 1))) : xa;
       } else {
-        const uint32_t wa = __shfl_sync(0xFFFFFFFFu, Yq.w, s_prev);
+        uint32_t wa = __shfl_sync(0xFFFFFFFFu, Yq.w, s_prev);
         const uint32_t wb = __shfl_sync(0xFFFFFFFFu, Yq.w, s_last);
+        if (SEG && seg_first) wa = eo;
         const uint32_t carry = ch > 0 ? (wa >> 31) : ((wa >> (lastbits - 1)) & 1u);
         edge = chunk_first ? (((wb << 1) | carry) & vm) : wa;
       }
@@ -691,12 +711,12 @@ __device__ __forceinline__ unsigned direct_group_split(const FlipArgs& a, unsign
     };
     using P0 = std::integral_constant<int, 0>;
     using P1 = std::integral_constant<int, 1>;
-    if ((G.row0 + lr0 + X) & 1) {  // warp-uniform
-      classify(P1(), U, Y0, Y1, O0, 0);
-      classify(P0(), Y0, Y1, D1, O1, 4);
+    if (p0) {  // warp-uniform
+      classify(P1(), U, Y0, Y1, O0, 0, e0);
+      classify(P0(), Y0, Y1, D1, O1, 4, e1);
     } else {
-      classify(P0(), U, Y0, Y1, O0, 0);
-      classify(P1(), Y0, Y1, D1, O1, 4);
+      classify(P0(), U, Y0, Y1, O0, 0, e0);
+      classify(P1(), Y0, Y1, D1, O1, 4, e1);
     }
   }
   __syncwarp();  // the key table
@@ -762,7 +782,7 @@ __device__ __forceinline__ unsigned direct_group_split(const FlipArgs& a, unsign
         const unsigned e = Q[i], sl = e & 31u, k = e >> 5;
         uint32_t und = st[512 + k * 32 + sl];
         const uint32_t c4 = st[256 + k * 32 + sl];
-        const int q2 = (int)(sl & (unsigned)(sq - 1)), w02 = q2 * 4;
+        const int q2 = (int)(sl & (unsigned)(sq - 1)) + (SEG ? (int)seg * sq : 0), w02 = q2 * 4;
         const int row = lrg + (int)(sl >> lsq) * 2 + (int)(k >> 2);
         const RowStream rs = row_stream(G.m, G.row0 + row, X);
         const unsigned long long sid = simbase + (unsigned long long)(rs.gamma - 1);
@@ -800,7 +820,14 @@ __device__ __forceinline__ unsigned direct_group_split(const FlipArgs& a, unsign
     const uint32_t f0 = A[(h * 4 + 0) * 32], f1 = A[(h * 4 + 1) * 32], f2 = A[(h * 4 + 2) * 32],
                    f3 = A[(h * 4 + 3) * 32];
     cnt += __popc(f0) + __popc(f1) + __popc(f2) + __popc(f3);
-    *reinterpret_cast<uint4*>(orow + h * Wp) = make_uint4(O.x ^ f0, O.y ^ f1, O.z ^ f2, O.w ^ f3);
+    const uint4 out = make_uint4(O.x ^ f0, O.y ^ f1, O.z ^ f2, O.w ^ f3);
+    *reinterpret_cast<uint4*>(orow + h * Wp) = out;
+    if (PUSH) {
+      if (lr0 + h == 0)  // our first row is the ghost below of the slab above
+        *reinterpret_cast<uint4*>(a.up_spins + (((size_t)s * 2 + X) * a.up_R + a.up_R - 1) * Wp + w0) = out;
+      if (lr0 + h == G.rows - 1)  // our last row is the ghost above of the slab below
+        *reinterpret_cast<uint4*>(a.down_spins + ((size_t)s * 2 + X) * a.down_R * Wp + w0) = out;
+    }
   }
   return cnt;
 }

@@ -888,8 +888,8 @@ __device__ __forceinline__ void win_body(const WinArgs& wa, const FlipArgs& fa0,
             }
             if (i > 0) group_wait_at(gflags, g, gl, gps, fbase + (unsigned)i);
             uint32_t* st = reinterpret_cast<uint32_t*>(jt) + (size_t)warp * kSplitWords;
-            if (kPksD && pksd) cnt += direct_group_split<kPksD>(fa, g, gs, gl, X, dp, st, kt_s);
-            else cnt += direct_group_split<false>(fa, g, gs, gl, X, dp, st, kt_s);
+            if (kPksD && pksd) cnt += direct_group_split<kPksD>(fa, gs, gl, 0u, X, dp, st, kt_s);
+            else cnt += direct_group_split<false>(fa, gs, gl, 0u, X, dp, st, kt_s);
             group_done(gflags, g, fbase + (unsigned)i + 1u);
             if (++gl == gps) {
               gl = 0;
@@ -924,6 +924,7 @@ __device__ __forceinline__ void win_body(const WinArgs& wa, const FlipArgs& fa0,
       go.gps = (unsigned)fa0.G.rows / (unsigned)(fa0.band_gb * fa0.band_h);
       go.nseg = (unsigned)fa0.band_nseg;
       constexpr bool GSEG = GFX == 2;
+      int kt_s = -1;  // replica whose key masks the warp's table holds (direct_group_split)
       for (int i = 0; i < 2 * count; i++) {
         const int X = i & 1;
         PbitsDirect dp;
@@ -936,6 +937,16 @@ __device__ __forceinline__ void win_body(const WinArgs& wa, const FlipArgs& fa0,
         }
         constexpr bool PG = DIRECT != 0;
         const GfHooks<HALO, PG> hk{&go, fbase + (unsigned)i, lo, hi, i > 0, HALO || i > 0};
+        if constexpr (kDirectSplit && DIRECT == 32) {
+          // the split form over the general group order (the hooks' cursor is the group's (s, l, seg))
+          uint32_t* st = reinterpret_cast<uint32_t*>(jt) + (size_t)warp * kSplitWords;
+          for (unsigned g = lo; g < hi; g++) {
+            hk.pre(g);
+            cnt += direct_group_split<false, GSEG, HALO>(fa, hk.cs, hk.cl, hk.cseg, X, dp, st, kt_s);
+            hk.post(g);
+          }
+          continue;
+        }
         cnt += flip_band_run<true, HALO, GSEG, DIRECT, true, GfHooks<HALO, PG>, CB == 16 && !DIRECT>(fa, lo, hi, X, &dp, hk);
         if (!PG) gf_publish_cta<HALO>(go, fbase + (unsigned)i + 1u, per, total, nwc, vgrid, vb, leader);
       }
@@ -1521,7 +1532,8 @@ int direct_run_impl(int nslabs, const msb_ring_slab* slabs, bool ring, int n_swe
   if (vg < 1) return fail(MSB_ERR_UNSUPPORTED, "more slabs than SMs");
   CUDA_TRY(cudaMemcpyAsync(ctx, host, sizeof(SlabCtx) * nslabs, cudaMemcpyHostToDevice, as_stream(stream)));
   cudaLaunchAttribute attr[1];
-  const cudaLaunchConfig_t cfg = coop_config((unsigned)(vg * nslabs), kDirectThreads, 0, stream, attr, true);
+  cudaLaunchConfig_t cfg = coop_config((unsigned)(vg * nslabs), kDirectThreads, 0, stream, attr, true);
+  if (kDirectSplit) cfg.dynamicSmemBytes = (size_t)(kDirectThreads / 32) * kSplitWords * 4;  // the warps' stashes
   return launch_direct<true, 2, true, 0>(cb, cfg, host[0].wa, host[0].fa, host[0].ha, WinIO{}, n_sweeps,
                                            reinterpret_cast<const SlabCtx*>(ctx), nslabs);
 }

@@ -64,9 +64,48 @@ for X in (0, 1):
                 lane_blocks.append(blk.mean())
                 warp_blocks.append(blk.max(-1).mean())
 lb, wb = float(np.mean(lane_blocks)), float(np.mean(warp_blocks))
+
+# Executed work of the split form (direct_group_split): a band group is 8 word
+# slots x 32 lanes.  Blocks 0 and 1 run for every word slot (warp-uniform); the
+# words with a test still open after 8 planes are queued and finished one per
+# lane: ceil(open / 32) passes, each as long as its slowest word (blocks 2..5).
+open_words, tail_iters = [], []
+for X in (0, 1):
+    for c0 in range(0, m, 16):
+        grp = []
+        for h in (0, 1):
+            for k in range(4):
+                words = []
+                for bi in range(8):
+                    c = c0 + 2 * bi + h
+                    for q in range(4):
+                        t = 4 * q + k
+                        cols = 2 * (16 * np.arange(32) + t) + ((c + X) & 1)
+                        words.append(need[:, c, cols])
+                grp.append(np.stack(words, 1))
+        wd = np.stack(grp, 1)                                  # [R, 8 slots, 32 lanes, 32 sites]
+        planes = np.minimum(rng.geometric(0.5, size=wd.shape), 23)
+        blk = np.where(wd, (planes + 3) // 4, 0).max(-1).reshape(R, -1)   # blocks per word, [R, 256]
+        extra = np.maximum(blk - 2, 0)
+        for r in range(R):
+            e = extra[r][extra[r] > 0]
+            open_words.append(len(e))
+            it = 0
+            for p0 in range(0, len(e), 32):
+                it += int(e[p0:p0 + 32].max())
+            tail_iters.append(it)
+ow, ti = float(np.mean(open_words)), float(np.mean(tail_iters))
+# thread instructions per word (SASS counts of the loops, rounded): classes and stash stores 22, prefix 10,
+# two blocks 2 x 49, stash update 6; the tail per group: per pass ~40 (queue entry decode, stream and prefix) +
+# 58 per block iteration, over the group's 8 word slots; the flips into the rows 6
+split_word = 22 + 10 + 2 * 49 + 6 + (40 * np.ceil(ow / 32) + 58 * ti) / 8 + 6
 print(json.dumps({"replicas": R, "sweeps": SW, "frac_sites_needing_draw": round(float(frac), 4),
                   "blocks_per_word": round(float(B), 4), "ops_per_word": round(float(ops_word), 2),
                   "ops_per_attempt": round(float(ops_word) / 32, 3),
                   "executed": {"lane_mean_blocks_per_word": round(lb, 3), "warp_blocks_per_word_slot": round(wb, 3),
                                "divergence_factor": round(wb / lb, 3),
-                               "block_loop_instr_per_word_slot (58 per block, SASS)": round(58 * wb, 1)}}))
+                               "block_loop_instr_per_word_slot (58 per block, SASS)": round(58 * wb, 1)},
+                  "executed_split": {"open_words_per_group_of_256": round(ow, 2),
+                                     "tail_block_iterations_per_group": round(ti, 2),
+                                     "instr_per_word": round(float(split_word), 1),
+                                     "instr_per_attempt": round(float(split_word) / 32, 2)}}))
