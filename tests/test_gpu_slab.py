@@ -153,3 +153,38 @@ def test_fused_ring_equals_single_slab_and_engine():
         assert (one.lattice_rows()[0] == lat).all()
         assert (np.concatenate([s.lattice_rows()[0] for s in ring], axis=0) == lat).all()
     assert one.flips == sum(s.flips for s in ring) == eng.flips
+
+
+# ---- direct sweeps in the split form over the general group order -------------
+
+@pytest.mark.parametrize("m,n,V,J,temps", [
+    (64, 14336, 1, 1.0, [0.4, 2.269, 1e9]),     # 7 row segments; tiny keys and K = 2^23 (always) beside ordinary ones
+    (64, 14336, 2, -1.0, [0.4, 2.269, 1e9]),    # two slabs, ANTI mode
+    (96, 32768, 3, 1.0, [0.25, 1e9]),           # 4 segments of 32 quads; K = 1 and K = 2^23 (always)
+    (32, 2048, 2, 1.0, [1.0, 3.0]),             # single-segment rows through the general order (slabs)
+    (64, 1024 * 33, 2, 1.0, [2.0, 2.5]),        # 33 chunks: segments of 4 quads
+])
+def test_direct_split_segments_and_slabs(m, n, V, J, temps):
+    """philox-bits direct sweeps (direct_group_split) on rows in several
+    segments, as a whole lattice and as a ring of V slabs in one launch:
+    bit-exact against the oracle, extreme keys included (tests that need no
+    draw are folded into the classification), several launches so the stash
+    and the key tables are reused across groups, replicas and phases."""
+    from oracle import oracle as orc
+    from paper_2404_16990_b200 import Engine, LatticeDims
+    from paper_2404_16990_b200.slab import FusedSlabRun, SlabLattice, slab_bounds
+    dims = LatticeDims(m, n)
+    o = orc.OracleEngine(m, n, temps, 31, coupling=J, sim_offset=2, stream="philox-bits")
+    e = Engine(dims, temps, 31, coupling=J, sim_offset=2, stream="philox-bits")
+    slabs = [SlabLattice(dims, temps, 31, a, b - a, coupling=J, sim_offset=2, stream="philox-bits")
+             for a, b in slab_bounds(m, V)]
+    run = FusedSlabRun(slabs, window=3)
+    for k in (1, 3, 2):
+        o.sweep(k)
+        e.run(k, measure_interval=k)
+        run.sweep(k)
+        assert (e.lattices() == o.spins).all(), f"engine after {k} more sweeps"
+        got = np.concatenate([s.lattice_rows() for s in slabs], axis=1)
+        assert (got == o.spins).all(), f"ring of {V} after {k} more sweeps"
+    assert e.flips == o.flips
+    assert sum(s.flips for s in slabs) == o.flips
