@@ -879,15 +879,17 @@ __device__ __forceinline__ void win_body(const WinArgs& wa, const FlipArgs& fa0,
         dp.thr9 = wa.thr9;
         dp.pk = wa.pk;
         dp.blk = wa.block0 + 2ull * (unsigned)(first + (i >> 1)) + (unsigned)X;
-        for (unsigned g = lo; g < hi; g++) {
-          if constexpr (kDirectSplit && DIRECT == 32) {
-            // (replica, band) of the group, stepped from the warp's first group
-            if (g == lo) {
-              gs = lo / gps;
-              gl = lo - gs * gps;
-            }
+        if constexpr (kDirectSplit && DIRECT == 32) {
+          // (replica, band) of the groups, stepped from the warp's first one.
+          // (Taking the range's first and last group -- the ones whose
+          // neighbours another warp owns -- after the interior ones, to give
+          // the neighbour warps a phase of slack, measured no gain: cfg3
+          // 2.949 against 2.954 T.)
+          uint32_t* st = reinterpret_cast<uint32_t*>(jt) + (size_t)warp * kSplitWords;
+          gs = lo / gps;
+          gl = lo - gs * gps;
+          for (unsigned g = lo; g < hi; g++) {
             if (i > 0) group_wait_at(gflags, g, gl, gps, fbase + (unsigned)i);
-            uint32_t* st = reinterpret_cast<uint32_t*>(jt) + (size_t)warp * kSplitWords;
             if (kPksD && pksd) cnt += direct_group_split<kPksD>(fa, gs, gl, 0u, X, dp, st, kt_s);
             else cnt += direct_group_split<false>(fa, gs, gl, 0u, X, dp, st, kt_s);
             group_done(gflags, g, fbase + (unsigned)i + 1u);
@@ -895,6 +897,11 @@ __device__ __forceinline__ void win_body(const WinArgs& wa, const FlipArgs& fa0,
               gl = 0;
               gs++;
             }
+          }
+        }
+        for (unsigned g = lo; g < hi; g++) {
+          if constexpr (kDirectSplit && DIRECT == 32) {
+            break;
           } else {
             if (i > 0) group_wait(gflags, g, gps, fbase + (unsigned)i);
             if (kPksD && pksd) cnt += flip_band_run<true, false, false, DIRECT, true, NoHooks, false, kPksD>(fa, g, g + 1, X, &dp);
