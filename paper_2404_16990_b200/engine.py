@@ -115,6 +115,17 @@ def _resolve_device(device):
     return torch.device("cuda", dev.index if dev.index is not None else torch.cuda.current_device())
 
 
+def _upload_shared(host_tensor, device):
+    """Device copy of a table every engine of the process shares.  The copy
+    runs on whatever stream is current; engines read the table on their own
+    (non-blocking) streams, so it is completed here, once, before any of them
+    can see it."""
+    torch = _torch()
+    dev = host_tensor.to(device)
+    torch.cuda.current_stream(device).synchronize()
+    return dev
+
+
 def _pow_tables(device):
     """Device copy of the 64 nibble tables of A^(2^b) (2 MiB)."""
     global _POW_HOST
@@ -126,7 +137,7 @@ def _pow_tables(device):
                 host = np.empty(64 * 8192, np.uint32)
                 call("msb_rng_power_tables", host.ctypes.data_as(ctypes.c_void_p))
                 _POW_HOST = host
-            _DEV_TABLES[key] = torch.from_numpy(_POW_HOST.view(np.int32)).to(device)
+            _DEV_TABLES[key] = _upload_shared(torch.from_numpy(_POW_HOST.view(np.int32)), device)
         return _DEV_TABLES[key]
 
 
@@ -138,7 +149,7 @@ def _jump_table(device, distance: int):
         if key not in _DEV_TABLES:
             host = np.empty(8192, np.uint32)
             call("msb_rng_jump_table", ctypes.c_uint64(distance), host.ctypes.data_as(ctypes.c_void_p))
-            _DEV_TABLES[key] = torch.from_numpy(host.view(np.int32)).to(device)
+            _DEV_TABLES[key] = _upload_shared(torch.from_numpy(host.view(np.int32)), device)
         return _DEV_TABLES[key]
 
 
