@@ -538,7 +538,11 @@ class FusedSlabRun:
             with s0.stream_ctx():
                 s._obs.zero_()
             call("msb_observe", ctypes.byref(s._g), _p(s._spins), _p(s._obs[: s.n_sim]), _p(s._obs[s.n_sim:]), s0._cs)
-            total = s._obs if total is None else total + s._obs
+            # the sum over the slabs on the slabs' stream too: on the caller's
+            # current stream it could read a slab's counters before msb_observe
+            # has written them
+            with s0.stream_ctx():
+                total = s._obs if total is None else total + s._obs
         return total
 
     def observables(self):

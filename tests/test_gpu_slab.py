@@ -188,3 +188,31 @@ def test_direct_split_segments_and_slabs(m, n, V, J, temps):
         assert (got == o.spins).all(), f"ring of {V} after {k} more sweeps"
     assert e.flips == o.flips
     assert sum(s.flips for s in slabs) == o.flips
+
+
+def test_ring_observables_are_stream_ordered():
+    """The sum of the slabs' observables is ordered behind their msb_observe
+    launches: with the slabs' stream held back (a long sleep kernel ahead of
+    the observe launches) the result is still the finished counters.  (The
+    sum once ran on the caller's current stream and could read a slab's
+    counters before they were written: a full-size ring test failed that
+    way on a cold GPU.)"""
+    import torch
+    from oracle import oracle as orc
+    from paper_2404_16990_b200 import LatticeDims
+    from paper_2404_16990_b200.slab import FusedSlabRun, SlabLattice, slab_bounds
+    m, n, V = 128, 2048, 4
+    dims = LatticeDims(m, n)
+    for stream in ("xoshiro", "philox-bits"):
+        slabs = [SlabLattice(dims, [2.269], 5, a, b - a, stream=stream) for a, b in slab_bounds(m, V)]
+        run = FusedSlabRun(slabs, window=4)
+        run.sweep(5)
+        o = orc.OracleEngine(m, n, [2.269], 5, stream=stream)
+        o.sweep(5)
+        run.synchronize()
+        with slabs[0].stream_ctx():
+            torch.cuda._sleep(200_000_000)  # ~0.1 s ahead of the observe launches
+        ups, unsat = run.observables()
+        o_ups, o_bonds = o.observe()
+        assert ups.tolist() == o_ups.tolist()
+        assert (2 * m * n - 2 * unsat).tolist() == o_bonds.tolist()
