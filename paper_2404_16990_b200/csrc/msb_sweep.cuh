@@ -576,8 +576,10 @@ __device__ __forceinline__ unsigned flip_band_run(const FlipArgs& a, unsigned g0
   return cnt;
 }
 
-// Direct sweeps, split form (whole lattices, single-segment rows, bands of 2
-// rows, 32-draw words; PKS: n = 512 packed rows).  flip_band_run<DIRECT>
+// Direct sweeps, split form (bands of 2 rows, 32-draw words: whole lattices
+// and slabs, rows of one or several segments; PKS: n = 512 packed rows; the
+// launches of every such shape use it, MSB_DIRECT_SPLIT=0 builds the walk
+// form instead).  flip_band_run<DIRECT>
 // resolves each word's tests inside its walk: the block loop of a word runs
 // as long as the slowest lane of the warp needs planes (3.1 blocks per word
 // slot against a lane mean of 1.9), next to the walk's live neighbour words.

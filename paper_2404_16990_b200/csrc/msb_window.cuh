@@ -732,8 +732,9 @@ __device__ __forceinline__ void win_export(const Geo& G, const uint32_t* spins, 
 // (1.99 T) against 768 (1.54 T) and 512 (1.68 T): with fewer warps the
 // band groups no longer spread one per warp, which costs more than the
 // 64-register cap's spills.
-// Direct sweeps of single-segment whole lattices in the split form
-// (direct_group_split, msb_sweep.cuh).
+// Direct sweeps over 32-draw words in the split form (direct_group_split,
+// msb_sweep.cuh): the group-flag path of single-segment whole lattices and the
+// general group order (rows in segments, slabs, rings).  0: the walk form.
 #ifndef MSB_DIRECT_SPLIT
 #define MSB_DIRECT_SPLIT 1
 #endif
