@@ -743,6 +743,10 @@ constexpr bool kDirectSplit = MSB_DIRECT_SPLIT != 0;
 #define MSB_CTA_BLOCKS 1
 #endif
 constexpr bool kCtaBlocks = MSB_CTA_BLOCKS != 0;
+#ifndef MSB_CHUNK_MAP
+#define MSB_CHUNK_MAP 4
+#endif
+constexpr unsigned kChunkMap = MSB_CHUNK_MAP;
 
 #ifndef MSB_DIRECT_THREADS
 #define MSB_DIRECT_THREADS 1024
@@ -845,6 +849,19 @@ __device__ __forceinline__ void win_body(const WinArgs& wa, const FlipArgs& fa0,
       const unsigned pw = (c_hi - c_lo + (unsigned)nwc - 1) / (unsigned)nwc;
       lo = min(c_hi, c_lo + (unsigned)(warp - pwarps) * pw);
       hi = min(c_hi, lo + pw);
+    }
+    if (kChunkMap && DIRECT && !GFX && band && per == 1 && nwc % kChunkMap == 0) {
+      // One group per warp (cfg2): chunks of kChunkMap consecutive groups
+      // per CTA, the chunks interleaved over the CTAs.  Half of the neighbour
+      // pairs then share an SM (see the block mapping above) while every SM
+      // still gets groups of every replica, i.e. of every temperature --
+      // whole blocks gave an SM the groups of one replica and the SMs of the
+      // hot replicas (more draws) became the launch's critical path.
+      // Measured at cfg2: chunks of 2 3.017, 4 3.030, 7 3.006, 14 2.955 T
+      // against 2.991 interleaved.
+      const unsigned w = (unsigned)(warp - pwarps), idx = (w / kChunkMap) * vgrid + vb;
+      lo = min(total, idx * kChunkMap + w % kChunkMap);
+      hi = min(total, lo + 1);
     }
     const unsigned i0 = lo + (threadIdx.x & 31);
     FlipArgs fa = fa0;
