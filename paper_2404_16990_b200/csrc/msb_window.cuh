@@ -833,7 +833,11 @@ __device__ __forceinline__ void win_body(const WinArgs& wa, const FlipArgs& fa0,
                                 : (unsigned)fa0.G.n_sim * (unsigned)fa0.G.rows * ((unsigned)fa0.G.Wp >> 2);
     const unsigned per = band ? (total + nc - 1) / nc : (((total + nc - 1) / nc + 31) & ~31u);
     unsigned lo = min(total, cw * per), hi = min(total, lo + per);
-    if (kCtaBlocks && DIRECT && GFX && band && vgrid == gridDim.x) {
+    // (also the flag path of single-segment lattices when a warp has several
+    // groups and every CTA's block spans several replicas, so that the
+    // blocks mix temperatures: cfg3 2.957 -> 2.984 T)
+    const bool many_replicas = !GFX && per >= 2 && (unsigned)fa0.G.n_sim >= 4u * vgrid;
+    if (kCtaBlocks && DIRECT && (GFX || many_replicas) && band && vgrid == gridDim.x) {
       // Direct flips in the general group order (rows in segments, one slab
       // per launch): a CTA's warps take one contiguous block of groups
       // (floor / ceil(total / CTAs) of them), so most neighbour groups live
